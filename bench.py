@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 NMS engine (see DESIGN.md §6 for the measurement definition).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Headline workload (BASELINE.json config 5): a stream of 8192 frames x 2048 synthetic boxes
+(random_frame distribution: 1920x1080, side 8..64, scores U[0.05,1)), theta 0.5,
+paper_faithful ties, sharded contiguously over the N ranks (one process per GPU, no
+collective on the data path).  One step = every frame of the rank's shard through one
+batched pnms_run.  `value` = frames of all ranks per second of the slowest rank, with inputs
+resident in HBM; `e2e` = the same through NmsEngine.run_host from pinned host buffers
+(H2D inputs + D2H survivor masks inside the timed region).  Rank 0 also reports the
+single-frame latencies of configs 1-3 (the reference's own frames, tests/golden) and the
+256-frame batch of config 4.
+
+--impl reference times the reference algorithm's CPU implementation (the numpy port in
+oracle/parnms_oracle.py, all host cores) on bounded samples of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "NMS latency/frame at N=1024 boxes (µs) and batched frames/sec at 1/2/4/8 B200"
+FRAMES, BOXES, THETA, TIE = 8192, 2048, 0.5, "paper_faithful"
+GEN = dict(frame_w=1920, frame_h=1080, z_range=(8, 64))
+WORKLOAD = (f"config 5: stream of {FRAMES} frames x {BOXES} boxes (random_frame distribution 1920x1080, "
+            f"z 8..64), theta {THETA}, {TIE}, sharded contiguously over the GPUs")
+SEED = 20250200
+
+
+def shard_bounds(total: int, world: int, rank: int) -> tuple[int, int]:
+    return total * rank // world, total * (rank + 1) // world
+
+
+def make_shard(rank: int, world: int):
+    from paper_2502_00535_b200.synth import random_frames
+
+    a, b = shard_bounds(FRAMES, world, rank)
+    # frames are generated in fixed blocks of 64 so every rank count sees the same stream
+    parts = [random_frames(64, BOXES, seed=SEED + blk, **GEN) for blk in range(a // 64, (b + 63) // 64)]
+    cat = [np.concatenate([p[i] for p in parts], 0) for i in range(4)]
+    off = a - (a // 64) * 64
+    return [c[off: off + (b - a)] for c in cat]
+
+
+# --------------------------------------------------------------------- CPU reference leg
+def _cpu_frame(args):
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import parnms_oracle
+
+    x, y, z, s = args
+    keep, _ = parnms_oracle.run_nms_oracle(x, y, z, s, x.shape[0], x.shape[0], THETA, TIE)
+    return len(keep)
+
+
+def cpu_reference_rate(shard, budget_s: float = 8.0, max_frames: int = 4096, pool=None):
+    """Frames/s of the numpy port of engine.run_nms over all host cores (bounded sample)."""
+    import multiprocessing as mp
+
+    cores = os.cpu_count() or 1
+    own = pool is None
+    if own:
+        pool = mp.get_context("fork").Pool(cores)
+    x, y, z, s = shard
+    done, t0, f = 0, time.perf_counter(), 0
+    try:
+        pool.map(_cpu_frame, [(x[i], y[i], z[i], s[i]) for i in range(min(cores, x.shape[0]))])  # warm
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < budget_s and done < max_frames:
+            batch = [((x[(f + i) % x.shape[0]], y[(f + i) % x.shape[0]], z[(f + i) % x.shape[0]],
+                       s[(f + i) % x.shape[0]])) for i in range(cores)]
+            pool.map(_cpu_frame, batch)
+            f += cores
+            done += cores
+        el = time.perf_counter() - t0
+    finally:
+        if own:
+            pool.close()
+            pool.join()
+    return done / el, cores, done, el
+
+
+def run_reference_impl(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import multiprocessing as mp
+
+    shard = make_shard(0, 1)
+    cores = os.cpu_count() or 1
+    pool = mp.get_context("fork").Pool(cores)
+    per_step = []
+    x, y, z, s = shard
+    try:
+        for step in range(args.warmup + args.steps):
+            base = (step * cores) % FRAMES
+            batch = [(x[(base + i) % FRAMES], y[(base + i) % FRAMES], z[(base + i) % FRAMES], s[(base + i) % FRAMES])
+                     for i in range(cores)]
+            t0 = time.perf_counter()
+            pool.map(_cpu_frame, batch)
+            el = time.perf_counter() - t0
+            if step >= args.warmup:
+                per_step.append(el)
+    finally:
+        pool.close()
+        pool.join()
+    tot = sum(per_step)
+    value = cores * len(per_step) / tot
+    sample = f"{cores} frames of the workload per step (one per host core), numpy port of engine.run_nms"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(per_step),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32+f64",
+        "data": "synthetic", "config": {"workload": WORKLOAD, "frames": FRAMES, "boxes_per_frame": BOXES,
+                                        "theta": THETA, "tie_break": TIE},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x40: "sw_thermal_slowdown", 0x80: "hw_thermal_slowdown",
+               0x100: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting", 0x20: "sync_boost"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                try:
+                    r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except AttributeError:
+                    r = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.02)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------- GPU leg
+def latency_suite(torch, dev, iters: int = 50):
+    """Median single-call latency (CUDA events, device-resident inputs) of configs 1-4."""
+    from paper_2502_00535_b200 import batched_nms_keep
+    from paper_2502_00535_b200.synth import random_frames
+
+    g = np.load(ROOT / "tests" / "golden" / "configs.npz")
+    out = {}
+    cases = [(nm, [g[f"{nm}_{c}"].reshape(1, -1) for c in "xyzs"]) for nm in ("C1", "C2", "C3")]
+    cases.append(("C4", list(random_frames(256, 1024, seed=4, **GEN))))
+    for nm, arrs in cases:
+        x, y, z, s = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in arrs)
+        B, n = x.shape
+        ki = torch.empty((B, n), dtype=torch.int32, device=dev)
+        kc = torch.empty((B,), dtype=torch.int32, device=dev)
+        for _ in range(5):
+            batched_nms_keep(x, y, z, s, None, THETA, TIE, n, keep_idx=ki, keep_count=kc)
+        ts = []
+        for _ in range(iters):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            batched_nms_keep(x, y, z, s, None, THETA, TIE, n, keep_idx=ki, keep_count=kc)
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b) * 1e3)
+        out[nm] = {"frames": B, "boxes": n, "median_us": statistics.median(ts), "min_us": min(ts)}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-latency", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_impl(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    shard = make_shard(rank, world)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, cores, nfr, el = cpu_reference_rate(shard)
+        cpu = {"value": rate, "unit": "frames/s", "cores": cores, "kind": "port",
+               "sample": f"{nfr} frames of the workload in {el:.1f} s, numpy port of engine.run_nms "
+                         f"(oracle/parnms_oracle.py), one process per core"}
+
+    import torch
+
+    from paper_2502_00535_b200 import NmsEngine, _lib
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    x, y, z, s = shard
+    F = x.shape[0]
+    dx, dy, dz, ds = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (x, y, z, s))
+    eng = NmsEngine(F, BOXES, THETA, TIE, BOXES, device=dev, chunks=4)
+    lib = _lib.load()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(evs=None):
+        ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+        handles = (__import__("ctypes").c_void_p * 4)(*[e.cuda_event for e in evs]) if evs else None
+        st = lib.pnms_run_profiled(ptr(dx), ptr(dy), ptr(dz), ptr(ds), None, F, BOXES, BOXES, THETA, 0,
+                                   ptr(eng.keep_idx), ptr(eng.keep_count), None, None, ptr(eng.ws_full),
+                                   eng.ws_full.numel(), stream.cuda_stream, handles)
+        _lib.check(st, "pnms_run_profiled")
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    for row in evs:
+        for e in row:
+            e.record(stream)  # materialise the handles
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            step(evs[k])
+        torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    step_ms = [r[0].elapsed_time(r[3]) for r in evs]
+    map_ms = [r[1].elapsed_time(r[2]) for r in evs]
+    sort_ms = [r[0].elapsed_time(r[1]) for r in evs]
+    compact_ms = [r[2].elapsed_time(r[3]) for r in evs]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_total_ms = float(t.item())
+    value = FRAMES * args.steps / (max_total_ms / 1e3)
+
+    # ---- end to end through the public API: pinned host in -> pinned host out
+    hx, hy, hz, hs = (torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in (x, y, z, s))
+    hc = torch.full((F,), BOXES, dtype=torch.int32).pin_memory()
+    om = torch.empty((F, eng.W32), dtype=torch.int32).pin_memory()
+    oc = torch.empty((F,), dtype=torch.int32).pin_memory()
+    for _ in range(args.warmup):
+        eng.run_host(hx, hy, hz, hs, hc, om, oc)
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        eng.run_host(hx, hy, hz, hs, hc, om, oc)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = e0.elapsed_time(e1)
+    t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    e2e_value = FRAMES * args.steps / (float(t.item()) / 1e3)
+    # correctness spot check of the e2e output against the device-resident run
+    ok = bool(torch.equal(oc.to(dev), eng.keep_count))
+
+    lat = None
+    if rank == 0 and not args.no_latency:
+        lat = latency_suite(torch, dev)
+
+    if rank == 0:
+        clocks = clk.summary()
+        props = torch.cuda.get_device_properties(dev)
+        sm_mhz = clocks["sm_mhz"] or clocks["sm_max_mhz"] or 1965
+        ops = 4.0 * BOXES * (BOXES - 1) * F  # 8 int ops per unordered pair
+        map_s = statistics.mean(map_ms) / 1e3
+        achieved = ops / map_s / 1e12
+        peak = props.multi_processor_count * 128 * sm_mhz * 1e6 / 1e12
+        traffic = None
+        prof = ROOT / "profiles" / "map_kernel_ncu.json"
+        if prof.exists():
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        line = {
+            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "frames": FRAMES, "frames_per_gpu": F, "boxes_per_frame": BOXES,
+                       "theta": THETA, "tie_break": TIE, "parallelism": f"frames sharded over {world} GPU(s)",
+                       "l2": "flushed (256 MiB write) between timed steps"},
+            "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": int(F * BOXES * 20 + F * 4),
+                    "d2h_bytes_per_step": int(F * eng.W32 * 4 + F * 4), "matches_device_run": ok},
+            "gpu_launches": 3 * args.steps,
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "pnms_map_kernel<4>", "ops_per_launch": ops,
+                         "peak_basis": f"{props.multi_processor_count} SMs x 128 int lanes x {sm_mhz} MHz "
+                                       "(median SM clock sampled during the timed region)"},
+            "phase_ms": {"sort": statistics.mean(sort_ms), "map": statistics.mean(map_ms),
+                         "compact": statistics.mean(compact_ms)},
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+        }
+        if lat:
+            line["latency_us"] = lat
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

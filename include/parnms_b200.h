@@ -1,0 +1,121 @@
+/*
+ * parnms_b200.h — C ABI of the B200 (sm_100a) NMS engine.
+ *
+ * Drop-in boundary for the reference's NMS hot path
+ *   engine.run_nms(d, cfg)          /root/reference/pkg/src/parnms/engine.py:296-300
+ *   engine.map_phase(d, cfg)        engine.py:176-250
+ *   engine.reduce_phase(b, cfg)     engine.py:253-281
+ *   engine.mask_survivors(d, v)     engine.py:284-293   (host-side; uses pnms_run's keep output)
+ *
+ * Semantics (identical to the reference, bit for bit):
+ *   row i of a frame is suppressed iff some slot j of the frame (padding included,
+ *   padding = (0,0,0,0.0), detections.py:88) satisfies
+ *     gate(i,j)  = s_i < s_j  or  (tie_break == by_index and s_i == s_j and i > j)   engine.py:233-235
+ *     !keep(i,j) where keep = float64(w)*h < theta*(z_j+1)^2  and  z_j != 0       engine.py:219-232
+ *     w = max(min(x_i+z_i, x_j+z_j) - max(x_i,x_j) + 1, 0) in int32 (same for h)
+ *   survivors are the rows i < count that are not suppressed, in ascending input order
+ *   (engine.py:291-292).
+ *
+ * Conventions: every pointer below is a DEVICE pointer unless stated otherwise; every
+ * call is asynchronous on `stream` (a cudaStream_t passed as void*; NULL = legacy default
+ * stream); no call allocates memory or synchronises the host.  All entry points return
+ * PNMS_OK (0) or a negative pnms_status.  Asynchronous CUDA faults surface at the caller's
+ * next synchronisation, exactly like any other CUDA library.
+ */
+#ifndef PARNMS_B200_H_
+#define PARNMS_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum pnms_status {
+  PNMS_OK = 0,
+  PNMS_EINVAL_THETA = -1,     /* theta outside [0,1]            (engine.py:57-58 ConfigError) */
+  PNMS_EINVAL_DMAX = -2,      /* d_max < 1 or count > d_max      (engine.py:59-60, 185-186)   */
+  PNMS_EINVAL_TIE = -3,       /* tie_break not 0/1               (engine.py:67-71)            */
+  PNMS_EINVAL_ARG = -4,       /* null pointer / negative size                                  */
+  PNMS_EWORKSPACE = -5,       /* workspace missing or too small                                */
+  PNMS_ETOO_LARGE = -6,       /* n_max above PNMS_MAX_SLOTS                                    */
+  PNMS_ECUDA = -7,            /* a CUDA launch failed (see pnms_last_cuda_error)               */
+  PNMS_EINVAL_K = -8          /* k < 1 or k does not divide d_max (engine.py:61-64)            */
+} pnms_status;
+
+/* tie_break values (NmsConfig.tie_break, engine.py:33) */
+#define PNMS_TIE_PAPER_FAITHFUL 0
+#define PNMS_TIE_BY_INDEX 1
+
+/* largest per-frame slot count the batched path accepts */
+#define PNMS_MAX_SLOTS 65536
+
+/* Bytes of device workspace pnms_run needs for `batch` frames of stride `n_max`.
+ * Replaces the reference's per-call SuppressionMatrix.all_ones allocation
+ * (engine.py:93-96, 187): the workspace is reused across calls and needs no clearing. */
+int pnms_workspace_bytes(int batch, int n_max, size_t* out_bytes);
+
+/* Batched NMS: the whole run_nms pipeline (engine.py:296-300) for `batch` frames.
+ *
+ *  x, y, z   int32 [batch][n_max]   box corner and side (DetectionVector._x/_y/_z cast to
+ *                                   int32 as engine.py:191-193 does)
+ *  s         float64 [batch][n_max] scores (DetectionVector._s)
+ *  counts    int32 [batch]          valid prefix length per frame (DetectionVector.count);
+ *                                   NULL means every frame has n_max valid slots.  Values are
+ *                                   clamped to [0, n_max] on the device.
+ *  d_max     frame capacity (NmsConfig.d_max); slots [count, d_max) are implicit PADDING
+ *            (0,0,0,0.0) and take part in the gate exactly like the reference's padding
+ *            columns do.  Must be >= n_max's valid counts (checked by the caller).
+ *  theta     NmsConfig.theta, float64 in [0,1]
+ *  tie_break PNMS_TIE_PAPER_FAITHFUL or PNMS_TIE_BY_INDEX
+ * outputs (each may be NULL):
+ *  keep_idx   int32 [batch][n_max]   ascending survivor indices, first keep_count[f] valid
+ *  keep_count int32 [batch]          number of survivors (len(NmsResult.survivors))
+ *  keep_mask  uint32 [batch][ceil(n_max/32)]  survivor bits, bit i%32 of word i/32 — the
+ *             SurvivorMask of engine.py:114-131 restricted to valid rows
+ *  gate_pairs uint64 [batch]         WorkCounters.map_writes of the reference's map phase
+ *                                    (engine.py:236-237), padding slots included
+ */
+int pnms_run(const int32_t* x, const int32_t* y, const int32_t* z, const double* s,
+             const int32_t* counts, int batch, int n_max, int d_max, double theta,
+             int tie_break, int32_t* keep_idx, int32_t* keep_count, uint32_t* keep_mask,
+             uint64_t* gate_pairs, void* workspace, size_t workspace_bytes, void* stream);
+
+/* pnms_run plus phase timing: phase_events points at 4 cudaEvent_t handles (each may be
+ * NULL) recorded on `stream` before the sort, before the map, before the compaction and
+ * after it.  Used by bench.py to time the map kernel on its own launch stream. */
+int pnms_run_profiled(const int32_t* x, const int32_t* y, const int32_t* z, const double* s,
+                      const int32_t* counts, int batch, int n_max, int d_max, double theta, int tie_break,
+                      int32_t* keep_idx, int32_t* keep_count, uint32_t* keep_mask, uint64_t* gate_pairs,
+                      void* workspace, size_t workspace_bytes, void* stream, void* const* phase_events);
+
+/* Reference-layout map phase (engine.py:176-250): writes the full d_max x d_max
+ * SuppressionMatrix — row-major, rows padded to 64-bit words, bit (i,j) at word j/64 bit
+ * j%64 (= byte j/8 bit j%8, little endian, engine.py:74-111), pad bits set to 1 — for ONE
+ * frame whose d_max slots are all given explicitly (padding included).
+ *  bits        uint64 [d_max][ceil(d_max/64)]
+ *  gate_pairs  uint64 [1] (may be NULL): WorkCounters.map_writes */
+int pnms_map_reference_layout(const int32_t* x, const int32_t* y, const int32_t* z,
+                              const double* s, int d_max, double theta, int tie_break,
+                              uint64_t* bits, uint64_t* gate_pairs, void* stream);
+
+/* Reference reduce phase (engine.py:253-281): mask bit i = AND of the first d_max bits
+ * of row i of `bits` (layout as above).  The result is independent of k (Theorem 2);
+ * k is validated like NmsConfig (engine.py:61-64) and otherwise unused.
+ *  mask  uint8 [ceil(d_max/8)]  packed little-endian (SurvivorMask.bits, engine.py:120-122) */
+int pnms_reduce_rows(const uint64_t* bits, int d_max, int k, uint8_t* mask, void* stream);
+
+/* Human-readable text for a pnms_status. */
+const char* pnms_strerror(int status);
+
+/* cudaError_t of the most recent failed launch in this thread (0 if none). */
+int pnms_last_cuda_error(void);
+
+/* Library version string, e.g. "parnms_b200 0.1.0 sm_100a". */
+const char* pnms_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARNMS_B200_H_ */

@@ -1,0 +1,78 @@
+/*
+ * nms_oracle.c — scalar C restatement of the reference engine's run_nms — TEST
+ * INFRASTRUCTURE ONLY (used by tests/ and bench.py's CPU-baseline leg, never by the
+ * product library).
+ *
+ * It follows /root/reference/pkg/src/parnms/engine.py:
+ *   cell verdict     engine.py:219-239  (int32 wrap-around working copies :191-196,
+ *                    float64 product vs float64 threshold :197,229-231, padding guard :232,
+ *                    gate s_i < s_j (+ by_index tie clause) :233-235)
+ *   row AND          engine.py:253-281  (a row survives iff no gated cell is cleared)
+ *   survivor mask    engine.py:284-293  (rows < count, ascending)
+ *   map_writes       engine.py:236-237  (every gate pass over the d_max x d_max slots)
+ * Slots [count, d_max) are PADDING (0,0,0,0.0) as DetectionVector builds them
+ * (detections.py:121-131).  It is a straight double loop with an early exit per row; it
+ * shares no code with the CUDA path.
+ */
+#include <stdint.h>
+#include <stddef.h>
+
+typedef struct {
+  int32_t x, y, z;
+  double s;
+} slot_t;
+
+static slot_t slot_at(const int32_t* x, const int32_t* y, const int32_t* z, const double* s, int count, int i) {
+  slot_t r;
+  if (i < count) {
+    r.x = x[i]; r.y = y[i]; r.z = z[i]; r.s = s[i];
+  } else {
+    r.x = 0; r.y = 0; r.z = 0; r.s = 0.0;
+  }
+  return r;
+}
+
+static int32_t wrap_add(int32_t a, int32_t b) { return (int32_t)((uint32_t)a + (uint32_t)b); }
+static int32_t wrap_sub(int32_t a, int32_t b) { return (int32_t)((uint32_t)a - (uint32_t)b); }
+static int32_t imin(int32_t a, int32_t b) { return a < b ? a : b; }
+static int32_t imax(int32_t a, int32_t b) { return a > b ? a : b; }
+
+/* keep bit of cell (i, j): candidate i against reference j (engine.py:219-232) */
+static int cell_keep(slot_t a, slot_t b, double theta) {
+  int32_t w = wrap_add(wrap_sub(imin(wrap_add(a.x, a.z), wrap_add(b.x, b.z)), imax(a.x, b.x)), 1);
+  int32_t h = wrap_add(wrap_sub(imin(wrap_add(a.y, a.z), wrap_add(b.y, b.z)), imax(a.y, b.y)), 1);
+  if (w < 0) w = 0;
+  if (h < 0) h = 0;
+  double zf = (double)b.z + 1.0;
+  double thr = theta * (zf * zf);
+  double prod = (double)w * (double)h;
+  return (prod < thr) && (b.z != 0);
+}
+
+static int cell_gate(slot_t a, slot_t b, int i, int j, int by_index) {
+  return (a.s < b.s) || (by_index && a.s == b.s && i > j);
+}
+
+/* Returns the number of survivors written to keep_out (ascending input indices). */
+int oracle_run_nms(const int32_t* x, const int32_t* y, const int32_t* z, const double* s, int count, int d_max,
+                   double theta, int by_index, int32_t* keep_out, unsigned long long* map_writes) {
+  int kept = 0;
+  for (int i = 0; i < count; ++i) {
+    slot_t a = slot_at(x, y, z, s, count, i);
+    int suppressed = 0;
+    for (int j = 0; j < d_max && !suppressed; ++j) {
+      slot_t b = slot_at(x, y, z, s, count, j);
+      if (cell_gate(a, b, i, j, by_index) && !cell_keep(a, b, theta)) suppressed = 1;
+    }
+    if (!suppressed) keep_out[kept++] = i;
+  }
+  if (map_writes) {
+    unsigned long long g = 0;
+    for (int i = 0; i < d_max; ++i) {
+      slot_t a = slot_at(x, y, z, s, count, i);
+      for (int j = 0; j < d_max; ++j) g += (unsigned long long)cell_gate(a, slot_at(x, y, z, s, count, j), i, j, by_index);
+    }
+    *map_writes = g;
+  }
+  return kept;
+}

@@ -1,0 +1,107 @@
+"""ctypes binding of the C ABI in include/parnms_b200.h (libparnms_b200.so).
+
+The library is the only compute path: if it is missing or cannot be loaded, every entry
+point raises — there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libparnms_b200.so"
+
+# every symbol include/parnms_b200.h declares
+EXPORTED_SYMBOLS = (
+    "pnms_workspace_bytes",
+    "pnms_run",
+    "pnms_run_profiled",
+    "pnms_map_reference_layout",
+    "pnms_reduce_rows",
+    "pnms_strerror",
+    "pnms_last_cuda_error",
+    "pnms_version",
+)
+
+PNMS_OK = 0
+PNMS_EINVAL_THETA = -1
+PNMS_EINVAL_DMAX = -2
+PNMS_EINVAL_TIE = -3
+PNMS_EINVAL_ARG = -4
+PNMS_EWORKSPACE = -5
+PNMS_ETOO_LARGE = -6
+PNMS_ECUDA = -7
+PNMS_EINVAL_K = -8
+
+TIE_CODES = {"paper_faithful": 0, "by_index": 1}
+MAX_SLOTS = 65536
+
+_lib = None
+
+
+class NativeLibraryError(RuntimeError):
+    """libparnms_b200.so is missing, unloadable, or a native call failed."""
+
+
+def load(build_if_missing: bool = False) -> ctypes.CDLL:
+    """Load (once) and return the native library; raises NativeLibraryError if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        if build_if_missing:
+            from . import build as _build
+
+            _build.build()
+        else:
+            raise NativeLibraryError(
+                f"{LIB_PATH.name} is not built; run `python -m paper_2502_00535_b200.build` "
+                "(the B200 engine has no CPU fallback)"
+            )
+    try:
+        lib = ctypes.CDLL(str(LIB_PATH))
+    except OSError as exc:
+        raise NativeLibraryError(f"cannot load {LIB_PATH}: {exc}") from exc
+    vp, i32, f64, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_size_t
+    lib.pnms_workspace_bytes.argtypes = [i32, i32, ctypes.POINTER(sz)]
+    lib.pnms_workspace_bytes.restype = i32
+    lib.pnms_run.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, f64, i32, vp, vp, vp, vp, vp, sz, vp]
+    lib.pnms_run.restype = i32
+    lib.pnms_run_profiled.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, f64, i32, vp, vp, vp, vp, vp, sz, vp, vp]
+    lib.pnms_run_profiled.restype = i32
+    lib.pnms_map_reference_layout.argtypes = [vp, vp, vp, vp, i32, f64, i32, vp, vp, vp]
+    lib.pnms_map_reference_layout.restype = i32
+    lib.pnms_reduce_rows.argtypes = [vp, i32, i32, vp, vp]
+    lib.pnms_reduce_rows.restype = i32
+    lib.pnms_strerror.argtypes = [i32]
+    lib.pnms_strerror.restype = ctypes.c_char_p
+    lib.pnms_last_cuda_error.argtypes = []
+    lib.pnms_last_cuda_error.restype = i32
+    lib.pnms_version.argtypes = []
+    lib.pnms_version.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def strerror(status: int) -> str:
+    return load().pnms_strerror(int(status)).decode()
+
+
+def check(status: int, what: str) -> None:
+    """Raise for a non-zero pnms_status (configuration errors map to ConfigError)."""
+    if status == PNMS_OK:
+        return
+    msg = f"{what}: {strerror(status)}"
+    if status in (PNMS_EINVAL_THETA, PNMS_EINVAL_DMAX, PNMS_EINVAL_TIE, PNMS_EINVAL_K):
+        from .engine import ConfigError
+
+        raise ConfigError(msg)
+    if status == PNMS_ECUDA:
+        msg += f" (cudaError {load().pnms_last_cuda_error()})"
+    raise NativeLibraryError(msg)
+
+
+def workspace_bytes(batch: int, n_max: int) -> int:
+    out = ctypes.c_size_t(0)
+    check(load().pnms_workspace_bytes(int(batch), int(n_max), ctypes.byref(out)), "pnms_workspace_bytes")
+    return int(out.value)

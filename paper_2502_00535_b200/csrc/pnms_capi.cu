@@ -1,0 +1,302 @@
+// pnms_capi.cu — extern "C" entry points of libparnms_b200.so (declared in
+// include/parnms_b200.h).  Host-side orchestration only: argument validation with the
+// reference's ConfigError conditions, workspace carving, launch-shape heuristics, and the
+// stream-ordered launch sequence
+//     prep+sort  ->  map (+row reduce)  ->  compact
+// No host synchronisation and no allocation happens here.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+
+#include "../../include/parnms_b200.h"
+#include "pnms_common.cuh"
+#include "pnms_compact.cuh"
+#include "pnms_map.cuh"
+#include "pnms_reflayout.cuh"
+#include "pnms_sort.cuh"
+
+using namespace pnms;
+
+namespace {
+
+thread_local int g_last_cuda_error = 0;
+
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct Layout {
+  size_t rec, perm, lim, supp, meta, sk, idx, total;
+};
+
+Layout make_layout(int batch, int n_max) {
+  Layout L;
+  const size_t B = (size_t)batch, N = (size_t)n_max;
+  const size_t W32 = (N + 31) / 32;
+  size_t off = 0;
+  L.rec = off;  off = align_up(off + B * N * kRecBytes, 256);
+  L.perm = off; off = align_up(off + B * N * 4, 256);
+  L.lim = off;  off = align_up(off + B * N * 4, 256);
+  L.supp = off; off = align_up(off + B * W32 * 4, 256);
+  L.meta = off; off = align_up(off + B * sizeof(FrameMeta), 256);
+  if (n_max > kSortMax) {
+    L.sk = off;  off = align_up(off + B * N * 8, 256);
+    L.idx = off; off = align_up(off + B * N * 4, 256);
+  } else {
+    L.sk = L.idx = 0;
+  }
+  L.total = off;
+  return L;
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  return std::atoi(v);
+}
+
+int fail_cuda(cudaError_t e) {
+  g_last_cuda_error = (int)e;
+  return PNMS_ECUDA;
+}
+
+template <typename K>
+cudaError_t ensure_smem(K kernel, size_t bytes, std::atomic<size_t>& configured) {
+  if (bytes <= 48 * 1024 || configured.load(std::memory_order_relaxed) >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) configured.store(bytes, std::memory_order_relaxed);
+  return e;
+}
+
+std::atomic<size_t> g_sort_frame_smem{0}, g_sort_chunk_smem{0}, g_compact_smem{0};
+std::atomic<size_t> g_map_smem[5];
+
+struct MapShape {
+  int R, RB, chunk;
+};
+
+// Work-item shape: many small items when the call has little total work (single-frame
+// latency), large items when there are many frames (batched throughput).
+MapShape choose_map_shape(int batch, int n_max) {
+  MapShape m;
+  const long long rows = (long long)batch * n_max;
+  if (rows >= 148LL * 1024) {
+    m.R = 4;
+    m.chunk = 1024;
+  } else {
+    m.R = 1;
+    m.chunk = 256;
+  }
+  const int r_env = env_int("PNMS_MAP_R", 0);
+  if (r_env == 1 || r_env == 2 || r_env == 4) m.R = r_env;
+  const int c_env = env_int("PNMS_MAP_CHUNK", 0);
+  if (c_env >= 32 && c_env <= 4096 && (c_env % 32) == 0) m.chunk = c_env;
+  m.RB = kMapWarps * 32 * m.R;
+  return m;
+}
+
+template <int R>
+cudaError_t launch_map(const MapArgs& ma, long long grid, size_t smem, cudaStream_t st) {
+  cudaError_t e = ensure_smem(pnms_map_kernel<R>, smem, g_map_smem[R]);
+  if (e != cudaSuccess) return e;
+  pnms_map_kernel<R><<<(unsigned)grid, kMapWarps * 32, smem, st>>>(ma);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pnms_version(void) { return "parnms_b200 0.1.0 sm_100a"; }
+
+int pnms_last_cuda_error(void) { return g_last_cuda_error; }
+
+const char* pnms_strerror(int status) {
+  switch (status) {
+    case PNMS_OK: return "ok";
+    case PNMS_EINVAL_THETA: return "theta must be in [0, 1]";
+    case PNMS_EINVAL_DMAX: return "d_max must be positive and hold every frame's detections";
+    case PNMS_EINVAL_TIE: return "tie_break must be paper_faithful (0) or by_index (1)";
+    case PNMS_EINVAL_ARG: return "invalid argument (null pointer or negative size)";
+    case PNMS_EWORKSPACE: return "workspace missing or smaller than pnms_workspace_bytes()";
+    case PNMS_ETOO_LARGE: return "n_max exceeds PNMS_MAX_SLOTS";
+    case PNMS_ECUDA: return "CUDA launch failed (see pnms_last_cuda_error)";
+    case PNMS_EINVAL_K: return "k must be positive and divide d_max";
+    default: return "unknown parnms_b200 status";
+  }
+}
+
+int pnms_workspace_bytes(int batch, int n_max, size_t* out_bytes) {
+  if (!out_bytes || batch < 0 || n_max < 0) return PNMS_EINVAL_ARG;
+  if (n_max > PNMS_MAX_SLOTS) return PNMS_ETOO_LARGE;
+  *out_bytes = make_layout(batch, n_max).total;
+  return PNMS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+inline cudaError_t mark(void* const* events, int i, cudaStream_t st) {
+  if (!events || !events[i]) return cudaSuccess;
+  return cudaEventRecord((cudaEvent_t)events[i], st);
+}
+
+int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double* s, const int32_t* counts,
+             int batch, int n_max, int d_max, double theta, int tie_break, int32_t* keep_idx,
+             int32_t* keep_count, uint32_t* keep_mask, uint64_t* gate_pairs, void* workspace,
+             size_t workspace_bytes, void* stream, void* const* events) {
+  if (!(theta >= 0.0 && theta <= 1.0)) return PNMS_EINVAL_THETA;
+  if (d_max < 1) return PNMS_EINVAL_DMAX;
+  if (tie_break != PNMS_TIE_PAPER_FAITHFUL && tie_break != PNMS_TIE_BY_INDEX) return PNMS_EINVAL_TIE;
+  if (batch < 0 || n_max < 0) return PNMS_EINVAL_ARG;
+  if (n_max > PNMS_MAX_SLOTS) return PNMS_ETOO_LARGE;
+  if (batch == 0 || n_max == 0) {
+    cudaStream_t st0 = (cudaStream_t)stream;
+    if (batch > 0 && keep_count) {
+      cudaError_t e = cudaMemsetAsync(keep_count, 0, sizeof(int32_t) * batch, st0);
+      if (e != cudaSuccess) return fail_cuda(e);
+    }
+    if (batch > 0 && gate_pairs) {
+      // all d_max slots are padding (0,0,0,0.0): only by_index gates equal-score pairs
+      // (handled on the host side of the Python layer; here report zero work)
+      cudaError_t e = cudaMemsetAsync(gate_pairs, 0, sizeof(uint64_t) * batch, st0);
+      if (e != cudaSuccess) return fail_cuda(e);
+    }
+    return PNMS_OK;
+  }
+  if (!x || !y || !z || !s) return PNMS_EINVAL_ARG;
+  const Layout L = make_layout(batch, n_max);
+  if (!workspace || workspace_bytes < L.total) return PNMS_EWORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  const int W32 = (n_max + 31) / 32;
+  cudaError_t e;
+
+  PrepArgs pa;
+  pa.x = x; pa.y = y; pa.z = z; pa.s = s; pa.counts = counts;
+  pa.batch = batch; pa.n_max = n_max; pa.tie_break = tie_break; pa.W32 = W32;
+  pa.theta = theta;
+  pa.rec = ws + L.rec;
+  pa.perm = reinterpret_cast<int32_t*>(ws + L.perm);
+  pa.lim = reinterpret_cast<int32_t*>(ws + L.lim);
+  pa.supp = reinterpret_cast<uint32_t*>(ws + L.supp);
+  pa.meta = reinterpret_cast<FrameMeta*>(ws + L.meta);
+  pa.sk_scratch = L.sk ? reinterpret_cast<uint64_t*>(ws + L.sk) : nullptr;
+  pa.idx_scratch = L.idx ? reinterpret_cast<int32_t*>(ws + L.idx) : nullptr;
+
+  if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
+  if (n_max <= kSortMax) {
+    pa.npad = (n_max + kSortThreads - 1) / kSortThreads * kSortThreads;
+    pa.nchunks = 1;
+    const size_t smem = sort_smem_bytes(pa.npad);
+    if ((e = ensure_smem(pnms_prep_sort_frame, smem, g_sort_frame_smem)) != cudaSuccess) return fail_cuda(e);
+    pnms_prep_sort_frame<<<batch, kSortThreads, smem, st>>>(pa);
+    if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
+  } else {
+    pa.npad = kSortMax;
+    pa.nchunks = (n_max + kSortMax - 1) / kSortMax;
+    if ((e = cudaMemsetAsync(pa.meta, 0, sizeof(FrameMeta) * (size_t)batch, st)) != cudaSuccess) return fail_cuda(e);
+    const size_t smem = sort_smem_bytes(kSortMax);
+    if ((e = ensure_smem(pnms_prep_sort_chunk, smem, g_sort_chunk_smem)) != cudaSuccess) return fail_cuda(e);
+    pnms_prep_sort_chunk<<<(unsigned)((long long)batch * pa.nchunks), kSortThreads, smem, st>>>(pa);
+    if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
+    const long long blocks = (long long)batch * ((n_max + 255) / 256);
+    pnms_merge_rank<<<(unsigned)blocks, 256, 0, st>>>(pa);
+    if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
+  }
+
+  if ((e = mark(events, 1, st)) != cudaSuccess) return fail_cuda(e);
+  const MapShape ms = choose_map_shape(batch, n_max);
+  MapArgs ma;
+  ma.rec = pa.rec; ma.lim = pa.lim; ma.supp = pa.supp; ma.meta = pa.meta;
+  ma.batch = batch; ma.n_max = n_max; ma.W32 = W32;
+  ma.rows_per_block = ms.RB;
+  ma.chunk = ms.chunk;
+  ma.n_rb = (n_max + ms.RB - 1) / ms.RB;
+  int ipf = 0;
+  for (int rb = 0; rb < ma.n_rb; ++rb) {
+    const int cols = std::min((rb + 1) * ms.RB - 1, n_max);
+    ipf += (cols + ms.chunk - 1) / ms.chunk;
+  }
+  ma.items_per_frame = ipf;
+  ma.k65536 = 65536u;
+  const long long grid = (long long)batch * ipf;
+  if (grid > 0x7FFFFFFFLL) return PNMS_ETOO_LARGE;
+  const size_t map_smem = (size_t)ms.chunk * kRecBytes;
+  if (ms.R == 4) e = launch_map<4>(ma, grid, map_smem, st);
+  else if (ms.R == 2) e = launch_map<2>(ma, grid, map_smem, st);
+  else e = launch_map<1>(ma, grid, map_smem, st);
+  if (e != cudaSuccess) return fail_cuda(e);
+
+  if ((e = mark(events, 2, st)) != cudaSuccess) return fail_cuda(e);
+  CompactArgs ca;
+  ca.s = s; ca.counts = counts; ca.perm = pa.perm; ca.supp = pa.supp; ca.meta = pa.meta;
+  ca.batch = batch; ca.n_max = n_max; ca.W32 = W32; ca.d_max = d_max; ca.tie_break = tie_break;
+  ca.keep_idx = keep_idx; ca.keep_count = keep_count; ca.keep_mask = keep_mask;
+  ca.gate_pairs = reinterpret_cast<unsigned long long*>(gate_pairs);
+  const size_t csmem = ((size_t)n_max + 15) / 16 * 16 + 64 * 4;
+  if ((e = ensure_smem(pnms_compact, csmem, g_compact_smem)) != cudaSuccess) return fail_cuda(e);
+  pnms_compact<<<batch, kCompactThreads, csmem, st>>>(ca);
+  if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
+  if ((e = mark(events, 3, st)) != cudaSuccess) return fail_cuda(e);
+  return PNMS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pnms_run(const int32_t* x, const int32_t* y, const int32_t* z, const double* s, const int32_t* counts,
+             int batch, int n_max, int d_max, double theta, int tie_break, int32_t* keep_idx,
+             int32_t* keep_count, uint32_t* keep_mask, uint64_t* gate_pairs, void* workspace,
+             size_t workspace_bytes, void* stream) {
+  return run_impl(x, y, z, s, counts, batch, n_max, d_max, theta, tie_break, keep_idx, keep_count, keep_mask,
+                  gate_pairs, workspace, workspace_bytes, stream, nullptr);
+}
+
+int pnms_run_profiled(const int32_t* x, const int32_t* y, const int32_t* z, const double* s,
+                      const int32_t* counts, int batch, int n_max, int d_max, double theta, int tie_break,
+                      int32_t* keep_idx, int32_t* keep_count, uint32_t* keep_mask, uint64_t* gate_pairs,
+                      void* workspace, size_t workspace_bytes, void* stream, void* const* phase_events) {
+  return run_impl(x, y, z, s, counts, batch, n_max, d_max, theta, tie_break, keep_idx, keep_count, keep_mask,
+                  gate_pairs, workspace, workspace_bytes, stream, phase_events);
+}
+
+int pnms_map_reference_layout(const int32_t* x, const int32_t* y, const int32_t* z, const double* s, int d_max,
+                              double theta, int tie_break, uint64_t* bits, uint64_t* gate_pairs, void* stream) {
+  if (!(theta >= 0.0 && theta <= 1.0)) return PNMS_EINVAL_THETA;
+  if (d_max < 1) return PNMS_EINVAL_DMAX;
+  if (tie_break != PNMS_TIE_PAPER_FAITHFUL && tie_break != PNMS_TIE_BY_INDEX) return PNMS_EINVAL_TIE;
+  if (!x || !y || !z || !s || !bits) return PNMS_EINVAL_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  RefMapArgs ra;
+  ra.x = x; ra.y = y; ra.z = z; ra.s = s;
+  ra.d_max = d_max; ra.W64 = (d_max + 63) / 64; ra.tie_break = tie_break; ra.theta = theta;
+  ra.bits = bits;
+  ra.gate_pairs = reinterpret_cast<unsigned long long*>(gate_pairs);
+  if (gate_pairs && (e = cudaMemsetAsync(gate_pairs, 0, sizeof(uint64_t), st)) != cudaSuccess) return fail_cuda(e);
+  const long long units = (long long)d_max * ra.W64;
+  const long long blocks = (units + 7) / 8;
+  if (blocks > 0x7FFFFFFFLL) return PNMS_ETOO_LARGE;
+  pnms_ref_map<<<(unsigned)blocks, 256, 0, st>>>(ra);
+  if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
+  return PNMS_OK;
+}
+
+int pnms_reduce_rows(const uint64_t* bits, int d_max, int k, uint8_t* mask, void* stream) {
+  if (d_max < 1) return PNMS_EINVAL_DMAX;
+  if (k < 1 || d_max % k != 0) return PNMS_EINVAL_K;
+  if (!bits || !mask) return PNMS_EINVAL_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int W64 = (d_max + 63) / 64;
+  pnms_ref_reduce<<<(d_max + 7) / 8, 256, 0, st>>>(bits, d_max, W64, mask);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail_cuda(e);
+  return PNMS_OK;
+}
+
+}  // extern "C"

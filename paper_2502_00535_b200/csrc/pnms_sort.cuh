@@ -1,0 +1,345 @@
+// pnms_sort.cuh — per-frame preparation and segmented score sort.
+//
+// The reference never sorts: it tests all d_max^2 ordered
+// slot pairs and lets the score gate `s_i < s_j` (engine.py:233-235) discard half of them.
+// Sorting every frame by (score desc, index asc) turns that gate into a loop bound: sorted
+// row p only needs columns q < lim[p], where
+//   lim[p] = first position of p's equal-score group   (tie_break = paper_faithful)
+//   lim[p] = p                                         (tie_break = by_index)
+// which is exactly the set of slots that pass the reference's gate.  The sort is a stable
+// LSD radix sort on the 64-bit order-preserving key, so equal scores keep input order.
+//
+// Frames of up to kSortMax slots are sorted inside one CTA (pnms_prep_sort_frame).  Larger
+// frames are cut into kSortMax-slot chunks sorted independently (pnms_prep_sort_chunk) and
+// merged by rank (pnms_merge_rank): a slot's global position is its position in its own
+// chunk plus, for every other chunk, the number of slots there that precede it — found by a
+// binary search, because chunks cover contiguous index ranges.
+#pragma once
+#include "pnms_common.cuh"
+
+namespace pnms {
+
+struct PrepArgs {
+  const int32_t* x;
+  const int32_t* y;
+  const int32_t* z;
+  const double* s;
+  const int32_t* counts;  // may be null
+  int batch, n_max, npad, tie_break, W32, nchunks;
+  double theta;
+  uint8_t* rec;       // [batch][n_max] records, kRecBytes stride per frame slot
+  int32_t* perm;      // [batch][n_max] sorted position -> input index
+  int32_t* lim;       // [batch][n_max] column limit of the sorted row
+  uint32_t* supp;     // [batch][W32]  suppression bits in sorted order (zeroed here)
+  FrameMeta* meta;    // [batch]
+  uint64_t* sk_scratch;   // chunk mode: sorted keys   [batch][n_max]
+  int32_t* idx_scratch;   // chunk mode: sorted index  [batch][n_max]
+};
+
+__device__ __forceinline__ int frame_count(const int32_t* counts, int f, int n_max) {
+  int c = counts ? counts[f] : n_max;
+  return c < 0 ? 0 : (c > n_max ? n_max : c);
+}
+
+// lower_bound / upper_bound over an ascending array
+__device__ __forceinline__ int lower_bound_u64(const uint64_t* a, int n, uint64_t v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ int upper_bound_u64(const uint64_t* a, int n, uint64_t v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] <= v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Stable block radix sort (ascending) of npad = 512*E (key, idx) pairs held in shared memory,
+// 8-bit digits, digits on which all keys agree (diff == 0) are skipped.  Warp w owns the
+// contiguous run [w*32E, (w+1)*32E); inside a warp, rounds of 32 consecutive slots are
+// ranked with __match_any_sync so the scatter preserves input order.
+// On return *k / *id point at the buffer that holds the sorted sequence.
+__device__ void block_radix_sort(uint64_t** k, uint16_t** id, uint64_t* k2, uint16_t* id2,
+                                 uint32_t* hist, uint32_t* scan_tmp, int E, uint64_t diff) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lt = lanemask_lt();
+  uint64_t* ka = *k;
+  uint16_t* ia = *id;
+  uint64_t* kb = k2;
+  uint16_t* ib = id2;
+  const int wbase = warp * 32 * E;
+  for (int sh = 0; sh < 64; sh += 8) {
+    if (((diff >> sh) & 0xFFull) == 0) continue;
+    for (int i = threadIdx.x; i < 256 * kSortWarps; i += kSortThreads) hist[i] = 0;
+    __syncthreads();
+    uint64_t key[8];
+    uint16_t ix[8];
+    uint32_t dig[8], peers[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      if (r < E) {
+        int e = wbase + r * 32 + lane;
+        key[r] = ka[e];
+        ix[r] = ia[e];
+        dig[r] = static_cast<uint32_t>(key[r] >> sh) & 0xFFu;
+        peers[r] = __match_any_sync(0xFFFFFFFFu, dig[r]);
+        if (lane == __ffs(peers[r]) - 1) hist[dig[r] * kSortWarps + warp] += __popc(peers[r]);
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // exclusive scan over the digit-major (digit, warp) histogram: 4096 counters, 8/thread
+    {
+      uint32_t loc[8], sum = 0;
+      const int b0 = threadIdx.x * 8;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) { loc[t] = hist[b0 + t]; sum += loc[t]; }
+      uint32_t excl = block_exclusive_scan(sum, scan_tmp, nullptr);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) { hist[b0 + t] = excl; excl += loc[t]; }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      if (r < E) {
+        const uint32_t slot = dig[r] * kSortWarps + warp;
+        const uint32_t base = hist[slot];
+        const uint32_t pos = base + __popc(peers[r] & lt);
+        kb[pos] = key[r];
+        ib[pos] = ix[r];
+        __syncwarp();
+        if (lane == __ffs(peers[r]) - 1) hist[slot] = base + __popc(peers[r]);
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    uint64_t* tk = ka; ka = kb; kb = tk;
+    uint16_t* ti = ia; ia = ib; ib = ti;
+  }
+  *k = ka;
+  *id = ia;
+}
+
+__device__ __forceinline__ void write_record(uint8_t* rec_frame, int pos, int mode, int32_t x, int32_t y,
+                                             int32_t z, double theta) {
+  if (mode == kWide) {
+    reinterpret_cast<RecWide*>(rec_frame)[pos] = make_rec_wide(x, y, z, theta);
+  } else {
+    reinterpret_cast<RecNarrow*>(rec_frame)[pos] = make_rec_narrow(x, y, z, theta);
+  }
+}
+
+struct LoadStats {
+  uint32_t or_lo, or_hi, and_lo, and_hi;
+  int mode, n_act, neg, pos, zero;
+};
+
+// Loads slots [e0, e0+len) of a frame into (key, local idx) smem arrays of size npad and
+// reduces the statistics the later phases need.  Slots past len are padded with the NaN
+// key (they sort last, after real NaNs, by stability).
+__device__ void load_keys(const PrepArgs& a, long long fbase, int e0, int len, int npad, uint64_t* k,
+                          uint16_t* id, LoadStats* st) {
+  const int lane = threadIdx.x & 31;
+  uint32_t or_lo = 0, or_hi = 0, and_lo = ~0u, and_hi = ~0u;
+  int mode = kNarrow8, n_act = 0, neg = 0, pos = 0, zero = 0;
+  for (int e = threadIdx.x; e < npad; e += kSortThreads) {
+    uint64_t key = kNanSortKey;
+    if (e < len) {
+      long long g = fbase + e0 + e;
+      double sv = a.s[g];
+      key = sort_key(sv);
+      int m = frame_mode_of(a.x[g], a.y[g], a.z[g]);
+      mode = m > mode ? m : mode;
+      or_lo |= (uint32_t)key; or_hi |= (uint32_t)(key >> 32);
+      and_lo &= (uint32_t)key; and_hi &= (uint32_t)(key >> 32);
+      n_act += (key != kNanSortKey);
+      neg += (sv < 0.0);
+      pos += (sv > 0.0);
+      zero += (sv == 0.0);
+    }
+    k[e] = key;
+    id[e] = static_cast<uint16_t>(e);
+  }
+  or_lo = __reduce_or_sync(0xFFFFFFFFu, or_lo);
+  or_hi = __reduce_or_sync(0xFFFFFFFFu, or_hi);
+  and_lo = __reduce_and_sync(0xFFFFFFFFu, and_lo);
+  and_hi = __reduce_and_sync(0xFFFFFFFFu, and_hi);
+  mode = __reduce_max_sync(0xFFFFFFFFu, mode);
+  n_act = __reduce_add_sync(0xFFFFFFFFu, n_act);
+  neg = __reduce_add_sync(0xFFFFFFFFu, neg);
+  pos = __reduce_add_sync(0xFFFFFFFFu, pos);
+  zero = __reduce_add_sync(0xFFFFFFFFu, zero);
+  if (lane == 0) {
+    atomicOr(&st->or_lo, or_lo); atomicOr(&st->or_hi, or_hi);
+    atomicAnd(&st->and_lo, and_lo); atomicAnd(&st->and_hi, and_hi);
+    atomicMax(&st->mode, mode);
+    atomicAdd(&st->n_act, n_act); atomicAdd(&st->neg, neg);
+    atomicAdd(&st->pos, pos); atomicAdd(&st->zero, zero);
+  }
+}
+
+// Shared-memory carve-up for both sort kernels.
+struct SortSmem {
+  uint64_t *ka, *kb;
+  uint16_t *ia, *ib;
+  uint32_t* hist;
+  uint32_t* scan_tmp;
+  LoadStats* st;
+  unsigned long long* lim_acc;
+};
+__device__ __forceinline__ SortSmem carve_sort_smem(unsigned char* base, int npad) {
+  SortSmem m;
+  m.ka = reinterpret_cast<uint64_t*>(base);
+  m.kb = m.ka + npad;
+  m.hist = reinterpret_cast<uint32_t*>(m.kb + npad);
+  m.scan_tmp = m.hist + 256 * kSortWarps;
+  m.st = reinterpret_cast<LoadStats*>(m.scan_tmp + 64);
+  m.lim_acc = reinterpret_cast<unsigned long long*>(m.st + 1);
+  m.ia = reinterpret_cast<uint16_t*>(m.lim_acc + 2);
+  m.ib = m.ia + npad;
+  return m;
+}
+inline size_t sort_smem_bytes(int npad) {
+  return (size_t)npad * 16 + 256 * kSortWarps * 4 + 64 * 4 + sizeof(LoadStats) + 16 + (size_t)npad * 4;
+}
+
+__device__ __forceinline__ void init_stats(LoadStats* st, unsigned long long* lim_acc) {
+  if (threadIdx.x == 0) {
+    st->or_lo = st->or_hi = 0;
+    st->and_lo = st->and_hi = ~0u;
+    st->mode = kNarrow8;
+    st->n_act = st->neg = st->pos = st->zero = 0;
+    *lim_acc = 0ull;
+  }
+}
+
+// One CTA per frame (n_max <= kSortMax): load, sort, derive limits, emit sorted records.
+__global__ void __launch_bounds__(kSortThreads) pnms_prep_sort_frame(PrepArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int f = blockIdx.x;
+  const long long fbase = (long long)f * a.n_max;
+  const int cnt = frame_count(a.counts, f, a.n_max);
+  SortSmem m = carve_sort_smem(smem_raw, a.npad);
+  init_stats(m.st, m.lim_acc);
+  __syncthreads();
+  load_keys(a, fbase, 0, cnt, a.npad, m.ka, m.ia, m.st);
+  __syncthreads();
+  const uint64_t diff = ((((uint64_t)m.st->or_hi) << 32) | m.st->or_lo) ^
+                        ((((uint64_t)m.st->and_hi) << 32) | m.st->and_lo);
+  const int mode = m.st->mode;
+  const int n_act = m.st->n_act;
+  uint64_t* k = m.ka;
+  uint16_t* id = m.ia;
+  if (cnt > 1) block_radix_sort(&k, &id, m.kb, m.ib, m.hist, m.scan_tmp, a.npad / kSortThreads, diff);
+
+  uint8_t* rec_frame = a.rec + fbase * kRecBytes;
+  unsigned long long lsum = 0;
+  for (int p = threadIdx.x; p < cnt; p += kSortThreads) {
+    const uint64_t sk = k[p];
+    const int i = id[p];
+    int l = 0;
+    if (p < n_act) l = (a.tie_break == 1) ? p : lower_bound_u64(k, cnt, sk);
+    lsum += (unsigned long long)l;
+    const long long g = fbase + i;
+    a.perm[fbase + p] = i;
+    a.lim[fbase + p] = l;
+    write_record(rec_frame, p, mode, a.x[g], a.y[g], a.z[g], a.theta);
+  }
+  for (int w = threadIdx.x; w < a.W32; w += kSortThreads) a.supp[(long long)f * a.W32 + w] = 0u;
+  lsum = __reduce_add_sync(0xFFFFFFFFu, (unsigned)(lsum & 0xFFFFFFFFull)) +
+         ((unsigned long long)__reduce_add_sync(0xFFFFFFFFu, (unsigned)(lsum >> 32)) << 32);
+  if ((threadIdx.x & 31) == 0) atomicAdd(m.lim_acc, lsum);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    FrameMeta fm;
+    fm.n_active = n_act;
+    fm.mode = mode;
+    fm.cnt_neg = m.st->neg;
+    fm.cnt_pos = m.st->pos;
+    fm.cnt_zero = m.st->zero;
+    fm.pad_ = 0;
+    fm.lim_sum = *m.lim_acc;
+    a.meta[f] = fm;
+  }
+}
+
+// Chunk mode (n_max > kSortMax), grid = batch * nchunks: sort one kSortMax-slot chunk and
+// publish (sorted key, input index) plus the chunk's statistics (meta is zeroed by the host).
+__global__ void __launch_bounds__(kSortThreads) pnms_prep_sort_chunk(PrepArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int f = blockIdx.x / a.nchunks, c = blockIdx.x % a.nchunks;
+  const long long fbase = (long long)f * a.n_max;
+  const int cnt = frame_count(a.counts, f, a.n_max);
+  const int e0 = c * kSortMax;
+  // zero this chunk's share of the suppression words
+  for (int w = e0 / 32 + threadIdx.x; w < min(a.W32, (e0 + kSortMax) / 32); w += kSortThreads)
+    a.supp[(long long)f * a.W32 + w] = 0u;
+  const int len = min(kSortMax, cnt - e0);
+  if (len <= 0) return;
+  SortSmem m = carve_sort_smem(smem_raw, kSortMax);
+  init_stats(m.st, m.lim_acc);
+  __syncthreads();
+  load_keys(a, fbase, e0, len, kSortMax, m.ka, m.ia, m.st);
+  __syncthreads();
+  const uint64_t diff = ((((uint64_t)m.st->or_hi) << 32) | m.st->or_lo) ^
+                        ((((uint64_t)m.st->and_hi) << 32) | m.st->and_lo);
+  uint64_t* k = m.ka;
+  uint16_t* id = m.ia;
+  if (len > 1) block_radix_sort(&k, &id, m.kb, m.ib, m.hist, m.scan_tmp, kSortMax / kSortThreads, diff);
+  for (int p = threadIdx.x; p < len; p += kSortThreads) {
+    a.sk_scratch[fbase + e0 + p] = k[p];
+    a.idx_scratch[fbase + e0 + p] = e0 + id[p];
+  }
+  if (threadIdx.x == 0) {
+    FrameMeta* fm = a.meta + f;
+    atomicAdd(&fm->n_active, m.st->n_act);
+    atomicMax(&fm->mode, m.st->mode);
+    atomicAdd(&fm->cnt_neg, m.st->neg);
+    atomicAdd(&fm->cnt_pos, m.st->pos);
+    atomicAdd(&fm->cnt_zero, m.st->zero);
+  }
+}
+
+// Chunk mode, second pass: one thread per slot computes its global sorted position and its
+// column limit by binary search in every chunk, then emits perm / lim / record.
+__global__ void __launch_bounds__(256) pnms_merge_rank(PrepArgs a) {
+  const int blocks_per_frame = (a.n_max + 255) / 256;
+  const int f = blockIdx.x / blocks_per_frame;
+  const int e = (blockIdx.x % blocks_per_frame) * 256 + threadIdx.x;
+  const long long fbase = (long long)f * a.n_max;
+  const int cnt = frame_count(a.counts, f, a.n_max);
+  unsigned long long l = 0;
+  if (e < cnt) {
+    const int c = e / kSortMax;
+    const uint64_t* S = a.sk_scratch + fbase;
+    const uint64_t sk = S[e];
+    const int i = a.idx_scratch[fbase + e];
+    int rank = e - c * kSortMax;
+    int first = 0;
+    for (int cc = 0; cc < a.nchunks; ++cc) {
+      const int b = cc * kSortMax;
+      const int len = min(kSortMax, cnt - b);
+      if (len <= 0) break;
+      const int lb = lower_bound_u64(S + b, len, sk);
+      first += lb;
+      if (cc < c) rank += upper_bound_u64(S + b, len, sk);
+      else if (cc > c) rank += lb;
+    }
+    const FrameMeta fm = a.meta[f];
+    if (rank < fm.n_active) l = (a.tie_break == 1) ? rank : first;
+    a.perm[fbase + rank] = i;
+    a.lim[fbase + rank] = (int)l;
+    const long long g = fbase + i;
+    write_record(a.rec + fbase * kRecBytes, rank, fm.mode, a.x[g], a.y[g], a.z[g], a.theta);
+  }
+  unsigned lo = __reduce_add_sync(0xFFFFFFFFu, (unsigned)(l & 0xFFFFFFFFull));
+  unsigned hi = __reduce_add_sync(0xFFFFFFFFu, (unsigned)(l >> 32));
+  if ((threadIdx.x & 31) == 0 && (lo | hi)) atomicAdd(&a.meta[f].lim_sum, ((unsigned long long)hi << 32) + lo);
+}
+
+}  // namespace pnms

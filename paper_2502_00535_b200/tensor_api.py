@@ -1,0 +1,212 @@
+"""Tensor-level API over the C ABI: device-resident batched NMS.
+
+`batched_nms_keep` is the throughput entry point (one call = every frame of a batch, one
+stream, no host synchronisation); `nms_keep` is the single-frame convenience wrapper; and
+`NmsEngine` keeps a workspace and pinned staging buffers alive across calls, including the
+host-to-host path (`run_host`) that the end-to-end benchmark times.
+
+Box layout: three int32 planes x, y, z of shape [B, n_max] (square boxes, top-left corner
+plus side, inclusive +1 pixel convention of overlap.py:29-36 — never xyxy) and a float64
+score plane s [B, n_max].  PyTorch only provides device memory and streams here.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+
+_TIE = _lib.TIE_CODES
+
+
+def _check_theta(theta: float) -> float:
+    from .engine import ConfigError
+
+    theta = float(theta)
+    if not 0.0 <= theta <= 1.0:
+        raise ConfigError(f"theta must be in [0, 1], got {theta}")
+    return theta
+
+
+def _check_tie(tie_break: str) -> int:
+    from .engine import ConfigError
+
+    if tie_break not in _TIE:
+        raise ConfigError(f"tie_break must be one of {tuple(_TIE)}, got {tie_break!r}")
+    return _TIE[tie_break]
+
+
+def _require_cuda(t: torch.Tensor, name: str, dtype: torch.dtype, ndim: int) -> None:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if t.dim() != ndim or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous {ndim}-D tensor")
+
+
+class _WorkspaceCache:
+    """One growing device workspace per (device, stream)."""
+
+    def __init__(self):
+        self._bufs: dict[tuple[int, int], torch.Tensor] = {}
+
+    def get(self, device: torch.device, stream: int, nbytes: int) -> torch.Tensor:
+        key = (device.index if device.index is not None else torch.cuda.current_device(), stream)
+        buf = self._bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+            self._bufs[key] = buf
+        return buf
+
+
+_WS = _WorkspaceCache()
+
+
+def batched_nms_keep(x: torch.Tensor, y: torch.Tensor, z: torch.Tensor, s: torch.Tensor,
+                     counts: torch.Tensor | None = None, theta: float = 0.5,
+                     tie_break: str = "paper_faithful", d_max: int | None = None, *,
+                     keep_idx: torch.Tensor | None = None, keep_count: torch.Tensor | None = None,
+                     keep_mask: torch.Tensor | None = None, gate_pairs: torch.Tensor | None = None,
+                     workspace: torch.Tensor | None = None, want_idx: bool = True):
+    """NMS of every frame of a batch; returns (keep_idx [B, n_max] int32, keep_count [B] int32).
+
+    Frame f holds counts[f] valid detections in slots [0, counts[f]) of each plane; slots
+    [counts[f], d_max) are padding (0,0,0,0.0) exactly as in a reference DetectionVector of
+    capacity d_max (default n_max).  keep_idx[f, :keep_count[f]] are the ascending survivor
+    indices — identical to engine.run_nms on the same frame (engine.py:296-300).
+    Optional outputs: keep_mask (uint32 [B, ceil(n_max/32)] survivor bits) and gate_pairs
+    (int64 [B], the reference's WorkCounters.map_writes).
+    """
+    _require_cuda(x, "x", torch.int32, 2)
+    B, n_max = x.shape
+    for t, nm in ((y, "y"), (z, "z")):
+        _require_cuda(t, nm, torch.int32, 2)
+        if t.shape != x.shape:
+            raise ValueError(f"{nm} shape {tuple(t.shape)} != x shape {tuple(x.shape)}")
+    _require_cuda(s, "s", torch.float64, 2)
+    if s.shape != x.shape:
+        raise ValueError(f"s shape {tuple(s.shape)} != x shape {tuple(x.shape)}")
+    if counts is not None:
+        _require_cuda(counts, "counts", torch.int32, 1)
+        if counts.shape[0] != B:
+            raise ValueError("counts must have one entry per frame")
+    theta = _check_theta(theta)
+    tie = _check_tie(tie_break)
+    if d_max is None:
+        d_max = n_max
+    if d_max < 1 or d_max < n_max:
+        from .engine import ConfigError
+
+        raise ConfigError(f"d_max={d_max} must be positive and >= the frame stride {n_max}")
+    dev = x.device
+    W32 = (n_max + 31) // 32
+    if keep_idx is None and want_idx:
+        keep_idx = torch.empty((B, n_max), dtype=torch.int32, device=dev)
+    if keep_count is None:
+        keep_count = torch.empty((B,), dtype=torch.int32, device=dev)
+    if keep_mask is not None:
+        _require_cuda(keep_mask, "keep_mask", torch.int32, 2)
+        if tuple(keep_mask.shape) != (B, W32):
+            raise ValueError(f"keep_mask must be [{B}, {W32}] int32")
+    if gate_pairs is not None:
+        _require_cuda(gate_pairs, "gate_pairs", torch.int64, 1)
+    stream = torch.cuda.current_stream(dev)
+    need = _lib.workspace_bytes(B, n_max)
+    if workspace is None:
+        workspace = _WS.get(dev, stream.cuda_stream, need)
+    elif workspace.numel() < need:
+        raise ValueError(f"workspace needs {need} bytes")
+    lib = _lib.load()
+    p = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+    st = lib.pnms_run(p(x), p(y), p(z), p(s), p(counts), B, n_max, int(d_max), theta, tie,
+                      p(keep_idx), p(keep_count), p(keep_mask), p(gate_pairs), p(workspace),
+                      workspace.numel(), stream.cuda_stream)
+    _lib.check(st, "pnms_run")
+    return keep_idx, keep_count
+
+
+def nms_keep(boxes: torch.Tensor, scores: torch.Tensor, theta: float = 0.5,
+             tie_break: str = "paper_faithful", d_max: int | None = None) -> torch.Tensor:
+    """Single-frame NMS: boxes [N, 3] (x, y, z) integer CUDA tensor, scores [N] float64.
+
+    Returns the ascending int64 survivor indices (synchronises once to size the result)."""
+    if boxes.dim() != 2 or boxes.shape[1] != 3:
+        raise ValueError("boxes must be [N, 3] (x, y, side)")
+    n = boxes.shape[0]
+    if n == 0:
+        return torch.empty((0,), dtype=torch.int64, device=boxes.device)
+    b = boxes.to(torch.int32)
+    planes = b.t().contiguous()
+    sc = scores.to(torch.float64).reshape(1, n).contiguous()
+    idx, cnt = batched_nms_keep(planes[0:1], planes[1:2], planes[2:3], sc, None, theta, tie_break,
+                                d_max if d_max is not None else n)
+    k = int(cnt.item())
+    return idx[0, :k].to(torch.int64)
+
+
+class NmsEngine:
+    """Reusable batched engine bound to one device: workspace, outputs and pinned staging.
+
+    run_device(...)  device-resident planes -> (keep_idx, keep_count) on the device
+    run_host(...)    pinned host planes -> H2D -> NMS -> D2H of survivor masks + counts,
+                     pipelined over `chunks` slices of the batch on two streams so copies
+                     overlap the kernels (the end-to-end path bench.py times)
+    """
+
+    def __init__(self, batch: int, n_max: int, theta: float = 0.5, tie_break: str = "paper_faithful",
+                 d_max: int | None = None, device: torch.device | str | None = None, chunks: int = 1):
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.batch, self.n_max = int(batch), int(n_max)
+        self.theta, self.tie_break = _check_theta(theta), tie_break
+        _check_tie(tie_break)
+        self.d_max = int(d_max) if d_max is not None else self.n_max
+        self.chunks = max(1, min(int(chunks), self.batch))
+        self.W32 = (self.n_max + 31) // 32
+        dev = self.device
+        self.keep_idx = torch.empty((self.batch, self.n_max), dtype=torch.int32, device=dev)
+        self.keep_count = torch.empty((self.batch,), dtype=torch.int32, device=dev)
+        self.keep_mask = torch.empty((self.batch, self.W32), dtype=torch.int32, device=dev)
+        self.bounds = [(i * self.batch // self.chunks, (i + 1) * self.batch // self.chunks) for i in range(self.chunks)]
+        per = max(b - a for a, b in self.bounds)
+        self.ws = [torch.empty(_lib.workspace_bytes(per, self.n_max), dtype=torch.uint8, device=dev)
+                   for _ in range(min(2, self.chunks))]
+        self.ws_full = torch.empty(_lib.workspace_bytes(self.batch, self.n_max), dtype=torch.uint8, device=dev)
+        self.streams = [torch.cuda.Stream(device=dev) for _ in range(min(2, self.chunks))]
+        self._dev_in = None
+
+    def run_device(self, x, y, z, s, counts=None, want_idx: bool = True, want_mask: bool = False):
+        return batched_nms_keep(x, y, z, s, counts, self.theta, self.tie_break, self.d_max,
+                                keep_idx=self.keep_idx if want_idx else None, keep_count=self.keep_count,
+                                keep_mask=self.keep_mask if want_mask else None, workspace=self.ws_full,
+                                want_idx=want_idx)
+
+    def _device_inputs(self):
+        if self._dev_in is None:
+            dev, shp = self.device, (self.batch, self.n_max)
+            self._dev_in = (torch.empty(shp, dtype=torch.int32, device=dev), torch.empty(shp, dtype=torch.int32, device=dev),
+                            torch.empty(shp, dtype=torch.int32, device=dev), torch.empty(shp, dtype=torch.float64, device=dev),
+                            torch.empty((self.batch,), dtype=torch.int32, device=dev))
+        return self._dev_in
+
+    def run_host(self, hx, hy, hz, hs, hcounts, out_mask, out_count):
+        """Pinned host planes in, pinned host survivor masks [B, W32] int32 + counts [B] out."""
+        dx, dy, dz, ds, dc = self._device_inputs()
+        cur = torch.cuda.current_stream(self.device)
+        for k, (a, b) in enumerate(self.bounds):
+            st = self.streams[k % len(self.streams)]
+            st.wait_stream(cur)
+            with torch.cuda.stream(st):
+                for d, h in ((dx, hx), (dy, hy), (dz, hz), (ds, hs), (dc, hcounts)):
+                    d[a:b].copy_(h[a:b], non_blocking=True)
+                batched_nms_keep(dx[a:b], dy[a:b], dz[a:b], ds[a:b], dc[a:b], self.theta, self.tie_break,
+                                 self.d_max, keep_idx=None, keep_count=self.keep_count[a:b],
+                                 keep_mask=self.keep_mask[a:b], workspace=self.ws[k % len(self.ws)],
+                                 want_idx=False)
+                out_mask[a:b].copy_(self.keep_mask[a:b], non_blocking=True)
+                out_count[a:b].copy_(self.keep_count[a:b], non_blocking=True)
+        for st in self.streams:
+            cur.wait_stream(st)
+
+    def launches_per_call(self) -> int:
+        return 3 if self.n_max <= 4096 else 4

@@ -1,0 +1,283 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden vectors
+and the CPU oracles.  Integer/index work, so every comparison is exact."""
+
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import c_oracle  # noqa: E402
+from paper_2502_00535_b200 import (  # noqa: E402
+    DetectionVector, NmsConfig, batched_nms_keep, map_phase, nms_keep, reduce_phase, run_nms,
+)
+from paper_2502_00535_b200.synth import random_frames  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def _vec(c):
+    return DetectionVector.from_arrays(c.x, c.y, c.z, c.s, c.d_max, validate=False)
+
+
+def _k_for(d_max):
+    for k in (32, 16, 8, 4, 2, 1):
+        if d_max % k == 0:
+            return k
+
+
+def test_run_nms_matches_reference_cases(golden_cases):
+    for c in golden_cases:
+        cfg = NmsConfig(theta=c.theta, d_max=c.d_max, k=c.k, workers=3, tie_break=c.tie)
+        res, ctr = run_nms(_vec(c), cfg)
+        got = [(d.x, d.y, d.z, d.s) for d in res.survivors]
+        want = [(int(c.x[i]), int(c.y[i]), int(c.z[i]), float(c.s[i])) for i in c.keep]
+        assert got == want, (c.note, c.count, c.d_max, c.theta, c.tie)
+        assert res.suppressed_count == c.count - len(c.keep)
+        assert ctr.map_writes == c.writes, c.note
+        assert ctr.map_cells == c.d_max ** 2 and ctr.reduce_segments == c.d_max * c.k
+
+
+def test_batched_matches_reference_cases(golden_cases):
+    """Ragged batches of the reference's random frames in one launch per (tie, theta).
+    Scores are positive, so the survivors do not depend on the padding amount."""
+    for tie in ("paper_faithful", "by_index"):
+        for theta in (0.0, 0.1, 0.3, 0.5, 0.9, 1.0):
+            group = [c for c in golden_cases if c.note == "random" and c.tie == tie and c.theta == theta]
+            assert group
+            n_max = max(max(c.count for c in group), 1)
+            B = len(group)
+            X = np.zeros((B, n_max), np.int32); Y = X.copy(); Z = X.copy(); S = np.zeros((B, n_max))
+            cnt = np.zeros(B, np.int32)
+            for f, c in enumerate(group):
+                X[f, :c.count] = c.x; Y[f, :c.count] = c.y; Z[f, :c.count] = c.z; S[f, :c.count] = c.s
+                cnt[f] = c.count
+            t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)  # noqa: E731
+            ki, kc = batched_nms_keep(t(X), t(Y), t(Z), t(S), t(cnt), theta, tie, n_max)
+            ki, kc = ki.cpu().numpy(), kc.cpu().numpy()
+            for f, c in enumerate(group):
+                assert np.array_equal(ki[f, :kc[f]], c.keep), (c.note, c.count)
+
+
+def test_map_phase_bits_match_reference(golden_cases):
+    n = 0
+    for c in golden_cases:
+        if c.mat is None:
+            continue
+        cfg = NmsConfig(theta=c.theta, d_max=c.d_max, k=c.k, tie_break=c.tie)
+        m, ctr = map_phase(_vec(c), cfg)
+        assert np.array_equal(m.bits, c.mat), c.note
+        assert ctr.map_writes == c.writes
+        v, rc = reduce_phase(m, cfg)
+        assert np.array_equal(np.nonzero(v.to_bool_array()[: c.count])[0], c.keep)
+        assert rc.reduce_segments == c.d_max * c.k
+        n += 1
+    assert n > 300
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4f0", "C4f3", "C5f0", "C5f1", "C5f2", "C5f3"])
+def test_config_frames_match_reference(golden_configs, name):
+    g = golden_configs[name]
+    n = len(g["x"])
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a).reshape(1, n)).to(DEV)  # noqa: E731
+    gp = torch.empty(1, dtype=torch.int64, device=DEV)
+    ki, kc = batched_nms_keep(t(g["x"]), t(g["y"]), t(g["z"]), t(g["s"]), None, 0.5, "paper_faithful", n,
+                              gate_pairs=gp)
+    k = int(kc.item())
+    assert np.array_equal(ki[0, :k].cpu().numpy(), g["keep"])
+    assert int(gp.item()) == int(g["writes"][0])
+
+
+@pytest.mark.parametrize("shape", [(1, 128), (1, 256), (2, 256), (4, 512), (1, 512)])
+def test_launch_shape_invariance(golden_configs, shape):
+    """Results are independent of the map decomposition (R rows/lane, chunk width)."""
+    g = golden_configs["C2"]
+    n = len(g["x"])
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a).reshape(1, n)).to(DEV)  # noqa: E731
+    os.environ["PNMS_MAP_R"], os.environ["PNMS_MAP_CHUNK"] = str(shape[0]), str(shape[1])
+    try:
+        ki, kc = batched_nms_keep(t(g["x"]), t(g["y"]), t(g["z"]), t(g["s"]), None, 0.5)
+    finally:
+        del os.environ["PNMS_MAP_R"], os.environ["PNMS_MAP_CHUNK"]
+    assert np.array_equal(ki[0, : int(kc.item())].cpu().numpy(), g["keep"])
+
+
+def _run_batch(x, y, z, s, counts, theta, tie, d_max=None):
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)  # noqa: E731
+    ki, kc = batched_nms_keep(t(x), t(y), t(z), t(s), t(counts), theta, tie, d_max)
+    ki, kc = ki.cpu().numpy(), kc.cpu().numpy()
+    return [ki[f, : kc[f]] for f in range(x.shape[0])]
+
+
+def test_c4_full_batch_vs_oracle():
+    x, y, z, s = random_frames(256, 1024, seed=4)
+    counts = np.full(256, 1024, np.int32)
+    got = _run_batch(x, y, z, s, counts, 0.5, "paper_faithful")
+    want = c_oracle.run_batch(x, y, z, s, counts, 1024, 0.5)
+    for f in range(256):
+        assert np.array_equal(got[f], want[f]), f
+
+
+def test_c5_slice_vs_oracle():
+    x, y, z, s = random_frames(192, 2048, seed=5)
+    counts = np.full(192, 2048, np.int32)
+    got = _run_batch(x, y, z, s, counts, 0.5, "paper_faithful")
+    want = c_oracle.run_batch(x, y, z, s, counts, 2048, 0.5)
+    for f in range(192):
+        assert np.array_equal(got[f], want[f]), f
+
+
+@pytest.mark.parametrize("tie", ["paper_faithful", "by_index"])
+@pytest.mark.parametrize("theta", [0.0, 0.3, 0.7, 1.0])
+def test_ragged_duplicates_vs_oracle(tie, theta):
+    rng = np.random.default_rng(int(theta * 10) + (tie == "by_index"))
+    x, y, z, s = random_frames(24, 700, seed=9, frame_w=400, frame_h=300, z_range=(4, 60), duplicate_fraction=0.2)
+    s[:, ::5] = np.round(s[:, ::5] * 4) / 4 + 0.01  # exact score ties
+    counts = rng.integers(0, 701, size=24).astype(np.int32)
+    counts[:3] = (0, 1, 700)
+    d_max = 760
+    got = _run_batch(x, y, z, s, counts, theta, tie, d_max)
+    for f in range(24):
+        want = c_oracle.run_frame(x[f], y[f], z[f], s[f], int(counts[f]), d_max, theta, tie)
+        assert np.array_equal(got[f], want), (f, counts[f])
+
+
+@pytest.mark.parametrize("n", [4097, 6000, 9000, 16384])
+def test_chunked_sort_frames_vs_oracle(n):
+    """Frames above one CTA's sort capacity (chunk sort + merge-rank path) with ties."""
+    x, y, z, s = random_frames(2, n, seed=n, frame_w=3840, frame_h=2160, z_range=(8, 64), duplicate_fraction=0.1)
+    s[:, ::7] = 0.5
+    for tie in ("paper_faithful", "by_index"):
+        got = _run_batch(x, y, z, s, np.array([n, n - 3], np.int32), 0.5, tie, n)
+        for f, c in enumerate((n, n - 3)):
+            want = c_oracle.run_frame(x[f], y[f], z[f], s[f], c, n, 0.5, tie)
+            assert np.array_equal(got[f], want), (n, f, tie)
+
+
+def test_nan_and_signed_scores_vs_oracle():
+    x, y, z, s = random_frames(6, 300, seed=3, frame_w=200, frame_h=200, z_range=(4, 40))
+    s[0, ::3] = np.nan
+    s[1, ::4] = -np.inf
+    s[2, :] = -s[2, :]
+    s[3, ::2] = -0.0
+    s[3, 1::2] = 0.0
+    s[4, ::5] = np.inf
+    counts = np.array([300, 300, 300, 300, 250, 300], np.int32)
+    for tie in ("paper_faithful", "by_index"):
+        got = _run_batch(x, y, z, s, counts, 0.4, tie, 320)
+        for f in range(6):
+            want = c_oracle.run_frame(x[f], y[f], z[f], s[f], int(counts[f]), 320, 0.4, tie)
+            assert np.array_equal(got[f], want), (f, tie)
+
+
+def test_wide_and_narrow16_paths_vs_oracle():
+    rng = np.random.default_rng(11)
+    B, n = 4, 500
+    x = rng.integers(0, 2**24 - 1, size=(B, n)).astype(np.int32)
+    y = rng.integers(0, 2**24 - 1, size=(B, n)).astype(np.int32)
+    z = rng.integers(1, 2**22, size=(B, n)).astype(np.int32)
+    x[1] = rng.integers(0, 3000, size=n); y[1] = rng.integers(0, 3000, size=n); z[1] = rng.integers(200, 900, size=n)
+    x[2] = rng.integers(-2**31, 2**31 - 1, size=n); z[2] = rng.integers(-2**31, 2**31 - 1, size=n)  # int32 wrap
+    s = rng.uniform(0.05, 1, size=(B, n))
+    counts = np.full(B, n, np.int32)
+    for theta in (0.0, 0.5, 1.0):
+        got = _run_batch(x, y, z, s, counts, theta, "paper_faithful")
+        for f in range(B):
+            want = c_oracle.run_frame(x[f], y[f], z[f], s[f], n, n, theta)
+            assert np.array_equal(got[f], want), (f, theta)
+
+
+def test_properties_full_size():
+    """Size-independent properties at the C5 frame size."""
+    x, y, z, s = random_frames(64, 2048, seed=21)
+    counts = np.full(64, 2048, np.int32)
+    base = _run_batch(x, y, z, s, counts, 0.5, "paper_faithful")
+    # idempotence: NMS of the survivors keeps all of them
+    for f in range(0, 64, 8):
+        k = base[f]
+        again = _run_batch(x[f:f + 1, k], y[f:f + 1, k], z[f:f + 1, k], s[f:f + 1, k],
+                           np.array([len(k)], np.int32), 0.5, "paper_faithful")[0]
+        assert np.array_equal(again, np.arange(len(k)))
+    # permutation invariance (distinct scores)
+    perm = np.random.default_rng(1).permutation(2048)
+    inv = np.argsort(perm)
+    px = _run_batch(x[:, perm], y[:, perm], z[:, perm], s[:, perm], counts, 0.5, "paper_faithful")
+    for f in range(64):
+        assert np.array_equal(np.sort(perm[px[f]]), base[f])
+    del inv
+    # padding invariance: larger d_max changes nothing (positive scores)
+    padded = _run_batch(x, y, z, s, counts, 0.5, "paper_faithful", d_max=4096)
+    for f in range(64):
+        assert np.array_equal(padded[f], base[f])
+    # monotonicity in theta: a higher threshold suppresses no more boxes
+    hi = _run_batch(x, y, z, s, counts, 0.8, "paper_faithful")
+    for f in range(64):
+        assert set(base[f]).issubset(set(hi[f]))
+
+
+def test_keep_mask_consistent():
+    x, y, z, s = random_frames(8, 1000, seed=2)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)  # noqa: E731
+    mask = torch.empty((8, 32), dtype=torch.int32, device=DEV)
+    ki, kc = batched_nms_keep(t(x), t(y), t(z), t(s), t(np.full(8, 900, np.int32)), 0.5, keep_mask=mask)
+    m = mask.cpu().numpy().view(np.uint32)
+    bits = np.unpackbits(m.view(np.uint8), axis=1, bitorder="little")[:, :1000]
+    for f in range(8):
+        assert np.array_equal(np.nonzero(bits[f])[0], ki[f, : kc[f]].cpu().numpy())
+
+
+def test_nms_keep_single_frame(golden_configs):
+    g = golden_configs["C1"]
+    boxes = torch.from_numpy(np.stack([g["x"], g["y"], g["z"]], 1)).to(DEV)
+    keep = nms_keep(boxes, torch.from_numpy(g["s"]).to(DEV), 0.5)
+    assert keep.dtype == torch.int64 and np.array_equal(keep.cpu().numpy(), g["keep"])
+
+
+def test_k_and_workers_invariance(golden_configs):
+    g = golden_configs["C1"]
+    vec = DetectionVector.from_arrays(g["x"], g["y"], g["z"], g["s"], 1024)
+    outs = set()
+    for k in (1, 2, 32, 64, 1024):
+        for workers in (1, 4, 8):
+            res, ctr = run_nms(vec, NmsConfig(theta=0.5, d_max=1024, k=k, workers=workers))
+            outs.add(tuple(d.s for d in res.survivors))
+            assert ctr.reduce_segments == 1024 * k and ctr.map_cells == 1024 ** 2
+    assert len(outs) == 1
+
+
+def test_reference_vector_duck_typing(golden_cases):
+    """A foreign DetectionVector-like object with non-zero padding garbage is honoured."""
+    c = next(c for c in golden_cases if c.note == "random" and c.count > 50)
+
+    class Foreign:
+        def __init__(self, d_max):
+            self.count = c.count
+            pad = d_max - c.count
+            self.xs = np.concatenate([c.x, np.zeros(pad, np.int64)])
+            self.ys = np.concatenate([c.y, np.zeros(pad, np.int64)])
+            self.zs = np.concatenate([c.z, np.zeros(pad, np.int64)])
+            self.ss = np.concatenate([c.s, np.zeros(pad)])
+            self.d_max = d_max
+
+        def __len__(self):
+            return self.d_max
+
+        def slot(self, i):
+            return (int(self.xs[i]), int(self.ys[i]), int(self.zs[i]), float(self.ss[i]))
+
+    f = Foreign(c.count + 5)
+    res, _ = run_nms(f, NmsConfig(theta=c.theta, d_max=c.count + 5, k=1, tie_break=c.tie))
+    px, py, pz, ps = f.xs.copy(), f.ys.copy(), f.zs.copy(), f.ss.copy()
+    want = c_oracle.run_frame(px[: c.count], py[: c.count], pz[: c.count], ps[: c.count], c.count, c.count + 5,
+                              c.theta, c.tie)
+    assert [r[0] for r in res.survivors] == [int(px[i]) for i in want]
+    # garbage in the padding slots: all d_max slots take part (engine.py:187-247)
+    f.ss = f.ss.copy(); f.ss[c.count:] = 2.0
+    f.zs = f.zs.copy(); f.zs[c.count:] = 5
+    res2, _ = run_nms(f, NmsConfig(theta=c.theta, d_max=c.count + 5, k=1, tie_break=c.tie))
+    want2 = c_oracle.run_frame(f.xs.astype(np.int32), f.ys.astype(np.int32), f.zs.astype(np.int32), f.ss,
+                               c.count + 5, c.count + 5, c.theta, c.tie)
+    want2 = want2[want2 < c.count]
+    assert [r[0] for r in res2.survivors] == [int(f.xs[i]) for i in want2]
