@@ -222,7 +222,6 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     ipf += (cols + ms.chunk - 1) / ms.chunk;
   }
   ma.items_per_frame = ipf;
-  ma.k65536 = 65536u;
   const long long grid = (long long)batch * ipf;
   if (grid > 0x7FFFFFFFLL) return PNMS_ETOO_LARGE;
   const size_t map_smem = (size_t)ms.chunk * kRecBytes;

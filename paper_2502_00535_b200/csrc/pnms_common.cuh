@@ -22,7 +22,7 @@ constexpr int kMapWarps = 4;          // warps per map CTA
 
 // Per-frame arithmetic path, decided on the device from the frame's own values.
 enum FrameMode : int {
-  kNarrow8 = 0,   // 0<=x,y; 0<=z<=254; x+z+1, y+z+1 <= 32767  -> s16x2 geometry, 2-IMAD product
+  kNarrow7 = 0,   // 0<=x,y; 0<=z<=126; x+z+1, y+z+1 <= 32767  -> s16x2 geometry, 1-IMAD product
   kNarrow16 = 1,  // as above but z up to 32766                  -> s16x2 geometry, split product
   kWide = 2       // anything representable in int32            -> exact int32-wrap + fp64 emulation
 };
@@ -42,8 +42,9 @@ static_assert(sizeof(FrameMeta) == 32, "FrameMeta layout");
 // (lo = x axis, hi = y axis).
 //   a   = (x+z+1, y+z+1)         inclusive far edge + 1
 //   nb  = (-x, -y)               negated near edge
-//   zz  = (z+1, z+1)             side + 1 (also the low word of the {zz, negT} IMAD addend)
-//   negT = -T  with T = ceil(fl64(theta*(z+1)^2)), T = 0 for z == 0 (engine.py:232)
+//   zz  = (z+1, z+1)             side + 1
+//   negT = -T * 2^17 (narrow7) or -T (narrow16), T = ceil(fl64(theta*(z+1)^2)) and T = 0
+//          for z == 0 (engine.py:232)
 struct __align__(16) RecNarrow {
   uint32_t a, nb, zz;
   int32_t negT;
@@ -83,10 +84,10 @@ __device__ __forceinline__ int frame_mode_of(int32_t x, int32_t y, int32_t z) {
   if (x < 0 || y < 0 || z < 0) return kWide;
   long long xe1 = (long long)x + z + 1, ye1 = (long long)y + z + 1;
   if (xe1 > 32767 || ye1 > 32767) return kWide;
-  return z <= 254 ? kNarrow8 : kNarrow16;
+  return z <= 126 ? kNarrow7 : kNarrow16;
 }
 
-__device__ __forceinline__ RecNarrow make_rec_narrow(int32_t x, int32_t y, int32_t z, double theta) {
+__device__ __forceinline__ RecNarrow make_rec_narrow(int32_t x, int32_t y, int32_t z, double theta, int mode) {
   RecNarrow r;
   uint32_t xe1 = static_cast<uint32_t>(x + z + 1), ye1 = static_cast<uint32_t>(y + z + 1);
   r.a = (xe1 & 0xFFFFu) | (ye1 << 16);
@@ -94,7 +95,7 @@ __device__ __forceinline__ RecNarrow make_rec_narrow(int32_t x, int32_t y, int32
   r.zz = static_cast<uint32_t>(z + 1) * 0x10001u;
   uint32_t T = 0;
   if (z != 0) T = static_cast<uint32_t>(ceil(ref_threshold(theta, z)));
-  r.negT = -static_cast<int32_t>(T);
+  r.negT = (mode == kNarrow7) ? -static_cast<int32_t>(T << 17) : -static_cast<int32_t>(T);
   return r;
 }
 

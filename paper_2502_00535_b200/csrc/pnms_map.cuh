@@ -9,18 +9,22 @@
 //
 // Work decomposition: a work item is (frame, row block of kMapWarps*32*R sorted rows, column
 // chunk of `chunk` columns).  The CTA stages its column chunk into shared memory with one
-// bulk async copy (cp.async.bulk, TMA engine) and each warp scans it for 32*R rows (R rows
-// per lane, the column record broadcast from shared memory).  Columns are visited in
-// descending position (nearest scores first) so suppressed rows end early; a warp stops as
-// soon as all its rows are decided.  Items are ordered heaviest-first within a frame.
+// bulk async copy (cp.async.bulk, TMA engine) and each warp scans it for 32*R rows: lane l
+// owns rows p0 + 32*g + l for the R row groups g.  Columns are visited in descending position
+// (nearest scores first).  Because lim[] is monotone in p, the column range splits into
+// per-group segments: in [lim_lo[g], lim_hi[g]) only group g needs a per-row mask, groups
+// above g are fully active and groups below are idle — no work is spent on masked-off pairs
+// beyond one 32-column band per group.  A warp stops once every row is decided.
 //
-// Narrow8 inner step (per row, per column) — 3 ALU-pipe + 2 FMA-pipe instructions:
-//   t1 = VIADDMNMX.S16x2      min(a_i + nb_j, zz_i)          = min(xe1_i - x_j, z_i+1)
-//   t2 = VIADDMNMX.S16x2.RELU max(min(a_j + nb_i, t1), 0)    = .. min(xe1_j - x_i)
-//   v  = VIMNMX.S16x2.RELU    min(t2, zz_j)                  -> (w, h) packed, exact
-//   s  = IMAD                 v * 65536                      = w << 16
-//   d  = IMAD.HI.U32          hi32(v*s + {zz_j, negT_j})     = w*h - T_j   (w <= 255)
-//   acc &= d   (LOP3, 3-input: one per two columns)          sign clear <=> suppressed
+// Narrow7 inner step (per row, per column; sides <= 126, coordinates < 32768):
+//   t1 = VIADDMNMX.S16x2       min(a_i + nb_j, zz_i)          = min(xe1_i - x_j, z_i+1)
+//   t2 = VIADDMNMX.S16x2.RELU  max(min(a_j + nb_i, t1), 0)    .. min(xe1_j - x_i)
+//   v  = VIMNMX.S16x2.RELU     min(t2, zz_j)                  -> (w, h) packed, exact
+//   d  = IMAD                  v*v - T_j*2^17                 = w^2 + (w*h - T_j)*2^17
+//   acc &= d   (LOP3, 3-input: one per two columns)           sign clear <=> suppressed
+// v*v mod 2^32 = w^2 + w*h*2^17 because h^2*2^32 vanishes; with w, h <= 127 nothing
+// overflows and w^2 < 2^17, so sign(d) = sign(w*h - T_j) with w*h == T_j giving d >= 0.
+// That is 3 ALU-pipe SIMD ops + 1 full-rate FMA-pipe IMAD + 1/2 LOP3 per pair.
 #pragma once
 #include "pnms_common.cuh"
 
@@ -36,7 +40,6 @@ struct MapArgs {
   int chunk;            // columns per work item
   int n_rb;             // row blocks per frame
   int items_per_frame;
-  uint32_t k65536;      // 65536, passed at run time so the multiply stays on the FMA pipe
 };
 
 // number of column chunks of row block rb: its rows' limits are < (rb+1)*RB
@@ -46,81 +49,105 @@ __device__ __forceinline__ int chunks_of(int rb, int RB, int chunk, int n_max) {
 }
 
 template <int R>
-struct RowState {
+struct NarrowRows {
   uint32_t a[R], nb[R], zz[R];
-  int acc[R];       // narrow: AND of (w*h - T); sign bit clear once a suppressor was seen
+  int acc[R];   // AND of d over the visited columns; >= 0 once decided (suppressed)
   int lim[R];
-  bool active[R];
-  bool pre[R];      // already suppressed by another work item
 };
 
 template <int R>
-__device__ __forceinline__ bool rows_done_narrow(const RowState<R>& st) {
+__device__ __forceinline__ bool all_decided(const NarrowRows<R>& st) {
   bool done = true;
 #pragma unroll
-  for (int r = 0; r < R; ++r) done &= (!st.active[r]) | st.pre[r] | (st.acc[r] >= 0);
-  return done;
+  for (int r = 0; r < R; ++r) done &= st.acc[r] >= 0;
+  return __all_sync(0xFFFFFFFFu, done);
 }
 
-// --- narrow (s16x2) column scans -------------------------------------------------------
-template <int R, bool kNarrow8>
-__device__ __forceinline__ void pair_narrow(RowState<R>& st, const uint4 c, uint32_t k65536) {
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    uint32_t t1 = __viaddmin_s16x2(st.a[r], c.y, st.zz[r]);
-    uint32_t t2 = __viaddmin_s16x2_relu(c.x, st.nb[r], t1);
-    uint32_t v = __vimin_s16x2_relu(t2, c.z);
-    int d;
-    if (kNarrow8) {
-      uint32_t s = v * k65536;
-      const uint64_t addend = ((uint64_t)c.w << 32) | c.z;
-      d = (int)(uint32_t)(((uint64_t)v * s + addend) >> 32);
-    } else {
-      d = (int)((v & 0xFFFFu) * (v >> 16)) + (int)c.w;
-    }
-    st.acc[r] &= d;
-  }
+template <int MODE>
+__device__ __forceinline__ int pair_d(uint32_t a_i, uint32_t nb_i, uint32_t zz_i, const uint4& c) {
+  const uint32_t t1 = __viaddmin_s16x2(a_i, c.y, zz_i);
+  const uint32_t t2 = __viaddmin_s16x2_relu(c.x, nb_i, t1);
+  const uint32_t v = __vimin_s16x2_relu(t2, c.z);
+  if (MODE == kNarrow7) return (int)(v * v) + (int)c.w;
+  return (int)((v & 0xFFFFu) * (v >> 16)) + (int)c.w;
 }
 
-template <int R, bool kNarrow8>
-__device__ __forceinline__ void pair_narrow_masked(RowState<R>& st, const uint4 c, int q, uint32_t k65536) {
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    uint32_t t1 = __viaddmin_s16x2(st.a[r], c.y, st.zz[r]);
-    uint32_t t2 = __viaddmin_s16x2_relu(c.x, st.nb[r], t1);
-    uint32_t v = __vimin_s16x2_relu(t2, c.z);
-    int d;
-    if (kNarrow8) {
-      uint32_t s = v * k65536;
-      const uint64_t addend = ((uint64_t)c.w << 32) | c.z;
-      d = (int)(uint32_t)(((uint64_t)v * s + addend) >> 32);
-    } else {
-      d = (int)((v & 0xFFFFu) * (v >> 16)) + (int)c.w;
-    }
-    st.acc[r] &= (q < st.lim[r]) ? d : -1;
-  }
-}
-
-template <int R, bool kNarrow8>
-__device__ __forceinline__ void scan_narrow(RowState<R>& st, const uint4* scol, int c0, int m_lo, int m_hi,
-                                            int u_hi, uint32_t k65536) {
-  // masked tail: columns [m_lo, m_hi) where some rows of the warp are past their limit
-  for (int q = m_hi - 1; q >= m_lo; --q) pair_narrow_masked<R, kNarrow8>(st, scol[q - c0], q, k65536);
-  if (__all_sync(0xFFFFFFFFu, rows_done_narrow(st))) return;
-  // unmasked body: columns [c0, u_hi), descending, decided-check every 32 columns
-  for (int qb = u_hi; qb > c0; qb -= 32) {
-    const int qlo = max(c0, qb - 32);
-    int q = qb - 1;
-    for (; q - 7 >= qlo; q -= 8) {
+// Columns [q_lo, q_hi), descending.  Row groups [G, R) take part; with MASK the rows of group
+// G only count columns below their own limit.  Returns true once every row is decided.
+template <int R, int MODE, int G, bool MASK>
+__device__ __forceinline__ bool scan_segment(NarrowRows<R>& st, const uint4* scol, int c0, int q_lo, int q_hi) {
+  int q = q_hi - 1;
+  while (q >= q_lo) {
+    const int stop = max(q_lo, q - 63);
+    for (; q - 7 >= stop; q -= 8) {
       uint4 cc[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) cc[u] = scol[q - u - c0];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) pair_narrow<R, kNarrow8>(st, cc[u], k65536);
+      for (int u = 0; u < 8; ++u) {
+#pragma unroll
+        for (int r = G; r < R; ++r) {
+          const int d = pair_d<MODE>(st.a[r], st.nb[r], st.zz[r], cc[u]);
+          if (MASK && r == G) st.acc[r] &= (q - u < st.lim[r]) ? d : -1;
+          else st.acc[r] &= d;
+        }
+      }
     }
-    for (; q >= qlo; --q) pair_narrow<R, kNarrow8>(st, scol[q - c0], k65536);
-    if (__all_sync(0xFFFFFFFFu, rows_done_narrow(st))) return;
+    for (; q >= stop; --q) {
+      const uint4 c = scol[q - c0];
+#pragma unroll
+      for (int r = G; r < R; ++r) {
+        const int d = pair_d<MODE>(st.a[r], st.nb[r], st.zz[r], c);
+        if (MASK && r == G) st.acc[r] &= (q < st.lim[r]) ? d : -1;
+        else st.acc[r] &= d;
+      }
+    }
+    if (all_decided(st)) return true;
   }
+  return false;
+}
+
+// Walk the per-group segments from the highest row group down (see header comment).
+template <int R, int MODE, int G>
+__device__ __forceinline__ bool scan_groups(NarrowRows<R>& st, const uint4* scol, int c0, int c1,
+                                            const int (&lim_lo)[R], const int (&lim_hi)[R]) {
+  if (scan_segment<R, MODE, G, true>(st, scol, c0, max(c0, lim_lo[G]), min(c1, lim_hi[G]))) return true;
+  const int below = (G > 0) ? lim_hi[G > 0 ? G - 1 : 0] : c0;
+  if (scan_segment<R, MODE, G, false>(st, scol, c0, max(c0, below), min(c1, lim_lo[G]))) return true;
+  if constexpr (G > 0) return scan_groups<R, MODE, G - 1>(st, scol, c0, c1, lim_lo, lim_hi);
+  return false;
+}
+
+template <int R, int MODE>
+__device__ __forceinline__ void warp_scan_narrow(const RecNarrow* rf, const uint4* scol, const int32_t* lim_frame,
+                                                 int c0, int c1, int pw, int p_end, const bool (&pre)[R],
+                                                 bool (&sup)[R]) {
+  const int lane = threadIdx.x & 31;
+  NarrowRows<R> st;
+  int lim_lo[R], lim_hi[R];
+  int last_hi = 0;
+#pragma unroll
+  for (int g = 0; g < R; ++g) {
+    const int p = pw + g * 32 + lane;
+    const bool active = p < p_end;
+    const RecNarrow rr = active ? rf[p] : RecNarrow{0u, 0u, 0u, 0};
+    st.a[g] = rr.a;
+    st.nb[g] = rr.nb;
+    st.zz[g] = rr.zz;
+    st.lim[g] = active ? lim_frame[p] : 0;
+    st.acc[g] = (!active || pre[g]) ? 0 : -1;
+    const int g0 = pw + g * 32;
+    if (g0 < p_end) {
+      lim_lo[g] = lim_frame[g0];
+      lim_hi[g] = lim_frame[min(g0 + 31, p_end - 1)];
+      last_hi = lim_hi[g];
+    } else {
+      lim_lo[g] = lim_hi[g] = last_hi;  // idle group: empty segments
+    }
+  }
+  scan_groups<R, MODE, R - 1>(st, scol, c0, c1, lim_lo, lim_hi);
+#pragma unroll
+  for (int g = 0; g < R; ++g) sup[g] = (pw + g * 32 + lane < p_end) && !pre[g] && st.acc[g] >= 0;
 }
 
 // --- wide (exact int32-wrap / float64 emulation) -----------------------------------------
@@ -134,9 +161,9 @@ __device__ __forceinline__ bool suppress_wide(const RecWide& ri, const RecWide& 
 }
 
 template <int R>
-__device__ __noinline__ void warp_scan_wide(const MapArgs& a, const RecWide* scol, const RecWide* rec_frame, int c0,
-                                            int c1, int pw, int p_end, const int32_t* lim_frame,
-                                            bool (&hit)[R], const bool (&pre)[R]) {
+__device__ __noinline__ void warp_scan_wide(const RecWide* scol, const RecWide* rec_frame, int c0, int c1, int pw,
+                                            int p_end, const int32_t* lim_frame, bool (&hit)[R],
+                                            const bool (&pre)[R]) {
   const int lane = threadIdx.x & 31;
   RecWide ri[R];
   int lim[R];
@@ -204,7 +231,6 @@ __global__ void __launch_bounds__(kMapWarps * 32) pnms_map_kernel(MapArgs a) {
   mbar_wait(&bar, 0);
   if (pw >= p_end) return;
   const int p_last = min(pw + 32 * R, p_end) - 1;
-  const int lim_lo = lim_frame[pw], lim_hi = lim_frame[p_last];
   uint32_t* supp_frame = a.supp + (long long)f * a.W32;
 
   bool pre[R];
@@ -221,35 +247,15 @@ __global__ void __launch_bounds__(kMapWarps * 32) pnms_map_kernel(MapArgs a) {
 
   bool sup[R];
   if (mode == kWide) {
-    bool hit[R];
-    warp_scan_wide<R>(a, reinterpret_cast<const RecWide*>(smem_raw), reinterpret_cast<const RecWide*>(rec_frame),
-                      c0, min(c1, lim_hi), pw, p_end, lim_frame, hit, pre);
-#pragma unroll
-    for (int r = 0; r < R; ++r) sup[r] = hit[r];
+    warp_scan_wide<R>(reinterpret_cast<const RecWide*>(smem_raw), reinterpret_cast<const RecWide*>(rec_frame), c0,
+                      min(c1, lim_frame[p_last]), pw, p_end, lim_frame, sup, pre);
   } else {
-    RowState<R> st;
     const RecNarrow* rf = reinterpret_cast<const RecNarrow*>(rec_frame);
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int p = pw + r * 32 + lane;
-      st.active[r] = p < p_end;
-      st.pre[r] = pre[r];
-      RecNarrow rr = st.active[r] ? rf[p] : RecNarrow{0u, 0u, 0u, 0};
-      st.a[r] = rr.a;
-      st.nb[r] = rr.nb;
-      st.zz[r] = rr.zz;
-      st.lim[r] = st.active[r] ? lim_frame[p] : 0;
-      st.acc[r] = -1;
-    }
     const uint4* scol = reinterpret_cast<const uint4*>(smem_raw);
-    const int m_lo = max(c0, lim_lo), m_hi = min(c1, lim_hi);
-    const int u_hi = min(c1, lim_lo);
-    if (mode == kNarrow8)
-      scan_narrow<R, true>(st, scol, c0, m_lo, m_hi, u_hi, a.k65536);
+    if (mode == kNarrow7)
+      warp_scan_narrow<R, kNarrow7>(rf, scol, lim_frame, c0, c1, pw, p_end, pre, sup);
     else
-      scan_narrow<R, false>(st, scol, c0, m_lo, m_hi, u_hi, a.k65536);
-#pragma unroll
-    for (int r = 0; r < R; ++r) sup[r] = st.active[r] && st.acc[r] >= 0;
+      warp_scan_narrow<R, kNarrow16>(rf, scol, lim_frame, c0, c1, pw, p_end, pre, sup);
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {

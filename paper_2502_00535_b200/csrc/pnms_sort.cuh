@@ -130,11 +130,11 @@ __device__ __forceinline__ void write_record(uint8_t* rec_frame, int pos, int mo
   if (mode == kWide) {
     reinterpret_cast<RecWide*>(rec_frame)[pos] = make_rec_wide(x, y, z, theta);
   } else {
-    reinterpret_cast<RecNarrow*>(rec_frame)[pos] = make_rec_narrow(x, y, z, theta);
+    reinterpret_cast<RecNarrow*>(rec_frame)[pos] = make_rec_narrow(x, y, z, theta, mode);
   }
 }
 
-struct LoadStats {
+struct __align__(16) LoadStats {
   uint32_t or_lo, or_hi, and_lo, and_hi;
   int mode, n_act, neg, pos, zero;
 };
@@ -146,7 +146,7 @@ __device__ void load_keys(const PrepArgs& a, long long fbase, int e0, int len, i
                           uint16_t* id, LoadStats* st) {
   const int lane = threadIdx.x & 31;
   uint32_t or_lo = 0, or_hi = 0, and_lo = ~0u, and_hi = ~0u;
-  int mode = kNarrow8, n_act = 0, neg = 0, pos = 0, zero = 0;
+  int mode = kNarrow7, n_act = 0, neg = 0, pos = 0, zero = 0;
   for (int e = threadIdx.x; e < npad; e += kSortThreads) {
     uint64_t key = kNanSortKey;
     if (e < len) {
@@ -199,12 +199,13 @@ __device__ __forceinline__ SortSmem carve_sort_smem(unsigned char* base, int npa
   m.hist = reinterpret_cast<uint32_t*>(m.kb + npad);
   m.scan_tmp = m.hist + 256 * kSortWarps;
   m.st = reinterpret_cast<LoadStats*>(m.scan_tmp + 64);
-  m.lim_acc = reinterpret_cast<unsigned long long*>(m.st + 1);
+  m.lim_acc = reinterpret_cast<unsigned long long*>(m.st + 1);  // LoadStats is 16-byte aligned
   m.ia = reinterpret_cast<uint16_t*>(m.lim_acc + 2);
   m.ib = m.ia + npad;
   return m;
 }
 inline size_t sort_smem_bytes(int npad) {
+  static_assert(sizeof(LoadStats) % 16 == 0, "keeps lim_acc 8-byte aligned");
   return (size_t)npad * 16 + 256 * kSortWarps * 4 + 64 * 4 + sizeof(LoadStats) + 16 + (size_t)npad * 4;
 }
 
@@ -212,7 +213,7 @@ __device__ __forceinline__ void init_stats(LoadStats* st, unsigned long long* li
   if (threadIdx.x == 0) {
     st->or_lo = st->or_hi = 0;
     st->and_lo = st->and_hi = ~0u;
-    st->mode = kNarrow8;
+    st->mode = kNarrow7;
     st->n_act = st->neg = st->pos = st->zero = 0;
     *lim_acc = 0ull;
   }

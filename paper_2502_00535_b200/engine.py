@@ -163,7 +163,7 @@ def run_nms(d: DetectionVector, cfg: NmsConfig) -> tuple[NmsResult, WorkCounters
         keep = np.zeros(0, dtype=np.int64)
         writes = dim * (dim - 1) // 2 if cfg.tie_break == "by_index" else 0
     else:
-        t = lambda a: torch.from_numpy(np.ascontiguousarray(a[:n])).reshape(1, n).to(dev)  # noqa: E731
+        t = lambda a: torch.from_numpy(np.array(a[:n])).reshape(1, n).to(dev)  # noqa: E731
         gp = torch.empty((1,), dtype=torch.int64, device=dev)
         idx, cnt = batched_nms_keep(t(x), t(y), t(z), t(s), None, cfg.theta, cfg.tie_break, dim, gate_pairs=gp)
         k = int(cnt.item())
@@ -182,7 +182,7 @@ def map_phase(d: DetectionVector, cfg: NmsConfig) -> tuple[SuppressionMatrix, Wo
         raise ConfigError(f"vector capacity {len(d)} does not match d_max={dim}")
     torch = _torch()
     dev = torch.device("cuda", torch.cuda.current_device())
-    x, y, z, s = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in _frame_columns(d))
+    x, y, z, s = (torch.from_numpy(np.array(a)).to(dev) for a in _frame_columns(d))
     W64 = (dim + 63) // 64
     bits = torch.empty((dim, W64), dtype=torch.int64, device=dev)
     gp = torch.empty((1,), dtype=torch.int64, device=dev)
