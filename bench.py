@@ -186,7 +186,10 @@ class ClockSampler:
 
 # --------------------------------------------------------------------- GPU leg
 def latency_suite(torch, dev, iters: int = 50):
-    """Median single-call latency (CUDA events, device-resident inputs) of configs 1-4."""
+    """Median single-call device latency (CUDA events, device-resident inputs) of configs 1-4.
+
+    A spin kernel is queued ahead of the start event so the events bracket only device time
+    (first kernel start to last kernel end), not the host's enqueue time."""
     from paper_2502_00535_b200 import batched_nms_keep
     from paper_2502_00535_b200.synth import random_frames
 
@@ -204,6 +207,7 @@ def latency_suite(torch, dev, iters: int = 50):
         ts = []
         for _ in range(iters):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda._sleep(200_000)  # GPU busy while the host enqueues: events see device time only
             a.record()
             batched_nms_keep(x, y, z, s, None, THETA, TIE, n, keep_idx=ki, keep_count=kc)
             b.record()

@@ -53,8 +53,13 @@ typedef enum pnms_status {
 
 /* Bytes of device workspace pnms_run needs for `batch` frames of stride `n_max`.
  * Replaces the reference's per-call SuppressionMatrix.all_ones allocation
- * (engine.py:93-96, 187): the workspace is reused across calls and needs no clearing. */
+ * (engine.py:93-96, 187).  The workspace starts with a small persistent scratch region that
+ * must be zero before the first call (allocate zeroed, or call pnms_workspace_init once);
+ * every call leaves it zero again, so a workspace is reused across calls with no clearing. */
 int pnms_workspace_bytes(int batch, int n_max, size_t* out_bytes);
+
+/* Zero the persistent scratch region of a workspace (stream-ordered). */
+int pnms_workspace_init(void* workspace, size_t workspace_bytes, void* stream);
 
 /* Batched NMS: the whole run_nms pipeline (engine.py:296-300) for `batch` frames.
  *

@@ -14,6 +14,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libparnms_b200.so"
 # every symbol include/parnms_b200.h declares
 EXPORTED_SYMBOLS = (
     "pnms_workspace_bytes",
+    "pnms_workspace_init",
     "pnms_run",
     "pnms_run_profiled",
     "pnms_map_reference_layout",
@@ -65,6 +66,8 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
     vp, i32, f64, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_size_t
     lib.pnms_workspace_bytes.argtypes = [i32, i32, ctypes.POINTER(sz)]
     lib.pnms_workspace_bytes.restype = i32
+    lib.pnms_workspace_init.argtypes = [vp, sz, vp]
+    lib.pnms_workspace_init.restype = i32
     lib.pnms_run.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, f64, i32, vp, vp, vp, vp, vp, sz, vp]
     lib.pnms_run.restype = i32
     lib.pnms_run_profiled.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, f64, i32, vp, vp, vp, vp, vp, sz, vp, vp]

@@ -17,6 +17,7 @@
 #include "pnms_compact.cuh"
 #include "pnms_map.cuh"
 #include "pnms_reflayout.cuh"
+#include "pnms_small.cuh"
 #include "pnms_sort.cuh"
 
 using namespace pnms;
@@ -35,7 +36,7 @@ Layout make_layout(int batch, int n_max) {
   Layout L;
   const size_t B = (size_t)batch, N = (size_t)n_max;
   const size_t W32 = (N + 31) / 32;
-  size_t off = 0;
+  size_t off = kSmallScratchBytes;  // [0, kSmallScratchBytes): persistent zeroed scratch
   L.rec = off;  off = align_up(off + B * N * kRecBytes, 256);
   L.perm = off; off = align_up(off + B * N * 4, 256);
   L.lim = off;  off = align_up(off + B * N * 4, 256);
@@ -51,11 +52,12 @@ Layout make_layout(int batch, int n_max) {
   return L;
 }
 
-int env_int(const char* name, int dflt) {
+long long env_ll(const char* name, long long dflt) {
   const char* v = std::getenv(name);
   if (!v || !*v) return dflt;
-  return std::atoi(v);
+  return std::strtoll(v, nullptr, 10);
 }
+int env_int(const char* name, int dflt) { return (int)env_ll(name, dflt); }
 
 int fail_cuda(cudaError_t e) {
   g_last_cuda_error = (int)e;
@@ -72,22 +74,37 @@ cudaError_t ensure_smem(K kernel, size_t bytes, std::atomic<size_t>& configured)
 
 std::atomic<size_t> g_sort_frame_smem{0}, g_sort_chunk_smem{0}, g_compact_smem{0};
 std::atomic<size_t> g_map_smem[5];
+std::atomic<size_t> g_small_smem[4];
+
+// Calls with little total work run the single-launch unsorted path (pnms_small.cuh).
+bool use_small_path(int batch, int n_max) {
+  const int W32 = (n_max + 31) / 32;
+  if (n_max > kSortMax || batch > kSmallMaxFrames || (long long)batch * W32 > kSmallMaxWords) return false;
+  const long long pairs = (long long)batch * n_max * n_max;
+  const long long limit = env_ll("PNMS_SMALL_PAIRS", 24LL << 20);
+  return pairs <= limit;
+}
 
 struct MapShape {
   int R, RB, chunk;
 };
 
-// Work-item shape: many small items when the call has little total work (single-frame
-// latency), large items when there are many frames (batched throughput).
+int items_per_frame(int n_max, int RB, int chunk) {
+  int ipf = 0;
+  for (int rb = 0; rb * RB < n_max; ++rb) ipf += (std::min((rb + 1) * RB - 1, n_max) + chunk - 1) / chunk;
+  return ipf;
+}
+
+// Work-item shape: the largest (rows-per-lane, chunk) whose item count still gives every SM
+// a few items to balance the triangular work (measured on B200 with tools/tune_map.py).
 MapShape choose_map_shape(int batch, int n_max) {
-  MapShape m;
-  const long long rows = (long long)batch * n_max;
-  if (rows >= 148LL * 1024) {
-    m.R = 4;
-    m.chunk = 1024;
-  } else {
-    m.R = 1;
-    m.chunk = 256;
+  static const int cand[][2] = {{4, 1024}, {4, 512}, {2, 512}, {2, 256}, {1, 256}};
+  MapShape m{1, kMapWarps * 32, 256};
+  for (const auto& c : cand) {
+    const long long items = (long long)batch * items_per_frame(n_max, kMapWarps * 32 * c[0], c[1]);
+    m.R = c[0];
+    m.chunk = c[1];
+    if (items >= 512) break;
   }
   const int r_env = env_int("PNMS_MAP_R", 0);
   if (r_env == 1 || r_env == 2 || r_env == 4) m.R = r_env;
@@ -126,6 +143,12 @@ const char* pnms_strerror(int status) {
     case PNMS_EINVAL_K: return "k must be positive and divide d_max";
     default: return "unknown parnms_b200 status";
   }
+}
+
+int pnms_workspace_init(void* workspace, size_t workspace_bytes, void* stream) {
+  if (!workspace || workspace_bytes < kSmallScratchBytes) return PNMS_EWORKSPACE;
+  cudaError_t e = cudaMemsetAsync(workspace, 0, kSmallScratchBytes, (cudaStream_t)stream);
+  return e == cudaSuccess ? PNMS_OK : fail_cuda(e);
 }
 
 int pnms_workspace_bytes(int batch, int n_max, size_t* out_bytes) {
@@ -175,6 +198,48 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
   const int W32 = (n_max + 31) / 32;
   cudaError_t e;
 
+  if (use_small_path(batch, n_max)) {
+    SmallArgs sa;
+    sa.x = x; sa.y = y; sa.z = z; sa.s = s; sa.counts = counts;
+    sa.batch = batch; sa.n_max = n_max; sa.d_max = d_max; sa.tie_break = tie_break; sa.W32 = W32;
+    sa.theta = theta;
+    sa.n_rt = (n_max + kSmallThreads * kSmallRows - 1) / (kSmallThreads * kSmallRows);
+    const int max_ct = (n_max + 31) / 32;
+    int n_ct = (int)std::min<long long>(max_ct, std::max<long long>(1, (2LL * 148 + (long long)batch * sa.n_rt - 1) /
+                                                                         ((long long)batch * sa.n_rt)));
+    const int ct_env = env_int("PNMS_SMALL_CT", 0);
+    if (ct_env > 0) n_ct = std::min(ct_env, max_ct);
+    sa.cols = ((n_max + n_ct - 1) / n_ct + 31) / 32 * 32;
+    sa.n_ct = (n_max + sa.cols - 1) / sa.cols;
+    sa.supp = reinterpret_cast<uint32_t*>(ws);
+    sa.ticket = reinterpret_cast<unsigned int*>(ws + kSmallMaxWords * 4);
+    sa.gacc = reinterpret_cast<unsigned long long*>(ws + kSmallMaxWords * 4 + kSmallMaxFrames * 4);
+    sa.keep_idx = keep_idx; sa.keep_count = keep_count; sa.keep_mask = keep_mask;
+    sa.gate_pairs = reinterpret_cast<unsigned long long*>(gate_pairs);
+    const size_t smem = (size_t)sa.cols * (8 + sizeof(RecWide));
+    const long long grid = (long long)batch * sa.n_rt * sa.n_ct;
+    if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
+    if ((e = mark(events, 1, st)) != cudaSuccess) return fail_cuda(e);
+    const bool by_index = tie_break == PNMS_TIE_BY_INDEX, count = gate_pairs != nullptr;
+    if (by_index && count) {
+      if ((e = ensure_smem(pnms_small_kernel<true, true>, smem, g_small_smem[3])) != cudaSuccess) return fail_cuda(e);
+      pnms_small_kernel<true, true><<<(unsigned)grid, kSmallThreads, smem, st>>>(sa);
+    } else if (by_index) {
+      if ((e = ensure_smem(pnms_small_kernel<true, false>, smem, g_small_smem[2])) != cudaSuccess) return fail_cuda(e);
+      pnms_small_kernel<true, false><<<(unsigned)grid, kSmallThreads, smem, st>>>(sa);
+    } else if (count) {
+      if ((e = ensure_smem(pnms_small_kernel<false, true>, smem, g_small_smem[1])) != cudaSuccess) return fail_cuda(e);
+      pnms_small_kernel<false, true><<<(unsigned)grid, kSmallThreads, smem, st>>>(sa);
+    } else {
+      if ((e = ensure_smem(pnms_small_kernel<false, false>, smem, g_small_smem[0])) != cudaSuccess) return fail_cuda(e);
+      pnms_small_kernel<false, false><<<(unsigned)grid, kSmallThreads, smem, st>>>(sa);
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
+    if ((e = mark(events, 2, st)) != cudaSuccess) return fail_cuda(e);
+    if ((e = mark(events, 3, st)) != cudaSuccess) return fail_cuda(e);
+    return PNMS_OK;
+  }
+
   PrepArgs pa;
   pa.x = x; pa.y = y; pa.z = z; pa.s = s; pa.counts = counts;
   pa.batch = batch; pa.n_max = n_max; pa.tie_break = tie_break; pa.W32 = W32;
@@ -191,7 +256,7 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
   if (n_max <= kSortMax) {
     pa.npad = (n_max + kSortThreads - 1) / kSortThreads * kSortThreads;
     pa.nchunks = 1;
-    const size_t smem = sort_smem_bytes(pa.npad);
+    const size_t smem = sort_frame_smem_bytes(pa.npad);
     if ((e = ensure_smem(pnms_prep_sort_frame, smem, g_sort_frame_smem)) != cudaSuccess) return fail_cuda(e);
     pnms_prep_sort_frame<<<batch, kSortThreads, smem, st>>>(pa);
     if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
@@ -216,11 +281,7 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
   ma.rows_per_block = ms.RB;
   ma.chunk = ms.chunk;
   ma.n_rb = (n_max + ms.RB - 1) / ms.RB;
-  int ipf = 0;
-  for (int rb = 0; rb < ma.n_rb; ++rb) {
-    const int cols = std::min((rb + 1) * ms.RB - 1, n_max);
-    ipf += (cols + ms.chunk - 1) / ms.chunk;
-  }
+  const int ipf = items_per_frame(n_max, ms.RB, ms.chunk);
   ma.items_per_frame = ipf;
   const long long grid = (long long)batch * ipf;
   if (grid > 0x7FFFFFFFLL) return PNMS_ETOO_LARGE;
@@ -236,7 +297,7 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
   ca.batch = batch; ca.n_max = n_max; ca.W32 = W32; ca.d_max = d_max; ca.tie_break = tie_break;
   ca.keep_idx = keep_idx; ca.keep_count = keep_count; ca.keep_mask = keep_mask;
   ca.gate_pairs = reinterpret_cast<unsigned long long*>(gate_pairs);
-  const size_t csmem = ((size_t)n_max + 15) / 16 * 16 + 64 * 4;
+  const size_t csmem = ((size_t)W32 + 3) / 4 * 16 + 64 * 4;
   if ((e = ensure_smem(pnms_compact, csmem, g_compact_smem)) != cudaSuccess) return fail_cuda(e);
   pnms_compact<<<batch, kCompactThreads, csmem, st>>>(ca);
   if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);

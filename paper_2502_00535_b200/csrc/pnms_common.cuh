@@ -146,6 +146,35 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* w
   return excl;
 }
 
+// Block-wide exclusive max-scan (identity -1), same contract as block_exclusive_scan.
+__device__ __forceinline__ int block_exclusive_max_scan(int v, int* warp_vals) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  int inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+    if (lane >= o) inc = max(inc, t);
+  }
+  if (lane == 31) warp_vals[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < nwarps ? warp_vals[lane] : -1;
+    int wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+      if (lane >= o) wi = max(wi, t);
+    }
+    int ex = __shfl_up_sync(0xFFFFFFFFu, wi, 1);
+    if (lane < nwarps) warp_vals[lane] = lane == 0 ? -1 : ex;
+  }
+  __syncthreads();
+  int prev = __shfl_up_sync(0xFFFFFFFFu, inc, 1);
+  int excl = max(warp_vals[warp], lane == 0 ? -1 : prev);
+  __syncthreads();
+  return excl;
+}
+
 // ---- 1-D bulk async copy (TMA bulk engine, SASS UBLKCP) with an mbarrier -----------------
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));

@@ -12,7 +12,7 @@
 
 namespace pnms {
 
-constexpr int kCompactThreads = 1024;
+constexpr int kCompactThreads = 256;
 
 struct CompactArgs {
   const double* s;
@@ -29,36 +29,31 @@ struct CompactArgs {
 
 __global__ void __launch_bounds__(kCompactThreads) pnms_compact(CompactArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint8_t* flags = smem_raw;                                              // [n_max]
-  uint32_t* warp_sums = reinterpret_cast<uint32_t*>(smem_raw + ((a.n_max + 15) & ~15));
+  uint32_t* kbits = reinterpret_cast<uint32_t*>(smem_raw);          // [W32] survivor bits, input order
+  uint32_t* warp_sums = kbits + ((a.W32 + 3) & ~3);
   const int f = blockIdx.x;
   const long long fbase = (long long)f * a.n_max;
   const int cnt = frame_count(a.counts, f, a.n_max);
   const int P = a.d_max > cnt ? a.d_max - cnt : 0;
   const uint32_t* supp_frame = a.supp + (long long)f * a.W32;
 
-  for (int p = threadIdx.x; p < a.n_max; p += kCompactThreads) flags[p] = 0;
+  for (int w = threadIdx.x; w < a.W32; w += kCompactThreads) kbits[w] = 0u;
   __syncthreads();
+  // scatter sorted-order verdicts to input order (one shared atomic per survivor)
   for (int p = threadIdx.x; p < cnt; p += kCompactThreads) {
     const int i = a.perm[fbase + p];
     bool keep = !((supp_frame[p >> 5] >> (p & 31)) & 1u);
-    if (P > 0 && a.s[fbase + i] < 0.0) keep = false;
-    flags[i] = keep ? 1 : 0;
+    if (P > 0 && keep && a.s[fbase + i] < 0.0) keep = false;
+    if (keep) atomicOr(&kbits[i >> 5], 1u << (i & 31));
   }
   __syncthreads();
 
-  // contiguous segments of whole 32-slot words per thread
   const int words_per_thread = (a.W32 + kCompactThreads - 1) / kCompactThreads;
   const int w0 = threadIdx.x * words_per_thread;
   const int w1 = min(w0 + words_per_thread, a.W32);
   uint32_t local = 0;
   for (int w = w0; w < w1; ++w) {
-    uint32_t bits = 0;
-    const int b = w * 32;
-    for (int t = 0; t < 32; ++t) {
-      const int i = b + t;
-      if (i < a.n_max && flags[i]) bits |= 1u << t;
-    }
+    const uint32_t bits = kbits[w];
     local += __popc(bits);
     if (a.keep_mask) a.keep_mask[(long long)f * a.W32 + w] = bits;
   }
@@ -66,8 +61,13 @@ __global__ void __launch_bounds__(kCompactThreads) pnms_compact(CompactArgs a) {
   uint32_t pos = block_exclusive_scan(local, warp_sums, &total);
   if (a.keep_idx) {
     int32_t* out = a.keep_idx + fbase;
-    for (int i = w0 * 32; i < min(w1 * 32, a.n_max); ++i)
-      if (flags[i]) out[pos++] = i;
+    for (int w = w0; w < w1; ++w) {
+      uint32_t bits = kbits[w];
+      while (bits) {
+        out[pos++] = w * 32 + __ffs(bits) - 1;
+        bits &= bits - 1;
+      }
+    }
   }
   if (threadIdx.x == 0) {
     if (a.keep_count) a.keep_count[f] = (int32_t)total;

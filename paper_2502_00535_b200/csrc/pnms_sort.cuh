@@ -59,13 +59,19 @@ __device__ __forceinline__ int upper_bound_u64(const uint64_t* a, int n, uint64_
   return lo;
 }
 
-// Stable block radix sort (ascending) of npad = 512*E (key, idx) pairs held in shared memory,
-// 8-bit digits, digits on which all keys agree (diff == 0) are skipped.  Warp w owns the
-// contiguous run [w*32E, (w+1)*32E); inside a warp, rounds of 32 consecutive slots are
-// ranked with __match_any_sync so the scatter preserves input order.
-// On return *k / *id point at the buffer that holds the sorted sequence.
-__device__ void block_radix_sort(uint64_t** k, uint16_t** id, uint64_t* k2, uint16_t* id2,
-                                 uint32_t* hist, uint32_t* scan_tmp, int E, uint64_t diff) {
+// Stable block sort (ascending) of npad = 512*E (key, idx) pairs held in shared memory.
+//  1. LSD radix passes with 8-bit digits over the HIGH 32 bits of the key only; digits on
+//     which every key agrees (diff_hi == 0 there) are skipped — for scores in [0.05, 1) the
+//     top byte is constant, so three passes run.  Warp w owns the contiguous run
+//     [w*32E, (w+1)*32E); inside a warp, rounds of 32 consecutive slots are ranked by a
+//     ballot multisplit (8 ballots) so the scatter preserves input order.  Per-warp digit
+//     counters live at hist[w*256 + d] (conflict-free for distinct digits).
+//  2. Runs of equal high words (rare: ~1 per 2048 random scores) are re-ranked exactly by
+//     (full key, idx) by counting inside the run; NaN keys and padding are left as they are
+//     (their order never matters: they are never columns of an active row).
+// On return *k / *id point at the sorted sequence of the first `cnt` slots.
+__device__ void block_sort_keys(uint64_t** k, uint16_t** id, uint64_t* k2, uint16_t* id2, uint32_t* hist,
+                                uint32_t* scan_tmp, int E, int cnt, uint32_t diff_hi) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t lt = lanemask_lt();
   uint64_t* ka = *k;
@@ -73,8 +79,9 @@ __device__ void block_radix_sort(uint64_t** k, uint16_t** id, uint64_t* k2, uint
   uint64_t* kb = k2;
   uint16_t* ib = id2;
   const int wbase = warp * 32 * E;
-  for (int sh = 0; sh < 64; sh += 8) {
-    if (((diff >> sh) & 0xFFull) == 0) continue;
+  uint32_t* whist = hist + warp * 256;
+  for (int sh = 0; sh < 32; sh += 8) {
+    if (((diff_hi >> sh) & 0xFFu) == 0) continue;
     for (int i = threadIdx.x; i < 256 * kSortWarps; i += kSortThreads) hist[i] = 0;
     __syncthreads();
     uint64_t key[8];
@@ -83,37 +90,47 @@ __device__ void block_radix_sort(uint64_t** k, uint16_t** id, uint64_t* k2, uint
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       if (r < E) {
-        int e = wbase + r * 32 + lane;
+        const int e = wbase + r * 32 + lane;
         key[r] = ka[e];
         ix[r] = ia[e];
-        dig[r] = static_cast<uint32_t>(key[r] >> sh) & 0xFFu;
-        peers[r] = __match_any_sync(0xFFFFFFFFu, dig[r]);
-        if (lane == __ffs(peers[r]) - 1) hist[dig[r] * kSortWarps + warp] += __popc(peers[r]);
+        const uint32_t d = (uint32_t)(key[r] >> (32 + sh)) & 0xFFu;
+        uint32_t pm = 0xFFFFFFFFu;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          const uint32_t bal = __ballot_sync(0xFFFFFFFFu, (d >> b) & 1u);
+          pm &= ((d >> b) & 1u) ? bal : ~bal;
+        }
+        dig[r] = d;
+        peers[r] = pm;
+        if (lane == __ffs(pm) - 1) whist[d] += __popc(pm);
         __syncwarp();
       }
     }
     __syncthreads();
-    // exclusive scan over the digit-major (digit, warp) histogram: 4096 counters, 8/thread
+    // digit-major exclusive offsets: base(d) + sum of warps before w for digit d
     {
-      uint32_t loc[8], sum = 0;
-      const int b0 = threadIdx.x * 8;
-#pragma unroll
-      for (int t = 0; t < 8; ++t) { loc[t] = hist[b0 + t]; sum += loc[t]; }
-      uint32_t excl = block_exclusive_scan(sum, scan_tmp, nullptr);
-#pragma unroll
-      for (int t = 0; t < 8; ++t) { hist[b0 + t] = excl; excl += loc[t]; }
+      uint32_t tot = 0;
+      if (threadIdx.x < 256) {
+        for (int w = 0; w < kSortWarps; ++w) {
+          const uint32_t v = hist[w * 256 + threadIdx.x];
+          hist[w * 256 + threadIdx.x] = tot;
+          tot += v;
+        }
+      }
+      const uint32_t base = block_exclusive_scan(threadIdx.x < 256 ? tot : 0u, scan_tmp, nullptr);
+      if (threadIdx.x < 256)
+        for (int w = 0; w < kSortWarps; ++w) hist[w * 256 + threadIdx.x] += base;
     }
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       if (r < E) {
-        const uint32_t slot = dig[r] * kSortWarps + warp;
-        const uint32_t base = hist[slot];
-        const uint32_t pos = base + __popc(peers[r] & lt);
+        const uint32_t b0 = whist[dig[r]];
+        const uint32_t pos = b0 + __popc(peers[r] & lt);
         kb[pos] = key[r];
         ib[pos] = ix[r];
         __syncwarp();
-        if (lane == __ffs(peers[r]) - 1) hist[slot] = base + __popc(peers[r]);
+        if (lane == __ffs(peers[r]) - 1) whist[dig[r]] = b0 + __popc(peers[r]);
         __syncwarp();
       }
     }
@@ -121,8 +138,143 @@ __device__ void block_radix_sort(uint64_t** k, uint16_t** id, uint64_t* k2, uint
     uint64_t* tk = ka; ka = kb; kb = tk;
     uint16_t* ti = ia; ia = ib; ib = ti;
   }
-  *k = ka;
-  *id = ia;
+  // exact fix-up of equal-high-word runs
+  for (int p = threadIdx.x; p < cnt; p += kSortThreads) {
+    const uint64_t sk = ka[p];
+    const uint32_t h = (uint32_t)(sk >> 32);
+    const bool run = sk != kNanSortKey && ((p > 0 && (uint32_t)(ka[p - 1] >> 32) == h) ||
+                                           (p + 1 < cnt && (uint32_t)(ka[p + 1] >> 32) == h));
+    int dst = p;
+    if (run) {
+      int rs = p, re = p + 1;
+      while (rs > 0 && (uint32_t)(ka[rs - 1] >> 32) == h) --rs;
+      while (re < cnt && (uint32_t)(ka[re] >> 32) == h) ++re;
+      const uint16_t me = ia[p];
+      int rank = 0;
+      for (int q = rs; q < re; ++q) {
+        const uint64_t o = ka[q];
+        rank += (o < sk) || (o == sk && ia[q] < me);
+      }
+      dst = rs + rank;
+    }
+    kb[dst] = sk;
+    ib[dst] = ia[p];
+  }
+  __syncthreads();
+  *k = kb;
+  *id = ib;
+}
+
+// u64 warp reductions (no native 64-bit redux)
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const uint64_t t = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    v = t < v ? t : v;
+  }
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const uint64_t t = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    v = t > v ? t : v;
+  }
+  return v;
+}
+
+constexpr int kBucketMaxLoad = 64;  // larger buckets fall back to the radix sort
+
+// Bucket sort with exact in-bucket ranking.  Keys of the non-NaN slots are mapped linearly
+// onto nb buckets over [kmin, kmax] (monotone, so a higher bucket always holds strictly
+// larger keys); one counting pass places every slot in its bucket, then each slot finds its
+// exact position inside the bucket by counting the members that precede it in
+// (key, index) order.  Valid NaN slots go to bucket nb and padding slots (e >= cnt) to
+// bucket nb+1, so NaN rows occupy [n_active, cnt) and padding stays past cnt; the internal
+// order of those two buckets is irrelevant.  Returns false (input untouched) when a real
+// bucket holds more than kBucketMaxLoad slots — the caller then runs block_sort_keys.
+// scratch: cnt_s needs nb + 2 words, off_s nb + 3 words.
+__device__ __forceinline__ int bucket_of(uint64_t sk, int e, int cnt, uint64_t kmin, int shift, int nb) {
+  if (e >= cnt) return nb + 1;
+  if (sk == kNanSortKey) return nb;
+  return (int)((sk - kmin) >> shift);
+}
+
+__device__ bool block_bucket_sort(uint64_t** k, uint16_t** id, uint64_t* k2, uint16_t* id2, uint32_t* cnt_s,
+                                  uint32_t* off_s, uint32_t* scan_tmp, int npad, int cnt, uint64_t kmin,
+                                  uint64_t kmax, int nb) {
+  uint64_t* ka = *k;
+  uint16_t* ia = *id;
+  const uint64_t range = kmax - kmin;
+  int shift = 0;
+  {
+    const int bits = range ? 64 - __clzll((long long)range) : 0;  // bits needed for the range
+    const int nb_bits = 31 - __clz(nb);
+    shift = bits > nb_bits ? bits - nb_bits : 0;
+  }
+  const int nbk = nb + 2;  // real buckets + NaN bucket + padding bucket
+  for (int b = threadIdx.x; b < nbk; b += kSortThreads) cnt_s[b] = 0u;
+  __syncthreads();
+  for (int e = threadIdx.x; e < npad; e += kSortThreads) atomicAdd(&cnt_s[bucket_of(ka[e], e, cnt, kmin, shift, nb)], 1u);
+  __syncthreads();
+  // exclusive scan of the counts; also the largest real bucket
+  const int per = (nbk + kSortThreads - 1) / kSortThreads;
+  const int b0 = threadIdx.x * per;
+  uint32_t sum = 0, big = 0;
+  for (int t = 0; t < per; ++t) {
+    const int b = b0 + t;
+    if (b < nbk) {
+      sum += cnt_s[b];
+      if (b < nb) big = max(big, cnt_s[b]);
+    }
+  }
+  big = __reduce_max_sync(0xFFFFFFFFu, big);
+  uint32_t total;
+  uint32_t run = block_exclusive_scan(sum, scan_tmp, &total);
+  if ((threadIdx.x & 31) == 0) atomicMax(&scan_tmp[40], big);
+  for (int t = 0; t < per; ++t) {
+    const int b = b0 + t;
+    if (b < nbk) {
+      off_s[b] = run;
+      run += cnt_s[b];
+    }
+  }
+  if (threadIdx.x == 0) off_s[nbk] = npad;
+  __syncthreads();
+  const bool ok = scan_tmp[40] <= (uint32_t)kBucketMaxLoad;
+  __syncthreads();
+  if (threadIdx.x == 0) scan_tmp[40] = 0u;
+  if (!ok) return false;
+  // scatter (cnt_s becomes the insertion cursor)
+  for (int b = threadIdx.x; b < nbk; b += kSortThreads) cnt_s[b] = off_s[b];
+  __syncthreads();
+  for (int e = threadIdx.x; e < npad; e += kSortThreads) {
+    const uint64_t sk = ka[e];
+    const uint32_t pos = atomicAdd(&cnt_s[bucket_of(sk, e, cnt, kmin, shift, nb)], 1u);
+    k2[pos] = sk;
+    id2[pos] = ia[e];
+  }
+  __syncthreads();
+  // exact rank inside each real bucket -> final position (written back into ka/ia)
+  for (int p = threadIdx.x; p < npad; p += kSortThreads) {
+    const uint64_t sk = k2[p];
+    const uint16_t me = id2[p];
+    int dst = p;
+    if (p < cnt && sk != kNanSortKey) {
+      const int b = (int)((sk - kmin) >> shift);
+      const int bs = (int)off_s[b], be = (int)off_s[b + 1];
+      int rank = 0;
+      for (int q = bs; q < be; ++q) {
+        const uint64_t o = k2[q];
+        rank += (o < sk) || (o == sk && id2[q] < me);
+      }
+      dst = bs + rank;
+    }
+    ka[dst] = sk;
+    ia[dst] = me;
+  }
+  __syncthreads();
+  return true;
 }
 
 __device__ __forceinline__ void write_record(uint8_t* rec_frame, int pos, int mode, int32_t x, int32_t y,
@@ -135,6 +287,7 @@ __device__ __forceinline__ void write_record(uint8_t* rec_frame, int pos, int mo
 }
 
 struct __align__(16) LoadStats {
+  unsigned long long kmin, kmax;   // range of the non-NaN sort keys
   uint32_t or_lo, or_hi, and_lo, and_hi;
   int mode, n_act, neg, pos, zero;
 };
@@ -143,9 +296,11 @@ struct __align__(16) LoadStats {
 // reduces the statistics the later phases need.  Slots past len are padded with the NaN
 // key (they sort last, after real NaNs, by stability).
 __device__ void load_keys(const PrepArgs& a, long long fbase, int e0, int len, int npad, uint64_t* k,
-                          uint16_t* id, LoadStats* st) {
+                          uint16_t* id, LoadStats* st, int32_t* sx = nullptr, int32_t* sy = nullptr,
+                          int32_t* sz = nullptr) {
   const int lane = threadIdx.x & 31;
   uint32_t or_lo = 0, or_hi = 0, and_lo = ~0u, and_hi = ~0u;
+  uint64_t kmin = ~0ull, kmax = 0ull;
   int mode = kNarrow7, n_act = 0, neg = 0, pos = 0, zero = 0;
   for (int e = threadIdx.x; e < npad; e += kSortThreads) {
     uint64_t key = kNanSortKey;
@@ -153,11 +308,17 @@ __device__ void load_keys(const PrepArgs& a, long long fbase, int e0, int len, i
       long long g = fbase + e0 + e;
       double sv = a.s[g];
       key = sort_key(sv);
-      int m = frame_mode_of(a.x[g], a.y[g], a.z[g]);
+      const int32_t xv = a.x[g], yv = a.y[g], zv = a.z[g];
+      if (sx) { sx[e] = xv; sy[e] = yv; sz[e] = zv; }
+      int m = frame_mode_of(xv, yv, zv);
       mode = m > mode ? m : mode;
       or_lo |= (uint32_t)key; or_hi |= (uint32_t)(key >> 32);
       and_lo &= (uint32_t)key; and_hi &= (uint32_t)(key >> 32);
       n_act += (key != kNanSortKey);
+      if (key != kNanSortKey) {
+        kmin = key < kmin ? key : kmin;
+        kmax = key > kmax ? key : kmax;
+      }
       neg += (sv < 0.0);
       pos += (sv > 0.0);
       zero += (sv == 0.0);
@@ -174,7 +335,11 @@ __device__ void load_keys(const PrepArgs& a, long long fbase, int e0, int len, i
   neg = __reduce_add_sync(0xFFFFFFFFu, neg);
   pos = __reduce_add_sync(0xFFFFFFFFu, pos);
   zero = __reduce_add_sync(0xFFFFFFFFu, zero);
+  kmin = warp_min_u64(kmin);
+  kmax = warp_max_u64(kmax);
   if (lane == 0) {
+    atomicMin(&st->kmin, (unsigned long long)kmin);
+    atomicMax(&st->kmax, (unsigned long long)kmax);
     atomicOr(&st->or_lo, or_lo); atomicOr(&st->or_hi, or_hi);
     atomicAnd(&st->and_lo, and_lo); atomicAnd(&st->and_hi, and_hi);
     atomicMax(&st->mode, mode);
@@ -187,6 +352,7 @@ __device__ void load_keys(const PrepArgs& a, long long fbase, int e0, int len, i
 struct SortSmem {
   uint64_t *ka, *kb;
   uint16_t *ia, *ib;
+  int32_t *sx, *sy, *sz;   // staged coordinates (frame kernel only)
   uint32_t* hist;
   uint32_t* scan_tmp;
   LoadStats* st;
@@ -197,20 +363,28 @@ __device__ __forceinline__ SortSmem carve_sort_smem(unsigned char* base, int npa
   m.ka = reinterpret_cast<uint64_t*>(base);
   m.kb = m.ka + npad;
   m.hist = reinterpret_cast<uint32_t*>(m.kb + npad);
-  m.scan_tmp = m.hist + 256 * kSortWarps;
+  m.scan_tmp = m.hist + 256 * kSortWarps + 64;  // hist has 64 spare words for the bucket offsets
   m.st = reinterpret_cast<LoadStats*>(m.scan_tmp + 64);
   m.lim_acc = reinterpret_cast<unsigned long long*>(m.st + 1);  // LoadStats is 16-byte aligned
   m.ia = reinterpret_cast<uint16_t*>(m.lim_acc + 2);
   m.ib = m.ia + npad;
+  m.sx = reinterpret_cast<int32_t*>(m.ib + npad);
+  m.sy = m.sx + npad;
+  m.sz = m.sy + npad;
   return m;
 }
 inline size_t sort_smem_bytes(int npad) {
   static_assert(sizeof(LoadStats) % 16 == 0, "keeps lim_acc 8-byte aligned");
-  return (size_t)npad * 16 + 256 * kSortWarps * 4 + 64 * 4 + sizeof(LoadStats) + 16 + (size_t)npad * 4;
+  return (size_t)npad * 16 + (256 * kSortWarps + 64) * 4 + 64 * 4 + sizeof(LoadStats) + 16 + (size_t)npad * 4;
+}
+inline size_t sort_frame_smem_bytes(int npad) {
+  return sort_smem_bytes(npad) + (size_t)npad * 12;
 }
 
 __device__ __forceinline__ void init_stats(LoadStats* st, unsigned long long* lim_acc) {
   if (threadIdx.x == 0) {
+    st->kmin = ~0ull;
+    st->kmax = 0ull;
     st->or_lo = st->or_hi = 0;
     st->and_lo = st->and_hi = ~0u;
     st->mode = kNarrow7;
@@ -227,29 +401,45 @@ __global__ void __launch_bounds__(kSortThreads) pnms_prep_sort_frame(PrepArgs a)
   const int cnt = frame_count(a.counts, f, a.n_max);
   SortSmem m = carve_sort_smem(smem_raw, a.npad);
   init_stats(m.st, m.lim_acc);
+  if (threadIdx.x == 0) m.scan_tmp[40] = 0u;
   __syncthreads();
-  load_keys(a, fbase, 0, cnt, a.npad, m.ka, m.ia, m.st);
+  load_keys(a, fbase, 0, cnt, a.npad, m.ka, m.ia, m.st, m.sx, m.sy, m.sz);
   __syncthreads();
-  const uint64_t diff = ((((uint64_t)m.st->or_hi) << 32) | m.st->or_lo) ^
-                        ((((uint64_t)m.st->and_hi) << 32) | m.st->and_lo);
+  const uint32_t diff_hi = m.st->or_hi ^ m.st->and_hi;
   const int mode = m.st->mode;
   const int n_act = m.st->n_act;
   uint64_t* k = m.ka;
   uint16_t* id = m.ia;
-  if (cnt > 1) block_radix_sort(&k, &id, m.kb, m.ib, m.hist, m.scan_tmp, a.npad / kSortThreads, diff);
+  bool sorted = cnt <= 1;
+  if (!sorted && n_act > 0) {
+    const int nb = a.npad >= 4096 ? 2048 : (a.npad >= 2048 ? 2048 : a.npad);
+    sorted = block_bucket_sort(&k, &id, m.kb, m.ib, m.hist, m.hist + 2052, m.scan_tmp, a.npad, cnt, m.st->kmin,
+                               m.st->kmax, nb);
+  }
+  if (!sorted) block_sort_keys(&k, &id, m.kb, m.ib, m.hist, m.scan_tmp, a.npad / kSortThreads, cnt, diff_hi);
 
   uint8_t* rec_frame = a.rec + fbase * kRecBytes;
   unsigned long long lsum = 0;
-  for (int p = threadIdx.x; p < cnt; p += kSortThreads) {
-    const uint64_t sk = k[p];
-    const int i = id[p];
-    int l = 0;
-    if (p < n_act) l = (a.tie_break == 1) ? p : lower_bound_u64(k, cnt, sk);
+  // thread t owns sorted positions [t*E, t*E+E); tie-group starts by a block max-scan
+  const int E = a.npad / kSortThreads;
+  const int pb = threadIdx.x * E;
+  int run = -1;
+  for (int t = 0; t < E; ++t) {
+    const int p = pb + t;
+    if (p < n_act && (p == 0 || k[p] != k[p - 1])) run = p;
+  }
+  const int carry = block_exclusive_max_scan(run, reinterpret_cast<int*>(m.scan_tmp));
+  run = carry;
+  for (int t = 0; t < E; ++t) {
+    const int p = pb + t;
+    if (p >= cnt) break;
+    if (p < n_act && (p == 0 || k[p] != k[p - 1])) run = p;
+    const int l = (p < n_act) ? ((a.tie_break == 1) ? p : run) : 0;
     lsum += (unsigned long long)l;
-    const long long g = fbase + i;
+    const int i = id[p];
     a.perm[fbase + p] = i;
     a.lim[fbase + p] = l;
-    write_record(rec_frame, p, mode, a.x[g], a.y[g], a.z[g], a.theta);
+    write_record(rec_frame, p, mode, m.sx[i], m.sy[i], m.sz[i], a.theta);
   }
   for (int w = threadIdx.x; w < a.W32; w += kSortThreads) a.supp[(long long)f * a.W32 + w] = 0u;
   lsum = __reduce_add_sync(0xFFFFFFFFu, (unsigned)(lsum & 0xFFFFFFFFull)) +
@@ -287,11 +477,10 @@ __global__ void __launch_bounds__(kSortThreads) pnms_prep_sort_chunk(PrepArgs a)
   __syncthreads();
   load_keys(a, fbase, e0, len, kSortMax, m.ka, m.ia, m.st);
   __syncthreads();
-  const uint64_t diff = ((((uint64_t)m.st->or_hi) << 32) | m.st->or_lo) ^
-                        ((((uint64_t)m.st->and_hi) << 32) | m.st->and_lo);
+  const uint32_t diff_hi = m.st->or_hi ^ m.st->and_hi;
   uint64_t* k = m.ka;
   uint16_t* id = m.ia;
-  if (len > 1) block_radix_sort(&k, &id, m.kb, m.ib, m.hist, m.scan_tmp, kSortMax / kSortThreads, diff);
+  if (len > 1) block_sort_keys(&k, &id, m.kb, m.ib, m.hist, m.scan_tmp, kSortMax / kSortThreads, len, diff_hi);
   for (int p = threadIdx.x; p < len; p += kSortThreads) {
     a.sk_scratch[fbase + e0 + p] = k[p];
     a.idx_scratch[fbase + e0 + p] = e0 + id[p];

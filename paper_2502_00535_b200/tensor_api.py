@@ -55,7 +55,8 @@ class _WorkspaceCache:
         key = (device.index if device.index is not None else torch.cuda.current_device(), stream)
         buf = self._bufs.get(key)
         if buf is None or buf.numel() < nbytes:
-            buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+            # zero-filled: the head of every workspace is persistent scratch (see pnms_workspace_bytes)
+            buf = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
             self._bufs[key] = buf
         return buf
 
@@ -169,9 +170,9 @@ class NmsEngine:
         self.keep_mask = torch.empty((self.batch, self.W32), dtype=torch.int32, device=dev)
         self.bounds = [(i * self.batch // self.chunks, (i + 1) * self.batch // self.chunks) for i in range(self.chunks)]
         per = max(b - a for a, b in self.bounds)
-        self.ws = [torch.empty(_lib.workspace_bytes(per, self.n_max), dtype=torch.uint8, device=dev)
+        self.ws = [torch.zeros(_lib.workspace_bytes(per, self.n_max), dtype=torch.uint8, device=dev)
                    for _ in range(min(2, self.chunks))]
-        self.ws_full = torch.empty(_lib.workspace_bytes(self.batch, self.n_max), dtype=torch.uint8, device=dev)
+        self.ws_full = torch.zeros(_lib.workspace_bytes(self.batch, self.n_max), dtype=torch.uint8, device=dev)
         self.streams = [torch.cuda.Stream(device=dev) for _ in range(min(2, self.chunks))]
         self._dev_in = None
 

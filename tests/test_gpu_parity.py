@@ -18,6 +18,13 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda"
 
 
+@pytest.fixture(params=["small", "pipeline"])
+def path(request, monkeypatch):
+    """Run a test through the single-launch unsorted path and through the sorted pipeline."""
+    monkeypatch.setenv("PNMS_SMALL_PAIRS", str(1 << 40) if request.param == "small" else "0")
+    return request.param
+
+
 def _vec(c):
     return DetectionVector.from_arrays(c.x, c.y, c.z, c.s, c.d_max, validate=False)
 
@@ -28,7 +35,7 @@ def _k_for(d_max):
             return k
 
 
-def test_run_nms_matches_reference_cases(golden_cases):
+def test_run_nms_matches_reference_cases(golden_cases, path):
     for c in golden_cases:
         cfg = NmsConfig(theta=c.theta, d_max=c.d_max, k=c.k, workers=3, tie_break=c.tie)
         res, ctr = run_nms(_vec(c), cfg)
@@ -40,7 +47,7 @@ def test_run_nms_matches_reference_cases(golden_cases):
         assert ctr.map_cells == c.d_max ** 2 and ctr.reduce_segments == c.d_max * c.k
 
 
-def test_batched_matches_reference_cases(golden_cases):
+def test_batched_matches_reference_cases(golden_cases, path):
     """Ragged batches of the reference's random frames in one launch per (tie, theta).
     Scores are positive, so the survivors do not depend on the padding amount."""
     ran = 0
@@ -82,7 +89,7 @@ def test_map_phase_bits_match_reference(golden_cases):
 
 
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4f0", "C4f3", "C5f0", "C5f1", "C5f2", "C5f3"])
-def test_config_frames_match_reference(golden_configs, name):
+def test_config_frames_match_reference(golden_configs, name, path):
     g = golden_configs[name]
     n = len(g["x"])
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a).reshape(1, n)).to(DEV)  # noqa: E731
@@ -95,8 +102,9 @@ def test_config_frames_match_reference(golden_configs, name):
 
 
 @pytest.mark.parametrize("shape", [(1, 128), (1, 256), (2, 256), (4, 512), (1, 512)])
-def test_launch_shape_invariance(golden_configs, shape):
+def test_launch_shape_invariance(golden_configs, shape, monkeypatch):
     """Results are independent of the map decomposition (R rows/lane, chunk width)."""
+    monkeypatch.setenv("PNMS_SMALL_PAIRS", "0")
     g = golden_configs["C2"]
     n = len(g["x"])
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a).reshape(1, n)).to(DEV)  # noqa: E731
@@ -135,7 +143,7 @@ def test_c5_slice_vs_oracle():
 
 @pytest.mark.parametrize("tie", ["paper_faithful", "by_index"])
 @pytest.mark.parametrize("theta", [0.0, 0.3, 0.7, 1.0])
-def test_ragged_duplicates_vs_oracle(tie, theta):
+def test_ragged_duplicates_vs_oracle(tie, theta, path):
     rng = np.random.default_rng(int(theta * 10) + (tie == "by_index"))
     x, y, z, s = random_frames(24, 700, seed=9, frame_w=400, frame_h=300, z_range=(4, 60), duplicate_fraction=0.2)
     s[:, ::5] = np.round(s[:, ::5] * 4) / 4 + 0.01  # exact score ties
@@ -160,7 +168,7 @@ def test_chunked_sort_frames_vs_oracle(n):
             assert np.array_equal(got[f], want), (n, f, tie)
 
 
-def test_nan_and_signed_scores_vs_oracle():
+def test_nan_and_signed_scores_vs_oracle(path):
     x, y, z, s = random_frames(6, 300, seed=3, frame_w=200, frame_h=200, z_range=(4, 40))
     s[0, ::3] = np.nan
     s[1, ::4] = -np.inf
@@ -176,7 +184,7 @@ def test_nan_and_signed_scores_vs_oracle():
             assert np.array_equal(got[f], want), (f, tie)
 
 
-def test_wide_and_narrow16_paths_vs_oracle():
+def test_wide_and_narrow16_paths_vs_oracle(path):
     rng = np.random.default_rng(11)
     B, n = 4, 500
     x = rng.integers(0, 2**24 - 1, size=(B, n)).astype(np.int32)
@@ -221,7 +229,19 @@ def test_properties_full_size():
         assert set(base[f]).issubset(set(hi[f]))
 
 
-def test_keep_mask_consistent():
+def test_small_path_tile_invariance(golden_configs, monkeypatch):
+    """The single-launch path gives the same survivors for any column tiling."""
+    monkeypatch.setenv("PNMS_SMALL_PAIRS", str(1 << 40))
+    g = golden_configs["C2"]
+    n = len(g["x"])
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a).reshape(1, n)).to(DEV)  # noqa: E731
+    for ct in (1, 3, 16, 128):
+        monkeypatch.setenv("PNMS_SMALL_CT", str(ct))
+        ki, kc = batched_nms_keep(t(g["x"]), t(g["y"]), t(g["z"]), t(g["s"]), None, 0.5)
+        assert np.array_equal(ki[0, : int(kc.item())].cpu().numpy(), g["keep"]), ct
+
+
+def test_keep_mask_consistent(path):
     x, y, z, s = random_frames(8, 1000, seed=2)
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)  # noqa: E731
     mask = torch.empty((8, 32), dtype=torch.int32, device=DEV)

@@ -19,7 +19,7 @@ def probe(name, arrs, iters=30):
     B, n = x.shape
     ki = torch.empty((B, n), dtype=torch.int32, device=dev)
     kc = torch.empty((B,), dtype=torch.int32, device=dev)
-    ws = torch.empty(_lib.workspace_bytes(B, n), dtype=torch.uint8, device=dev)
+    ws = torch.zeros(_lib.workspace_bytes(B, n), dtype=torch.uint8, device=dev)
     lib = _lib.load()
     st = torch.cuda.current_stream(dev)
     res = []
@@ -28,6 +28,7 @@ def probe(name, arrs, iters=30):
         for e in ev:
             e.record(st)
         h = (ctypes.c_void_p * 4)(*[e.cuda_event for e in ev])
+        torch.cuda._sleep(200_000)  # keep the GPU busy while the host enqueues: device time only
         rc = lib.pnms_run_profiled(x.data_ptr(), y.data_ptr(), z.data_ptr(), s.data_ptr(), None, B, n, n, 0.5, 0,
                                    ki.data_ptr(), kc.data_ptr(), None, None, ws.data_ptr(), ws.numel(),
                                    st.cuda_stream, h)
@@ -37,7 +38,7 @@ def probe(name, arrs, iters=30):
             res.append([ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3]),
                         ev[0].elapsed_time(ev[3])])
     med = [statistics.median(r[i] for r in res) * 1e3 for i in range(4)]
-    print(f"{name:4s} B={B:5d} n={n:6d}  sort {med[0]:9.1f} us  map {med[1]:9.1f} us  compact {med[2]:8.1f} us"
+    print(f"{name:16s} B={B:5d} n={n:6d}  sort {med[0]:9.1f} us  map {med[1]:9.1f} us  compact {med[2]:8.1f} us"
           f"  total {med[3]:9.1f} us", flush=True)
 
 
