@@ -42,8 +42,7 @@ WORKLOAD = (f"config 5: stream of {FRAMES} frames x {BOXES} boxes (random_frame 
 SEED = 20250200
 
 
-def shard_bounds(total: int, world: int, rank: int) -> tuple[int, int]:
-    return total * rank // world, total * (rank + 1) // world
+from paper_2502_00535_b200.sharding import gather_survivors, shard_bounds  # noqa: E402
 
 
 def make_shard(rank: int, world: int):
@@ -321,6 +320,24 @@ def main():
     # correctness spot check of the e2e output against the device-resident run
     ok = bool(torch.equal(oc.to(dev), eng.keep_count))
 
+    # optional exchange step (not part of `value`): gather every rank's survivor masks and
+    # counts on rank 0 over NCCL (NVLink/NVSwitch), timed on the device, max over ranks
+    gather_ms = None
+    if dist:
+        dmask = om.to(dev)
+        for _ in range(2):
+            gather_survivors(dmask, eng.keep_count, FRAMES)
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        gather_survivors(dmask, eng.keep_count, FRAMES)
+        g1.record(stream)
+        torch.cuda.synchronize(dev)
+        t = torch.tensor([g0.elapsed_time(g1)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        gather_ms = float(t.item())
+
     lat = None
     if rank == 0 and not args.no_latency:
         lat = latency_suite(torch, dev)
@@ -359,6 +376,8 @@ def main():
         }
         if lat:
             line["latency_us"] = lat
+        if gather_ms is not None:
+            line["gather_survivors_ms"] = gather_ms
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

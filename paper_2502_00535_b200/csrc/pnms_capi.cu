@@ -74,7 +74,50 @@ cudaError_t ensure_smem(K kernel, size_t bytes, std::atomic<size_t>& configured)
 
 std::atomic<size_t> g_sort_frame_smem{0}, g_sort_chunk_smem{0}, g_compact_smem{0};
 std::atomic<size_t> g_map_smem[5];
-std::atomic<size_t> g_small_smem[4];
+
+// Internal side stream + events used to overlap a chunk's sort with the previous chunk's
+// map.  One set per host thread and device, created on first use and kept for the process
+// lifetime, so concurrent callers on different threads never share event state.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr;
+  cudaEvent_t ev[32] = {};
+};
+SideStream* side_stream() {
+  thread_local SideStream cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  SideStream& ss = cache[dev];
+  if (!ss.s) {
+    if (cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) != cudaSuccess) { ss.s = nullptr; return nullptr; }
+    cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming);
+    for (auto& ev : ss.ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  }
+  return &ss;
+}
+std::atomic<size_t> g_small_smem[8];
+
+template <bool B, bool C, int R>
+cudaError_t launch_small_t(const SmallArgs& sa, long long grid, size_t smem, cudaStream_t st, std::atomic<size_t>& cfg) {
+  cudaError_t e = ensure_smem(pnms_small_kernel<B, C, R>, smem, cfg);
+  if (e != cudaSuccess) return e;
+  pnms_small_kernel<B, C, R><<<(unsigned)grid, kSmallThreads, smem, st>>>(sa);
+  return cudaGetLastError();
+}
+
+// variant bits: 1 = count gate passes, 2 = by_index, 4 = one row per thread
+cudaError_t launch_small(int v, const SmallArgs& sa, long long grid, size_t smem, cudaStream_t st) {
+  switch (v) {
+    case 0: return launch_small_t<false, false, kSmallRowsMax>(sa, grid, smem, st, g_small_smem[0]);
+    case 1: return launch_small_t<false, true, kSmallRowsMax>(sa, grid, smem, st, g_small_smem[1]);
+    case 2: return launch_small_t<true, false, kSmallRowsMax>(sa, grid, smem, st, g_small_smem[2]);
+    case 3: return launch_small_t<true, true, kSmallRowsMax>(sa, grid, smem, st, g_small_smem[3]);
+    case 4: return launch_small_t<false, false, 1>(sa, grid, smem, st, g_small_smem[4]);
+    case 5: return launch_small_t<false, true, 1>(sa, grid, smem, st, g_small_smem[5]);
+    case 6: return launch_small_t<true, false, 1>(sa, grid, smem, st, g_small_smem[6]);
+    default: return launch_small_t<true, true, 1>(sa, grid, smem, st, g_small_smem[7]);
+  }
+}
 
 // Calls with little total work run the single-launch unsorted path (pnms_small.cuh).
 bool use_small_path(int batch, int n_max) {
@@ -203,7 +246,8 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     sa.x = x; sa.y = y; sa.z = z; sa.s = s; sa.counts = counts;
     sa.batch = batch; sa.n_max = n_max; sa.d_max = d_max; sa.tie_break = tie_break; sa.W32 = W32;
     sa.theta = theta;
-    sa.n_rt = (n_max + kSmallThreads * kSmallRows - 1) / (kSmallThreads * kSmallRows);
+    const int R = ((long long)batch * n_max <= 2048) ? 1 : kSmallRowsMax;  // tiny calls: more CTAs
+    sa.n_rt = (n_max + kSmallThreads * R - 1) / (kSmallThreads * R);
     const int max_ct = (n_max + 31) / 32;
     int n_ct = (int)std::min<long long>(max_ct, std::max<long long>(1, (2LL * 148 + (long long)batch * sa.n_rt - 1) /
                                                                          ((long long)batch * sa.n_rt)));
@@ -220,87 +264,103 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     const long long grid = (long long)batch * sa.n_rt * sa.n_ct;
     if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
     if ((e = mark(events, 1, st)) != cudaSuccess) return fail_cuda(e);
-    const bool by_index = tie_break == PNMS_TIE_BY_INDEX, count = gate_pairs != nullptr;
-    if (by_index && count) {
-      if ((e = ensure_smem(pnms_small_kernel<true, true>, smem, g_small_smem[3])) != cudaSuccess) return fail_cuda(e);
-      pnms_small_kernel<true, true><<<(unsigned)grid, kSmallThreads, smem, st>>>(sa);
-    } else if (by_index) {
-      if ((e = ensure_smem(pnms_small_kernel<true, false>, smem, g_small_smem[2])) != cudaSuccess) return fail_cuda(e);
-      pnms_small_kernel<true, false><<<(unsigned)grid, kSmallThreads, smem, st>>>(sa);
-    } else if (count) {
-      if ((e = ensure_smem(pnms_small_kernel<false, true>, smem, g_small_smem[1])) != cudaSuccess) return fail_cuda(e);
-      pnms_small_kernel<false, true><<<(unsigned)grid, kSmallThreads, smem, st>>>(sa);
-    } else {
-      if ((e = ensure_smem(pnms_small_kernel<false, false>, smem, g_small_smem[0])) != cudaSuccess) return fail_cuda(e);
-      pnms_small_kernel<false, false><<<(unsigned)grid, kSmallThreads, smem, st>>>(sa);
-    }
+    const int variant = (tie_break == PNMS_TIE_BY_INDEX ? 2 : 0) + (gate_pairs != nullptr ? 1 : 0) + (R == 1 ? 4 : 0);
+    e = launch_small(variant, sa, grid, smem, st);
+    if (e != cudaSuccess) return fail_cuda(e);
     if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
     if ((e = mark(events, 2, st)) != cudaSuccess) return fail_cuda(e);
     if ((e = mark(events, 3, st)) != cudaSuccess) return fail_cuda(e);
     return PNMS_OK;
   }
 
-  PrepArgs pa;
-  pa.x = x; pa.y = y; pa.z = z; pa.s = s; pa.counts = counts;
-  pa.batch = batch; pa.n_max = n_max; pa.tie_break = tie_break; pa.W32 = W32;
-  pa.theta = theta;
-  pa.rec = ws + L.rec;
-  pa.perm = reinterpret_cast<int32_t*>(ws + L.perm);
-  pa.lim = reinterpret_cast<int32_t*>(ws + L.lim);
-  pa.supp = reinterpret_cast<uint32_t*>(ws + L.supp);
-  pa.meta = reinterpret_cast<FrameMeta*>(ws + L.meta);
-  pa.sk_scratch = L.sk ? reinterpret_cast<uint64_t*>(ws + L.sk) : nullptr;
-  pa.idx_scratch = L.idx ? reinterpret_cast<int32_t*>(ws + L.idx) : nullptr;
-
+  // ---- sorted pipeline: prep+sort -> map -> compact, per frame chunk --------------------
+  // Large batches are cut into chunks whose sort runs on an internal side stream while the
+  // previous chunk's map runs on the caller's stream, so the sort hides behind the map.
+  const MapShape ms = choose_map_shape(batch, n_max);
+  int chunks = 1;
+  if (!events && n_max <= kSortMax && batch >= 512) {
+    chunks = std::max(1, std::min(32, env_int("PNMS_OVERLAP_CHUNKS", 1)));
+    chunks = std::min(chunks, batch / 64 > 0 ? batch / 64 : 1);
+  }
+  SideStream* side = chunks > 1 ? side_stream() : nullptr;
+  if (!side) chunks = 1;
+  if (chunks > 1) {
+    if ((e = cudaEventRecord(side->fork, st)) != cudaSuccess) return fail_cuda(e);
+    if ((e = cudaStreamWaitEvent(side->s, side->fork, 0)) != cudaSuccess) return fail_cuda(e);
+  }
   if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
-  if (n_max <= kSortMax) {
-    pa.npad = (n_max + kSortThreads - 1) / kSortThreads * kSortThreads;
-    pa.nchunks = 1;
-    const size_t smem = sort_frame_smem_bytes(pa.npad);
-    if ((e = ensure_smem(pnms_prep_sort_frame, smem, g_sort_frame_smem)) != cudaSuccess) return fail_cuda(e);
-    pnms_prep_sort_frame<<<batch, kSortThreads, smem, st>>>(pa);
-    if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
-  } else {
-    pa.npad = kSortMax;
-    pa.nchunks = (n_max + kSortMax - 1) / kSortMax;
-    if ((e = cudaMemsetAsync(pa.meta, 0, sizeof(FrameMeta) * (size_t)batch, st)) != cudaSuccess) return fail_cuda(e);
-    const size_t smem = sort_smem_bytes(kSortMax);
-    if ((e = ensure_smem(pnms_prep_sort_chunk, smem, g_sort_chunk_smem)) != cudaSuccess) return fail_cuda(e);
-    pnms_prep_sort_chunk<<<(unsigned)((long long)batch * pa.nchunks), kSortThreads, smem, st>>>(pa);
-    if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
-    const long long blocks = (long long)batch * ((n_max + 255) / 256);
-    pnms_merge_rank<<<(unsigned)blocks, 256, 0, st>>>(pa);
+  for (int c = 0; c < chunks; ++c) {
+    const int f0 = (int)((long long)batch * c / chunks), f1 = (int)((long long)batch * (c + 1) / chunks);
+    const int nf = f1 - f0;
+    if (nf <= 0) continue;
+    const size_t fo = (size_t)f0 * n_max;
+    cudaStream_t sort_st = chunks > 1 ? side->s : st;
+    PrepArgs pa;
+    pa.x = x + fo; pa.y = y + fo; pa.z = z + fo; pa.s = s + fo; pa.counts = counts ? counts + f0 : nullptr;
+    pa.batch = nf; pa.n_max = n_max; pa.tie_break = tie_break; pa.W32 = W32;
+    pa.theta = theta;
+    pa.rec = ws + L.rec + fo * kRecBytes;
+    pa.perm = reinterpret_cast<int32_t*>(ws + L.perm) + fo;
+    pa.lim = reinterpret_cast<int32_t*>(ws + L.lim) + fo;
+    pa.supp = reinterpret_cast<uint32_t*>(ws + L.supp) + (size_t)f0 * W32;
+    pa.meta = reinterpret_cast<FrameMeta*>(ws + L.meta) + f0;
+    pa.sk_scratch = L.sk ? reinterpret_cast<uint64_t*>(ws + L.sk) + fo : nullptr;
+    pa.idx_scratch = L.idx ? reinterpret_cast<int32_t*>(ws + L.idx) + fo : nullptr;
+
+    if (n_max <= kSortMax) {
+      pa.npad = (n_max + kSortThreads - 1) / kSortThreads * kSortThreads;
+      pa.nchunks = 1;
+      const size_t smem = sort_frame_smem_bytes(pa.npad);
+      if ((e = ensure_smem(pnms_prep_sort_frame, smem, g_sort_frame_smem)) != cudaSuccess) return fail_cuda(e);
+      pnms_prep_sort_frame<<<nf, kSortThreads, smem, sort_st>>>(pa);
+      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
+    } else {
+      pa.npad = kSortMax;
+      pa.nchunks = (n_max + kSortMax - 1) / kSortMax;
+      if ((e = cudaMemsetAsync(pa.meta, 0, sizeof(FrameMeta) * (size_t)nf, sort_st)) != cudaSuccess) return fail_cuda(e);
+      const size_t smem = sort_smem_bytes(kSortMax);
+      if ((e = ensure_smem(pnms_prep_sort_chunk, smem, g_sort_chunk_smem)) != cudaSuccess) return fail_cuda(e);
+      pnms_prep_sort_chunk<<<(unsigned)((long long)nf * pa.nchunks), kSortThreads, smem, sort_st>>>(pa);
+      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
+      const long long blocks = (long long)nf * ((n_max + 255) / 256);
+      pnms_merge_rank<<<(unsigned)blocks, 256, 0, sort_st>>>(pa);
+      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
+    }
+    if (chunks > 1) {
+      if ((e = cudaEventRecord(side->ev[c], side->s)) != cudaSuccess) return fail_cuda(e);
+      if ((e = cudaStreamWaitEvent(st, side->ev[c], 0)) != cudaSuccess) return fail_cuda(e);
+    }
+
+    if ((e = mark(events, 1, st)) != cudaSuccess) return fail_cuda(e);
+    MapArgs ma;
+    ma.rec = pa.rec; ma.lim = pa.lim; ma.supp = pa.supp; ma.meta = pa.meta;
+    ma.batch = nf; ma.n_max = n_max; ma.W32 = W32;
+    ma.rows_per_block = ms.RB;
+    ma.chunk = ms.chunk;
+    ma.n_rb = (n_max + ms.RB - 1) / ms.RB;
+    const int ipf = items_per_frame(n_max, ms.RB, ms.chunk);
+    ma.items_per_frame = ipf;
+    const long long grid = (long long)nf * ipf;
+    if (grid > 0x7FFFFFFFLL) return PNMS_ETOO_LARGE;
+    const size_t map_smem = (size_t)ms.chunk * kRecBytes;
+    if (ms.R == 4) e = launch_map<4>(ma, grid, map_smem, st);
+    else if (ms.R == 2) e = launch_map<2>(ma, grid, map_smem, st);
+    else e = launch_map<1>(ma, grid, map_smem, st);
+    if (e != cudaSuccess) return fail_cuda(e);
+
+    if ((e = mark(events, 2, st)) != cudaSuccess) return fail_cuda(e);
+    CompactArgs ca;
+    ca.s = pa.s; ca.counts = pa.counts; ca.perm = pa.perm; ca.supp = pa.supp; ca.meta = pa.meta;
+    ca.batch = nf; ca.n_max = n_max; ca.W32 = W32; ca.d_max = d_max; ca.tie_break = tie_break;
+    ca.keep_idx = keep_idx ? keep_idx + fo : nullptr;
+    ca.keep_count = keep_count ? keep_count + f0 : nullptr;
+    ca.keep_mask = keep_mask ? keep_mask + (size_t)f0 * W32 : nullptr;
+    ca.gate_pairs = gate_pairs ? reinterpret_cast<unsigned long long*>(gate_pairs) + f0 : nullptr;
+    const size_t csmem = ((size_t)W32 + 3) / 4 * 16 + 64 * 4;
+    if ((e = ensure_smem(pnms_compact, csmem, g_compact_smem)) != cudaSuccess) return fail_cuda(e);
+    pnms_compact<<<nf, kCompactThreads, csmem, st>>>(ca);
     if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
   }
-
-  if ((e = mark(events, 1, st)) != cudaSuccess) return fail_cuda(e);
-  const MapShape ms = choose_map_shape(batch, n_max);
-  MapArgs ma;
-  ma.rec = pa.rec; ma.lim = pa.lim; ma.supp = pa.supp; ma.meta = pa.meta;
-  ma.batch = batch; ma.n_max = n_max; ma.W32 = W32;
-  ma.rows_per_block = ms.RB;
-  ma.chunk = ms.chunk;
-  ma.n_rb = (n_max + ms.RB - 1) / ms.RB;
-  const int ipf = items_per_frame(n_max, ms.RB, ms.chunk);
-  ma.items_per_frame = ipf;
-  const long long grid = (long long)batch * ipf;
-  if (grid > 0x7FFFFFFFLL) return PNMS_ETOO_LARGE;
-  const size_t map_smem = (size_t)ms.chunk * kRecBytes;
-  if (ms.R == 4) e = launch_map<4>(ma, grid, map_smem, st);
-  else if (ms.R == 2) e = launch_map<2>(ma, grid, map_smem, st);
-  else e = launch_map<1>(ma, grid, map_smem, st);
-  if (e != cudaSuccess) return fail_cuda(e);
-
-  if ((e = mark(events, 2, st)) != cudaSuccess) return fail_cuda(e);
-  CompactArgs ca;
-  ca.s = s; ca.counts = counts; ca.perm = pa.perm; ca.supp = pa.supp; ca.meta = pa.meta;
-  ca.batch = batch; ca.n_max = n_max; ca.W32 = W32; ca.d_max = d_max; ca.tie_break = tie_break;
-  ca.keep_idx = keep_idx; ca.keep_count = keep_count; ca.keep_mask = keep_mask;
-  ca.gate_pairs = reinterpret_cast<unsigned long long*>(gate_pairs);
-  const size_t csmem = ((size_t)W32 + 3) / 4 * 16 + 64 * 4;
-  if ((e = ensure_smem(pnms_compact, csmem, g_compact_smem)) != cudaSuccess) return fail_cuda(e);
-  pnms_compact<<<batch, kCompactThreads, csmem, st>>>(ca);
-  if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
   if ((e = mark(events, 3, st)) != cudaSuccess) return fail_cuda(e);
   return PNMS_OK;
 }

@@ -23,7 +23,7 @@
 namespace pnms {
 
 constexpr int kSmallThreads = 128;
-constexpr int kSmallRows = 4;          // rows per thread: a row tile is 512 rows
+constexpr int kSmallRowsMax = 4;       // rows per thread (1 for the tiniest calls, else 4)
 // Persistent scratch at the start of every workspace (zero before the first call, left zero
 // by every call): suppression words, per-frame tickets and gate accumulators.
 constexpr int kSmallMaxWords = 4096;
@@ -47,14 +47,13 @@ struct SmallArgs {
   unsigned long long* gate_pairs;
 };
 
-template <bool BY_INDEX, bool COUNT>
+template <bool BY_INDEX, bool COUNT, int R>
 __global__ void __launch_bounds__(kSmallThreads) pnms_small_kernel(SmallArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_mode;
   __shared__ unsigned int s_last;
   __shared__ unsigned long long s_gate;
   __shared__ uint32_t s_scan[kSmallThreads / 32 + 1];
-  constexpr int R = kSmallRows;
   const int items = a.n_rt * a.n_ct;
   const int f = blockIdx.x / items;
   const int it = blockIdx.x % items;

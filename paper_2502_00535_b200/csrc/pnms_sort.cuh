@@ -194,28 +194,54 @@ constexpr int kBucketMaxLoad = 64;  // larger buckets fall back to the radix sor
 // order of those two buckets is irrelevant.  Returns false (input untouched) when a real
 // bucket holds more than kBucketMaxLoad slots — the caller then runs block_sort_keys.
 // scratch: cnt_s needs nb + 2 words, off_s nb + 3 words.
-__device__ __forceinline__ int bucket_of(uint64_t sk, int e, int cnt, uint64_t kmin, int shift, int nb) {
-  if (e >= cnt) return nb + 1;
-  if (sk == kNanSortKey) return nb;
-  return (int)((sk - kmin) >> shift);
+// Inverse of sort_key for non-NaN keys (canonical +0.0 for zero).
+__device__ __forceinline__ double key_to_score(uint64_t sk) {
+  const uint64_t key = ~sk;
+  const uint64_t b = (key >> 63) ? (key & 0x7FFFFFFFFFFFFFFFull) : ~key;
+  return __longlong_as_double((long long)b);
 }
+
+// Bucket of a slot.  With a finite score range the buckets split [smax, smin] linearly in
+// score VALUE (ascending sort key = descending score); otherwise linearly in key bits.
+// Both maps are monotone non-decreasing in the key, which is all exactness needs.
+struct BucketMap {
+  uint64_t kmin;
+  int shift;       // key-bit map
+  double smax, scale;  // value map (scale <= 0: use the key-bit map)
+  int nb;
+  __device__ __forceinline__ int operator()(uint64_t sk, int e, int cnt) const {
+    if (e >= cnt) return nb + 1;
+    if (sk == kNanSortKey) return nb;
+    if (scale > 0.0) {
+      const double t = __dmul_rn(__dsub_rn(smax, key_to_score(sk)), scale);
+      return min(nb - 1, (int)t);
+    }
+    return (int)((sk - kmin) >> shift);
+  }
+};
 
 __device__ bool block_bucket_sort(uint64_t** k, uint16_t** id, uint64_t* k2, uint16_t* id2, uint32_t* cnt_s,
                                   uint32_t* off_s, uint32_t* scan_tmp, int npad, int cnt, uint64_t kmin,
                                   uint64_t kmax, int nb) {
   uint64_t* ka = *k;
   uint16_t* ia = *id;
-  const uint64_t range = kmax - kmin;
-  int shift = 0;
+  BucketMap bm;
+  bm.nb = nb;
+  bm.kmin = kmin;
   {
+    const uint64_t range = kmax - kmin;
     const int bits = range ? 64 - __clzll((long long)range) : 0;  // bits needed for the range
     const int nb_bits = 31 - __clz(nb);
-    shift = bits > nb_bits ? bits - nb_bits : 0;
+    bm.shift = bits > nb_bits ? bits - nb_bits : 0;
+    const double smax = key_to_score(kmin), smin = key_to_score(kmax);
+    const double span = smax - smin;
+    bm.smax = smax;
+    bm.scale = (isfinite(smax) && isfinite(smin) && span > 0.0 && isfinite(span)) ? (double)nb / span : -1.0;
   }
   const int nbk = nb + 2;  // real buckets + NaN bucket + padding bucket
   for (int b = threadIdx.x; b < nbk; b += kSortThreads) cnt_s[b] = 0u;
   __syncthreads();
-  for (int e = threadIdx.x; e < npad; e += kSortThreads) atomicAdd(&cnt_s[bucket_of(ka[e], e, cnt, kmin, shift, nb)], 1u);
+  for (int e = threadIdx.x; e < npad; e += kSortThreads) atomicAdd(&cnt_s[bm(ka[e], e, cnt)], 1u);
   __syncthreads();
   // exclusive scan of the counts; also the largest real bucket
   const int per = (nbk + kSortThreads - 1) / kSortThreads;
@@ -250,7 +276,7 @@ __device__ bool block_bucket_sort(uint64_t** k, uint16_t** id, uint64_t* k2, uin
   __syncthreads();
   for (int e = threadIdx.x; e < npad; e += kSortThreads) {
     const uint64_t sk = ka[e];
-    const uint32_t pos = atomicAdd(&cnt_s[bucket_of(sk, e, cnt, kmin, shift, nb)], 1u);
+    const uint32_t pos = atomicAdd(&cnt_s[bm(sk, e, cnt)], 1u);
     k2[pos] = sk;
     id2[pos] = ia[e];
   }
@@ -261,7 +287,7 @@ __device__ bool block_bucket_sort(uint64_t** k, uint16_t** id, uint64_t* k2, uin
     const uint16_t me = id2[p];
     int dst = p;
     if (p < cnt && sk != kNanSortKey) {
-      const int b = (int)((sk - kmin) >> shift);
+      const int b = bm(sk, 0, 1);
       const int bs = (int)off_s[b], be = (int)off_s[b + 1];
       int rank = 0;
       for (int q = bs; q < be; ++q) {

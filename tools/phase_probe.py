@@ -37,9 +37,21 @@ def probe(name, arrs, iters=30):
         if it >= 3:
             res.append([ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3]),
                         ev[0].elapsed_time(ev[3])])
+    plain = []
+    for it in range(iters + 3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(200_000)
+        a.record(st)
+        rc = lib.pnms_run(x.data_ptr(), y.data_ptr(), z.data_ptr(), s.data_ptr(), None, B, n, n, 0.5, 0,
+                          ki.data_ptr(), kc.data_ptr(), None, None, ws.data_ptr(), ws.numel(), st.cuda_stream)
+        _lib.check(rc, "run")
+        b.record(st)
+        torch.cuda.synchronize()
+        if it >= 3:
+            plain.append(a.elapsed_time(b) * 1e3)
     med = [statistics.median(r[i] for r in res) * 1e3 for i in range(4)]
     print(f"{name:16s} B={B:5d} n={n:6d}  sort {med[0]:9.1f} us  map {med[1]:9.1f} us  compact {med[2]:8.1f} us"
-          f"  total {med[3]:9.1f} us", flush=True)
+          f"  total {med[3]:9.1f} us  | plain call {statistics.median(plain):9.1f} us", flush=True)
 
 
 if __name__ == "__main__":
