@@ -111,6 +111,10 @@ int pnms_map_reference_layout(const int32_t* x, const int32_t* y, const int32_t*
  *  mask  uint8 [ceil(d_max/8)]  packed little-endian (SurvivorMask.bits, engine.py:120-122) */
 int pnms_reduce_rows(const uint64_t* bits, int d_max, int k, uint8_t* mask, void* stream);
 
+/* Diagnostics: device counter (uint64) that the binned path atomically increments by the
+ * number of pair tests it executes; NULL disables (default).  Process-wide, not reentrant. */
+int pnms_debug_count_pairs(uint64_t* device_counter);
+
 /* Human-readable text for a pnms_status. */
 const char* pnms_strerror(int status);
 

@@ -18,6 +18,7 @@
 #include "pnms_map.cuh"
 #include "pnms_reflayout.cuh"
 #include "pnms_small.cuh"
+#include "pnms_binned.cuh"
 #include "pnms_sort.cuh"
 
 using namespace pnms;
@@ -25,11 +26,12 @@ using namespace pnms;
 namespace {
 
 thread_local int g_last_cuda_error = 0;
+unsigned long long* g_pairs_counter = nullptr;  // diagnostics: binned pair tests (pnms_debug_pairs_counter)
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Layout {
-  size_t rec, perm, lim, supp, meta, sk, idx, total;
+  size_t rec, perm, lim, supp, meta, sk, idx, dense, total;
 };
 
 Layout make_layout(int batch, int n_max) {
@@ -42,6 +44,7 @@ Layout make_layout(int batch, int n_max) {
   L.lim = off;  off = align_up(off + B * N * 4, 256);
   L.supp = off; off = align_up(off + B * W32 * 4, 256);
   L.meta = off; off = align_up(off + B * sizeof(FrameMeta), 256);
+  L.dense = off; off = align_up(off + B, 256);
   if (n_max > kSortMax) {
     L.sk = off;  off = align_up(off + B * N * 8, 256);
     L.idx = off; off = align_up(off + B * N * 4, 256);
@@ -96,6 +99,7 @@ SideStream* side_stream() {
   return &ss;
 }
 std::atomic<size_t> g_small_smem[8];
+std::atomic<size_t> g_binned_smem[2];
 
 template <bool B, bool C, int R>
 cudaError_t launch_small_t(const SmallArgs& sa, long long grid, size_t smem, cudaStream_t st, std::atomic<size_t>& cfg) {
@@ -188,6 +192,11 @@ const char* pnms_strerror(int status) {
   }
 }
 
+int pnms_debug_count_pairs(uint64_t* device_counter) {
+  g_pairs_counter = reinterpret_cast<unsigned long long*>(device_counter);
+  return PNMS_OK;
+}
+
 int pnms_workspace_init(void* workspace, size_t workspace_bytes, void* stream) {
   if (!workspace || workspace_bytes < kSmallScratchBytes) return PNMS_EWORKSPACE;
   cudaError_t e = cudaMemsetAsync(workspace, 0, kSmallScratchBytes, (cudaStream_t)stream);
@@ -273,6 +282,37 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     return PNMS_OK;
   }
 
+  // ---- binned path (sparse frames): exact, one CTA per frame; declined frames fall through
+  // to the dense pipeline below, which then only processes those frames.
+  const uint8_t* dense_flags = nullptr;
+  void* ev_local[4];
+  const long long algo = env_ll("PNMS_ALGO", 0);  // 0 auto, 1 dense only
+  if (algo == 0 && gate_pairs == nullptr && n_max <= kBinMaxSlots) {
+    BinArgs ba;
+    ba.x = x; ba.y = y; ba.z = z; ba.s = s; ba.counts = counts;
+    ba.batch = batch; ba.n_max = n_max; ba.d_max = d_max; ba.tie_break = tie_break; ba.W32 = W32;
+    ba.theta = theta;
+    ba.fallback = ws + L.dense;
+    ba.keep_idx = keep_idx; ba.keep_count = keep_count; ba.keep_mask = keep_mask;
+    ba.pairs_tested = g_pairs_counter;
+    const size_t smem = binned_smem_bytes(binned_npad(n_max));
+    if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
+    if (tie_break == PNMS_TIE_BY_INDEX) {
+      if ((e = ensure_smem(pnms_binned_frame<true>, smem, g_binned_smem[1])) != cudaSuccess) return fail_cuda(e);
+      pnms_binned_frame<true><<<batch, kBinThreads, smem, st>>>(ba);
+    } else {
+      if ((e = ensure_smem(pnms_binned_frame<false>, smem, g_binned_smem[0])) != cudaSuccess) return fail_cuda(e);
+      pnms_binned_frame<false><<<batch, kBinThreads, smem, st>>>(ba);
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
+    dense_flags = ws + L.dense;
+    if (events) {
+      // phases become: [0,1) binned kernel, [1,2) dense prep of declined frames, [2,3) their map+compact
+      ev_local[0] = events[1]; ev_local[1] = events[2]; ev_local[2] = nullptr; ev_local[3] = events[3];
+      events = ev_local;
+    }
+  }
+
   // ---- sorted pipeline: prep+sort -> map -> compact, per frame chunk --------------------
   // Large batches are cut into chunks whose sort runs on an internal side stream while the
   // previous chunk's map runs on the caller's stream, so the sort hides behind the map.
@@ -306,6 +346,7 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     pa.meta = reinterpret_cast<FrameMeta*>(ws + L.meta) + f0;
     pa.sk_scratch = L.sk ? reinterpret_cast<uint64_t*>(ws + L.sk) + fo : nullptr;
     pa.idx_scratch = L.idx ? reinterpret_cast<int32_t*>(ws + L.idx) + fo : nullptr;
+    pa.dense = dense_flags ? dense_flags + f0 : nullptr;
 
     if (n_max <= kSortMax) {
       pa.npad = (n_max + kSortThreads - 1) / kSortThreads * kSortThreads;
@@ -340,6 +381,7 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     ma.n_rb = (n_max + ms.RB - 1) / ms.RB;
     const int ipf = items_per_frame(n_max, ms.RB, ms.chunk);
     ma.items_per_frame = ipf;
+    ma.dense = pa.dense;
     const long long grid = (long long)nf * ipf;
     if (grid > 0x7FFFFFFFLL) return PNMS_ETOO_LARGE;
     const size_t map_smem = (size_t)ms.chunk * kRecBytes;
@@ -356,6 +398,7 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     ca.keep_count = keep_count ? keep_count + f0 : nullptr;
     ca.keep_mask = keep_mask ? keep_mask + (size_t)f0 * W32 : nullptr;
     ca.gate_pairs = gate_pairs ? reinterpret_cast<unsigned long long*>(gate_pairs) + f0 : nullptr;
+    ca.dense = pa.dense;
     const size_t csmem = ((size_t)W32 + 3) / 4 * 16 + 64 * 4;
     if ((e = ensure_smem(pnms_compact, csmem, g_compact_smem)) != cudaSuccess) return fail_cuda(e);
     pnms_compact<<<nf, kCompactThreads, csmem, st>>>(ca);

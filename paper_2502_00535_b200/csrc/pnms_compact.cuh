@@ -25,6 +25,7 @@ struct CompactArgs {
   int32_t* keep_count;     // may be null
   uint32_t* keep_mask;     // may be null
   unsigned long long* gate_pairs;  // may be null
+  const uint8_t* dense;   // optional [batch]: process frame f only if dense[f] != 0
 };
 
 __global__ void __launch_bounds__(kCompactThreads) pnms_compact(CompactArgs a) {
@@ -32,6 +33,7 @@ __global__ void __launch_bounds__(kCompactThreads) pnms_compact(CompactArgs a) {
   uint32_t* kbits = reinterpret_cast<uint32_t*>(smem_raw);          // [W32] survivor bits, input order
   uint32_t* warp_sums = kbits + ((a.W32 + 3) & ~3);
   const int f = blockIdx.x;
+  if (a.dense && !a.dense[f]) return;
   const long long fbase = (long long)f * a.n_max;
   const int cnt = frame_count(a.counts, f, a.n_max);
   const int P = a.d_max > cnt ? a.d_max - cnt : 0;

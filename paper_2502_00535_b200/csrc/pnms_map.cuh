@@ -40,6 +40,7 @@ struct MapArgs {
   int chunk;            // columns per work item
   int n_rb;             // row blocks per frame
   int items_per_frame;
+  const uint8_t* dense;   // optional [batch]: process frame f only if dense[f] != 0
 };
 
 // number of column chunks of row block rb: its rows' limits are < (rb+1)*RB
@@ -195,6 +196,7 @@ __global__ void __launch_bounds__(kMapWarps * 32) pnms_map_kernel(MapArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bar;
   const int f = blockIdx.x / a.items_per_frame;
+  if (a.dense && !a.dense[f]) return;
   int item = blockIdx.x % a.items_per_frame;
   const int RB = a.rows_per_block;
   int rb = a.n_rb - 1;

@@ -34,7 +34,10 @@ struct PrepArgs {
   FrameMeta* meta;    // [batch]
   uint64_t* sk_scratch;   // chunk mode: sorted keys   [batch][n_max]
   int32_t* idx_scratch;   // chunk mode: sorted index  [batch][n_max]
+  const uint8_t* dense;   // optional [batch]: process frame f only if dense[f] != 0
 };
+
+__device__ __forceinline__ bool frame_skipped(const uint8_t* dense, int f) { return dense && !dense[f]; }
 
 __device__ __forceinline__ int frame_count(const int32_t* counts, int f, int n_max) {
   int c = counts ? counts[f] : n_max;
@@ -423,6 +426,7 @@ __device__ __forceinline__ void init_stats(LoadStats* st, unsigned long long* li
 __global__ void __launch_bounds__(kSortThreads) pnms_prep_sort_frame(PrepArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int f = blockIdx.x;
+  if (frame_skipped(a.dense, f)) return;
   const long long fbase = (long long)f * a.n_max;
   const int cnt = frame_count(a.counts, f, a.n_max);
   SortSmem m = carve_sort_smem(smem_raw, a.npad);
@@ -490,6 +494,7 @@ __global__ void __launch_bounds__(kSortThreads) pnms_prep_sort_frame(PrepArgs a)
 __global__ void __launch_bounds__(kSortThreads) pnms_prep_sort_chunk(PrepArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int f = blockIdx.x / a.nchunks, c = blockIdx.x % a.nchunks;
+  if (frame_skipped(a.dense, f)) return;
   const long long fbase = (long long)f * a.n_max;
   const int cnt = frame_count(a.counts, f, a.n_max);
   const int e0 = c * kSortMax;
@@ -526,6 +531,7 @@ __global__ void __launch_bounds__(kSortThreads) pnms_prep_sort_chunk(PrepArgs a)
 __global__ void __launch_bounds__(256) pnms_merge_rank(PrepArgs a) {
   const int blocks_per_frame = (a.n_max + 255) / 256;
   const int f = blockIdx.x / blocks_per_frame;
+  if (frame_skipped(a.dense, f)) return;
   const int e = (blockIdx.x % blocks_per_frame) * 256 + threadIdx.x;
   const long long fbase = (long long)f * a.n_max;
   const int cnt = frame_count(a.counts, f, a.n_max);

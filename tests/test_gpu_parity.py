@@ -18,10 +18,12 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda"
 
 
-@pytest.fixture(params=["small", "pipeline"])
+@pytest.fixture(params=["small", "binned", "dense"])
 def path(request, monkeypatch):
-    """Run a test through the single-launch unsorted path and through the sorted pipeline."""
+    """Run a test through each device path: the single-launch unsorted kernel, the binned
+    kernel (with the dense pipeline for the frames it declines), and the dense pipeline only."""
     monkeypatch.setenv("PNMS_SMALL_PAIRS", str(1 << 40) if request.param == "small" else "0")
+    monkeypatch.setenv("PNMS_ALGO", "1" if request.param == "dense" else "0")
     return request.param
 
 
@@ -121,6 +123,37 @@ def _run_batch(x, y, z, s, counts, theta, tie, d_max=None):
     ki, kc = batched_nms_keep(t(x), t(y), t(z), t(s), t(counts), theta, tie, d_max)
     ki, kc = ki.cpu().numpy(), kc.cpu().numpy()
     return [ki[f, : kc[f]] for f in range(x.shape[0])]
+
+
+def test_binned_mixed_batch_vs_oracle(monkeypatch):
+    """A batch where the binned kernel takes some frames and declines others (z > 126, a
+    zero side, a crowded cell, NaN scores, theta-independent ties) — all must be exact."""
+    monkeypatch.setenv("PNMS_SMALL_PAIRS", "0")
+    monkeypatch.setenv("PNMS_ALGO", "0")
+    from paper_2502_00535_b200 import _lib
+
+    x, y, z, s = random_frames(12, 900, seed=123, frame_w=800, frame_h=600, z_range=(4, 60), duplicate_fraction=0.1)
+    z[1, 5] = 200                        # narrow16 frame -> declined
+    z[2, 7] = 0                          # zero side: T = 0 column -> declined
+    x[3, :300] = 10; y[3, :300] = 10     # 300 boxes in one cell -> declined
+    s[4, ::4] = np.nan                   # NaN rows/columns (binned)
+    s[5, ::3] = 0.5                      # exact score ties (binned)
+    x[6] = np.minimum(x[6], 5); y[6] = np.minimum(y[6], 5)   # dense crowd -> declined
+    counts = np.full(12, 900, np.int32)
+    counts[7] = 1
+    counts[8] = 0
+    counter = torch.zeros(1, dtype=torch.int64, device=DEV)
+    _lib.load().pnms_debug_count_pairs(counter.data_ptr())
+    try:
+        for tie in ("paper_faithful", "by_index"):
+            for theta in (0.3, 0.5, 1.0):
+                got = _run_batch(x, y, z, s, counts, theta, tie, 950)
+                for f in range(12):
+                    want = c_oracle.run_frame(x[f], y[f], z[f], s[f], int(counts[f]), 950, theta, tie)
+                    assert np.array_equal(got[f], want), (f, tie, theta)
+    finally:
+        _lib.load().pnms_debug_count_pairs(None)
+    assert int(counter.item()) > 0  # the binned kernel did run
 
 
 def test_c4_full_batch_vs_oracle():
