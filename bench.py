@@ -164,7 +164,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            self._stop.wait(0.02)
+            self._stop.wait(0.005)
 
     def __enter__(self):
         if self.nv:
@@ -219,7 +219,7 @@ def latency_suite(torch, dev, iters: int = 50):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -243,13 +243,21 @@ def main():
 
     from paper_2502_00535_b200 import NmsEngine, _lib
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ndev = torch.cuda.device_count()
+    dev_index = local % max(ndev, 1)
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        # NCCL over NVLink/NVSwitch; PNMS_DIST_BACKEND=gloo lets several ranks share one GPU
+        # (used to exercise the multi-rank path on a single-GPU box)
+        backend = os.environ.get("PNMS_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     x, y, z, s = shard
     F = x.shape[0]
     dx, dy, dz, ds = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (x, y, z, s))
@@ -266,34 +274,51 @@ def main():
                                    eng.ws_full.numel(), stream.cuda_stream, handles)
         _lib.check(st, "pnms_run_profiled")
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize(dev)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
-    for row in evs:
-        for e in row:
-            e.record(stream)  # materialise the handles
-    torch.cuda.synchronize(dev)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clk:
-        for k in range(args.steps):
-            flush.zero_()  # L2 flush between timed steps (outside the events)
-            step(evs[k])
+    def timed(algo: str):
+        """Warm-up + K profiled steps with PNMS_ALGO=algo; returns per-step phase times (ms)."""
+        os.environ["PNMS_ALGO"] = algo
+        for _ in range(args.warmup):
+            step()
         torch.cuda.synchronize(dev)
-    if dist:
-        dist.barrier()
-    step_ms = [r[0].elapsed_time(r[3]) for r in evs]
-    map_ms = [r[1].elapsed_time(r[2]) for r in evs]
-    sort_ms = [r[0].elapsed_time(r[1]) for r in evs]
-    compact_ms = [r[2].elapsed_time(r[3]) for r in evs]
-    total_ms = sum(step_ms)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_total_ms = float(t.item())
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+        for row in evs:
+            for e in row:
+                e.record(stream)  # materialise the handles
+        torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        with ClockSampler(dev_index) as clk:
+            for k in range(args.steps):
+                flush.zero_()  # L2 flush between timed steps (outside the events)
+                step(evs[k])
+            torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+        ph = [[r[0].elapsed_time(r[1]), r[1].elapsed_time(r[2]), r[2].elapsed_time(r[3]), r[0].elapsed_time(r[3])]
+              for r in evs]
+        total_ms = sum(p[3] for p in ph)
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        if dist:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return ph, float(t.item()), clk
+
+    # headline: the default algorithm (binned kernel; declined frames fall back to dense)
+    ph, max_total_ms, clk = timed("0")
     value = FRAMES * args.steps / (max_total_ms / 1e3)
+    binned_ms = [p[0] for p in ph]
+    fallback_ms = [p[1] + p[2] for p in ph]
+    # dense sorted pipeline on the same workload (roofline of the N x N map kernel)
+    ph_d, max_total_d, clk_d = timed("1")
+    value_dense = FRAMES * args.steps / (max_total_d / 1e3)
+    os.environ["PNMS_ALGO"] = "0"
+    # executed pair tests of the binned kernel (one extra untimed step)
+    counter = torch.zeros(1, dtype=torch.int64, device=dev)
+    lib.pnms_debug_count_pairs(counter.data_ptr())
+    step()
+    torch.cuda.synchronize(dev)
+    lib.pnms_debug_count_pairs(None)
+    pairs_executed = int(counter.item())
 
     # ---- end to end through the public API: pinned host in -> pinned host out
     hx, hy, hz, hs = (torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in (x, y, z, s))
@@ -346,33 +371,49 @@ def main():
         clocks = clk.summary()
         props = torch.cuda.get_device_properties(dev)
         sm_mhz = clocks["sm_mhz"] or clocks["sm_max_mhz"] or 1965
-        ops = 4.0 * BOXES * (BOXES - 1) * F  # 8 int ops per unordered pair
-        map_s = statistics.mean(map_ms) / 1e3
-        achieved = ops / map_s / 1e12
-        peak = props.multi_processor_count * 128 * sm_mhz * 1e6 / 1e12
-        traffic = None
-        prof = ROOT / "profiles" / "map_kernel_ncu.json"
-        if prof.exists():
-            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        sms = props.multi_processor_count
+        ops = 4.0 * BOXES * (BOXES - 1) * F  # 8 int ops per unordered pair, dense basis
+        peak = sms * 128 * sm_mhz * 1e6 / 1e12
+        peak_basis = f"{sms} SMs x 128 int lanes x {sm_mhz} MHz (median SM clock sampled during the timed region)"
+
+        def prof(name):
+            f = ROOT / "profiles" / name
+            return json.loads(f.read_text()).get("dram_bytes_per_launch") if f.exists() else None
+
+        b_s = statistics.mean(binned_ms) / 1e3
+        achieved = ops / b_s / 1e12
+        map_d = statistics.mean(p[1] for p in ph_d) / 1e3
+        achieved_d = ops / map_d / 1e12
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": WORKLOAD, "frames": FRAMES, "frames_per_gpu": F, "boxes_per_frame": BOXES,
                        "theta": THETA, "tie_break": TIE, "parallelism": f"frames sharded over {world} GPU(s)",
+                       "algorithm": "binned (exact spatial culling) with dense fallback",
                        "l2": "flushed (256 MiB write) between timed steps"},
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": int(F * BOXES * 20 + F * 4),
                     "d2h_bytes_per_step": int(F * eng.W32 * 4 + F * 4), "matches_device_run": ok},
-            "gpu_launches": 3 * args.steps,
+            "gpu_launches": 4 * args.steps,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "pnms_map_kernel<4>", "ops_per_launch": ops,
-                         "peak_basis": f"{props.multi_processor_count} SMs x 128 int lanes x {sm_mhz} MHz "
-                                       "(median SM clock sampled during the timed region)"},
-            "phase_ms": {"sort": statistics.mean(sort_ms), "map": statistics.mean(map_ms),
-                         "compact": statistics.mean(compact_ms)},
+                         "frac": achieved / peak, "traffic": prof("binned_kernel_ncu.json"),
+                         "kernel": "pnms_binned_frame", "ops_per_launch": ops, "basis": "dense-equivalent ops "
+                         "(BASELINE.md §4); the binned kernel culls pairs that cannot overlap",
+                         "pair_tests_executed_per_launch": pairs_executed,
+                         "pair_tests_dense_per_launch": int(BOXES * (BOXES - 1) // 2 * F),
+                         "peak_basis": peak_basis},
+            "phase_ms": {"binned": statistics.mean(binned_ms), "dense_fallback": statistics.mean(fallback_ms)},
+            "dense_path": {"value": value_dense, "unit": "frames/s", "ms_per_step": max_total_d / args.steps,
+                           "phase_ms": {"sort": statistics.mean(p[0] for p in ph_d),
+                                        "map": statistics.mean(p[1] for p in ph_d),
+                                        "compact": statistics.mean(p[2] for p in ph_d)},
+                           "roofline": {"bound": "alu", "achieved": achieved_d, "peak": peak, "unit": "Tops/s",
+                                        "frac": achieved_d / peak, "traffic": prof("map_kernel_ncu.json"),
+                                        "kernel": "pnms_map_kernel<4>", "ops_per_launch": ops},
+                           "gpu_launches": 3 * args.steps},
             "cpu_baseline": cpu,
             "clocks": clocks,
+            "clocks_dense_run": clk_d.summary(),
         }
         if lat:
             line["latency_us"] = lat

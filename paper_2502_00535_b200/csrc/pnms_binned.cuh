@@ -190,40 +190,45 @@ __global__ void __launch_bounds__(kBinThreads) pnms_binned_frame(BinArgs a) {
     }
   }
   __syncthreads();
-  // ---- scan: each valid box against the gate-passing prefix of its 3x3 neighbour cells
+  // ---- scan: each valid box against the gate-passing prefix of its neighbour cells.  Rows
+  // are taken in cell order so a warp's lanes walk the same few cell lists (broadcast reads,
+  // similar trip counts).  A row only visits the cells its own extent can reach: a column j
+  // overlapping row i has x_j in [x_i - max_z, x_i + z_i] (and the same for y).
   unsigned long long tested = 0;
-  for (int i = threadIdx.x; i < cnt; i += kBinThreads) {
+  const int maxz = st->maxz;
+  const bool pad_rule = a.d_max > cnt;
+  for (int p = threadIdx.x; p < st->n_act; p += kBinThreads) {
+    const int i = list[p];
     const uint64_t ki = key[i];
+    const RecNarrow ri = rec[i];
+    const int32_t ix = a.x[fbase + i], iy = a.y[fbase + i], iz = a.z[fbase + i];
+    const int lx = ix - maxz - ox, ly = iy - maxz - oy;
+    const int cx0 = lx < 0 ? 0 : lx / S, cy0 = ly < 0 ? 0 : ly / S;
+    const int cx1 = min(GX - 1, (ix + iz - ox) / S), cy1 = min(GY - 1, (iy + iz - oy) / S);
     bool sup = false;
-    if (ki != kNanSortKey) {
-      const RecNarrow ri = rec[i];
-      const int32_t ix = a.x[fbase + i], iy = a.y[fbase + i];
-      const int cx = (ix - ox) / S, cy = (iy - oy) / S;
-      for (int dy = -1; dy <= 1 && !sup; ++dy) {
-        const int yy = cy + dy;
-        if (yy < 0 || yy >= GY) continue;
-        for (int dx = -1; dx <= 1 && !sup; ++dx) {
-          const int xx = cx + dx;
-          if (xx < 0 || xx >= GX) continue;
-          const int c = yy * GX + xx;
-          const int en = cstart[c + 1];
-          for (int p = cstart[c]; p < en; ++p) {
-            const int j = list[p];
-            const uint64_t kj = key[j];
-            const bool gate = kj < ki || (BY_INDEX && kj == ki && j < i);
-            if (!gate) break;
-            ++tested;
-            const RecNarrow rj = rec[j];
-            const uint4 cj = make_uint4(rj.a, rj.nb, rj.zz, (uint32_t)rj.negT);
-            if (pair_d<kNarrow7>(ri.a, ri.nb, ri.zz, cj) >= 0) { sup = true; break; }
-          }
+    for (int yy = cy0; yy <= cy1 && !sup; ++yy) {
+      for (int xx = cx0; xx <= cx1 && !sup; ++xx) {
+        const int c = yy * GX + xx;
+        const int en = cstart[c + 1];
+        for (int q = cstart[c]; q < en; ++q) {
+          const int j = list[q];
+          const uint64_t kj = key[j];
+          const bool gate = kj < ki || (BY_INDEX && kj == ki && j < i);
+          if (!gate) break;
+          ++tested;
+          const RecNarrow rj = rec[j];
+          const uint4 cj = make_uint4(rj.a, rj.nb, rj.zz, (uint32_t)rj.negT);
+          if (pair_d<kNarrow7>(ri.a, ri.nb, ri.zz, cj) >= 0) { sup = true; break; }
         }
       }
     }
-    // survivors: valid rows not suppressed; the implicit padding gate drops s < 0 rows
-    if (!sup && a.d_max > cnt && a.s[fbase + i] < 0.0) sup = true;
+    // implicit padding gate (engine.py:233 with s_j = 0, z_j = 0): rows with s < 0 drop
+    if (!sup && pad_rule && a.s[fbase + i] < 0.0) sup = true;
     if (!sup) atomicOr(&kbits[i >> 5], 1u << (i & 31));
   }
+  // NaN rows pass no gate: always survivors
+  for (int e = threadIdx.x; e < cnt; e += kBinThreads)
+    if (key[e] == kNanSortKey) atomicOr(&kbits[e >> 5], 1u << (e & 31));
   if (a.pairs_tested) {
     tested = __reduce_add_sync(0xFFFFFFFFu, (unsigned)tested);
     if ((threadIdx.x & 31) == 0 && tested) atomicAdd(a.pairs_tested, tested);
