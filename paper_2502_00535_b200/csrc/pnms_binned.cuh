@@ -60,12 +60,13 @@ __global__ void __launch_bounds__(kBinThreads) pnms_binned_frame(BinArgs a) {
   const long long fbase = (long long)f * a.n_max;
   const int cnt = frame_count(a.counts, f, a.n_max);
   const int npad = binned_npad(a.n_max);
-  RecNarrow* rec = reinterpret_cast<RecNarrow*>(smem_raw);                    // [npad]
-  uint64_t* key = reinterpret_cast<uint64_t*>(rec + npad);                    // [npad] sort keys
-  uint16_t* cellof = reinterpret_cast<uint16_t*>(key + npad);                 // [npad]
-  uint16_t* list = cellof + npad;                                             // [npad]
+  // per-box data stored in cell order (positions [cstart[c], cstart[c+1]) = cell c)
+  RecNarrow* recS = reinterpret_cast<RecNarrow*>(smem_raw);                   // [npad] records
+  uint64_t* keyS = reinterpret_cast<uint64_t*>(recS + npad);                  // [npad] sort keys
+  uint16_t* cellof = reinterpret_cast<uint16_t*>(keyS + npad);                // [npad] cell of input slot
+  uint16_t* idxS = cellof + npad;                                             // [npad] input slot
   const int max_cells = binned_max_cells(npad);
-  uint32_t* cstart = reinterpret_cast<uint32_t*>(list + npad);                // [cells+2]
+  uint32_t* cstart = reinterpret_cast<uint32_t*>(idxS + npad);                // [cells+2]
   uint32_t* ccur = cstart + max_cells + 4;                                    // [cells+2]
   uint32_t* kbits = ccur + max_cells + 4;                                     // [npad/32] survivors
   uint32_t* scan_tmp = kbits + npad / 32 + 4;                                 // [64]
@@ -90,13 +91,11 @@ __global__ void __launch_bounds__(kBinThreads) pnms_binned_frame(BinArgs a) {
       const long long g = fbase + e;
       const int32_t xv = a.x[g], yv = a.y[g], zv = a.z[g];
       const uint64_t sk = sort_key(a.s[g]);
-      key[e] = sk;
       const int m = frame_mode_of(xv, yv, zv);
       mode = max(mode, m);
-      if (m == kNarrow7) rec[e] = make_rec_narrow(xv, yv, zv, a.theta, kNarrow7);
       if (sk != kNanSortKey) {
         ++n_act;
-        const int T = (m == kNarrow7) ? (int)((uint32_t)(-rec[e].negT) >> 17) : 0;
+        const int T = (m == kNarrow7) ? (int)((uint32_t)(-make_rec_narrow(xv, yv, zv, a.theta, kNarrow7).negT) >> 17) : 0;
         minT = min(minT, T);
         maxz = max(maxz, zv);
         minx = min(minx, xv); maxx = max(maxx, xv);
@@ -136,7 +135,10 @@ __global__ void __launch_bounds__(kBinThreads) pnms_binned_frame(BinArgs a) {
   for (int c = threadIdx.x; c < cells + 1; c += kBinThreads) cstart[c] = 0u;
   __syncthreads();
   for (int e = threadIdx.x; e < cnt; e += kBinThreads) {
-    if (key[e] == kNanSortKey) continue;  // NaN boxes never suppress and are never suppressed
+    if (a.s[fbase + e] != a.s[fbase + e]) {  // NaN: passes no gate, never suppresses -> survivor
+      atomicOr(&kbits[e >> 5], 1u << (e & 31));
+      continue;
+    }
     const int32_t ex = a.x[fbase + e], ey = a.y[fbase + e];
     const int c = ((ey - oy) / S) * GX + (ex - ox) / S;
     cellof[e] = (uint16_t)c;
@@ -166,27 +168,37 @@ __global__ void __launch_bounds__(kBinThreads) pnms_binned_frame(BinArgs a) {
     if (threadIdx.x == 0) a.fallback[f] = 1;
     return;
   }
+  // scatter records, keys and input slots straight into cell order
   for (int e = threadIdx.x; e < cnt; e += kBinThreads) {
-    if (key[e] == kNanSortKey) continue;
+    const long long g = fbase + e;
+    const double sv = a.s[g];
+    if (sv != sv) continue;
     const uint32_t pos = atomicAdd(&ccur[cellof[e]], 1u);
-    list[pos] = (uint16_t)e;
+    recS[pos] = make_rec_narrow(a.x[g], a.y[g], a.z[g], a.theta, kNarrow7);
+    keyS[pos] = sort_key(sv);
+    idxS[pos] = (uint16_t)e;
   }
   __syncthreads();
   // ---- order every cell by (sort key asc == score desc, index asc): insertion sort
   for (int c = threadIdx.x; c < cells; c += kBinThreads) {
     const int b = cstart[c], en = cstart[c + 1];
     for (int i = b + 1; i < en; ++i) {
-      const uint16_t v = list[i];
-      const uint64_t kv = key[v];
+      const uint64_t kv = keyS[i];
+      const uint16_t v = idxS[i];
+      const RecNarrow rv = recS[i];
       int j = i - 1;
       while (j >= b) {
-        const uint16_t u = list[j];
-        const uint64_t ku = key[u];
+        const uint64_t ku = keyS[j];
+        const uint16_t u = idxS[j];
         if (ku < kv || (ku == kv && u < v)) break;
-        list[j + 1] = u;
+        keyS[j + 1] = ku;
+        idxS[j + 1] = u;
+        recS[j + 1] = recS[j];
         --j;
       }
-      list[j + 1] = v;
+      keyS[j + 1] = kv;
+      idxS[j + 1] = v;
+      recS[j + 1] = rv;
     }
   }
   __syncthreads();
@@ -198,10 +210,12 @@ __global__ void __launch_bounds__(kBinThreads) pnms_binned_frame(BinArgs a) {
   const int maxz = st->maxz;
   const bool pad_rule = a.d_max > cnt;
   for (int p = threadIdx.x; p < st->n_act; p += kBinThreads) {
-    const int i = list[p];
-    const uint64_t ki = key[i];
-    const RecNarrow ri = rec[i];
-    const int32_t ix = a.x[fbase + i], iy = a.y[fbase + i], iz = a.z[fbase + i];
+    const int i = idxS[p];
+    const uint64_t ki = keyS[p];
+    const RecNarrow ri = recS[p];
+    // corner and side back from the packed record: nb = (-x, -y), zz = (z+1, z+1)
+    const int32_t ix = -(int32_t)(int16_t)(ri.nb & 0xFFFFu), iy = -(int32_t)(int16_t)(ri.nb >> 16);
+    const int32_t iz = (int32_t)(ri.zz & 0xFFFFu) - 1;
     const int lx = ix - maxz - ox, ly = iy - maxz - oy;
     const int cx0 = lx < 0 ? 0 : lx / S, cy0 = ly < 0 ? 0 : ly / S;
     const int cx1 = min(GX - 1, (ix + iz - ox) / S), cy1 = min(GY - 1, (iy + iz - oy) / S);
@@ -211,14 +225,15 @@ __global__ void __launch_bounds__(kBinThreads) pnms_binned_frame(BinArgs a) {
         const int c = yy * GX + xx;
         const int en = cstart[c + 1];
         for (int q = cstart[c]; q < en; ++q) {
-          const int j = list[q];
-          const uint64_t kj = key[j];
-          const bool gate = kj < ki || (BY_INDEX && kj == ki && j < i);
+          const uint64_t kj = keyS[q];
+          const bool gate = kj < ki || (BY_INDEX && kj == ki && idxS[q] < i);
           if (!gate) break;
           ++tested;
-          const RecNarrow rj = rec[j];
-          const uint4 cj = make_uint4(rj.a, rj.nb, rj.zz, (uint32_t)rj.negT);
-          if (pair_d<kNarrow7>(ri.a, ri.nb, ri.zz, cj) >= 0) { sup = true; break; }
+          const RecNarrow rj = recS[q];
+          if (pair_d<kNarrow7>(ri.a, ri.nb, ri.zz, make_uint4(rj.a, rj.nb, rj.zz, (uint32_t)rj.negT)) >= 0) {
+            sup = true;
+            break;
+          }
         }
       }
     }
@@ -226,9 +241,6 @@ __global__ void __launch_bounds__(kBinThreads) pnms_binned_frame(BinArgs a) {
     if (!sup && pad_rule && a.s[fbase + i] < 0.0) sup = true;
     if (!sup) atomicOr(&kbits[i >> 5], 1u << (i & 31));
   }
-  // NaN rows pass no gate: always survivors
-  for (int e = threadIdx.x; e < cnt; e += kBinThreads)
-    if (key[e] == kNanSortKey) atomicOr(&kbits[e >> 5], 1u << (e & 31));
   if (a.pairs_tested) {
     tested = __reduce_add_sync(0xFFFFFFFFu, (unsigned)tested);
     if ((threadIdx.x & 31) == 0 && tested) atomicAdd(a.pairs_tested, tested);
