@@ -111,6 +111,15 @@ int pnms_map_reference_layout(const int32_t* x, const int32_t* y, const int32_t*
  *  mask  uint8 [ceil(d_max/8)]  packed little-endian (SurvivorMask.bits, engine.py:120-122) */
 int pnms_reduce_rows(const uint64_t* bits, int d_max, int k, uint8_t* mask, void* stream);
 
+/* Device-side ingest validation (detections.py:60-85, Detection.validate): for each frame,
+ * first_bad[f] = the smallest slot index in [0, counts[f]) violating the detection invariants
+ * (integer coordinates in [0, 2^24), side >= 1, finite score > 0), or -1; reason[f] says which
+ * check failed (1..3 negative x/y/z, 4..6 x/y/z >= 2^24, 7 side < 1, 8 score not finite,
+ * 9 score <= 0, 0 valid).  first_bad, reason: int32 [batch] device arrays. */
+int pnms_validate(const int32_t* x, const int32_t* y, const int32_t* z, const double* s,
+                  const int32_t* counts, int batch, int n_max, int32_t* first_bad, int32_t* reason,
+                  void* stream);
+
 /* Diagnostics: device counter (uint64) that the binned path atomically increments by the
  * number of pair tests it executes; NULL disables (default).  Process-wide, not reentrant. */
 int pnms_debug_count_pairs(uint64_t* device_counter);

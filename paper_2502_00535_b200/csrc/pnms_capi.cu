@@ -19,6 +19,7 @@
 #include "pnms_reflayout.cuh"
 #include "pnms_small.cuh"
 #include "pnms_binned.cuh"
+#include "pnms_validate.cuh"
 #include "pnms_sort.cuh"
 
 using namespace pnms;
@@ -190,6 +191,16 @@ const char* pnms_strerror(int status) {
     case PNMS_EINVAL_K: return "k must be positive and divide d_max";
     default: return "unknown parnms_b200 status";
   }
+}
+
+int pnms_validate(const int32_t* x, const int32_t* y, const int32_t* z, const double* s, const int32_t* counts,
+                  int batch, int n_max, int32_t* first_bad, int32_t* reason, void* stream) {
+  if (batch < 0 || n_max < 0) return PNMS_EINVAL_ARG;
+  if (batch == 0) return PNMS_OK;
+  if (!first_bad || !reason || (n_max > 0 && (!x || !y || !z || !s))) return PNMS_EINVAL_ARG;
+  pnms_validate_kernel<<<batch, 256, 0, (cudaStream_t)stream>>>(x, y, z, s, counts, n_max, first_bad, reason);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? PNMS_OK : fail_cuda(e);
 }
 
 int pnms_debug_count_pairs(uint64_t* device_counter) {

@@ -69,7 +69,7 @@ def batched_nms_keep(x: torch.Tensor, y: torch.Tensor, z: torch.Tensor, s: torch
                      tie_break: str = "paper_faithful", d_max: int | None = None, *,
                      keep_idx: torch.Tensor | None = None, keep_count: torch.Tensor | None = None,
                      keep_mask: torch.Tensor | None = None, gate_pairs: torch.Tensor | None = None,
-                     workspace: torch.Tensor | None = None, want_idx: bool = True):
+                     workspace: torch.Tensor | None = None, want_idx: bool = True, validate: bool = False):
     """NMS of every frame of a batch; returns (keep_idx [B, n_max] int32, keep_count [B] int32).
 
     Frame f holds counts[f] valid detections in slots [0, counts[f]) of each plane; slots
@@ -77,7 +77,9 @@ def batched_nms_keep(x: torch.Tensor, y: torch.Tensor, z: torch.Tensor, s: torch
     capacity d_max (default n_max).  keep_idx[f, :keep_count[f]] are the ascending survivor
     indices — identical to engine.run_nms on the same frame (engine.py:296-300).
     Optional outputs: keep_mask (uint32 [B, ceil(n_max/32)] survivor bits) and gate_pairs
-    (int64 [B], the reference's WorkCounters.map_writes).
+    (int64 [B], the reference's WorkCounters.map_writes).  validate=True first checks every
+    valid slot on the device (validate_batch) and raises ValidationError like the reference's
+    DetectionVector construction would.
     """
     _require_cuda(x, "x", torch.int32, 2)
     B, n_max = x.shape
@@ -94,6 +96,8 @@ def batched_nms_keep(x: torch.Tensor, y: torch.Tensor, z: torch.Tensor, s: torch
             raise ValueError("counts must have one entry per frame")
     theta = _check_theta(theta)
     tie = _check_tie(tie_break)
+    if validate:
+        validate_batch(x, y, z, s, counts)
     if d_max is None:
         d_max = n_max
     if d_max < 1 or d_max < n_max:
@@ -125,6 +129,50 @@ def batched_nms_keep(x: torch.Tensor, y: torch.Tensor, z: torch.Tensor, s: torch
                       workspace.numel(), stream.cuda_stream)
     _lib.check(st, "pnms_run")
     return keep_idx, keep_count
+
+
+_REASONS = {
+    1: ("x", "neg"), 2: ("y", "neg"), 3: ("z", "neg"),
+    4: ("x", "big"), 5: ("y", "big"), 6: ("z", "big"),
+    7: ("z", "side"), 8: ("s", "finite"), 9: ("s", "positive"),
+}
+
+
+def validate_batch(x: torch.Tensor, y: torch.Tensor, z: torch.Tensor, s: torch.Tensor,
+                   counts: torch.Tensor | None = None) -> None:
+    """Check every valid slot against Detection.validate's invariants (detections.py:60-85)
+    on the device; raise ValidationError (reference message) for the first offender of the
+    first offending frame.  One small device-to-host copy, no host loop over detections."""
+    from .detections import COORD_LIMIT, ValidationError
+
+    B, n_max = x.shape
+    dev = x.device
+    first = torch.empty((B,), dtype=torch.int32, device=dev)
+    reason = torch.empty((B,), dtype=torch.int32, device=dev)
+    p = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+    st = _lib.load().pnms_validate(p(x), p(y), p(z), p(s), p(counts), B, n_max, p(first), p(reason),
+                                   torch.cuda.current_stream(dev).cuda_stream)
+    _lib.check(st, "pnms_validate")
+    bad = torch.nonzero(first >= 0)
+    if bad.numel() == 0:
+        return
+    f = int(bad[0, 0])
+    i = int(first[f])
+    field, kind = _REASONS[int(reason[f])]
+    v = {"x": x, "y": y, "z": z, "s": s}[field][f, i].item()
+    if kind == "neg":
+        msg = f"{field} must be non-negative, got {v}"
+    elif kind == "big":
+        msg = f"{field}={v} exceeds the coordinate limit {COORD_LIMIT}"
+    elif kind == "side":
+        msg = f"side length must be >= 1, got {v}"
+    elif kind == "finite":
+        msg = f"score must be finite, got {v}"
+    else:
+        msg = f"score must be strictly positive, got {v}"
+    err = ValidationError(msg)
+    err.frame, err.slot = f, i
+    raise err
 
 
 def nms_keep(boxes: torch.Tensor, scores: torch.Tensor, theta: float = 0.5,

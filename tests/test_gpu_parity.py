@@ -338,3 +338,28 @@ def test_reference_vector_duck_typing(golden_cases):
                                c.count + 5, c.count + 5, c.theta, c.tie)
     want2 = want2[want2 < c.count]
     assert [r[0] for r in res2.survivors] == [int(f.xs[i]) for i in want2]
+
+
+def test_device_validation_matches_reference_messages():
+    """validate=True raises the reference's ValidationError text for the first bad slot."""
+    from paper_2502_00535_b200 import Detection, ValidationError
+
+    x, y, z, s = random_frames(3, 64, seed=8)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)  # noqa: E731
+    counts = np.array([64, 64, 10], np.int32)
+    batched_nms_keep(t(x), t(y), t(z), t(s), t(counts), 0.5, validate=True)  # all valid: no raise
+    cases = [("x", 5, -3), ("y", 9, 2**24), ("z", 2, 0), ("s", 7, float("nan")), ("s", 1, 0.0), ("s", 3, -1.0),
+             ("z", 4, 2**24 + 1)]
+    for field, slot, val in cases:
+        xx, yy, zz, ss = x.copy(), y.copy(), z.copy(), s.copy()
+        {"x": xx, "y": yy, "z": zz, "s": ss}[field][1, slot] = val
+        {"x": xx, "y": yy, "z": zz, "s": ss}[field][1, slot + 1] = val  # a later offender is not reported
+        with pytest.raises(ValidationError) as ei:
+            batched_nms_keep(t(xx), t(yy), t(zz), t(ss), t(counts), 0.5, validate=True)
+        d = Detection(int(xx[1, slot]), int(yy[1, slot]), int(zz[1, slot]), float(ss[1, slot]))
+        with pytest.raises(ValidationError) as ref:
+            d.validate()
+        assert str(ei.value) == str(ref.value) and (ei.value.frame, ei.value.slot) == (1, slot)
+    # slots past the frame's count are padding and are not validated
+    xx = x.copy(); xx[2, 20] = -1
+    batched_nms_keep(t(xx), t(y), t(z), t(s), t(counts), 0.5, validate=True)
