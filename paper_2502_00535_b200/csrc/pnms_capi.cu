@@ -20,6 +20,7 @@
 #include "pnms_small.cuh"
 #include "pnms_binned.cuh"
 #include "pnms_validate.cuh"
+#include "pnms_binned_grid.cuh"
 #include "pnms_sort.cuh"
 
 using namespace pnms;
@@ -32,7 +33,7 @@ unsigned long long* g_pairs_counter = nullptr;  // diagnostics: binned pair test
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Layout {
-  size_t rec, perm, lim, supp, meta, sk, idx, dense, total;
+  size_t rec, perm, lim, supp, meta, sk, idx, dense, grid, total;
 };
 
 Layout make_layout(int batch, int n_max) {
@@ -46,6 +47,11 @@ Layout make_layout(int batch, int n_max) {
   L.supp = off; off = align_up(off + B * W32 * 4, 256);
   L.meta = off; off = align_up(off + B * sizeof(FrameMeta), 256);
   L.dense = off; off = align_up(off + B, 256);
+  if (n_max > kBinMaxSlots) {
+    L.grid = off; off = align_up(off + binned_grid_scratch_bytes(n_max), 256);
+  } else {
+    L.grid = 0;
+  }
   if (n_max > kSortMax) {
     L.sk = off;  off = align_up(off + B * N * 8, 256);
     L.idx = off; off = align_up(off + B * N * 4, 256);
@@ -101,6 +107,22 @@ SideStream* side_stream() {
 }
 std::atomic<size_t> g_small_smem[8];
 std::atomic<size_t> g_binned_smem[2];
+
+// co-resident CTAs for the cooperative binned kernel on the current device (cached)
+int cooperative_blocks(bool by_index) {
+  static std::atomic<int> cached[2] = {{-1}, {-1}};
+  int v = cached[by_index].load();
+  if (v >= 0) return v;
+  int dev = 0, sms = 0, per_sm = 0, coop = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  const void* fn = by_index ? (const void*)pnms_binned_grid<true> : (const void*)pnms_binned_grid<false>;
+  if (!coop || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGridThreads, 0) != cudaSuccess) per_sm = 0;
+  v = sms * std::min(per_sm, 2);
+  cached[by_index].store(v);
+  return v;
+}
 
 template <bool B, bool C, int R>
 cudaError_t launch_small_t(const SmallArgs& sa, long long grid, size_t smem, cudaStream_t st, std::atomic<size_t>& cfg) {
@@ -321,6 +343,41 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
       // phases become: [0,1) binned kernel, [1,2) dense prep of declined frames, [2,3) their map+compact
       ev_local[0] = events[1]; ev_local[1] = events[2]; ev_local[2] = nullptr; ev_local[3] = events[3];
       events = ev_local;
+    }
+  }
+
+  if (!dense_flags && algo == 0 && gate_pairs == nullptr && n_max > kBinMaxSlots && env_int("PNMS_GRID", 0) == 1) {
+    // large frames: one cooperative launch over the whole GPU (pnms_binned_grid.cuh).  Opt-in:
+    // measured on B200 it is grid-sync/latency bound (~110 us for BASELINE config 3, issue
+    // active 3.6 %), no faster than the dense sorted pipeline (~105 us).
+    uint8_t* g = ws + L.grid;
+    BinGridArgs ga;
+    ga.x = x; ga.y = y; ga.z = z; ga.s = s; ga.counts = counts;
+    ga.batch = batch; ga.n_max = n_max; ga.d_max = d_max; ga.tie_break = tie_break; ga.W32 = W32;
+    ga.theta = theta;
+    size_t o = 0;
+    ga.recS = reinterpret_cast<RecNarrow*>(g + o); o = align_up(o + (size_t)n_max * 16, 256);
+    ga.keyS = reinterpret_cast<uint64_t*>(g + o); o = align_up(o + (size_t)n_max * 8, 256);
+    ga.idxS = reinterpret_cast<int32_t*>(g + o); o = align_up(o + (size_t)n_max * 4, 256);
+    ga.cellof = reinterpret_cast<int32_t*>(g + o); o = align_up(o + (size_t)n_max * 4, 256);
+    ga.cstart = reinterpret_cast<uint32_t*>(g + o); o = align_up(o + (size_t)(kGridMaxCells + 4) * 4, 256);
+    ga.ccur = reinterpret_cast<uint32_t*>(g + o); o = align_up(o + (size_t)(kGridMaxCells + 4) * 4, 256);
+    ga.kbits = reinterpret_cast<uint32_t*>(g + o); o = align_up(o + (size_t)W32 * 4, 256);
+    ga.gst = reinterpret_cast<GridStats*>(g + o);
+    ga.fallback = ws + L.dense;
+    ga.keep_idx = keep_idx; ga.keep_count = keep_count; ga.keep_mask = keep_mask;
+    int blocks = cooperative_blocks(tie_break == PNMS_TIE_BY_INDEX);
+    if (blocks > 0) {
+      if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
+      void* kargs[] = {&ga};
+      void* fn = tie_break == PNMS_TIE_BY_INDEX ? (void*)pnms_binned_grid<true> : (void*)pnms_binned_grid<false>;
+      if ((e = cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kGridThreads), kargs, 0, st)) != cudaSuccess)
+        return fail_cuda(e);
+      dense_flags = ws + L.dense;
+      if (events) {
+        ev_local[0] = events[1]; ev_local[1] = events[2]; ev_local[2] = nullptr; ev_local[3] = events[3];
+        events = ev_local;
+      }
     }
   }
 

@@ -190,8 +190,11 @@ def test_ragged_duplicates_vs_oracle(tie, theta, path):
 
 
 @pytest.mark.parametrize("n", [4097, 6000, 9000, 16384])
-def test_chunked_sort_frames_vs_oracle(n):
-    """Frames above one CTA's sort capacity (chunk sort + merge-rank path) with ties."""
+@pytest.mark.parametrize("grid", ["0", "1"])
+def test_chunked_sort_frames_vs_oracle(n, path, grid, monkeypatch):
+    """Frames above one CTA's capacity (cooperative binned kernel when PNMS_GRID=1; chunk sort
+    + merge-rank in the dense pipeline) with exact score ties."""
+    monkeypatch.setenv("PNMS_GRID", grid)
     x, y, z, s = random_frames(2, n, seed=n, frame_w=3840, frame_h=2160, z_range=(8, 64), duplicate_fraction=0.1)
     s[:, ::7] = 0.5
     for tie in ("paper_faithful", "by_index"):
