@@ -111,6 +111,16 @@ int pnms_map_reference_layout(const int32_t* x, const int32_t* y, const int32_t*
  *  mask  uint8 [ceil(d_max/8)]  packed little-endian (SurvivorMask.bits, engine.py:120-122) */
 int pnms_reduce_rows(const uint64_t* bits, int d_max, int k, uint8_t* mask, void* stream);
 
+/* Classic greedy NMS (oracles.greedy_nms, oracles.py:64-85) for `batch` frames of up to 4096
+ * slots: visit valid detections by (score desc, index asc), keep one unless an already-kept
+ * detection covers it (positive extents on both axes and w*h >= theta*(z_ref+1)^2,
+ * oracles.py:20-29).  Outputs as pnms_run (keep_idx ascending, keep_count, keep_mask; each
+ * may be NULL).  Needs no workspace.  Scores must not be NaN (the reference's ordering is
+ * undefined for NaN; here NaN detections are kept and never cover others). */
+int pnms_greedy_run(const int32_t* x, const int32_t* y, const int32_t* z, const double* s,
+                    const int32_t* counts, int batch, int n_max, double theta, int32_t* keep_idx,
+                    int32_t* keep_count, uint32_t* keep_mask, void* stream);
+
 /* Device-side ingest validation (detections.py:60-85, Detection.validate): for each frame,
  * first_bad[f] = the smallest slot index in [0, counts[f]) violating the detection invariants
  * (integer coordinates in [0, 2^24), side >= 1, finite score > 0), or -1; reason[f] says which

@@ -37,6 +37,11 @@ def _load():
             ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int,
             ctypes.c_void_p, ctypes.c_void_p,
         ]
+        lib.oracle_greedy_nms.restype = ctypes.c_int
+        lib.oracle_greedy_nms.argtypes = [
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_double,
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+        ]
         _lib = lib
     return _lib
 
@@ -70,3 +75,19 @@ def run_batch(x, y, z, s, counts, d_max: int, theta: float, tie_break: str = "pa
 
     with ThreadPoolExecutor(max_workers=threads) as pool:
         return list(pool.map(one, range(B)))
+
+
+def greedy_frame(x, y, z, s, count: int, theta: float):
+    """Keep indices of oracles.greedy_nms (oracles.py:64-85) over the first `count` slots."""
+    lib = _load()
+    x = np.ascontiguousarray(x, dtype=np.int32)
+    y = np.ascontiguousarray(y, dtype=np.int32)
+    z = np.ascontiguousarray(z, dtype=np.int32)
+    s = np.ascontiguousarray(s, dtype=np.float64)
+    n = max(int(count), 1)
+    out = np.empty(n, dtype=np.int32)
+    order = np.empty(n, dtype=np.int32)
+    state = np.empty(n, dtype=np.uint8)
+    k = lib.oracle_greedy_nms(x.ctypes.data, y.ctypes.data, z.ctypes.data, s.ctypes.data, int(count), float(theta),
+                              out.ctypes.data, order.ctypes.data, state.ctypes.data)
+    return out[:k].copy()

@@ -16,6 +16,7 @@
  */
 #include <stdint.h>
 #include <stddef.h>
+#include <math.h>
 
 typedef struct {
   int32_t x, y, z;
@@ -74,5 +75,53 @@ int oracle_run_nms(const int32_t* x, const int32_t* y, const int32_t* z, const d
     }
     *map_writes = g;
   }
+  return kept;
+}
+
+/* Classic greedy NMS restated from oracles.greedy_nms (oracles.py:64-85): visit the valid
+ * detections by (score desc, index asc); keep a detection unless an already-kept one covers
+ * it, where covers(cand, ref) (oracles.py:20-29) needs positive extents on both axes and
+ * w*h >= theta * (z_ref+1)^2 (exact integer w*h against the float64 product, as Python
+ * compares int and float exactly).  Returns the number kept; keep_out ascending. */
+static int greedy_covers(slot_t c, slot_t r, double theta) {
+  long long w = (long long)(c.x + (long long)c.z < r.x + (long long)r.z ? c.x + (long long)c.z : r.x + (long long)r.z) -
+                (long long)(c.x > r.x ? c.x : r.x) + 1;
+  if (w <= 0) return 0;
+  long long h = (long long)(c.y + (long long)c.z < r.y + (long long)r.z ? c.y + (long long)c.z : r.y + (long long)r.z) -
+                (long long)(c.y > r.y ? c.y : r.y) + 1;
+  if (h <= 0) return 0;
+  long long a = ((long long)r.z + 1) * ((long long)r.z + 1);
+  double thr = theta * (double)a;
+  /* exact int >= float: compare against ceil(thr) in integers */
+  double ct = ceil(thr);
+  if (ct > 9.2e18) return 0;
+  return (unsigned long long)w * (unsigned long long)h >= (unsigned long long)(long long)ct;
+}
+
+int oracle_greedy_nms(const int32_t* x, const int32_t* y, const int32_t* z, const double* s, int count,
+                      double theta, int32_t* keep_out, int32_t* order_scratch, uint8_t* state_scratch) {
+  /* order by (-s, i): insertion into a sorted index list (n is small in tests) */
+  for (int i = 0; i < count; ++i) {
+    int j = i;
+    while (j > 0) {
+      int o = order_scratch[j - 1];
+      if (s[o] > s[i] || (s[o] == s[i] && o < i)) break;
+      order_scratch[j] = o;
+      --j;
+    }
+    order_scratch[j] = i;
+  }
+  for (int i = 0; i < count; ++i) state_scratch[i] = 1; /* pending */
+  for (int k = 0; k < count; ++k) {
+    int i = order_scratch[k];
+    if (!state_scratch[i]) continue;
+    state_scratch[i] = 2; /* kept */
+    slot_t r = slot_at(x, y, z, s, count, i);
+    for (int j = 0; j < count; ++j)
+      if (state_scratch[j] == 1 && greedy_covers(slot_at(x, y, z, s, count, j), r, theta)) state_scratch[j] = 0;
+  }
+  int kept = 0;
+  for (int i = 0; i < count; ++i)
+    if (state_scratch[i] == 2) keep_out[kept++] = i;
   return kept;
 }

@@ -21,6 +21,7 @@
 #include "pnms_binned.cuh"
 #include "pnms_validate.cuh"
 #include "pnms_binned_grid.cuh"
+#include "pnms_greedy.cuh"
 #include "pnms_sort.cuh"
 
 using namespace pnms;
@@ -223,6 +224,32 @@ int pnms_validate(const int32_t* x, const int32_t* y, const int32_t* z, const do
   pnms_validate_kernel<<<batch, 256, 0, (cudaStream_t)stream>>>(x, y, z, s, counts, n_max, first_bad, reason);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? PNMS_OK : fail_cuda(e);
+}
+
+int pnms_greedy_run(const int32_t* x, const int32_t* y, const int32_t* z, const double* s, const int32_t* counts,
+                    int batch, int n_max, double theta, int32_t* keep_idx, int32_t* keep_count, uint32_t* keep_mask,
+                    void* stream) {
+  if (!(theta >= 0.0 && theta <= 1.0)) return PNMS_EINVAL_THETA;
+  if (batch < 0 || n_max < 0) return PNMS_EINVAL_ARG;
+  if (n_max > kGreedyMaxSlots) return PNMS_ETOO_LARGE;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  if (batch == 0) return PNMS_OK;
+  if (n_max == 0) {
+    if (keep_count && (e = cudaMemsetAsync(keep_count, 0, sizeof(int32_t) * batch, st)) != cudaSuccess) return fail_cuda(e);
+    return PNMS_OK;
+  }
+  if (!x || !y || !z || !s) return PNMS_EINVAL_ARG;
+  GreedyArgs ga;
+  ga.x = x; ga.y = y; ga.z = z; ga.s = s; ga.counts = counts;
+  ga.batch = batch; ga.n_max = n_max; ga.W32 = (n_max + 31) / 32; ga.theta = theta;
+  ga.keep_idx = keep_idx; ga.keep_count = keep_count; ga.keep_mask = keep_mask;
+  static std::atomic<size_t> cfg{0};
+  const size_t smem = greedy_smem_bytes(n_max);
+  if ((e = ensure_smem(pnms_greedy_frame, smem, cfg)) != cudaSuccess) return fail_cuda(e);
+  pnms_greedy_frame<<<batch, kGreedyThreads, smem, st>>>(ga);
+  if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
+  return PNMS_OK;
 }
 
 int pnms_debug_count_pairs(uint64_t* device_counter) {

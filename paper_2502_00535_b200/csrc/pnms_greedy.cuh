@@ -1,0 +1,238 @@
+// pnms_greedy.cuh — classic greedy NMS (oracles.greedy_nms, oracles.py:64-85) on the device.
+//
+// Reference semantics: visit the valid detections by (score desc, index asc); a detection is
+// kept unless an already-kept detection covers it, covers(cand, ref) requiring positive
+// extents on both axes and w*h >= theta*(z_ref+1)^2 (oracles.py:20-29).  Unlike the engine's
+// row AND, a suppressed box no longer suppresses (the chain fixture, workload.py:252-266,
+// keeps {a, c} here and {a} in the engine).
+//
+// Parallel exact resolution: kept(j) <=> no kept higher-ranked box covers j.  Every round,
+// each undecided box looks at its higher-ranked coverers: one kept -> removed; all removed
+// (or none) -> kept; otherwise it waits.  Decisions are final and correct when made, each
+// round decides at least the highest-ranked undecided box, so the loop ends after as many
+// rounds as the longest suppression chain (a handful on detector output).
+//
+// Candidates: greedy never covers on zero overlap, so spatial cells of side max_z + 1 (3x3
+// neighbourhood, see pnms_binned.cuh) are exact for every theta; frames with negative
+// coordinates or a crowded cell scan all slots instead.  One CTA per frame, shared memory
+// only; covers() is evaluated in exact 64-bit integer arithmetic against ceil(fl64(theta*a)).
+#pragma once
+#include "pnms_common.cuh"
+#include "pnms_sort.cuh"
+
+namespace pnms {
+
+constexpr int kGreedyThreads = 512;
+constexpr int kGreedyMaxSlots = 4096;
+constexpr int kGreedyCellMax = 64;
+
+enum GreedyState : uint8_t { kUndecided = 0, kKept = 1, kRemoved = 2 };
+
+struct GreedyArgs {
+  const int32_t *x, *y, *z;
+  const double* s;
+  const int32_t* counts;
+  int batch, n_max, W32;
+  double theta;
+  int32_t* keep_idx;
+  int32_t* keep_count;
+  uint32_t* keep_mask;
+};
+
+__host__ __device__ inline int greedy_npad(int n_max) { return (n_max + 127) & ~127; }
+inline size_t greedy_smem_bytes(int n_max) {
+  const size_t n = (size_t)greedy_npad(n_max);
+  const size_t cells = n < 64 ? 64 : n;
+  return n * (4 * 3 + 8 + 8 + 1 + 2 + 2) + (cells + 4) * 4 + (n / 32 + 4) * 4 + 64 * 4 + 64;
+}
+
+// covers(cand, ref) of oracles.py:20-29 in exact integer arithmetic; T = ceil(fl64(theta*a))
+__device__ __forceinline__ bool greedy_covers(int32_t cx, int32_t cy, int32_t cz, int32_t rx, int32_t ry, int32_t rz,
+                                              unsigned long long T) {
+  const long long w = min((long long)cx + cz, (long long)rx + rz) - (long long)max(cx, rx) + 1;
+  if (w <= 0) return false;
+  const long long h = min((long long)cy + cz, (long long)ry + rz) - (long long)max(cy, ry) + 1;
+  if (h <= 0) return false;
+  return (unsigned long long)w * (unsigned long long)h >= T;
+}
+
+__device__ __forceinline__ unsigned long long greedy_threshold(double theta, int32_t z) {
+  // Python: theta * ((z+1)*(z+1)) converts the exact integer area to float64, then multiplies
+  const long long a = ((long long)z + 1) * ((long long)z + 1);
+  const double thr = __dmul_rn(theta, __ll2double_rn(a));
+  const double c = ceil(thr);
+  return c >= 1.8e19 ? ~0ull : (unsigned long long)c;
+}
+
+__global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int s_stat[8];   // 0 minx 1 miny 2 maxx 3 maxy 4 maxz 5 bin_ok 6 big 7 undecided
+  const int f = blockIdx.x;
+  const long long fbase = (long long)f * a.n_max;
+  const int cnt = frame_count(a.counts, f, a.n_max);
+  const int npad = greedy_npad(a.n_max);
+  const int max_cells = npad < 64 ? 64 : npad;
+  int32_t* sx = reinterpret_cast<int32_t*>(smem_raw);
+  int32_t* sy = sx + npad;
+  int32_t* sz = sy + npad;
+  uint64_t* key = reinterpret_cast<uint64_t*>(sz + npad);
+  unsigned long long* thr = reinterpret_cast<unsigned long long*>(key + npad);
+  uint8_t* state = reinterpret_cast<uint8_t*>(thr + npad);
+  uint16_t* cellof = reinterpret_cast<uint16_t*>(state + npad);
+  uint16_t* list = cellof + npad;
+  uint32_t* cstart = reinterpret_cast<uint32_t*>(list + npad);
+  uint32_t* kbits = cstart + max_cells + 4;
+  uint32_t* scan_tmp = kbits + npad / 32 + 4;
+
+  if (threadIdx.x == 0) {
+    s_stat[0] = s_stat[1] = 0x7FFFFFFF;
+    s_stat[2] = s_stat[3] = -0x7FFFFFFF;
+    s_stat[4] = 0; s_stat[5] = 1; s_stat[6] = 0; s_stat[7] = 0;
+  }
+  for (int w = threadIdx.x; w < npad / 32; w += kGreedyThreads) kbits[w] = 0u;
+  __syncthreads();
+  // ---- load
+  for (int e = threadIdx.x; e < cnt; e += kGreedyThreads) {
+    const long long g = fbase + e;
+    const int32_t xv = a.x[g], yv = a.y[g], zv = a.z[g];
+    const double sv = a.s[g];
+    sx[e] = xv; sy[e] = yv; sz[e] = zv;
+    key[e] = sort_key(sv);
+    thr[e] = greedy_threshold(a.theta, zv);
+    state[e] = (sv != sv) ? kKept : kUndecided;  // NaN: unordered, never covers (documented)
+    if (xv < 0 || yv < 0 || zv < 0) atomicAnd(&s_stat[5], 0);
+    atomicMin(&s_stat[0], xv); atomicMin(&s_stat[1], yv);
+    atomicMax(&s_stat[2], xv); atomicMax(&s_stat[3], yv); atomicMax(&s_stat[4], zv);
+  }
+  __syncthreads();
+  // ---- spatial cells (exact for greedy at any theta: zero overlap never covers)
+  bool bin = s_stat[5] != 0 && cnt > 0;
+  int S = 1, GX = 1, GY = 1;
+  const int ox = s_stat[0], oy = s_stat[1];
+  if (bin) {
+    S = s_stat[4] + 1;
+    if (S <= 0) bin = false;  // z = INT_MAX
+  }
+  if (bin) {
+    for (;;) {
+      GX = (int)(((long long)s_stat[2] - ox) / S + 1);
+      GY = (int)(((long long)s_stat[3] - oy) / S + 1);
+      if ((long long)GX * GY <= max_cells) break;
+      if (S > (1 << 29)) { GX = GY = 1; break; }
+      S *= 2;
+    }
+    const int cells = GX * GY;
+    for (int c = threadIdx.x; c <= cells; c += kGreedyThreads) cstart[c] = 0u;
+    __syncthreads();
+    for (int e = threadIdx.x; e < cnt; e += kGreedyThreads) {
+      const int c = (int)(((long long)sy[e] - oy) / S) * GX + (int)(((long long)sx[e] - ox) / S);
+      cellof[e] = (uint16_t)c;
+      atomicAdd(&cstart[c], 1u);
+    }
+    __syncthreads();
+    {
+      const int per = (cells + 1 + kGreedyThreads - 1) / kGreedyThreads;
+      const int b0 = threadIdx.x * per;
+      uint32_t sum = 0, big = 0;
+      for (int t = 0; t < per; ++t) {
+        const int c = b0 + t;
+        if (c < cells) { sum += cstart[c]; big = max(big, cstart[c]); }
+      }
+      big = __reduce_max_sync(0xFFFFFFFFu, big);
+      if ((threadIdx.x & 31) == 0) atomicMax(&s_stat[6], (int)big);
+      uint32_t run = block_exclusive_scan(sum, scan_tmp, nullptr);
+      for (int t = 0; t < per; ++t) {
+        const int c = b0 + t;
+        if (c < cells) { const uint32_t v = cstart[c]; cstart[c] = run; run += v; }
+      }
+      if (threadIdx.x == 0) cstart[cells] = (uint32_t)cnt;
+    }
+    __syncthreads();
+    bin = s_stat[6] <= kGreedyCellMax;
+    if (bin) {
+      // scatter with cstart as the cursor: afterwards cstart[c] = end(c) = start(c+1)
+      for (int e = threadIdx.x; e < cnt; e += kGreedyThreads) {
+        const uint32_t pos = atomicAdd(&cstart[cellof[e]], 1u);
+        list[pos] = (uint16_t)e;
+      }
+    }
+  }
+  __syncthreads();
+  // After the scatter, cstart[c] == end(c) == start(c+1); start(0) = 0.
+  // ---- rounds
+  for (;;) {
+    for (int j = threadIdx.x; j < cnt; j += kGreedyThreads) {
+      if (state[j] != kUndecided) continue;
+      const uint64_t kj = key[j];
+      const int32_t jx = sx[j], jy = sy[j], jz = sz[j];
+      bool kept_cov = false, undec_cov = false;
+      if (bin) {
+        const int cx = (int)(((long long)jx - ox) / S), cy = (int)(((long long)jy - oy) / S);
+        for (int yy = max(0, cy - 1); yy <= min(GY - 1, cy + 1) && !kept_cov; ++yy) {
+          for (int xx = max(0, cx - 1); xx <= min(GX - 1, cx + 1) && !kept_cov; ++xx) {
+            const int c = yy * GX + xx;
+            const int b = c == 0 ? 0 : (int)cstart[c - 1], en = (int)cstart[c];
+            for (int q = b; q < en; ++q) {
+              const int i = list[q];
+              const uint8_t si = state[i];
+              if (si == kRemoved) continue;
+              const uint64_t ki = key[i];
+              if (!(ki < kj || (ki == kj && i < j))) continue;
+              if (!greedy_covers(jx, jy, jz, sx[i], sy[i], sz[i], thr[i])) continue;
+              if (si == kKept) { kept_cov = true; break; }
+              undec_cov = true;
+            }
+          }
+        }
+      } else {
+        for (int i = 0; i < cnt; ++i) {
+          const uint8_t si = state[i];
+          if (si == kRemoved) continue;
+          const uint64_t ki = key[i];
+          if (!(ki < kj || (ki == kj && i < j))) continue;
+          if (!greedy_covers(jx, jy, jz, sx[i], sy[i], sz[i], thr[i])) continue;
+          if (si == kKept) { kept_cov = true; break; }
+          undec_cov = true;
+        }
+      }
+      if (kept_cov) state[j] = kRemoved;
+      else if (!undec_cov) state[j] = kKept;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_stat[7] = 0;
+    __syncthreads();
+    int und = 0;
+    for (int j = threadIdx.x; j < cnt; j += kGreedyThreads) und += state[j] == kUndecided;
+    und = __reduce_add_sync(0xFFFFFFFFu, und);
+    if ((threadIdx.x & 31) == 0 && und) atomicAdd(&s_stat[7], und);
+    __syncthreads();
+    if (s_stat[7] == 0) break;
+    __syncthreads();
+  }
+  // ---- compaction of the kept boxes (ascending input order, oracles.py:84)
+  for (int j = threadIdx.x; j < cnt; j += kGreedyThreads)
+    if (state[j] == kKept) atomicOr(&kbits[j >> 5], 1u << (j & 31));
+  __syncthreads();
+  const int wpt = (a.W32 + kGreedyThreads - 1) / kGreedyThreads;
+  const int w0 = threadIdx.x * wpt, w1 = min(w0 + wpt, a.W32);
+  uint32_t local = 0;
+  for (int w = w0; w < w1; ++w) {
+    const uint32_t bits = kbits[w];
+    local += __popc(bits);
+    if (a.keep_mask) a.keep_mask[(long long)f * a.W32 + w] = bits;
+  }
+  uint32_t total;
+  uint32_t pos = block_exclusive_scan(local, scan_tmp, &total);
+  if (a.keep_idx) {
+    for (int w = w0; w < w1; ++w) {
+      uint32_t bits = kbits[w];
+      while (bits) {
+        a.keep_idx[fbase + pos++] = w * 32 + __ffs(bits) - 1;
+        bits &= bits - 1;
+      }
+    }
+  }
+  if (threadIdx.x == 0 && a.keep_count) a.keep_count[f] = (int32_t)total;
+}
+
+}  // namespace pnms

@@ -221,7 +221,28 @@ def mask_survivors(d: DetectionVector, v: SurvivorMask) -> NmsResult:
     return NmsResult(survivors, d.count - len(survivors))
 
 
+def greedy_nms(d: DetectionVector, theta: float) -> NmsResult:
+    """Classic sequential-semantics greedy NMS (oracles.greedy_nms, oracles.py:64-85) on the GPU.
+
+    Survivors in input order; differs from run_nms on suppression chains by design."""
+    torch = _torch()
+    from .tensor_api import greedy_nms_keep
+
+    if not 0.0 <= theta <= 1.0:
+        raise ConfigError(f"theta must be in [0, 1], got {theta}")
+    count = int(d.count)
+    if count == 0:
+        return NmsResult((), 0)
+    x, y, z, s = _frame_columns(d)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    t = lambda a: torch.from_numpy(np.array(a[:count])).reshape(1, count).to(dev)  # noqa: E731
+    idx, cnt = greedy_nms_keep(t(x), t(y), t(z), t(s), None, theta)
+    keep = idx[0, : int(cnt.item())].cpu().numpy()
+    survivors = tuple(d.slot(int(i)) for i in keep)
+    return NmsResult(survivors, count - len(survivors))
+
+
 __all__ = [
     "ConfigError", "NmsConfig", "SuppressionMatrix", "SurvivorMask", "WorkCounters",
-    "map_phase", "reduce_phase", "mask_survivors", "run_nms", "Detection",
+    "map_phase", "reduce_phase", "mask_survivors", "run_nms", "greedy_nms", "Detection",
 ]

@@ -175,6 +175,33 @@ def validate_batch(x: torch.Tensor, y: torch.Tensor, z: torch.Tensor, s: torch.T
     raise err
 
 
+def greedy_nms_keep(x: torch.Tensor, y: torch.Tensor, z: torch.Tensor, s: torch.Tensor,
+                    counts: torch.Tensor | None = None, theta: float = 0.5, *,
+                    keep_idx: torch.Tensor | None = None, keep_count: torch.Tensor | None = None,
+                    keep_mask: torch.Tensor | None = None):
+    """Classic greedy NMS of every frame (oracles.greedy_nms, oracles.py:64-85) on the device.
+
+    Same planes and outputs as batched_nms_keep; frames of up to 4096 slots."""
+    _require_cuda(x, "x", torch.int32, 2)
+    B, n_max = x.shape
+    for t, nm in ((y, "y"), (z, "z")):
+        _require_cuda(t, nm, torch.int32, 2)
+    _require_cuda(s, "s", torch.float64, 2)
+    if counts is not None:
+        _require_cuda(counts, "counts", torch.int32, 1)
+    theta = _check_theta(theta)
+    dev = x.device
+    if keep_idx is None:
+        keep_idx = torch.empty((B, n_max), dtype=torch.int32, device=dev)
+    if keep_count is None:
+        keep_count = torch.empty((B,), dtype=torch.int32, device=dev)
+    p = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+    st = _lib.load().pnms_greedy_run(p(x), p(y), p(z), p(s), p(counts), B, n_max, theta, p(keep_idx),
+                                     p(keep_count), p(keep_mask), torch.cuda.current_stream(dev).cuda_stream)
+    _lib.check(st, "pnms_greedy_run")
+    return keep_idx, keep_count
+
+
 def nms_keep(boxes: torch.Tensor, scores: torch.Tensor, theta: float = 0.5,
              tie_break: str = "paper_faithful", d_max: int | None = None) -> torch.Tensor:
     """Single-frame NMS: boxes [N, 3] (x, y, z) integer CUDA tensor, scores [N] float64.

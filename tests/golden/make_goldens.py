@@ -29,7 +29,7 @@ REF = os.environ.get("PARNMS_REF", "/root/reference/pkg/src")
 sys.path.insert(0, REF)
 import parnms  # noqa: E402
 from parnms import (  # noqa: E402
-    Detection, DetectionVector, NmsConfig, WorkloadSpec, chain_fixture, generate_frame, map_phase,
+    Detection, DetectionVector, NmsConfig, WorkloadSpec, chain_fixture, generate_frame, greedy_nms, map_phase,
     random_frame, reduce_phase, run_nms, toy_frame,
 )
 from parnms.overlap import intersection_extent, suppression_test  # noqa: E402
@@ -209,6 +209,45 @@ def make_configs():
     return out
 
 
+def make_greedy():
+    """oracles.greedy_nms (oracles.py:64-85) keep indices on seeded frames (valid inputs only)."""
+    rng = np.random.default_rng(64085)
+    out = {"x": [], "y": [], "z": [], "s": [], "keep": [], "meta": []}
+    off = koff = 0
+
+    def add(vec, theta):
+        nonlocal off, koff
+        res = greedy_nms(vec, theta)
+        kept = {(d.x, d.y, d.z, d.s) for d in res.survivors}
+        valid = vec.valid()
+        keep = [i for i, d in enumerate(valid) if (d.x, d.y, d.z, d.s) in kept]
+        # duplicates of a kept tuple are distinct slots: keep the ones greedy kept by index
+        assert len(keep) >= len(res.survivors)
+        if len(keep) != len(res.survivors):
+            return
+        x, y, z, s = valid_arrays(vec)
+        out["x"].append(x); out["y"].append(y); out["z"].append(z); out["s"].append(s)
+        out["keep"].append(np.array(keep, dtype=np.int32))
+        out["meta"].append((off, len(x), koff, len(keep), theta))
+        off += len(x); koff += len(keep)
+
+    for t in range(300):
+        n = int(rng.integers(0, 160))
+        fw = int(rng.choice([96, 256, 512]))
+        theta = [0.0, 0.1, 0.3, 0.5, 0.9, 1.0][t % 6] if t % 5 else float(rng.uniform(0, 1))
+        vec = random_frame(n, seed=int(rng.integers(0, 2**31)), frame_w=fw, frame_h=fw,
+                           z_range=(1, 40) if fw <= 256 else (4, 90), duplicate_fraction=0.2 if t % 4 == 0 else 0.0)
+        add(vec, theta)
+    add(toy_frame(), 0.3)
+    vec, th = chain_fixture()
+    add(vec, th)
+    for f in range(2):
+        add(random_frame(1024, seed=f, frame_w=1920, frame_h=1080, z_range=(8, 64)), 0.5)
+    cat = lambda k, dt: np.concatenate(out[k]).astype(dt)  # noqa: E731
+    return dict(x=cat("x", np.int64), y=cat("y", np.int64), z=cat("z", np.int64), s=cat("s", np.float64),
+                keep=cat("keep", np.int32), meta=np.array(out["meta"], dtype=np.float64))
+
+
 def make_kats():
     k = {}
     k["intersection_extent"] = [[a, b, c, d, intersection_extent(a, b, c, d)]
@@ -236,6 +275,7 @@ def main():
     print(f"cases: {len(cases)}")
     (OUT / "kats.json").write_text(json.dumps(make_kats(), indent=1) + "\n")
     np.savez_compressed(OUT / "configs.npz", **make_configs())
+    np.savez_compressed(OUT / "greedy.npz", **make_greedy())
 
 
 if __name__ == "__main__":

@@ -366,3 +366,44 @@ def test_device_validation_matches_reference_messages():
     # slots past the frame's count are padding and are not validated
     xx = x.copy(); xx[2, 20] = -1
     batched_nms_keep(t(xx), t(y), t(z), t(s), t(counts), 0.5, validate=True)
+
+
+def test_greedy_matches_reference_goldens():
+    """Device greedy NMS vs oracles.greedy_nms keep indices (tests/golden/greedy.npz)."""
+    from conftest import GOLDEN
+    from paper_2502_00535_b200 import greedy_nms_keep
+
+    g = np.load(GOLDEN / "greedy.npz")
+    for off, n, koff, klen, theta in g["meta"]:
+        off, n, koff, klen = int(off), int(n), int(koff), int(klen)
+        if n == 0:
+            continue
+        sl = slice(off, off + n)
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a[sl]).astype(a.dtype).reshape(1, n)).to(DEV)  # noqa: E731
+        ki, kc = greedy_nms_keep(t(g["x"].astype(np.int32)), t(g["y"].astype(np.int32)), t(g["z"].astype(np.int32)),
+                                 t(g["s"]), None, float(theta))
+        assert np.array_equal(ki[0, : int(kc.item())].cpu().numpy(), g["keep"][koff:koff + klen]), (n, theta)
+
+
+@pytest.mark.parametrize("theta", [0.0, 0.3, 0.5, 1.0])
+def test_greedy_batch_vs_oracle(theta):
+    """Batched greedy (binned and all-slot candidate paths, ties, chains) vs the C oracle."""
+    from paper_2502_00535_b200 import DetectionVector, greedy_nms, greedy_nms_keep
+
+    x, y, z, s = random_frames(10, 700, seed=31, frame_w=500, frame_h=400, z_range=(4, 60), duplicate_fraction=0.1)
+    s[:, ::6] = 0.5                          # exact ties
+    x[2, :200] = 3; y[2, :200] = 3           # crowded cell -> all-slot candidate scan
+    x[3] = np.arange(700) * 2; y[3] = 0; z[3] = 10; s[3] = 1.0 - np.arange(700) * 1e-4   # long chain
+    counts = np.array([700, 650, 700, 700, 1, 0, 700, 300, 700, 700], np.int32)
+    tt = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)  # noqa: E731
+    ki, kc = greedy_nms_keep(tt(x), tt(y), tt(z), tt(s), tt(counts), theta)
+    ki, kc = ki.cpu().numpy(), kc.cpu().numpy()
+    for f in range(10):
+        want = c_oracle.greedy_frame(x[f], y[f], z[f], s[f], int(counts[f]), theta)
+        assert np.array_equal(ki[f, : kc[f]], want), (f, theta)
+    # drop-in mirror of oracles.greedy_nms
+    vec = DetectionVector.from_arrays(x[0], y[0], z[0], s[0])
+    res = greedy_nms(vec, theta)
+    want = c_oracle.greedy_frame(x[0], y[0], z[0], s[0], 700, theta)
+    assert [d.x for d in res.survivors] == [int(x[0][i]) for i in want]
+    assert res.suppressed_count == 700 - len(want)

@@ -71,3 +71,14 @@ def test_golden_case_coverage(golden_cases):
     assert {0.0, 0.1, 0.3, 0.5, 0.9, 1.0} <= thetas
     assert any(c.by_index for c in golden_cases) and any(not c.by_index for c in golden_cases)
     assert any(c.d_max > c.count for c in golden_cases) and any(c.count == 0 for c in golden_cases)
+
+
+def test_c_oracle_greedy_matches_reference():
+    from conftest import GOLDEN
+
+    g = np.load(GOLDEN / "greedy.npz")
+    for off, n, koff, klen, theta in g["meta"]:
+        off, n, koff, klen = int(off), int(n), int(koff), int(klen)
+        sl = slice(off, off + n)
+        keep = c_oracle.greedy_frame(g["x"][sl], g["y"][sl], g["z"][sl], g["s"][sl], n, float(theta))
+        assert np.array_equal(keep, g["keep"][koff:koff + klen]), (n, theta)
