@@ -130,6 +130,11 @@ int pnms_validate(const int32_t* x, const int32_t* y, const int32_t* z, const do
                   const int32_t* counts, int batch, int n_max, int32_t* first_bad, int32_t* reason,
                   void* stream);
 
+/* Compact ingest: widen int16 x/y/z planes (pixel coordinates of images < 32768 px, 6 B per
+ * box instead of 12) into the int32 planes pnms_run consumes.  n = number of slots. */
+int pnms_widen_i16(const int16_t* x16, const int16_t* y16, const int16_t* z16, int32_t* x, int32_t* y,
+                   int32_t* z, long long n, void* stream);
+
 /* Diagnostics: device counter (uint64) that the binned path atomically increments by the
  * number of pair tests it executes; NULL disables (default).  Process-wide, not reentrant. */
 int pnms_debug_count_pairs(uint64_t* device_counter);

@@ -21,6 +21,7 @@ EXPORTED_SYMBOLS = (
     "pnms_reduce_rows",
     "pnms_validate",
     "pnms_greedy_run",
+    "pnms_widen_i16",
     "pnms_debug_count_pairs",
     "pnms_strerror",
     "pnms_last_cuda_error",
@@ -83,6 +84,8 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
     lib.pnms_validate.restype = i32
     lib.pnms_greedy_run.argtypes = [vp, vp, vp, vp, vp, i32, i32, f64, vp, vp, vp, vp]
     lib.pnms_greedy_run.restype = i32
+    lib.pnms_widen_i16.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_longlong, vp]
+    lib.pnms_widen_i16.restype = i32
     lib.pnms_debug_count_pairs.argtypes = [vp]
     lib.pnms_debug_count_pairs.restype = i32
     lib.pnms_strerror.argtypes = [i32]

@@ -26,6 +26,29 @@
 
 using namespace pnms;
 
+namespace pnms {
+// int16 ingest planes -> the int32 planes the engine consumes (4 slots per thread, vectorised)
+__global__ void __launch_bounds__(256) pnms_widen_i16_kernel(const int16_t* __restrict__ x16, const int16_t* __restrict__ y16,
+                                                             const int16_t* __restrict__ z16, int32_t* __restrict__ x,
+                                                             int32_t* __restrict__ y, int32_t* __restrict__ z, long long n) {
+  const long long stride = (long long)gridDim.x * blockDim.x * 4;
+  for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < n; i += stride) {
+    if (i + 3 < n && ((reinterpret_cast<uintptr_t>(x16 + i) | reinterpret_cast<uintptr_t>(y16 + i) |
+                       reinterpret_cast<uintptr_t>(z16 + i)) & 7) == 0 &&
+        ((reinterpret_cast<uintptr_t>(x + i) | reinterpret_cast<uintptr_t>(y + i) | reinterpret_cast<uintptr_t>(z + i)) & 15) == 0) {
+      const short4 a = *reinterpret_cast<const short4*>(x16 + i);
+      const short4 b = *reinterpret_cast<const short4*>(y16 + i);
+      const short4 c = *reinterpret_cast<const short4*>(z16 + i);
+      *reinterpret_cast<int4*>(x + i) = make_int4(a.x, a.y, a.z, a.w);
+      *reinterpret_cast<int4*>(y + i) = make_int4(b.x, b.y, b.z, b.w);
+      *reinterpret_cast<int4*>(z + i) = make_int4(c.x, c.y, c.z, c.w);
+    } else {
+      for (long long k = i; k < min(i + 4, n); ++k) { x[k] = x16[k]; y[k] = y16[k]; z[k] = z16[k]; }
+    }
+  }
+}
+}  // namespace pnms
+
 namespace {
 
 thread_local int g_last_cuda_error = 0;
@@ -250,6 +273,16 @@ int pnms_greedy_run(const int32_t* x, const int32_t* y, const int32_t* z, const 
   pnms_greedy_frame<<<batch, kGreedyThreads, smem, st>>>(ga);
   if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
   return PNMS_OK;
+}
+
+int pnms_widen_i16(const int16_t* x16, const int16_t* y16, const int16_t* z16, int32_t* x, int32_t* y, int32_t* z,
+                   long long n, void* stream) {
+  if (n < 0 || (n > 0 && (!x16 || !y16 || !z16 || !x || !y || !z))) return PNMS_EINVAL_ARG;
+  if (n == 0) return PNMS_OK;
+  const long long blocks = std::min<long long>((n + 1023) / 1024, 148LL * 16);
+  pnms_widen_i16_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x16, y16, z16, x, y, z, n);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? PNMS_OK : fail_cuda(e);
 }
 
 int pnms_debug_count_pairs(uint64_t* device_counter) {

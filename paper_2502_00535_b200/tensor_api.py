@@ -266,14 +266,33 @@ class NmsEngine:
         return self._dev_in
 
     def run_host(self, hx, hy, hz, hs, hcounts, out_mask, out_count):
-        """Pinned host planes in, pinned host survivor masks [B, W32] int32 + counts [B] out."""
+        """Pinned host planes in, pinned host survivor masks [B, W32] int32 + counts [B] out.
+
+        x/y/z may be int32 or int16 planes (int16: pixel coordinates < 32768, 6 B per box on
+        the wire instead of 12; widened on the device by pnms_widen_i16)."""
         dx, dy, dz, ds, dc = self._device_inputs()
+        packed = hx.dtype == torch.int16
+        if packed and getattr(self, "_dev16", None) is None:
+            shp = (self.batch, self.n_max)
+            self._dev16 = tuple(torch.empty(shp, dtype=torch.int16, device=self.device) for _ in range(3))
         cur = torch.cuda.current_stream(self.device)
+        lib = _lib.load()
         for k, (a, b) in enumerate(self.bounds):
             st = self.streams[k % len(self.streams)]
             st.wait_stream(cur)
             with torch.cuda.stream(st):
-                for d, h in ((dx, hx), (dy, hy), (dz, hz), (ds, hs), (dc, hcounts)):
+                if packed:
+                    x16, y16, z16 = self._dev16
+                    for d, h in ((x16, hx), (y16, hy), (z16, hz)):
+                        d[a:b].copy_(h[a:b], non_blocking=True)
+                    rc = lib.pnms_widen_i16(x16[a:b].data_ptr(), y16[a:b].data_ptr(), z16[a:b].data_ptr(),
+                                            dx[a:b].data_ptr(), dy[a:b].data_ptr(), dz[a:b].data_ptr(),
+                                            (b - a) * self.n_max, st.cuda_stream)
+                    _lib.check(rc, "pnms_widen_i16")
+                    planes = ((ds, hs), (dc, hcounts))
+                else:
+                    planes = ((dx, hx), (dy, hy), (dz, hz), (ds, hs), (dc, hcounts))
+                for d, h in planes:
                     d[a:b].copy_(h[a:b], non_blocking=True)
                 batched_nms_keep(dx[a:b], dy[a:b], dz[a:b], ds[a:b], dc[a:b], self.theta, self.tie_break,
                                  self.d_max, keep_idx=None, keep_count=self.keep_count[a:b],

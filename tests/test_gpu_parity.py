@@ -407,3 +407,24 @@ def test_greedy_batch_vs_oracle(theta):
     want = c_oracle.greedy_frame(x[0], y[0], z[0], s[0], 700, theta)
     assert [d.x for d in res.survivors] == [int(x[0][i]) for i in want]
     assert res.suppressed_count == 700 - len(want)
+
+
+def test_engine_run_host_int16_and_int32_agree():
+    """NmsEngine.run_host: pinned host planes (int32 and compact int16) -> same masks/counts
+    as the device-resident run."""
+    from paper_2502_00535_b200 import NmsEngine
+
+    x, y, z, s = random_frames(37, 500, seed=12)
+    eng = NmsEngine(37, 500, 0.5, chunks=3)
+    dev = [torch.from_numpy(a).to(DEV) for a in (x, y, z, s)]
+    eng.run_device(*dev, want_mask=True)
+    ref_mask, ref_cnt = eng.keep_mask.clone(), eng.keep_count.clone()
+    for dt in (np.int32, np.int16):
+        hx, hy, hz = (torch.from_numpy(a.astype(dt)).pin_memory() for a in (x, y, z))
+        hs = torch.from_numpy(s).pin_memory()
+        hc = torch.full((37,), 500, dtype=torch.int32).pin_memory()
+        om = torch.empty((37, eng.W32), dtype=torch.int32).pin_memory()
+        oc = torch.empty((37,), dtype=torch.int32).pin_memory()
+        eng.run_host(hx, hy, hz, hs, hc, om, oc)
+        torch.cuda.synchronize()
+        assert torch.equal(om, ref_mask.cpu()) and torch.equal(oc, ref_cnt.cpu()), dt
