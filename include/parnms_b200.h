@@ -135,6 +135,11 @@ int pnms_validate(const int32_t* x, const int32_t* y, const int32_t* z, const do
 int pnms_widen_i16(const int16_t* x16, const int16_t* y16, const int16_t* z16, int32_t* x, int32_t* y,
                    int32_t* z, long long n, void* stream);
 
+/* Compact ingest: unpack 32-bit boxes  box = x | y << 12 | z << 24  (x, y < 4096, z < 256:
+ * frames up to 4096x4096 px, e.g. 1080p and 4K; 4 B per box instead of 12) into the int32
+ * planes pnms_run consumes.  n = number of slots. */
+int pnms_unpack_box32(const uint32_t* box, int32_t* x, int32_t* y, int32_t* z, long long n, void* stream);
+
 /* Diagnostics: device counter (uint64) that the binned path atomically increments by the
  * number of pair tests it executes; NULL disables (default).  Process-wide, not reentrant. */
 int pnms_debug_count_pairs(uint64_t* device_counter);

@@ -22,6 +22,7 @@ EXPORTED_SYMBOLS = (
     "pnms_validate",
     "pnms_greedy_run",
     "pnms_widen_i16",
+    "pnms_unpack_box32",
     "pnms_debug_count_pairs",
     "pnms_strerror",
     "pnms_last_cuda_error",
@@ -86,6 +87,8 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
     lib.pnms_greedy_run.restype = i32
     lib.pnms_widen_i16.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_longlong, vp]
     lib.pnms_widen_i16.restype = i32
+    lib.pnms_unpack_box32.argtypes = [vp, vp, vp, vp, ctypes.c_longlong, vp]
+    lib.pnms_unpack_box32.restype = i32
     lib.pnms_debug_count_pairs.argtypes = [vp]
     lib.pnms_debug_count_pairs.restype = i32
     lib.pnms_strerror.argtypes = [i32]

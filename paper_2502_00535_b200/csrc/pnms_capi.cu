@@ -47,6 +47,27 @@ __global__ void __launch_bounds__(256) pnms_widen_i16_kernel(const int16_t* __re
     }
   }
 }
+
+// packed 32-bit boxes (x | y << 12 | z << 24) -> the int32 planes the engine consumes
+__global__ void __launch_bounds__(256) pnms_unpack_box32_kernel(const uint32_t* __restrict__ box,
+                                                                int32_t* __restrict__ x, int32_t* __restrict__ y,
+                                                                int32_t* __restrict__ z, long long n) {
+  const long long stride = (long long)gridDim.x * blockDim.x * 4;
+  for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < n; i += stride) {
+    if (i + 3 < n && (reinterpret_cast<uintptr_t>(box + i) & 15) == 0 &&
+        ((reinterpret_cast<uintptr_t>(x + i) | reinterpret_cast<uintptr_t>(y + i) | reinterpret_cast<uintptr_t>(z + i)) & 15) == 0) {
+      const uint4 b = __ldcs(reinterpret_cast<const uint4*>(box + i));
+      *reinterpret_cast<int4*>(x + i) = make_int4(b.x & 0xFFF, b.y & 0xFFF, b.z & 0xFFF, b.w & 0xFFF);
+      *reinterpret_cast<int4*>(y + i) = make_int4((b.x >> 12) & 0xFFF, (b.y >> 12) & 0xFFF, (b.z >> 12) & 0xFFF, (b.w >> 12) & 0xFFF);
+      *reinterpret_cast<int4*>(z + i) = make_int4(b.x >> 24, b.y >> 24, b.z >> 24, b.w >> 24);
+    } else {
+      for (long long k = i; k < min(i + 4, n); ++k) {
+        const uint32_t v = box[k];
+        x[k] = v & 0xFFF; y[k] = (v >> 12) & 0xFFF; z[k] = v >> 24;
+      }
+    }
+  }
+}
 }  // namespace pnms
 
 namespace {
@@ -281,6 +302,15 @@ int pnms_widen_i16(const int16_t* x16, const int16_t* y16, const int16_t* z16, i
   if (n == 0) return PNMS_OK;
   const long long blocks = std::min<long long>((n + 1023) / 1024, 148LL * 16);
   pnms_widen_i16_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x16, y16, z16, x, y, z, n);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? PNMS_OK : fail_cuda(e);
+}
+
+int pnms_unpack_box32(const uint32_t* box, int32_t* x, int32_t* y, int32_t* z, long long n, void* stream) {
+  if (n < 0 || (n > 0 && (!box || !x || !y || !z))) return PNMS_EINVAL_ARG;
+  if (n == 0) return PNMS_OK;
+  const long long blocks = std::min<long long>((n + 1023) / 1024, 148LL * 16);
+  pnms_unpack_box32_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(box, x, y, z, n);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? PNMS_OK : fail_cuda(e);
 }

@@ -221,6 +221,25 @@ def nms_keep(boxes: torch.Tensor, scores: torch.Tensor, theta: float = 0.5,
     return idx[0, :k].to(torch.int64)
 
 
+BOX32_MAX_XY = 4095
+BOX32_MAX_Z = 255
+
+
+def pack_box32(x, y, z):
+    """Pack integer x, y, z arrays into the 32-bit box words pnms_unpack_box32 reads:
+    x | y << 12 | z << 24 (x, y in [0, 4095], z in [0, 255] — any frame up to 4096 px on a
+    side).  Returns an int32 numpy array of the same shape (the bit pattern of the uint32
+    word).  Raises ValueError for values outside the packable domain."""
+    import numpy as np
+
+    x, y, z = (np.asarray(a) for a in (x, y, z))
+    if x.size and (x.min() < 0 or y.min() < 0 or z.min() < 0 or x.max() > BOX32_MAX_XY or y.max() > BOX32_MAX_XY
+                   or z.max() > BOX32_MAX_Z):
+        raise ValueError("pack_box32: x, y must be in [0, 4095] and z in [0, 255]")
+    w = x.astype(np.uint32) | (y.astype(np.uint32) << np.uint32(12)) | (z.astype(np.uint32) << np.uint32(24))
+    return w.view(np.int32)
+
+
 class NmsEngine:
     """Reusable batched engine bound to one device: workspace, outputs and pinned staging.
 
@@ -270,30 +289,55 @@ class NmsEngine:
 
         x/y/z may be int32 or int16 planes (int16: pixel coordinates < 32768, 6 B per box on
         the wire instead of 12; widened on the device by pnms_widen_i16)."""
-        dx, dy, dz, ds, dc = self._device_inputs()
-        packed = hx.dtype == torch.int16
-        if packed and getattr(self, "_dev16", None) is None:
-            shp = (self.batch, self.n_max)
-            self._dev16 = tuple(torch.empty(shp, dtype=torch.int16, device=self.device) for _ in range(3))
-        cur = torch.cuda.current_stream(self.device)
+        dx, dy, dz, _, _ = self._device_inputs()
         lib = _lib.load()
+        if hx.dtype == torch.int16:
+            if getattr(self, "_dev16", None) is None:
+                self._dev16 = tuple(torch.empty((self.batch, self.n_max), dtype=torch.int16, device=self.device)
+                                    for _ in range(3))
+            x16, y16, z16 = self._dev16
+
+            def stage(a, b, st):
+                for d, h in ((x16, hx), (y16, hy), (z16, hz)):
+                    d[a:b].copy_(h[a:b], non_blocking=True)
+                _lib.check(lib.pnms_widen_i16(x16[a:b].data_ptr(), y16[a:b].data_ptr(), z16[a:b].data_ptr(),
+                                              dx[a:b].data_ptr(), dy[a:b].data_ptr(), dz[a:b].data_ptr(),
+                                              (b - a) * self.n_max, st.cuda_stream), "pnms_widen_i16")
+        else:
+            def stage(a, b, st):
+                for d, h in ((dx, hx), (dy, hy), (dz, hz)):
+                    d[a:b].copy_(h[a:b], non_blocking=True)
+        self._pipeline(stage, hs, hcounts, out_mask, out_count)
+
+    def run_host_box32(self, hbox, hs, hcounts, out_mask, out_count):
+        """run_host with the packed 32-bit box format of `pack_box32` (x | y<<12 | z<<24 in an
+        int32 plane [B, n_max]): 4 B of geometry per box on the wire, 12 B with the score;
+        unpacked on the device by pnms_unpack_box32."""
+        if hbox.dtype != torch.int32 or hbox.shape != (self.batch, self.n_max):
+            raise ValueError("hbox must be an int32 [batch, n_max] plane of pack_box32 words")
+        dx, dy, dz, _, _ = self._device_inputs()
+        lib = _lib.load()
+        if getattr(self, "_dev32", None) is None:
+            self._dev32 = torch.empty((self.batch, self.n_max), dtype=torch.int32, device=self.device)
+        db = self._dev32
+
+        def stage(a, b, st):
+            db[a:b].copy_(hbox[a:b], non_blocking=True)
+            _lib.check(lib.pnms_unpack_box32(db[a:b].data_ptr(), dx[a:b].data_ptr(), dy[a:b].data_ptr(),
+                                             dz[a:b].data_ptr(), (b - a) * self.n_max, st.cuda_stream),
+                       "pnms_unpack_box32")
+        self._pipeline(stage, hs, hcounts, out_mask, out_count)
+
+    def _pipeline(self, stage, hs, hcounts, out_mask, out_count):
+        dx, dy, dz, ds, dc = self._device_inputs()
+        cur = torch.cuda.current_stream(self.device)
         for k, (a, b) in enumerate(self.bounds):
             st = self.streams[k % len(self.streams)]
             st.wait_stream(cur)
             with torch.cuda.stream(st):
-                if packed:
-                    x16, y16, z16 = self._dev16
-                    for d, h in ((x16, hx), (y16, hy), (z16, hz)):
-                        d[a:b].copy_(h[a:b], non_blocking=True)
-                    rc = lib.pnms_widen_i16(x16[a:b].data_ptr(), y16[a:b].data_ptr(), z16[a:b].data_ptr(),
-                                            dx[a:b].data_ptr(), dy[a:b].data_ptr(), dz[a:b].data_ptr(),
-                                            (b - a) * self.n_max, st.cuda_stream)
-                    _lib.check(rc, "pnms_widen_i16")
-                    planes = ((ds, hs), (dc, hcounts))
-                else:
-                    planes = ((dx, hx), (dy, hy), (dz, hz), (ds, hs), (dc, hcounts))
-                for d, h in planes:
-                    d[a:b].copy_(h[a:b], non_blocking=True)
+                stage(a, b, st)
+                ds[a:b].copy_(hs[a:b], non_blocking=True)
+                dc[a:b].copy_(hcounts[a:b], non_blocking=True)
                 batched_nms_keep(dx[a:b], dy[a:b], dz[a:b], ds[a:b], dc[a:b], self.theta, self.tie_break,
                                  self.d_max, keep_idx=None, keep_count=self.keep_count[a:b],
                                  keep_mask=self.keep_mask[a:b], workspace=self.ws[k % len(self.ws)],

@@ -428,3 +428,28 @@ def test_engine_run_host_int16_and_int32_agree():
         eng.run_host(hx, hy, hz, hs, hc, om, oc)
         torch.cuda.synchronize()
         assert torch.equal(om, ref_mask.cpu()) and torch.equal(oc, ref_cnt.cpu()), dt
+    # packed 32-bit boxes (x | y<<12 | z<<24), 12 B per box with the score
+    from paper_2502_00535_b200 import pack_box32
+
+    hb = torch.from_numpy(pack_box32(x, y, z)).pin_memory()
+    om.zero_(); oc.zero_()
+    eng.run_host_box32(hb, hs, hc, om, oc)
+    torch.cuda.synchronize()
+    assert torch.equal(om, ref_mask.cpu()) and torch.equal(oc, ref_cnt.cpu())
+
+
+def test_unpack_box32_extremes():
+    """pnms_unpack_box32 round-trips the packable domain edges, ragged lengths included."""
+    from paper_2502_00535_b200 import _lib, pack_box32
+
+    rng = np.random.default_rng(3)
+    for n in (1, 3, 4, 5, 1027):
+        x = rng.integers(0, 4096, n); y = rng.integers(0, 4096, n); z = rng.integers(0, 256, n)
+        x[0], y[0], z[0] = 4095, 4095, 255
+        b = torch.from_numpy(pack_box32(x, y, z)).to(DEV)
+        out = [torch.full((n,), -1, dtype=torch.int32, device=DEV) for _ in range(3)]
+        _lib.check(_lib.load().pnms_unpack_box32(b.data_ptr(), *(o.data_ptr() for o in out), n,
+                                                 torch.cuda.current_stream().cuda_stream), "unpack")
+        torch.cuda.synchronize()
+        for o, want in zip(out, (x, y, z)):
+            assert np.array_equal(o.cpu().numpy(), want)

@@ -122,3 +122,17 @@ def test_synth_distribution():
     assert z.min() >= 8 and z.max() <= 64
     assert (x + z <= 1920).all() and (y + z <= 1080).all() and x.min() >= 0
     assert s.min() >= 0.05 and s.max() < 1.0
+
+
+def test_pack_box32_layout_and_domain():
+    """pack_box32 word layout x | y<<12 | z<<24 and its domain checks (host side only)."""
+    import numpy as np
+    import pytest
+
+    from paper_2502_00535_b200.tensor_api import pack_box32
+
+    w = pack_box32(np.array([0, 4095, 7]), np.array([0, 4095, 9]), np.array([0, 255, 1])).view(np.uint32)
+    assert list(w) == [0, 0xFFFFFFFF, 7 | (9 << 12) | (1 << 24)]
+    for bad in ((4096, 0, 0), (0, -1, 0), (0, 0, 256)):
+        with pytest.raises(ValueError):
+            pack_box32(*(np.array([v]) for v in bad))
