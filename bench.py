@@ -333,15 +333,15 @@ def main():
     # the link bound of this path: raw pinned H2D bandwidth of one 256 MiB copy
     lh = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
     ld = flush
-    for _ in range(2):
+    for _ in range(4):
         ld.copy_(lh, non_blocking=True)
     l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0.record(stream)
-    for _ in range(3):
+    for _ in range(10):
         ld.copy_(lh, non_blocking=True)
     l1.record(stream)
     torch.cuda.synchronize(dev)
-    h2d_gbs = 3 * lh.numel() / (l0.elapsed_time(l1) / 1e3) / 1e9
+    h2d_gbs = 10 * lh.numel() / (l0.elapsed_time(l1) / 1e3) / 1e9
     del lh
     for _ in range(args.warmup):
         eng.run_host_box32(hb, hs, hc, om, oc)

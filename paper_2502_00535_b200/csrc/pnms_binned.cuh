@@ -28,6 +28,22 @@ constexpr int kBinMaxSlots = 4096;
 constexpr int kBinMaxCells = 4096;   // upper bound; a frame uses at most max(64, npad) cells
 constexpr int kBinCellMax = 64;
 
+// Binned record (16 B, one LDS.128 per candidate column), narrow7 geometry as RecNarrow:
+//   a  = (x+z+1, y+z+1), nb = (-x, -y)                       packed s16x2
+//   w  = -(T << 17) | skip << 8 | (z+1)                       T = ceil(fl64(theta*(z+1)^2))
+//   k  = high 32 bits of the 64-bit sort key (ascending == score descending)
+// skip = boxes left to the end of the box's cell (<= kBinCellMax).  The pair value
+// d = v*v + w = w_x^2 + skip*2^8 + (z+1) + (w_x*h - T)*2^17 keeps sign(w_x*h - T): the low
+// terms stay below 16129 + 64*256 + 127 < 2^17 (the argument of pair_d).
+// The full keys and input slots live in separate arrays: a column whose high key half equals
+// the row's is resolved by an exact rescan of that row (rare: equal 32-bit prefixes).
+struct __align__(16) RecBin {
+  uint32_t a, nb;
+  int32_t w;
+  uint32_t k;
+};
+static_assert(sizeof(RecBin) == 16, "RecBin layout");
+
 struct BinArgs {
   const int32_t *x, *y, *z;
   const double* s;
@@ -42,107 +58,128 @@ struct BinArgs {
 };
 
 struct __align__(16) BinStats {
-  int mode, minT, maxz, minx, miny, maxx, maxy, big, n_act, pad_;
+  int mode, minz, maxz, minx, miny, maxx, maxy, big, n_act, pad_;
 };
 
 __host__ __device__ inline int binned_max_cells(int npad) { return npad < 64 ? 64 : (npad > kBinMaxCells ? kBinMaxCells : npad); }
 // npad is a multiple of 128, so every region below starts 16-byte aligned
 __host__ __device__ inline int binned_npad(int n_max) { return (n_max + 127) & ~127; }
 inline size_t binned_smem_bytes(int npad) {
-  return (size_t)npad * (16 + 8 + 2 + 2) + (size_t)(binned_max_cells(npad) + 4) * 4 * 2 + (size_t)(npad / 32 + 4) * 4 +
+  return (size_t)npad * (sizeof(RecBin) + 8 + 2) + (size_t)(binned_max_cells(npad) + 4) * 4 + (size_t)(npad / 32 + 4) * 4 +
          64 * 4 + sizeof(BinStats) + 64;
 }
+// boxes each thread keeps in registers between the load, binning and scatter passes
+inline int binned_per_thread(int n_max) { return n_max <= 4 * kBinThreads ? 4 : 8; }
 
-template <bool BY_INDEX>
-__global__ void __launch_bounds__(kBinThreads) pnms_binned_frame(BinArgs a) {
+// floor(v / S) for 0 <= v < 2^16 as one IMAD.HI: M = floor(2^32 / S) + 1 is exact there
+// (v * (M*S - 2^32) < 2^32).  S >= 2^15 makes every quotient 0 (M = 0).
+__device__ __forceinline__ uint32_t div_magic(int S) {
+  return S >= 32768 ? 0u : (uint32_t)(0xFFFFFFFFu / (uint32_t)S) + 1u;
+}
+__device__ __forceinline__ int qdiv(int v, uint32_t M) { return (int)__umulhi((uint32_t)v, M); }
+
+template <bool BY_INDEX, bool COUNT, int PER>
+__global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int f = blockIdx.x;
   const long long fbase = (long long)f * a.n_max;
   const int cnt = frame_count(a.counts, f, a.n_max);
   const int npad = binned_npad(a.n_max);
   // per-box data stored in cell order (positions [cstart[c], cstart[c+1]) = cell c)
-  RecNarrow* recS = reinterpret_cast<RecNarrow*>(smem_raw);                   // [npad] records
-  uint64_t* keyS = reinterpret_cast<uint64_t*>(recS + npad);                  // [npad] sort keys
-  uint16_t* cellof = reinterpret_cast<uint16_t*>(keyS + npad);                // [npad] cell of input slot
-  uint16_t* idxS = cellof + npad;                                             // [npad] input slot
+  RecBin* recS = reinterpret_cast<RecBin*>(smem_raw);                         // [npad] records
+  uint64_t* keyS = reinterpret_cast<uint64_t*>(recS + npad);                  // [npad] full sort keys
+  uint16_t* idxS = reinterpret_cast<uint16_t*>(keyS + npad);                  // [npad] input slots
   const int max_cells = binned_max_cells(npad);
   uint32_t* cstart = reinterpret_cast<uint32_t*>(idxS + npad);                // [cells+2]
-  uint32_t* ccur = cstart + max_cells + 4;                                    // [cells+2]
-  uint32_t* kbits = ccur + max_cells + 4;                                     // [npad/32] survivors
+  uint32_t* kbits = cstart + max_cells + 4;                                   // [npad/32] survivors
   uint32_t* scan_tmp = kbits + npad / 32 + 4;                                 // [64]
   BinStats* st = reinterpret_cast<BinStats*>(scan_tmp + 64);
 
   if (threadIdx.x == 0) {
-    st->mode = kNarrow7; st->minT = 0x7FFFFFFF; st->maxz = 0;
+    st->mode = kNarrow7; st->minz = 0x7FFFFFFF; st->maxz = 0;
     st->minx = st->miny = 0x7FFFFFFF; st->maxx = st->maxy = -0x7FFFFFFF;
     st->big = 0; st->n_act = 0;
   }
   for (int w = threadIdx.x; w < npad / 32; w += kBinThreads) kbits[w] = 0u;
   __syncthreads();
-  if (a.n_max > kBinMaxSlots) {
+  if (a.n_max > PER * kBinThreads) {
     if (threadIdx.x == 0) a.fallback[f] = 1;
     return;
   }
-  // ---- load: records, keys, frame statistics
+  // ---- pass 1: the frame is read from HBM once; each thread keeps its PER boxes in
+  // registers (xy packed as two 16-bit halves — exact for every frame that stays on this
+  // path — and z | cell << 16 | rank-in-cell << 8 later).  Frame statistics.
+  uint32_t xy[PER], zc[PER];
   {
-    int mode = kNarrow7, minT = 0x7FFFFFFF, maxz = 0, n_act = 0;
+    int mode = kNarrow7, minz = 0x7FFFFFFF, maxz = 0, n_act = 0;
     int minx = 0x7FFFFFFF, miny = 0x7FFFFFFF, maxx = -0x7FFFFFFF, maxy = -0x7FFFFFFF;
-    for (int e = threadIdx.x; e < cnt; e += kBinThreads) {
-      const long long g = fbase + e;
-      const int32_t xv = a.x[g], yv = a.y[g], zv = a.z[g];
-      const uint64_t sk = sort_key(a.s[g]);
-      const int m = frame_mode_of(xv, yv, zv);
-      mode = max(mode, m);
-      if (sk != kNanSortKey) {
-        ++n_act;
-        const int T = (m == kNarrow7) ? (int)((uint32_t)(-make_rec_narrow(xv, yv, zv, a.theta, kNarrow7).negT) >> 17) : 0;
-        minT = min(minT, T);
-        maxz = max(maxz, zv);
-        minx = min(minx, xv); maxx = max(maxx, xv);
-        miny = min(miny, yv); maxy = max(maxy, yv);
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int e = threadIdx.x + k * kBinThreads;
+      xy[k] = 0u; zc[k] = 0xFFFFFFFFu;  // 0xFFFFFFFF = no box (slot >= count, or NaN score)
+      if (e < cnt) {
+        const long long g = fbase + e;
+        const int32_t xv = a.x[g], yv = a.y[g], zv = a.z[g];
+        const double sv = a.s[g];
+        mode = max(mode, frame_mode_of(xv, yv, zv));
+        if (sv == sv) {
+          ++n_act;
+          minz = min(minz, zv); maxz = max(maxz, zv);
+          minx = min(minx, xv); maxx = max(maxx, xv);
+          miny = min(miny, yv); maxy = max(maxy, yv);
+          xy[k] = ((uint32_t)xv & 0xFFFFu) | ((uint32_t)yv << 16);
+          zc[k] = (uint32_t)zv & 0xFFu;
+        } else {
+          atomicOr(&kbits[e >> 5], 1u << (e & 31));  // NaN: passes no gate, never suppresses -> survivor
+        }
       }
     }
     mode = __reduce_max_sync(0xFFFFFFFFu, mode);
-    minT = __reduce_min_sync(0xFFFFFFFFu, minT);
+    minz = __reduce_min_sync(0xFFFFFFFFu, minz);
     maxz = __reduce_max_sync(0xFFFFFFFFu, maxz);
     n_act = __reduce_add_sync(0xFFFFFFFFu, n_act);
     minx = __reduce_min_sync(0xFFFFFFFFu, minx); maxx = __reduce_max_sync(0xFFFFFFFFu, maxx);
     miny = __reduce_min_sync(0xFFFFFFFFu, miny); maxy = __reduce_max_sync(0xFFFFFFFFu, maxy);
     if ((threadIdx.x & 31) == 0) {
-      atomicMax(&st->mode, mode); atomicMin(&st->minT, minT); atomicMax(&st->maxz, maxz);
+      atomicMax(&st->mode, mode); atomicMin(&st->minz, minz); atomicMax(&st->maxz, maxz);
       atomicAdd(&st->n_act, n_act);
       atomicMin(&st->minx, minx); atomicMax(&st->maxx, maxx);
       atomicMin(&st->miny, miny); atomicMax(&st->maxy, maxy);
     }
   }
   __syncthreads();
-  const bool eligible = st->mode == kNarrow7 && (st->n_act == 0 || st->minT >= 1);
+  // T_j >= 1 for every active column  <=>  theta > 0 and no zero side (T = 0 only for z = 0,
+  // engine.py:232, or theta*(z+1)^2 == 0)
+  const int n_act = st->n_act;
+  const bool eligible = st->mode == kNarrow7 && (n_act == 0 || (a.theta > 0.0 && st->minz >= 1));
   if (!eligible) {
     if (threadIdx.x == 0) a.fallback[f] = 1;
     return;
   }
   // ---- grid of square cells, side >= max side + 1
   int S = st->maxz + 1, GX = 1, GY = 1;
-  if (st->n_act > 0) {
+  const int ox = st->minx, oy = st->miny;
+  if (n_act > 0) {
     for (;;) {
-      GX = (st->maxx - st->minx) / S + 1;
-      GY = (st->maxy - st->miny) / S + 1;
+      GX = (st->maxx - ox) / S + 1;
+      GY = (st->maxy - oy) / S + 1;
       if ((long long)GX * GY <= max_cells) break;
       S *= 2;
     }
   }
-  const int cells = GX * GY, ox = st->minx, oy = st->miny;
+  const uint32_t M = div_magic(S);
+  const int cells = GX * GY;
   for (int c = threadIdx.x; c < cells + 1; c += kBinThreads) cstart[c] = 0u;
   __syncthreads();
-  for (int e = threadIdx.x; e < cnt; e += kBinThreads) {
-    if (a.s[fbase + e] != a.s[fbase + e]) {  // NaN: passes no gate, never suppresses -> survivor
-      atomicOr(&kbits[e >> 5], 1u << (e & 31));
-      continue;
+  // ---- pass 2: histogram; the atomic's return value is the box's rank inside its cell
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    if (zc[k] != 0xFFFFFFFFu) {
+      const int ex = (int)(xy[k] & 0xFFFFu), ey = (int)(xy[k] >> 16);
+      const int c = qdiv(ey - oy, M) * GX + qdiv(ex - ox, M);
+      const uint32_t r = atomicAdd(&cstart[c], 1u);
+      zc[k] |= ((uint32_t)c << 16) | (min(r, 255u) << 8);
     }
-    const int32_t ex = a.x[fbase + e], ey = a.y[fbase + e];
-    const int c = ((ey - oy) / S) * GX + (ex - ox) / S;
-    cellof[e] = (uint16_t)c;
-    atomicAdd(&cstart[c], 1u);
   }
   __syncthreads();
   // exclusive scan of the cell counts (+ largest cell)
@@ -159,33 +196,40 @@ __global__ void __launch_bounds__(kBinThreads) pnms_binned_frame(BinArgs a) {
     uint32_t run = block_exclusive_scan(sum, scan_tmp, nullptr);
     for (int t = 0; t < per; ++t) {
       const int c = b0 + t;
-      if (c < cells) { const uint32_t v = cstart[c]; cstart[c] = run; ccur[c] = run; run += v; }
+      if (c < cells) { const uint32_t v = cstart[c]; cstart[c] = run; run += v; }
     }
-    if (threadIdx.x == 0) cstart[cells] = st->n_act;
+    if (threadIdx.x == 0) cstart[cells] = n_act;
   }
   __syncthreads();
   if (st->big > kBinCellMax) {
     if (threadIdx.x == 0) a.fallback[f] = 1;
     return;
   }
-  // scatter records, keys and input slots straight into cell order
-  for (int e = threadIdx.x; e < cnt; e += kBinThreads) {
-    const long long g = fbase + e;
-    const double sv = a.s[g];
-    if (sv != sv) continue;
-    const uint32_t pos = atomicAdd(&ccur[cellof[e]], 1u);
-    recS[pos] = make_rec_narrow(a.x[g], a.y[g], a.z[g], a.theta, kNarrow7);
-    keyS[pos] = sort_key(sv);
-    idxS[pos] = (uint16_t)e;
+  // ---- pass 3: scatter records, keys and input slots straight into cell order
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    if (zc[k] != 0xFFFFFFFFu) {
+      const int e = threadIdx.x + k * kBinThreads;
+      const uint32_t pos = cstart[zc[k] >> 16] + ((zc[k] >> 8) & 0xFFu);
+      const int32_t xv = (int32_t)(xy[k] & 0xFFFFu), yv = (int32_t)(xy[k] >> 16), zv = (int32_t)(zc[k] & 0xFFu);
+      const RecNarrow rn = make_rec_narrow(xv, yv, zv, a.theta, kNarrow7);
+      const uint64_t key = sort_key(a.s[fbase + e]);
+      RecBin rb;
+      rb.a = rn.a; rb.nb = rn.nb; rb.w = rn.negT | (zv + 1); rb.k = (uint32_t)(key >> 32);
+      recS[pos] = rb;
+      keyS[pos] = key;
+      idxS[pos] = (uint16_t)e;
+    }
   }
   __syncthreads();
-  // ---- order every cell by (sort key asc == score desc, index asc): insertion sort
+  // ---- order every cell by (sort key asc == score desc, index asc): insertion sort; every
+  // position learns where its cell ends
   for (int c = threadIdx.x; c < cells; c += kBinThreads) {
     const int b = cstart[c], en = cstart[c + 1];
     for (int i = b + 1; i < en; ++i) {
       const uint64_t kv = keyS[i];
       const uint16_t v = idxS[i];
-      const RecNarrow rv = recS[i];
+      const RecBin rv = recS[i];
       int j = i - 1;
       while (j >= b) {
         const uint64_t ku = keyS[j];
@@ -200,48 +244,80 @@ __global__ void __launch_bounds__(kBinThreads) pnms_binned_frame(BinArgs a) {
       idxS[j + 1] = v;
       recS[j + 1] = rv;
     }
+    for (int i = b; i < en; ++i) recS[i].w |= (en - i) << 8;
   }
   __syncthreads();
-  // ---- scan: each valid box against the gate-passing prefix of its neighbour cells.  Rows
-  // are taken in cell order so a warp's lanes walk the same few cell lists (broadcast reads,
-  // similar trip counts).  A row only visits the cells its own extent can reach: a column j
-  // overlapping row i has x_j in [x_i - max_z, x_i + z_i] (and the same for y).
+  // ---- scan: each valid box against the gate-passing prefix of every cell its extent can
+  // reach.  A column j overlapping row i has x_j in [x_i - max_z, x_i + z_i] (same for y), so
+  // the reachable cells of one cell row are contiguous in cell order: one run per cell row.
+  // Inside a run the scan jumps to the end of the current cell at the first column that
+  // fails the gate (the cell's gate-passing columns are its prefix).
   unsigned long long tested = 0;
   const int maxz = st->maxz;
   const bool pad_rule = a.d_max > cnt;
-  for (int p = threadIdx.x; p < st->n_act; p += kBinThreads) {
-    const int i = idxS[p];
-    const uint64_t ki = keyS[p];
-    const RecNarrow ri = recS[p];
-    // corner and side back from the packed record: nb = (-x, -y), zz = (z+1, z+1)
+  const char* rbase = reinterpret_cast<const char*>(recS);
+  for (int p = threadIdx.x; p < n_act; p += kBinThreads) {
+    const RecBin ri = recS[p];
+    const uint32_t zzi = __byte_perm((uint32_t)ri.w, 0u, 0x4040);  // (z+1, z+1)
+    // corner and side back from the packed record: nb = (-x, -y)
     const int32_t ix = -(int32_t)(int16_t)(ri.nb & 0xFFFFu), iy = -(int32_t)(int16_t)(ri.nb >> 16);
-    const int32_t iz = (int32_t)(ri.zz & 0xFFFFu) - 1;
-    const int lx = ix - maxz - ox, ly = iy - maxz - oy;
-    const int cx0 = lx < 0 ? 0 : lx / S, cy0 = ly < 0 ? 0 : ly / S;
-    const int cx1 = min(GX - 1, (ix + iz - ox) / S), cy1 = min(GY - 1, (iy + iz - oy) / S);
-    bool sup = false;
+    const int32_t iz = (int32_t)(ri.w & 0xFF) - 1;
+    const int cx0 = qdiv(max(ix - maxz - ox, 0), M), cy0 = qdiv(max(iy - maxz - oy, 0), M);
+    const int cx1 = min(GX - 1, qdiv(ix + iz - ox, M)), cy1 = min(GY - 1, qdiv(iy + iz - oy, M));
+    const uint32_t pb = (uint32_t)p * (uint32_t)sizeof(RecBin);
+    bool sup = false, tie = false;
     for (int yy = cy0; yy <= cy1 && !sup; ++yy) {
-      for (int xx = cx0; xx <= cx1 && !sup; ++xx) {
-        const int c = yy * GX + xx;
-        const int en = cstart[c + 1];
-        for (int q = cstart[c]; q < en; ++q) {
+      // byte offsets of the run's first record and its end
+      uint32_t qb = cstart[yy * GX + cx0] * (uint32_t)sizeof(RecBin);
+      const uint32_t qe = cstart[yy * GX + cx1 + 1] * (uint32_t)sizeof(RecBin);
+      while (qb < qe) {
+        const uint4 g = *reinterpret_cast<const uint4*>(rbase + qb);  // a, nb, w, k
+        // strict on the high key halves: a subset of the reference's gate; an equal half
+        // (another box) flags the row for the exact rescan below
+        const bool gate = g.w < ri.k;
+        tie |= (g.w == ri.k) & (qb != pb);
+        const uint32_t t1 = __viaddmin_s16x2(ri.a, g.y, zzi);
+        const uint32_t t2 = __viaddmin_s16x2_relu(g.x, ri.nb, t1);
+        const uint32_t v = __vimin_s16x2_relu(t2, __byte_perm(g.z, 0u, 0x4040));
+        if (COUNT && gate) ++tested;
+        if (gate && (int)(v * v) + (int)g.z >= 0) {
+          sup = true;
+          break;
+        }
+        qb += (gate ? 1u : __byte_perm(g.z, 0u, 0x4441)) * (uint32_t)sizeof(RecBin);
+      }
+    }
+    if (!sup && tie) {
+      // exact rescan of this row: the reference's gate on full keys (and slots for by_index)
+      const uint64_t ki = keyS[p];
+      const int ii = idxS[p];
+      for (int yy = cy0; yy <= cy1 && !sup; ++yy) {
+        int q = cstart[yy * GX + cx0];
+        const int qe = cstart[yy * GX + cx1 + 1];
+        while (q < qe) {
           const uint64_t kj = keyS[q];
-          const bool gate = kj < ki || (BY_INDEX && kj == ki && idxS[q] < i);
-          if (!gate) break;
-          ++tested;
-          const RecNarrow rj = recS[q];
-          if (pair_d<kNarrow7>(ri.a, ri.nb, ri.zz, make_uint4(rj.a, rj.nb, rj.zz, (uint32_t)rj.negT)) >= 0) {
-            sup = true;
-            break;
+          const RecBin rj = recS[q];
+          if (kj < ki || (BY_INDEX && kj == ki && (int)idxS[q] < ii)) {
+            const uint32_t t1 = __viaddmin_s16x2(ri.a, rj.nb, zzi);
+            const uint32_t t2 = __viaddmin_s16x2_relu(rj.a, ri.nb, t1);
+            const uint32_t v = __vimin_s16x2_relu(t2, __byte_perm((uint32_t)rj.w, 0u, 0x4040));
+            if ((int)(v * v) + rj.w >= 0) {
+              sup = true;
+              break;
+            }
+            ++q;
+          } else {
+            q += __byte_perm((uint32_t)rj.w, 0u, 0x4441);
           }
         }
       }
     }
+    const int i = idxS[p];
     // implicit padding gate (engine.py:233 with s_j = 0, z_j = 0): rows with s < 0 drop
     if (!sup && pad_rule && a.s[fbase + i] < 0.0) sup = true;
     if (!sup) atomicOr(&kbits[i >> 5], 1u << (i & 31));
   }
-  if (a.pairs_tested) {
+  if (COUNT && a.pairs_tested) {
     tested = __reduce_add_sync(0xFFFFFFFFu, (unsigned)tested);
     if ((threadIdx.x & 31) == 0 && tested) atomicAdd(a.pairs_tested, tested);
   }

@@ -151,7 +151,28 @@ SideStream* side_stream() {
   return &ss;
 }
 std::atomic<size_t> g_small_smem[8];
-std::atomic<size_t> g_binned_smem[2];
+std::atomic<size_t> g_binned_smem[8];
+
+template <bool B, bool C, int P>
+cudaError_t launch_binned_t(const BinArgs& ba, int batch, size_t smem, cudaStream_t st, std::atomic<size_t>& cfg) {
+  cudaError_t e = ensure_smem(pnms_binned_frame<B, C, P>, smem, cfg);
+  if (e != cudaSuccess) return e;
+  pnms_binned_frame<B, C, P><<<batch, kBinThreads, smem, st>>>(ba);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_binned(int variant, const BinArgs& ba, int batch, size_t smem, cudaStream_t st) {
+  switch (variant) {
+    case 0: return launch_binned_t<false, false, 4>(ba, batch, smem, st, g_binned_smem[0]);
+    case 1: return launch_binned_t<true, false, 4>(ba, batch, smem, st, g_binned_smem[1]);
+    case 2: return launch_binned_t<false, true, 4>(ba, batch, smem, st, g_binned_smem[2]);
+    case 3: return launch_binned_t<true, true, 4>(ba, batch, smem, st, g_binned_smem[3]);
+    case 4: return launch_binned_t<false, false, 8>(ba, batch, smem, st, g_binned_smem[4]);
+    case 5: return launch_binned_t<true, false, 8>(ba, batch, smem, st, g_binned_smem[5]);
+    case 6: return launch_binned_t<false, true, 8>(ba, batch, smem, st, g_binned_smem[6]);
+    default: return launch_binned_t<true, true, 8>(ba, batch, smem, st, g_binned_smem[7]);
+  }
+}
 
 // co-resident CTAs for the cooperative binned kernel on the current device (cached)
 int cooperative_blocks(bool by_index) {
@@ -420,13 +441,9 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     ba.pairs_tested = g_pairs_counter;
     const size_t smem = binned_smem_bytes(binned_npad(n_max));
     if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
-    if (tie_break == PNMS_TIE_BY_INDEX) {
-      if ((e = ensure_smem(pnms_binned_frame<true>, smem, g_binned_smem[1])) != cudaSuccess) return fail_cuda(e);
-      pnms_binned_frame<true><<<batch, kBinThreads, smem, st>>>(ba);
-    } else {
-      if ((e = ensure_smem(pnms_binned_frame<false>, smem, g_binned_smem[0])) != cudaSuccess) return fail_cuda(e);
-      pnms_binned_frame<false><<<batch, kBinThreads, smem, st>>>(ba);
-    }
+    const int variant = (tie_break == PNMS_TIE_BY_INDEX ? 1 : 0) + (g_pairs_counter ? 2 : 0) +
+                        (binned_per_thread(n_max) == 8 ? 4 : 0);
+    if ((e = launch_binned(variant, ba, batch, smem, st)) != cudaSuccess) return fail_cuda(e);
     if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
     dense_flags = ws + L.dense;
     if (events) {

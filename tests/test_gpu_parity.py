@@ -156,6 +156,26 @@ def test_binned_mixed_batch_vs_oracle(monkeypatch):
     assert int(counter.item()) > 0  # the binned kernel did run
 
 
+def test_binned_key_prefix_collisions(path):
+    """Scores whose 64-bit keys share the high 32 bits (the binned kernel's fast gate) — plus
+    exact duplicates — force the exact per-row rescan; both tie policies, vs the C oracle."""
+    rng = np.random.default_rng(21)
+    x, y, z, _ = random_frames(16, 700, seed=21)
+    s = np.empty((16, 700))
+    for f in range(16):
+        base = [0.5, 0.75, 0.3125, 0.9][f % 4]
+        s[f] = base + rng.integers(0, 1 << 20, 700) * 2.0 ** -52 * base   # same high key half
+        if f % 2:
+            s[f, ::5] = s[f, 1]                                              # exact ties
+    counts = np.full(16, 700, np.int32)
+    for tie in ("paper_faithful", "by_index"):
+        for theta in (0.2, 0.5):
+            got = _run_batch(x, y, z, s, counts, theta, tie, 700)
+            for f in range(16):
+                want = c_oracle.run_frame(x[f], y[f], z[f], s[f], 700, 700, theta, tie)
+                assert np.array_equal(got[f], want), (f, tie, theta)
+
+
 def test_c4_full_batch_vs_oracle():
     x, y, z, s = random_frames(256, 1024, seed=4)
     counts = np.full(256, 1024, np.int32)
