@@ -121,6 +121,20 @@ int pnms_greedy_run(const int32_t* x, const int32_t* y, const int32_t* z, const 
                     const int32_t* counts, int batch, int n_max, double theta, int32_t* keep_idx,
                     int32_t* keep_count, uint32_t* keep_mask, void* stream);
 
+/* Soft-NMS rescoring (oracles.soft_nms_rescore, oracles.py:88-123) for `batch` frames of up
+ * to 4096 slots: repeatedly select the pending detection with the highest current score
+ * (ties: lowest index) and rescale every pending score by its coverage cov = w*h/(z_sel+1)^2
+ * of the selected box: mode 0 (linear) s *= 1 - cov when cov >= theta; mode 1 (gaussian)
+ * s *= exp(-cov^2 / sigma).  out_s [batch, n_max] float64 receives the rescored scores in
+ * input order (0.0 in padding slots).  status [batch]: 0 ok, 1 a valid score is not finite
+ * and > 0 (the validated domain, detections.py:79-84; frame left unwritten).  rounds
+ * [batch] (may be NULL): parallel resolution rounds used.  Linear mode is bit-identical to
+ * the reference; gaussian mode uses the device exp (<= 1 ulp per factor from libm's).
+ * mode not 0/1 or sigma <= 0 -> PNMS_EINVAL_ARG (oracles.py:108-111).  No workspace. */
+int pnms_soft_rescore(const int32_t* x, const int32_t* y, const int32_t* z, const double* s,
+                      const int32_t* counts, int batch, int n_max, int mode, double theta, double sigma,
+                      double* out_s, int32_t* status, int32_t* rounds, void* stream);
+
 /* Device-side ingest validation (detections.py:60-85, Detection.validate): for each frame,
  * first_bad[f] = the smallest slot index in [0, counts[f]) violating the detection invariants
  * (integer coordinates in [0, 2^24), side >= 1, finite score > 0), or -1; reason[f] says which

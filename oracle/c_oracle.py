@@ -42,6 +42,11 @@ def _load():
             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_double,
             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
         ]
+        lib.oracle_soft_nms.restype = None
+        lib.oracle_soft_nms.argtypes = [
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+            ctypes.c_double, ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p,
+        ]
         _lib = lib
     return _lib
 
@@ -91,3 +96,18 @@ def greedy_frame(x, y, z, s, count: int, theta: float):
     k = lib.oracle_greedy_nms(x.ctypes.data, y.ctypes.data, z.ctypes.data, s.ctypes.data, int(count), float(theta),
                               out.ctypes.data, order.ctypes.data, state.ctypes.data)
     return out[:k].copy()
+
+
+def soft_frame(x, y, z, s, count: int, mode: str, theta: float, sigma: float = 0.5):
+    """Rescored scores of oracles.soft_nms_rescore (oracles.py:88-123), input order."""
+    lib = _load()
+    x = np.ascontiguousarray(x, dtype=np.int32)
+    y = np.ascontiguousarray(y, dtype=np.int32)
+    z = np.ascontiguousarray(z, dtype=np.int32)
+    s = np.ascontiguousarray(s, dtype=np.float64)
+    n = max(int(count), 1)
+    out = np.empty(n, dtype=np.float64)
+    pend = np.empty(n, dtype=np.uint8)
+    lib.oracle_soft_nms(x.ctypes.data, y.ctypes.data, z.ctypes.data, s.ctypes.data, int(count),
+                        0 if mode == "linear" else 1, float(theta), float(sigma), out.ctypes.data, pend.ctypes.data)
+    return out[:count].copy()

@@ -125,3 +125,45 @@ int oracle_greedy_nms(const int32_t* x, const int32_t* y, const int32_t* z, cons
     if (state_scratch[i] == 2) keep_out[kept++] = i;
   return kept;
 }
+
+/* Soft-NMS rescoring restated from oracles.soft_nms_rescore (oracles.py:88-123): repeatedly
+ * select the pending detection with the highest current score (ties: lowest index), drop it
+ * from the pending set, and rescale every pending score by the coverage of the selected box
+ * (oracles.py:31-34: cov = w*h / (z_ref+1)^2 with clamped inclusive extents, computed as a
+ * correctly rounded float64 quotient of exact integers, as Python's int / int is).
+ *   mode 0 (linear):   if cov >= theta: s *= 1.0 - cov
+ *   mode 1 (gaussian): s *= exp(-(cov * cov) / sigma)      (libm exp, as math.exp)
+ * Writes the rescored scores in input order.  Quadratic per selection, like the reference. */
+static double soft_coverage(slot_t c, slot_t r) {
+  long long w = (long long)(c.x + (long long)c.z < r.x + (long long)r.z ? c.x + (long long)c.z : r.x + (long long)r.z) -
+                (long long)(c.x > r.x ? c.x : r.x) + 1;
+  long long h = (long long)(c.y + (long long)c.z < r.y + (long long)r.z ? c.y + (long long)c.z : r.y + (long long)r.z) -
+                (long long)(c.y > r.y ? c.y : r.y) + 1;
+  if (w < 0) w = 0;
+  if (h < 0) h = 0;
+  long long a = ((long long)r.z + 1) * ((long long)r.z + 1);
+  return (double)(w * h) / (double)a;
+}
+
+void oracle_soft_nms(const int32_t* x, const int32_t* y, const int32_t* z, const double* s, int count, int mode,
+                     double theta, double sigma, double* out_s, uint8_t* pending) {
+  for (int i = 0; i < count; ++i) { out_s[i] = s[i]; pending[i] = 1; }
+  for (int left = count; left > 0; --left) {
+    int best = -1;
+    for (int i = 0; i < count; ++i) {
+      if (!pending[i]) continue;
+      if (best < 0 || out_s[i] > out_s[best]) best = i;   /* min over (-s, i) */
+    }
+    pending[best] = 0;
+    slot_t r = slot_at(x, y, z, s, count, best);
+    for (int j = 0; j < count; ++j) {
+      if (!pending[j]) continue;
+      double cov = soft_coverage(slot_at(x, y, z, s, count, j), r);
+      if (mode == 0) {
+        if (cov >= theta) out_s[j] *= 1.0 - cov;
+      } else {
+        out_s[j] *= exp(-(cov * cov) / sigma);
+      }
+    }
+  }
+}

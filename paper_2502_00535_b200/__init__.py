@@ -24,6 +24,7 @@ from .engine import (
     SurvivorMask,
     WorkCounters,
     greedy_nms,
+    soft_nms_rescore,
     map_phase,
     mask_survivors,
     reduce_phase,
@@ -35,7 +36,8 @@ __version__ = "0.1.0"
 
 def __getattr__(name):
     # torch-dependent entry points load lazily so the host-only API imports without CUDA
-    if name in ("batched_nms_keep", "nms_keep", "NmsEngine", "validate_batch", "greedy_nms_keep", "pack_box32"):
+    if name in ("batched_nms_keep", "nms_keep", "NmsEngine", "validate_batch", "greedy_nms_keep", "pack_box32",
+                "soft_nms_rescore_batched"):
         from . import tensor_api
 
         return getattr(tensor_api, name)
@@ -47,4 +49,5 @@ __all__ = [
     "DetectionVector", "NmsConfig", "NmsResult", "ParseError", "SuppressionMatrix", "SurvivorMask",
     "ValidationError", "WorkCounters", "map_phase", "mask_survivors", "reduce_phase", "run_nms",
     "batched_nms_keep", "nms_keep", "NmsEngine", "validate_batch", "greedy_nms", "greedy_nms_keep", "pack_box32",
+    "soft_nms_rescore", "soft_nms_rescore_batched",
 ]

@@ -21,6 +21,7 @@ EXPORTED_SYMBOLS = (
     "pnms_reduce_rows",
     "pnms_validate",
     "pnms_greedy_run",
+    "pnms_soft_rescore",
     "pnms_widen_i16",
     "pnms_unpack_box32",
     "pnms_debug_count_pairs",
@@ -85,6 +86,8 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
     lib.pnms_validate.restype = i32
     lib.pnms_greedy_run.argtypes = [vp, vp, vp, vp, vp, i32, i32, f64, vp, vp, vp, vp]
     lib.pnms_greedy_run.restype = i32
+    lib.pnms_soft_rescore.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, f64, f64, vp, vp, vp, vp]
+    lib.pnms_soft_rescore.restype = i32
     lib.pnms_widen_i16.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_longlong, vp]
     lib.pnms_widen_i16.restype = i32
     lib.pnms_unpack_box32.argtypes = [vp, vp, vp, vp, ctypes.c_longlong, vp]

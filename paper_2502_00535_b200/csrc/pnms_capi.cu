@@ -22,6 +22,7 @@
 #include "pnms_validate.cuh"
 #include "pnms_binned_grid.cuh"
 #include "pnms_greedy.cuh"
+#include "pnms_soft.cuh"
 #include "pnms_sort.cuh"
 
 using namespace pnms;
@@ -313,6 +314,34 @@ int pnms_greedy_run(const int32_t* x, const int32_t* y, const int32_t* z, const 
   const size_t smem = greedy_smem_bytes(n_max);
   if ((e = ensure_smem(pnms_greedy_frame, smem, cfg)) != cudaSuccess) return fail_cuda(e);
   pnms_greedy_frame<<<batch, kGreedyThreads, smem, st>>>(ga);
+  if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
+  return PNMS_OK;
+}
+
+int pnms_soft_rescore(const int32_t* x, const int32_t* y, const int32_t* z, const double* s, const int32_t* counts,
+                      int batch, int n_max, int mode, double theta, double sigma, double* out_s, int32_t* status,
+                      int32_t* rounds, void* stream) {
+  if (mode != 0 && mode != 1) return PNMS_EINVAL_ARG;
+  if (!(sigma > 0.0)) return PNMS_EINVAL_ARG;
+  if (batch < 0 || n_max < 0) return PNMS_EINVAL_ARG;
+  if (n_max > kSoftMaxSlots) return PNMS_ETOO_LARGE;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  if (batch == 0) return PNMS_OK;
+  if (!status) return PNMS_EINVAL_ARG;
+  if (n_max == 0) {
+    if ((e = cudaMemsetAsync(status, 0, sizeof(int32_t) * batch, st)) != cudaSuccess) return fail_cuda(e);
+    return PNMS_OK;
+  }
+  if (!x || !y || !z || !s || !out_s) return PNMS_EINVAL_ARG;
+  SoftArgs sa;
+  sa.x = x; sa.y = y; sa.z = z; sa.s = s; sa.counts = counts;
+  sa.batch = batch; sa.n_max = n_max; sa.mode = mode; sa.theta = theta; sa.sigma = sigma;
+  sa.out_s = out_s; sa.status = status; sa.rounds = rounds;
+  static std::atomic<size_t> cfg{0};
+  const size_t smem = soft_smem_bytes(n_max);
+  if ((e = ensure_smem(pnms_soft_frame, smem, cfg)) != cudaSuccess) return fail_cuda(e);
+  pnms_soft_frame<<<batch, kSoftThreads, smem, st>>>(sa);
   if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
   return PNMS_OK;
 }

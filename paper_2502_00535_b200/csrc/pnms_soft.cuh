@@ -1,0 +1,331 @@
+// pnms_soft.cuh — Soft-NMS rescoring (oracles.soft_nms_rescore, oracles.py:88-123) on the
+// device, bit-identical to the reference's sequential loop for linear mode.
+//
+// Reference semantics: repeatedly select the pending detection with the highest current
+// score (ties: lowest index), remove it from the pending set, and multiply every pending
+// score by a factor of its coverage by the selected box, cov = w*h / (z_sel+1)^2
+// (oracles.py:31-34, clamped inclusive extents, a correctly rounded float64 quotient):
+//   linear:   s *= 1 - cov   when cov >= theta
+//   gaussian: s *= exp(-(cov*cov) / sigma)
+// Non-overlapping pairs have cov = 0 and factor exactly 1.0, so only overlapping pairs
+// interact.
+//
+// Parallel exact resolution.  Factors are <= 1 and scores positive, so scores only fall and
+// the selection keys (-score at selection, index) strictly increase along the reference's
+// sequence.  Hence a box's final score is its initial score times the factors of the
+// overlapping boxes selected before it, applied in selection order.  Every round, each
+// pending box recomputes its tentative score from its already-final overlapping neighbours
+// in key order (an upper bound of its final score, exact once nothing pending can precede
+// it), and a pending box whose (tentative score, index) key precedes the keys of all its
+// pending overlapping neighbours is final: nothing pending can be selected before it.  The
+// box with the globally smallest key always qualifies, so every round finalizes at least one
+// box; typical frames finish in a handful of rounds.  After kSoftMaxRounds rounds (dense
+// crowds) the remaining boxes are finished by the reference's own one-at-a-time loop.
+//
+// Candidates come from spatial cells of side max_z + 1 (3x3 neighbourhood, exact because
+// zero overlap never changes a score); frames with negative coordinates or a crowded cell
+// use every slot.  Scores must be finite and > 0 (the validated domain, detections.py:79-84);
+// frames outside it are flagged in `status` and left unwritten.  Gaussian mode uses CUDA's
+// exp (max 1 ulp from the correctly rounded value; the reference uses libm exp), so its
+// scores match the reference within a few ulps rather than bit for bit.
+#pragma once
+#include "pnms_common.cuh"
+
+namespace pnms {
+
+constexpr int kSoftThreads = 512;
+constexpr int kSoftMaxSlots = 4096;
+constexpr int kSoftCellMax = 64;
+constexpr int kSoftMaxRounds = 96;
+
+enum SoftState : uint8_t { kSoftPending = 0, kSoftReady = 1, kSoftFinal = 2 };
+
+struct SoftArgs {
+  const int32_t *x, *y, *z;
+  const double* s;
+  const int32_t* counts;
+  int batch, n_max;
+  int mode;        // 0 linear, 1 gaussian
+  double theta, sigma;
+  double* out_s;   // [batch, n_max] rescored scores (0.0 in padding slots)
+  int32_t* status; // [batch] 0 ok, 1 scores outside the domain (frame left unwritten)
+  int32_t* rounds; // optional [batch] rounds used (diagnostics)
+};
+
+__host__ __device__ inline int soft_npad(int n_max) { return (n_max + 127) & ~127; }
+inline size_t soft_smem_bytes(int n_max) {
+  const size_t n = (size_t)soft_npad(n_max);
+  const size_t cells = n < 64 ? 64 : n;
+  return n * (4 * 3 + 8 + 8 + 8 + 1 + 1 + 2 + 2) + (cells + 4) * 4 + 64 * 4 + 64;
+}
+
+// the reference's factor of box b on pending box j (oracles.py:31-34, 115-120); `ovl` is
+// false when the boxes do not overlap (factor exactly 1.0)
+__device__ __forceinline__ double soft_apply(double sj, int32_t jx, int32_t jy, int32_t jz, int32_t bx, int32_t by,
+                                             int32_t bz, int mode, double theta, double sigma) {
+  const long long w = min((long long)jx + jz, (long long)bx + bz) - (long long)max(jx, bx) + 1;
+  const long long h = min((long long)jy + jz, (long long)by + bz) - (long long)max(jy, by) + 1;
+  if (w <= 0 || h <= 0) return sj;
+  const long long area = ((long long)bz + 1) * ((long long)bz + 1);
+  const double cov = __ddiv_rn(__ll2double_rn(w * h), __ll2double_rn(area));
+  if (mode == 0) return cov >= theta ? __dmul_rn(sj, __dsub_rn(1.0, cov)) : sj;
+  return __dmul_rn(sj, exp(__ddiv_rn(-__dmul_rn(cov, cov), sigma)));
+}
+
+__device__ __forceinline__ bool soft_overlap(int32_t ax, int32_t ay, int32_t az, int32_t bx, int32_t by, int32_t bz) {
+  const long long w = min((long long)ax + az, (long long)bx + bz) - (long long)max(ax, bx) + 1;
+  const long long h = min((long long)ay + az, (long long)by + bz) - (long long)max(ay, by) + 1;
+  return w > 0 && h > 0;
+}
+
+// (key, index) order: the reference's selection order (oracles.py:113, min over (-s, i))
+__device__ __forceinline__ bool soft_before(uint64_t ka, int ia, uint64_t kb, int ib) {
+  return ka < kb || (ka == kb && ia < ib);
+}
+
+struct SoftFrame {
+  int32_t *sx, *sy, *sz;
+  double *s0, *cur;
+  uint64_t* fkey;
+  uint8_t *state, *dirty;
+  uint16_t *cellof, *list;
+  uint32_t* cstart;   // after the scatter: cstart[c] = end(c) = start(c+1), start(0) = 0
+  int cnt, GX, GY, S, ox, oy;
+  bool bin;
+
+  // visit every candidate slot that may overlap box j (3x3 cells, or every slot)
+  template <class F>
+  __device__ __forceinline__ void for_candidates(int j, F&& fn) const {
+    if (bin) {
+      const int cx = (int)(((long long)sx[j] - ox) / S), cy = (int)(((long long)sy[j] - oy) / S);
+      for (int yy = max(0, cy - 1); yy <= min(GY - 1, cy + 1); ++yy) {
+        const int c0 = yy * GX + max(0, cx - 1), c1 = yy * GX + min(GX - 1, cx + 1);
+        const int b = c0 == 0 ? 0 : (int)cstart[c0 - 1], en = (int)cstart[c1];
+        for (int q = b; q < en; ++q) fn((int)list[q]);
+      }
+    } else {
+      for (int q = 0; q < cnt; ++q) fn(q);
+    }
+  }
+};
+
+__global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int s_stat[10];  // 0 minx 1 miny 2 maxx 3 maxy 4 maxz 5 bin_ok 6 big 7 pending 8 bad 9 arg
+  __shared__ unsigned long long s_best[kSoftThreads / 32];
+  const int f = blockIdx.x;
+  const long long fbase = (long long)f * a.n_max;
+  const int cnt = frame_count(a.counts, f, a.n_max);
+  const int npad = soft_npad(a.n_max);
+  const int max_cells = npad < 64 ? 64 : npad;
+  SoftFrame F;
+  F.sx = reinterpret_cast<int32_t*>(smem_raw);
+  F.sy = F.sx + npad;
+  F.sz = F.sy + npad;
+  F.s0 = reinterpret_cast<double*>(F.sz + npad);
+  F.cur = F.s0 + npad;
+  F.fkey = reinterpret_cast<uint64_t*>(F.cur + npad);
+  F.state = reinterpret_cast<uint8_t*>(F.fkey + npad);
+  F.dirty = F.state + npad;
+  F.cellof = reinterpret_cast<uint16_t*>(F.dirty + npad);
+  F.list = F.cellof + npad;
+  F.cstart = reinterpret_cast<uint32_t*>(F.list + npad);
+  F.cnt = cnt;
+  uint32_t* scan_tmp = F.cstart + max_cells + 4;
+
+  if (threadIdx.x == 0) {
+    s_stat[0] = s_stat[1] = 0x7FFFFFFF;
+    s_stat[2] = s_stat[3] = -0x7FFFFFFF;
+    s_stat[4] = 0; s_stat[5] = 1; s_stat[6] = 0; s_stat[7] = 0; s_stat[8] = 0;
+  }
+  __syncthreads();
+  if (a.n_max > kSoftMaxSlots) {
+    if (threadIdx.x == 0) a.status[f] = 2;
+    return;
+  }
+  // ---- load
+  for (int e = threadIdx.x; e < cnt; e += kSoftThreads) {
+    const long long g = fbase + e;
+    const int32_t xv = a.x[g], yv = a.y[g], zv = a.z[g];
+    const double sv = a.s[g];
+    F.sx[e] = xv; F.sy[e] = yv; F.sz[e] = zv;
+    F.s0[e] = sv; F.cur[e] = sv;
+    F.state[e] = kSoftPending; F.dirty[e] = 0;
+    if (!(sv > 0.0 && sv <= 1.7976931348623157e308)) atomicOr(&s_stat[8], 1);
+    if (xv < 0 || yv < 0 || zv < 0) atomicAnd(&s_stat[5], 0);
+    atomicMin(&s_stat[0], xv); atomicMin(&s_stat[1], yv);
+    atomicMax(&s_stat[2], xv); atomicMax(&s_stat[3], yv); atomicMax(&s_stat[4], zv);
+  }
+  __syncthreads();
+  if (s_stat[8]) {
+    if (threadIdx.x == 0) a.status[f] = 1;
+    return;
+  }
+  // ---- spatial cells (exact: zero overlap leaves a score unchanged)
+  F.bin = s_stat[5] != 0 && cnt > 0;
+  F.S = 1; F.GX = 1; F.GY = 1;
+  F.ox = s_stat[0]; F.oy = s_stat[1];
+  if (F.bin) {
+    F.S = s_stat[4] + 1;
+    if (F.S <= 0) F.bin = false;
+  }
+  if (F.bin) {
+    for (;;) {
+      F.GX = (int)(((long long)s_stat[2] - F.ox) / F.S + 1);
+      F.GY = (int)(((long long)s_stat[3] - F.oy) / F.S + 1);
+      if ((long long)F.GX * F.GY <= max_cells) break;
+      if (F.S > (1 << 29)) { F.GX = F.GY = 1; break; }
+      F.S *= 2;
+    }
+    const int cells = F.GX * F.GY;
+    for (int c = threadIdx.x; c <= cells; c += kSoftThreads) F.cstart[c] = 0u;
+    __syncthreads();
+    for (int e = threadIdx.x; e < cnt; e += kSoftThreads) {
+      const int c = (int)(((long long)F.sy[e] - F.oy) / F.S) * F.GX + (int)(((long long)F.sx[e] - F.ox) / F.S);
+      F.cellof[e] = (uint16_t)c;
+      atomicAdd(&F.cstart[c], 1u);
+    }
+    __syncthreads();
+    {
+      const int per = (cells + 1 + kSoftThreads - 1) / kSoftThreads;
+      const int b0 = threadIdx.x * per;
+      uint32_t sum = 0, big = 0;
+      for (int t = 0; t < per; ++t) {
+        const int c = b0 + t;
+        if (c < cells) { sum += F.cstart[c]; big = max(big, F.cstart[c]); }
+      }
+      big = __reduce_max_sync(0xFFFFFFFFu, big);
+      if ((threadIdx.x & 31) == 0) atomicMax(&s_stat[6], (int)big);
+      uint32_t run = block_exclusive_scan(sum, scan_tmp, nullptr);
+      for (int t = 0; t < per; ++t) {
+        const int c = b0 + t;
+        if (c < cells) { const uint32_t v = F.cstart[c]; F.cstart[c] = run; run += v; }
+      }
+    }
+    __syncthreads();
+    F.bin = s_stat[6] <= kSoftCellMax;
+    if (F.bin) {
+      for (int e = threadIdx.x; e < cnt; e += kSoftThreads) {
+        const uint32_t pos = atomicAdd(&F.cstart[F.cellof[e]], 1u);
+        F.list[pos] = (uint16_t)e;
+      }
+    }
+  }
+  __syncthreads();
+
+  const int mode = a.mode;
+  const double theta = a.theta, sigma = a.sigma;
+  // ---- rounds
+  int round = 0;
+  for (;; ++round) {
+    // A: exact tentative scores of pending boxes whose final neighbour set grew:
+    //    s0 times the factors of the final overlapping neighbours in selection order
+    for (int j = threadIdx.x; j < cnt; j += kSoftThreads) {
+      if (F.state[j] != kSoftPending || !F.dirty[j]) continue;
+      F.dirty[j] = 0;
+      const int32_t jx = F.sx[j], jy = F.sy[j], jz = F.sz[j];
+      double t = F.s0[j];
+      uint64_t lk = 0;
+      int li = -1;
+      for (;;) {
+        uint64_t bk = ~0ull;
+        int bi = 0x7FFFFFFF;
+        F.for_candidates(j, [&](int b) {
+          if (F.state[b] != kSoftFinal) return;
+          const uint64_t kb = F.fkey[b];
+          if (!soft_before(lk, li, kb, b) || !soft_before(kb, b, bk, bi)) return;
+          if (!soft_overlap(jx, jy, jz, F.sx[b], F.sy[b], F.sz[b])) return;
+          bk = kb; bi = b;
+        });
+        if (bi == 0x7FFFFFFF) break;
+        t = soft_apply(t, jx, jy, jz, F.sx[bi], F.sy[bi], F.sz[bi], mode, theta, sigma);
+        lk = bk; li = bi;
+      }
+      F.cur[j] = t;
+    }
+    __syncthreads();
+    if (round >= kSoftMaxRounds) break;
+    // B: a pending box that precedes every pending overlapping neighbour is final
+    for (int j = threadIdx.x; j < cnt; j += kSoftThreads) {
+      if (F.state[j] != kSoftPending) continue;
+      const int32_t jx = F.sx[j], jy = F.sy[j], jz = F.sz[j];
+      const uint64_t kj = sort_key(F.cur[j]);
+      bool ready = true;
+      F.for_candidates(j, [&](int n) {
+        if (!ready || n == j || F.state[n] == kSoftFinal) return;
+        if (!soft_before(sort_key(F.cur[n]), n, kj, j)) return;
+        if (soft_overlap(jx, jy, jz, F.sx[n], F.sy[n], F.sz[n])) ready = false;
+      });
+      if (ready) F.state[j] = kSoftReady;
+    }
+    __syncthreads();
+    // C: finalize; pending overlapping neighbours must recompute
+    for (int j = threadIdx.x; j < cnt; j += kSoftThreads) {
+      if (F.state[j] != kSoftReady) continue;
+      F.fkey[j] = sort_key(F.cur[j]);
+      F.state[j] = kSoftFinal;
+      const int32_t jx = F.sx[j], jy = F.sy[j], jz = F.sz[j];
+      F.for_candidates(j, [&](int n) {
+        if (F.state[n] == kSoftPending && soft_overlap(jx, jy, jz, F.sx[n], F.sy[n], F.sz[n])) F.dirty[n] = 1;
+      });
+    }
+    if (threadIdx.x == 0) s_stat[7] = 0;
+    __syncthreads();
+    int pend = 0;
+    for (int j = threadIdx.x; j < cnt; j += kSoftThreads) pend += F.state[j] != kSoftFinal;
+    pend = __reduce_add_sync(0xFFFFFFFFu, pend);
+    if ((threadIdx.x & 31) == 0 && pend) atomicAdd(&s_stat[7], pend);
+    __syncthreads();
+    if (s_stat[7] == 0) break;
+    __syncthreads();
+  }
+  // ---- dense crowds: finish with the reference's loop (cur is exact for every pending box)
+  if (round >= kSoftMaxRounds) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (;;) {
+      // argmin over pending of (sort key, index): pack (key >> 12 is not exact) -> two passes
+      uint64_t bk = ~0ull;
+      int bi = 0x7FFFFFFF;
+      for (int j = threadIdx.x; j < cnt; j += kSoftThreads) {
+        if (F.state[j] == kSoftFinal) continue;
+        const uint64_t kj = sort_key(F.cur[j]);
+        if (soft_before(kj, j, bk, bi)) { bk = kj; bi = j; }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const uint64_t ok = __shfl_xor_sync(0xFFFFFFFFu, bk, o);
+        const int oi = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
+        if (soft_before(ok, oi, bk, bi)) { bk = ok; bi = oi; }
+      }
+      if (lane == 0) { s_best[warp] = bk; scan_tmp[warp] = (uint32_t)bi; }
+      __syncthreads();
+      if (warp == 0) {
+        bk = lane < kSoftThreads / 32 ? s_best[lane] : ~0ull;
+        bi = lane < kSoftThreads / 32 ? (int)scan_tmp[lane] : 0x7FFFFFFF;
+        for (int o = 16; o; o >>= 1) {
+          const uint64_t ok = __shfl_xor_sync(0xFFFFFFFFu, bk, o);
+          const int oi = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
+          if (soft_before(ok, oi, bk, bi)) { bk = ok; bi = oi; }
+        }
+        if (lane == 0) s_stat[9] = bi;
+      }
+      __syncthreads();
+      const int b = s_stat[9];
+      if (b == 0x7FFFFFFF) break;
+      const int32_t bx = F.sx[b], by = F.sy[b], bz = F.sz[b];
+      for (int j = threadIdx.x; j < cnt; j += kSoftThreads) {
+        if (j == b || F.state[j] == kSoftFinal) continue;
+        F.cur[j] = soft_apply(F.cur[j], F.sx[j], F.sy[j], F.sz[j], bx, by, bz, mode, theta, sigma);
+      }
+      if (threadIdx.x == 0) F.state[b] = kSoftFinal;
+      __syncthreads();
+    }
+  }
+  // ---- rescored scores, input order
+  for (int e = threadIdx.x; e < a.n_max; e += kSoftThreads) a.out_s[fbase + e] = e < cnt ? F.cur[e] : 0.0;
+  if (threadIdx.x == 0) {
+    a.status[f] = 0;
+    if (a.rounds) a.rounds[f] = round;
+  }
+}
+
+}  // namespace pnms

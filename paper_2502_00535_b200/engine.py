@@ -242,7 +242,31 @@ def greedy_nms(d: DetectionVector, theta: float) -> NmsResult:
     return NmsResult(survivors, count - len(survivors))
 
 
+def soft_nms_rescore(d: DetectionVector, mode: str, theta: float, sigma: float = 0.5) -> DetectionVector:
+    """Soft-NMS rescoring (oracles.soft_nms_rescore, oracles.py:88-123) on the GPU.
+
+    Same arguments, errors and result as the reference: the rescored vector in input order,
+    capacity d.d_max, built without validation (decayed scores may reach zero)."""
+    torch = _torch()
+    from .detections import ValidationError
+    from .tensor_api import _check_soft, soft_nms_rescore_batched
+
+    _check_soft(mode, sigma)
+    count = int(d.count)
+    if count == 0:
+        return DetectionVector([], d.d_max, validate=False)
+    x, y, z, s = _frame_columns(d)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    t = lambda a: torch.from_numpy(np.array(a[:count])).reshape(1, count).to(dev)  # noqa: E731
+    out, status = soft_nms_rescore_batched(t(x), t(y), t(z), t(s), None, mode, theta, sigma)
+    if int(status.item()) != 0:
+        raise ValidationError("soft_nms_rescore needs finite scores > 0 (Detection.validate domain)")
+    sc = out[0].cpu().numpy()
+    return DetectionVector.from_arrays(np.asarray(x[:count]), np.asarray(y[:count]), np.asarray(z[:count]), sc,
+                                       d.d_max, validate=False)
+
+
 __all__ = [
     "ConfigError", "NmsConfig", "SuppressionMatrix", "SurvivorMask", "WorkCounters",
-    "map_phase", "reduce_phase", "mask_survivors", "run_nms", "greedy_nms", "Detection",
+    "map_phase", "reduce_phase", "mask_survivors", "run_nms", "greedy_nms", "soft_nms_rescore", "Detection",
 ]

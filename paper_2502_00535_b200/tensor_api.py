@@ -202,6 +202,43 @@ def greedy_nms_keep(x: torch.Tensor, y: torch.Tensor, z: torch.Tensor, s: torch.
     return keep_idx, keep_count
 
 
+SOFT_MODES = {"linear": 0, "gaussian": 1}
+
+
+def _check_soft(mode: str, sigma: float) -> int:
+    # the reference's own checks and messages (oracles.py:108-111)
+    if mode not in SOFT_MODES:
+        raise ValueError(f"unknown mode {mode!r}")
+    if sigma <= 0:
+        raise ValueError(f"sigma must be positive, got {sigma}")
+    return SOFT_MODES[mode]
+
+
+def soft_nms_rescore_batched(x: torch.Tensor, y: torch.Tensor, z: torch.Tensor, s: torch.Tensor,
+                             counts: torch.Tensor | None = None, mode: str = "linear", theta: float = 0.3,
+                             sigma: float = 0.5, *, out: torch.Tensor | None = None, rounds: torch.Tensor | None = None):
+    """Soft-NMS rescoring of every frame (oracles.soft_nms_rescore, oracles.py:88-123) on the
+    device.  Returns (scores [B, n_max] float64 in input order, status [B] int32: 0 ok, 1 a
+    score outside the validated domain (finite, > 0)).  Frames of up to 4096 slots."""
+    code = _check_soft(mode, sigma)
+    _require_cuda(x, "x", torch.int32, 2)
+    B, n_max = x.shape
+    for t, nm in ((y, "y"), (z, "z")):
+        _require_cuda(t, nm, torch.int32, 2)
+    _require_cuda(s, "s", torch.float64, 2)
+    if counts is not None:
+        _require_cuda(counts, "counts", torch.int32, 1)
+    dev = x.device
+    if out is None:
+        out = torch.empty((B, n_max), dtype=torch.float64, device=dev)
+    status = torch.empty((B,), dtype=torch.int32, device=dev)
+    p = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+    st = _lib.load().pnms_soft_rescore(p(x), p(y), p(z), p(s), p(counts), B, n_max, code, float(theta), float(sigma),
+                                       p(out), p(status), p(rounds), torch.cuda.current_stream(dev).cuda_stream)
+    _lib.check(st, "pnms_soft_rescore")
+    return out, status
+
+
 def nms_keep(boxes: torch.Tensor, scores: torch.Tensor, theta: float = 0.5,
              tie_break: str = "paper_faithful", d_max: int | None = None) -> torch.Tensor:
     """Single-frame NMS: boxes [N, 3] (x, y, z) integer CUDA tensor, scores [N] float64.

@@ -13,6 +13,8 @@ Writes, next to this script:
                C4[0:8]  = random_frame(1024, f, 1920, 1080, (8, 64))
                C5[0:4]  = random_frame(2048, f, 1920, 1080, (8, 64))
   kats.json    SPEC.md known-answer examples evaluated by the reference itself.
+  greedy.npz   oracles.greedy_nms keep indices on seeded frames.
+  soft.npz     oracles.soft_nms_rescore rescored scores (linear and gaussian) on seeded frames.
 The reference is only imported here; nothing at test/bench time reads /root/reference.
 """
 
@@ -32,6 +34,7 @@ from parnms import (  # noqa: E402
     Detection, DetectionVector, NmsConfig, WorkloadSpec, chain_fixture, generate_frame, greedy_nms, map_phase,
     random_frame, reduce_phase, run_nms, toy_frame,
 )
+from parnms.oracles import soft_nms_rescore  # noqa: E402
 from parnms.overlap import intersection_extent, suppression_test  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
@@ -248,6 +251,42 @@ def make_greedy():
                 keep=cat("keep", np.int32), meta=np.array(out["meta"], dtype=np.float64))
 
 
+def make_soft():
+    """oracles.soft_nms_rescore (oracles.py:88-123) rescored scores on seeded frames, both
+    modes, several theta / sigma (valid inputs: finite positive scores)."""
+    rng = np.random.default_rng(88123)
+    out = {"x": [], "y": [], "z": [], "s": [], "out": [], "meta": []}
+    off = 0
+
+    def add(vec, mode, theta, sigma):
+        nonlocal off
+        res = soft_nms_rescore(vec, mode, theta, sigma)
+        x, y, z, s = valid_arrays(vec)
+        out["x"].append(x); out["y"].append(y); out["z"].append(z); out["s"].append(s)
+        out["out"].append(np.array([d.s for d in res.valid()], dtype=np.float64))
+        out["meta"].append((off, len(x), 0 if mode == "linear" else 1, theta, sigma))
+        off += len(x)
+
+    for t in range(160):
+        n = int(rng.integers(0, 130))
+        fw = int(rng.choice([96, 256, 512]))
+        mode = "linear" if t % 2 == 0 else "gaussian"
+        theta = [0.0, 0.1, 0.3, 0.5, 0.9, 1.0][t % 6] if t % 5 else float(rng.uniform(0, 1))
+        sigma = [0.5, 0.1, 1.0, 2.5][t % 4]
+        vec = random_frame(n, seed=int(rng.integers(0, 2**31)), frame_w=fw, frame_h=fw,
+                           z_range=(1, 40) if fw <= 256 else (4, 90), duplicate_fraction=0.2 if t % 4 == 0 else 0.0)
+        add(vec, mode, theta, sigma)
+    add(toy_frame(), "linear", 0.3, 0.5)
+    vec, th = chain_fixture()
+    add(vec, "linear", th, 0.5)
+    add(vec, "gaussian", th, 0.5)
+    for f, mode in enumerate(("linear", "gaussian")):
+        add(random_frame(512, seed=f, frame_w=1920 // 2, frame_h=1080 // 2, z_range=(8, 64)), mode, 0.3, 0.5)
+    cat = lambda k, dt: np.concatenate(out[k]).astype(dt)  # noqa: E731
+    return dict(x=cat("x", np.int64), y=cat("y", np.int64), z=cat("z", np.int64), s=cat("s", np.float64),
+                out=cat("out", np.float64), meta=np.array(out["meta"], dtype=np.float64))
+
+
 def make_kats():
     k = {}
     k["intersection_extent"] = [[a, b, c, d, intersection_extent(a, b, c, d)]
@@ -270,12 +309,16 @@ def make_kats():
 
 
 def main():
+    if "--only-soft" in sys.argv:
+        np.savez_compressed(OUT / "soft.npz", **make_soft())
+        return
     cases = make_cases()
     np.savez_compressed(OUT / "cases.npz", **pack_cases(cases))
     print(f"cases: {len(cases)}")
     (OUT / "kats.json").write_text(json.dumps(make_kats(), indent=1) + "\n")
     np.savez_compressed(OUT / "configs.npz", **make_configs())
     np.savez_compressed(OUT / "greedy.npz", **make_greedy())
+    np.savez_compressed(OUT / "soft.npz", **make_soft())
 
 
 if __name__ == "__main__":

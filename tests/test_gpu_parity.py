@@ -473,3 +473,91 @@ def test_unpack_box32_extremes():
         torch.cuda.synchronize()
         for o, want in zip(out, (x, y, z)):
             assert np.array_equal(o.cpu().numpy(), want)
+
+
+# ---------------------------------------------------------------- Soft-NMS (oracles.py:88-123)
+GAUSS_RTOL = 1e-13   # gaussian mode: device exp vs libm exp (<= 1 ulp per factor); linear is exact
+
+
+def _soft_check(got, want, mode, what):
+    if mode in (0, "linear"):
+        assert np.array_equal(np.asarray(got).view(np.uint64), np.asarray(want).view(np.uint64)), what
+    else:
+        np.testing.assert_allclose(got, want, rtol=GAUSS_RTOL, atol=0, err_msg=str(what))
+
+
+def test_soft_nms_matches_reference_goldens():
+    """Every soft.npz frame (the reference's own rescored scores) through the engine-level
+    drop-in soft_nms_rescore."""
+    from conftest import GOLDEN
+    from paper_2502_00535_b200 import soft_nms_rescore
+
+    g = np.load(GOLDEN / "soft.npz")
+    for off, n, mode, theta, sigma in g["meta"]:
+        off, n = int(off), int(n)
+        sl = slice(off, off + n)
+        vec = DetectionVector.from_arrays(g["x"][sl], g["y"][sl], g["z"][sl], g["s"][sl], max(n, 1))
+        res = soft_nms_rescore(vec, "linear" if mode == 0 else "gaussian", float(theta), float(sigma))
+        assert res.count == n and res.d_max == max(n, 1)
+        assert np.array_equal(res.xs[:n], g["x"][sl]) and np.array_equal(res.zs[:n], g["z"][sl])
+        _soft_check(res.ss[:n], g["out"][sl], int(mode), (n, mode, theta, sigma))
+
+
+@pytest.mark.parametrize("mode", ["linear", "gaussian"])
+def test_soft_nms_batched_vs_oracle(mode):
+    """A ragged batch of C4-sized frames (and clustered, duplicated ones) vs the C oracle."""
+    from paper_2502_00535_b200 import soft_nms_rescore_batched
+
+    x, y, z, s = random_frames(24, 1024, seed=31, duplicate_fraction=0.1)
+    x[3:6] //= 4; y[3:6] //= 4                      # dense frames: long dependency chains
+    counts = np.full(24, 1024, np.int32)
+    counts[1], counts[2], counts[7] = 0, 1, 333
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)  # noqa: E731
+    rounds = torch.zeros(24, dtype=torch.int32, device=DEV)
+    out, status = soft_nms_rescore_batched(t(x), t(y), t(z), t(s), t(counts), mode, 0.3, 0.5, rounds=rounds)
+    out, status = out.cpu().numpy(), status.cpu().numpy()
+    assert (status == 0).all()
+    for f in range(24):
+        c = int(counts[f])
+        want = c_oracle.soft_frame(x[f], y[f], z[f], s[f], c, mode, 0.3, 0.5)
+        _soft_check(out[f, :c], want, mode, (f, c))
+        assert (out[f, c:] == 0).all()
+
+
+def test_soft_nms_crowd_fallback_and_unbinned():
+    """A crowd where every box overlaps every other (the parallel rounds give way to the
+    reference's one-at-a-time loop) and a frame with negative coordinates (no cells)."""
+    from paper_2502_00535_b200 import soft_nms_rescore_batched
+
+    rng = np.random.default_rng(5)
+    n = 400
+    x = np.zeros((2, n), np.int32); y = x.copy(); z = x.copy(); s = np.zeros((2, n))
+    x[0] = rng.integers(0, 20, n); y[0] = rng.integers(0, 20, n); z[0] = rng.integers(40, 60, n)
+    x[1] = rng.integers(-300, 300, n); y[1] = rng.integers(-300, 300, n); z[1] = rng.integers(5, 80, n)
+    s[:] = rng.uniform(0.05, 1.0, (2, n))
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)  # noqa: E731
+    for mode in ("linear", "gaussian"):
+        rounds = torch.zeros(2, dtype=torch.int32, device=DEV)
+        out, status = soft_nms_rescore_batched(t(x), t(y), t(z), t(s), None, mode, 0.1, 0.5, rounds=rounds)
+        out = out.cpu().numpy()
+        assert (status.cpu().numpy() == 0).all()
+        assert int(rounds[0].item()) >= 96          # the fallback ran
+        for f in range(2):
+            _soft_check(out[f], c_oracle.soft_frame(x[f], y[f], z[f], s[f], n, mode, 0.1, 0.5), mode, (f, mode))
+
+
+def test_soft_nms_domain_and_argument_errors():
+    from paper_2502_00535_b200 import ValidationError, soft_nms_rescore, soft_nms_rescore_batched
+
+    x, y, z, s = random_frames(2, 50, seed=2)
+    s[1, 7] = 0.0
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)  # noqa: E731
+    out, status = soft_nms_rescore_batched(t(x), t(y), t(z), t(s), None, "linear", 0.3)
+    assert status.cpu().tolist() == [0, 1]
+    vec = DetectionVector.from_arrays(x[1], y[1], z[1], s[1], validate=False)
+    with pytest.raises(ValidationError):
+        soft_nms_rescore(vec, "linear", 0.3)
+    with pytest.raises(ValueError, match="unknown mode 'box'"):
+        soft_nms_rescore(vec, "box", 0.3)
+    with pytest.raises(ValueError, match="sigma must be positive, got 0"):
+        soft_nms_rescore(vec, "gaussian", 0.3, 0)

@@ -82,3 +82,20 @@ def test_c_oracle_greedy_matches_reference():
         sl = slice(off, off + n)
         keep = c_oracle.greedy_frame(g["x"][sl], g["y"][sl], g["z"][sl], g["s"][sl], n, float(theta))
         assert np.array_equal(keep, g["keep"][koff:koff + klen]), (n, theta)
+
+
+def test_c_oracle_soft_nms_matches_reference():
+    """The C restatement of oracles.soft_nms_rescore is bit-identical to the reference's
+    rescored scores (both modes; libm exp is the exp Python's math.exp calls)."""
+    from conftest import GOLDEN
+
+    g = np.load(GOLDEN / "soft.npz")
+    n_frames = 0
+    for off, n, mode, theta, sigma in g["meta"]:
+        off, n = int(off), int(n)
+        sl = slice(off, off + n)
+        got = c_oracle.soft_frame(g["x"][sl], g["y"][sl], g["z"][sl], g["s"][sl], n,
+                                  "linear" if mode == 0 else "gaussian", float(theta), float(sigma))
+        assert np.array_equal(got.view(np.uint64), g["out"][sl].view(np.uint64)), (n, mode, theta, sigma)
+        n_frames += 1
+    assert n_frames > 150
