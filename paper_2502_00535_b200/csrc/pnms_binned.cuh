@@ -51,6 +51,8 @@ struct BinArgs {
   int batch, n_max, d_max, tie_break, W32;
   double theta;
   uint8_t* fallback;      // [batch] 1 = frame left to the dense pipeline
+  int32_t* decl_list;     // declined frames, appended in any order ...
+  int* decl_count;        // ... count (zero before the launch)
   int32_t* keep_idx;
   int32_t* keep_count;
   uint32_t* keep_mask;
@@ -78,6 +80,11 @@ __device__ __forceinline__ uint32_t div_magic(int S) {
 }
 __device__ __forceinline__ int qdiv(int v, uint32_t M) { return (int)__umulhi((uint32_t)v, M); }
 
+__device__ __forceinline__ void binned_decline(const BinArgs& a, int f) {
+  a.fallback[f] = 1;
+  a.decl_list[atomicAdd(a.decl_count, 1)] = f;
+}
+
 template <bool BY_INDEX, bool COUNT, int PER>
 __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -103,7 +110,7 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
   for (int w = threadIdx.x; w < npad / 32; w += kBinThreads) kbits[w] = 0u;
   __syncthreads();
   if (a.n_max > PER * kBinThreads) {
-    if (threadIdx.x == 0) a.fallback[f] = 1;
+    if (threadIdx.x == 0) binned_decline(a, f);
     return;
   }
   // ---- pass 1: the frame is read from HBM once; each thread keeps its PER boxes in
@@ -153,7 +160,7 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
   const int n_act = st->n_act;
   const bool eligible = st->mode == kNarrow7 && (n_act == 0 || (a.theta > 0.0 && st->minz >= 1));
   if (!eligible) {
-    if (threadIdx.x == 0) a.fallback[f] = 1;
+    if (threadIdx.x == 0) binned_decline(a, f);
     return;
   }
   // ---- grid of square cells, side >= max side + 1
@@ -202,7 +209,7 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
   }
   __syncthreads();
   if (st->big > kBinCellMax) {
-    if (threadIdx.x == 0) a.fallback[f] = 1;
+    if (threadIdx.x == 0) binned_decline(a, f);
     return;
   }
   // ---- pass 3: scatter records, keys and input slots straight into cell order

@@ -79,7 +79,7 @@ unsigned long long* g_pairs_counter = nullptr;  // diagnostics: binned pair test
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Layout {
-  size_t rec, perm, lim, supp, meta, sk, idx, dense, grid, total;
+  size_t rec, perm, lim, supp, meta, sk, idx, dense, list, grid, total;
 };
 
 Layout make_layout(int batch, int n_max) {
@@ -93,6 +93,7 @@ Layout make_layout(int batch, int n_max) {
   L.supp = off; off = align_up(off + B * W32 * 4, 256);
   L.meta = off; off = align_up(off + B * sizeof(FrameMeta), 256);
   L.dense = off; off = align_up(off + B, 256);
+  L.list = off; off = align_up(off + (B + 1) * 4, 256);  // [0] = count, then frame ids
   if (n_max > kBinMaxSlots) {
     L.grid = off; off = align_up(off + binned_grid_scratch_bytes(n_max), 256);
   } else {
@@ -458,6 +459,8 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
   // ---- binned path (sparse frames): exact, one CTA per frame; declined frames fall through
   // to the dense pipeline below, which then only processes those frames.
   const uint8_t* dense_flags = nullptr;
+  const int32_t* decl_list = nullptr;  // binned path: the declined frames, read on the device
+  const int* decl_count = nullptr;
   void* ev_local[4];
   const long long algo = env_ll("PNMS_ALGO", 0);  // 0 auto, 1 dense only
   if (algo == 0 && gate_pairs == nullptr && n_max <= kBinMaxSlots) {
@@ -466,6 +469,9 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     ba.batch = batch; ba.n_max = n_max; ba.d_max = d_max; ba.tie_break = tie_break; ba.W32 = W32;
     ba.theta = theta;
     ba.fallback = ws + L.dense;
+    ba.decl_count = reinterpret_cast<int*>(ws + L.list);
+    ba.decl_list = reinterpret_cast<int32_t*>(ws + L.list) + 1;
+    if ((e = cudaMemsetAsync(ba.decl_count, 0, sizeof(int), st)) != cudaSuccess) return fail_cuda(e);
     ba.keep_idx = keep_idx; ba.keep_count = keep_count; ba.keep_mask = keep_mask;
     ba.pairs_tested = g_pairs_counter;
     const size_t smem = binned_smem_bytes(binned_npad(n_max));
@@ -473,6 +479,8 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     const int variant = (tie_break == PNMS_TIE_BY_INDEX ? 1 : 0) + (g_pairs_counter ? 2 : 0) +
                         (binned_per_thread(n_max) == 8 ? 4 : 0);
     if ((e = launch_binned(variant, ba, batch, smem, st)) != cudaSuccess) return fail_cuda(e);
+    decl_list = ba.decl_list;
+    decl_count = ba.decl_count;
     if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
     dense_flags = ws + L.dense;
     if (events) {
@@ -522,7 +530,7 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
   // previous chunk's map runs on the caller's stream, so the sort hides behind the map.
   const MapShape ms = choose_map_shape(batch, n_max);
   int chunks = 1;
-  if (!events && n_max <= kSortMax && batch >= 512) {
+  if (!events && !decl_list && n_max <= kSortMax && batch >= 512) {
     chunks = std::max(1, std::min(32, env_int("PNMS_OVERLAP_CHUNKS", 1)));
     chunks = std::min(chunks, batch / 64 > 0 ? batch / 64 : 1);
   }
@@ -551,13 +559,16 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     pa.sk_scratch = L.sk ? reinterpret_cast<uint64_t*>(ws + L.sk) + fo : nullptr;
     pa.idx_scratch = L.idx ? reinterpret_cast<int32_t*>(ws + L.idx) + fo : nullptr;
     pa.dense = dense_flags ? dense_flags + f0 : nullptr;
+    pa.list = decl_list;          // chunks == 1 whenever the list is set
+    pa.list_count = decl_count;
 
     if (n_max <= kSortMax) {
       pa.npad = (n_max + kSortThreads - 1) / kSortThreads * kSortThreads;
       pa.nchunks = 1;
       const size_t smem = sort_frame_smem_bytes(pa.npad);
       if ((e = ensure_smem(pnms_prep_sort_frame, smem, g_sort_frame_smem)) != cudaSuccess) return fail_cuda(e);
-      pnms_prep_sort_frame<<<nf, kSortThreads, smem, sort_st>>>(pa);
+      const int pgrid = decl_list ? std::min(nf, 148 * 2) : nf;
+      pnms_prep_sort_frame<<<pgrid, kSortThreads, smem, sort_st>>>(pa);
       if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
     } else {
       pa.npad = kSortMax;
@@ -586,7 +597,9 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     const int ipf = items_per_frame(n_max, ms.RB, ms.chunk);
     ma.items_per_frame = ipf;
     ma.dense = pa.dense;
-    const long long grid = (long long)nf * ipf;
+    ma.list = decl_list;
+    ma.list_count = decl_count;
+    const long long grid = decl_list ? std::min<long long>((long long)nf * ipf, 148 * 8) : (long long)nf * ipf;
     if (grid > 0x7FFFFFFFLL) return PNMS_ETOO_LARGE;
     const size_t map_smem = (size_t)ms.chunk * kRecBytes;
     if (ms.R == 4) e = launch_map<4>(ma, grid, map_smem, st);
@@ -603,9 +616,11 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     ca.keep_mask = keep_mask ? keep_mask + (size_t)f0 * W32 : nullptr;
     ca.gate_pairs = gate_pairs ? reinterpret_cast<unsigned long long*>(gate_pairs) + f0 : nullptr;
     ca.dense = pa.dense;
+    ca.list = decl_list;
+    ca.list_count = decl_count;
     const size_t csmem = ((size_t)W32 + 3) / 4 * 16 + 64 * 4;
     if ((e = ensure_smem(pnms_compact, csmem, g_compact_smem)) != cudaSuccess) return fail_cuda(e);
-    pnms_compact<<<nf, kCompactThreads, csmem, st>>>(ca);
+    pnms_compact<<<decl_list ? std::min(nf, 148 * 4) : nf, kCompactThreads, csmem, st>>>(ca);
     if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
   }
   if ((e = mark(events, 3, st)) != cudaSuccess) return fail_cuda(e);

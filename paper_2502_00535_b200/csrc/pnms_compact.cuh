@@ -26,14 +26,13 @@ struct CompactArgs {
   uint32_t* keep_mask;     // may be null
   unsigned long long* gate_pairs;  // may be null
   const uint8_t* dense;   // optional [batch]: process frame f only if dense[f] != 0
+  const int32_t* list;    // optional: process only frames list[0 .. *list_count) (grid-stride)
+  const int* list_count;
 };
 
-__global__ void __launch_bounds__(kCompactThreads) pnms_compact(CompactArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__device__ __forceinline__ void compact_body(const CompactArgs& a, int f, unsigned char* smem_raw) {
   uint32_t* kbits = reinterpret_cast<uint32_t*>(smem_raw);          // [W32] survivor bits, input order
   uint32_t* warp_sums = kbits + ((a.W32 + 3) & ~3);
-  const int f = blockIdx.x;
-  if (a.dense && !a.dense[f]) return;
   const long long fbase = (long long)f * a.n_max;
   const int cnt = frame_count(a.counts, f, a.n_max);
   const int P = a.d_max > cnt ? a.d_max - cnt : 0;
@@ -83,6 +82,20 @@ __global__ void __launch_bounds__(kCompactThreads) pnms_compact(CompactArgs a) {
       a.gate_pairs[f] = g;
     }
   }
+}
+
+__global__ void __launch_bounds__(kCompactThreads) pnms_compact(CompactArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (a.list) {
+    const int n = *a.list_count;
+    for (int li = blockIdx.x; li < n; li += gridDim.x) {
+      compact_body(a, a.list[li], smem_raw);
+      __syncthreads();
+    }
+    return;
+  }
+  if (a.dense && !a.dense[blockIdx.x]) return;
+  compact_body(a, blockIdx.x, smem_raw);
 }
 
 }  // namespace pnms

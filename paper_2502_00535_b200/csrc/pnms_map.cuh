@@ -41,6 +41,8 @@ struct MapArgs {
   int n_rb;             // row blocks per frame
   int items_per_frame;
   const uint8_t* dense;   // optional [batch]: process frame f only if dense[f] != 0
+  const int32_t* list;    // optional: process only frames list[0 .. *list_count) (grid-stride)
+  const int* list_count;
 };
 
 // number of column chunks of row block rb: its rows' limits are < (rb+1)*RB
@@ -192,12 +194,7 @@ __device__ __noinline__ void warp_scan_wide(const RecWide* scol, const RecWide* 
 }
 
 template <int R>
-__global__ void __launch_bounds__(kMapWarps * 32) pnms_map_kernel(MapArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t bar;
-  const int f = blockIdx.x / a.items_per_frame;
-  if (a.dense && !a.dense[f]) return;
-  int item = blockIdx.x % a.items_per_frame;
+__device__ __forceinline__ void map_item(const MapArgs& a, int f, int item, unsigned char* smem_raw, uint64_t& bar) {
   const int RB = a.rows_per_block;
   int rb = a.n_rb - 1;
   for (; rb > 0; --rb) {
@@ -264,6 +261,23 @@ __global__ void __launch_bounds__(kMapWarps * 32) pnms_map_kernel(MapArgs a) {
     const uint32_t bits = __ballot_sync(0xFFFFFFFFu, sup[r] && !pre[r]);
     if (lane == 0 && bits) atomicOr(supp_frame + (pw >> 5) + r, bits);
   }
+}
+
+template <int R>
+__global__ void __launch_bounds__(kMapWarps * 32) pnms_map_kernel(MapArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bar;
+  if (a.list) {
+    const long long n = (long long)*a.list_count * a.items_per_frame;
+    for (long long it = blockIdx.x; it < n; it += gridDim.x) {
+      map_item<R>(a, a.list[it / a.items_per_frame], (int)(it % a.items_per_frame), smem_raw, bar);
+      __syncthreads();  // every warp is past the barrier wait and done with the column chunk
+    }
+    return;
+  }
+  const int f = blockIdx.x / a.items_per_frame;
+  if (a.dense && !a.dense[f]) return;
+  map_item<R>(a, f, blockIdx.x % a.items_per_frame, smem_raw, bar);
 }
 
 }  // namespace pnms

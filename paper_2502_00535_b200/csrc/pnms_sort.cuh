@@ -35,6 +35,8 @@ struct PrepArgs {
   uint64_t* sk_scratch;   // chunk mode: sorted keys   [batch][n_max]
   int32_t* idx_scratch;   // chunk mode: sorted index  [batch][n_max]
   const uint8_t* dense;   // optional [batch]: process frame f only if dense[f] != 0
+  const int32_t* list;    // optional: process only frames list[0 .. *list_count) (grid-stride)
+  const int* list_count;
 };
 
 __device__ __forceinline__ bool frame_skipped(const uint8_t* dense, int f) { return dense && !dense[f]; }
@@ -423,10 +425,7 @@ __device__ __forceinline__ void init_stats(LoadStats* st, unsigned long long* li
 }
 
 // One CTA per frame (n_max <= kSortMax): load, sort, derive limits, emit sorted records.
-__global__ void __launch_bounds__(kSortThreads) pnms_prep_sort_frame(PrepArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int f = blockIdx.x;
-  if (frame_skipped(a.dense, f)) return;
+__device__ __forceinline__ void prep_sort_frame_body(const PrepArgs& a, int f, unsigned char* smem_raw) {
   const long long fbase = (long long)f * a.n_max;
   const int cnt = frame_count(a.counts, f, a.n_max);
   SortSmem m = carve_sort_smem(smem_raw, a.npad);
@@ -487,6 +486,20 @@ __global__ void __launch_bounds__(kSortThreads) pnms_prep_sort_frame(PrepArgs a)
     fm.lim_sum = *m.lim_acc;
     a.meta[f] = fm;
   }
+}
+
+__global__ void __launch_bounds__(kSortThreads) pnms_prep_sort_frame(PrepArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (a.list) {
+    const int n = *a.list_count;
+    for (int li = blockIdx.x; li < n; li += gridDim.x) {
+      prep_sort_frame_body(a, a.list[li], smem_raw);
+      __syncthreads();
+    }
+    return;
+  }
+  if (frame_skipped(a.dense, blockIdx.x)) return;
+  prep_sort_frame_body(a, blockIdx.x, smem_raw);
 }
 
 // Chunk mode (n_max > kSortMax), grid = batch * nchunks: sort one kSortMax-slot chunk and
