@@ -20,7 +20,7 @@
 #include "pnms_small.cuh"
 #include "pnms_binned.cuh"
 #include "pnms_validate.cuh"
-#include "pnms_binned_grid.cuh"
+#include "pnms_binned_cluster.cuh"
 #include "pnms_greedy.cuh"
 #include "pnms_soft.cuh"
 #include "pnms_sort.cuh"
@@ -79,7 +79,7 @@ unsigned long long* g_pairs_counter = nullptr;  // diagnostics: binned pair test
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Layout {
-  size_t rec, perm, lim, supp, meta, sk, idx, dense, list, grid, total;
+  size_t rec, perm, lim, supp, meta, sk, idx, dense, list, total;
 };
 
 Layout make_layout(int batch, int n_max) {
@@ -94,11 +94,6 @@ Layout make_layout(int batch, int n_max) {
   L.meta = off; off = align_up(off + B * sizeof(FrameMeta), 256);
   L.dense = off; off = align_up(off + B, 256);
   L.list = off; off = align_up(off + (B + 1) * 4, 256);  // [0] = count, then frame ids
-  if (n_max > kBinMaxSlots) {
-    L.grid = off; off = align_up(off + binned_grid_scratch_bytes(n_max), 256);
-  } else {
-    L.grid = 0;
-  }
   if (n_max > kSortMax) {
     L.sk = off;  off = align_up(off + B * N * 8, 256);
     L.idx = off; off = align_up(off + B * N * 4, 256);
@@ -163,6 +158,79 @@ cudaError_t launch_binned_t(const BinArgs& ba, int batch, size_t smem, cudaStrea
   return cudaGetLastError();
 }
 
+// input slots per cluster CTA (a multiple of 32) for cluster size cs, or 0 when too large
+int cluster_slice(int n_max, int cs) {
+  const int slice = ((n_max + cs - 1) / cs + 31) / 32 * 32;
+  return slice <= kClMaxSlice ? slice : 0;
+}
+
+template <bool B, int CS, int P>
+cudaError_t launch_cluster_t(const BinArgs& ba, int batch, int slice, cudaStream_t st) {
+  static std::atomic<size_t> cfg{0};
+  static std::atomic<int> nonportable{0};
+  const size_t smem = binned_cluster_smem_bytes();
+  cudaError_t e = ensure_smem(pnms_binned_cluster<B, CS, P>, smem, cfg);
+  if (e != cudaSuccess) return e;
+  if (CS > 8 && !nonportable.load()) {
+    e = cudaFuncSetAttribute(pnms_binned_cluster<B, CS, P>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    nonportable.store(1);
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)batch * CS);
+  lc.blockDim = dim3(kClThreads);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  return cudaLaunchKernelEx(&lc, pnms_binned_cluster<B, CS, P>, ba, slice);
+}
+
+// cluster size: 16 CTAs (non-portable; one GPC) when the device can co-schedule them, else 8
+int cluster_size_for(int n_max) {
+  static int cs16 = -1;
+  if (cs16 < 0) {
+    int n = 0;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(16);
+    lc.blockDim = dim3(kClThreads);
+    lc.dynamicSmemBytes = binned_cluster_smem_bytes();
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 16;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    const void* fn = (const void*)pnms_binned_cluster<false, 16, 1>;
+    bool ok = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+              cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lc.dynamicSmemBytes) ==
+                  cudaSuccess &&
+              cudaOccupancyMaxActiveClusters(&n, fn, &lc) == cudaSuccess && n > 0;
+    cudaGetLastError();
+    cs16 = ok ? 1 : 0;
+  }
+  const int want = env_int("PNMS_CLUSTER", 0);
+  if (want == 8 || want == 16) return (want == 16 && !cs16) ? 8 : want;
+  return (cs16 && n_max > 8 * 1024) ? 16 : 8;
+}
+
+cudaError_t launch_cluster(const BinArgs& ba, int batch, int n_max, bool by_index, cudaStream_t st) {
+  const int cs = cluster_size_for(n_max);
+  const int slice = cluster_slice(n_max, cs);
+  const int per = slice <= kClThreads ? 1 : (slice <= 2 * kClThreads ? 2 : 4);
+#define PNMS_CL(CS, P) (by_index ? launch_cluster_t<true, CS, P>(ba, batch, slice, st) \
+                                 : launch_cluster_t<false, CS, P>(ba, batch, slice, st))
+  if (cs == 16) return per == 1 ? PNMS_CL(16, 1) : (per == 2 ? PNMS_CL(16, 2) : PNMS_CL(16, 4));
+  return per == 1 ? PNMS_CL(8, 1) : (per == 2 ? PNMS_CL(8, 2) : PNMS_CL(8, 4));
+#undef PNMS_CL
+}
+
 cudaError_t launch_binned(int variant, const BinArgs& ba, int batch, size_t smem, cudaStream_t st) {
   switch (variant) {
     case 0: return launch_binned_t<false, false, 4>(ba, batch, smem, st, g_binned_smem[0]);
@@ -174,22 +242,6 @@ cudaError_t launch_binned(int variant, const BinArgs& ba, int batch, size_t smem
     case 6: return launch_binned_t<false, true, 8>(ba, batch, smem, st, g_binned_smem[6]);
     default: return launch_binned_t<true, true, 8>(ba, batch, smem, st, g_binned_smem[7]);
   }
-}
-
-// co-resident CTAs for the cooperative binned kernel on the current device (cached)
-int cooperative_blocks(bool by_index) {
-  static std::atomic<int> cached[2] = {{-1}, {-1}};
-  int v = cached[by_index].load();
-  if (v >= 0) return v;
-  int dev = 0, sms = 0, per_sm = 0, coop = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-  const void* fn = by_index ? (const void*)pnms_binned_grid<true> : (const void*)pnms_binned_grid<false>;
-  if (!coop || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGridThreads, 0) != cudaSuccess) per_sm = 0;
-  v = sms * std::min(per_sm, 2);
-  cached[by_index].store(v);
-  return v;
 }
 
 template <bool B, bool C, int R>
@@ -490,38 +542,26 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     }
   }
 
-  if (!dense_flags && algo == 0 && gate_pairs == nullptr && n_max > kBinMaxSlots && env_int("PNMS_GRID", 0) == 1) {
-    // large frames: one cooperative launch over the whole GPU (pnms_binned_grid.cuh).  Opt-in:
-    // measured on B200 it is grid-sync/latency bound (~110 us for BASELINE config 3, issue
-    // active 3.6 %), no faster than the dense sorted pipeline (~105 us).
-    uint8_t* g = ws + L.grid;
-    BinGridArgs ga;
-    ga.x = x; ga.y = y; ga.z = z; ga.s = s; ga.counts = counts;
-    ga.batch = batch; ga.n_max = n_max; ga.d_max = d_max; ga.tie_break = tie_break; ga.W32 = W32;
-    ga.theta = theta;
-    size_t o = 0;
-    ga.recS = reinterpret_cast<RecNarrow*>(g + o); o = align_up(o + (size_t)n_max * 16, 256);
-    ga.keyS = reinterpret_cast<uint64_t*>(g + o); o = align_up(o + (size_t)n_max * 8, 256);
-    ga.idxS = reinterpret_cast<int32_t*>(g + o); o = align_up(o + (size_t)n_max * 4, 256);
-    ga.cellof = reinterpret_cast<int32_t*>(g + o); o = align_up(o + (size_t)n_max * 4, 256);
-    ga.cstart = reinterpret_cast<uint32_t*>(g + o); o = align_up(o + (size_t)(kGridMaxCells + 4) * 4, 256);
-    ga.ccur = reinterpret_cast<uint32_t*>(g + o); o = align_up(o + (size_t)(kGridMaxCells + 4) * 4, 256);
-    ga.kbits = reinterpret_cast<uint32_t*>(g + o); o = align_up(o + (size_t)W32 * 4, 256);
-    ga.gst = reinterpret_cast<GridStats*>(g + o);
-    ga.fallback = ws + L.dense;
-    ga.keep_idx = keep_idx; ga.keep_count = keep_count; ga.keep_mask = keep_mask;
-    int blocks = cooperative_blocks(tie_break == PNMS_TIE_BY_INDEX);
-    if (blocks > 0) {
-      if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
-      void* kargs[] = {&ga};
-      void* fn = tie_break == PNMS_TIE_BY_INDEX ? (void*)pnms_binned_grid<true> : (void*)pnms_binned_grid<false>;
-      if ((e = cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kGridThreads), kargs, 0, st)) != cudaSuccess)
-        return fail_cuda(e);
-      dense_flags = ws + L.dense;
-      if (events) {
-        ev_local[0] = events[1]; ev_local[1] = events[2]; ev_local[2] = nullptr; ev_local[3] = events[3];
-        events = ev_local;
-      }
+  if (!dense_flags && algo == 0 && gate_pairs == nullptr && n_max > kBinMaxSlots &&
+      cluster_slice(n_max, 16) > 0 && cluster_slice(n_max, cluster_size_for(n_max)) > 0) {
+    // large frames: one thread-block cluster per frame, cell data in distributed shared
+    // memory (pnms_binned_cluster.cuh); declined frames go to the dense pipeline by flag
+    BinArgs ba;
+    ba.x = x; ba.y = y; ba.z = z; ba.s = s; ba.counts = counts;
+    ba.batch = batch; ba.n_max = n_max; ba.d_max = d_max; ba.tie_break = tie_break; ba.W32 = W32;
+    ba.theta = theta;
+    ba.fallback = ws + L.dense;
+    ba.decl_count = reinterpret_cast<int*>(ws + L.list);
+    ba.decl_list = reinterpret_cast<int32_t*>(ws + L.list) + 1;
+    ba.keep_idx = keep_idx; ba.keep_count = keep_count; ba.keep_mask = keep_mask;
+    ba.pairs_tested = g_pairs_counter;  // diagnostics: phase trace of the cluster kernel
+    if ((e = cudaMemsetAsync(ba.decl_count, 0, sizeof(int), st)) != cudaSuccess) return fail_cuda(e);
+    if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
+    if ((e = launch_cluster(ba, batch, n_max, tie_break == PNMS_TIE_BY_INDEX, st)) != cudaSuccess) return fail_cuda(e);
+    dense_flags = ws + L.dense;
+    if (events) {
+      ev_local[0] = events[1]; ev_local[1] = events[2]; ev_local[2] = nullptr; ev_local[3] = events[3];
+      events = ev_local;
     }
   }
 

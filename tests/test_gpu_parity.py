@@ -156,6 +156,43 @@ def test_binned_mixed_batch_vs_oracle(monkeypatch):
     assert int(counter.item()) > 0  # the binned kernel did run
 
 
+def test_declined_frame_list_grid_stride(monkeypatch):
+    """Every frame declined by the binned kernel (theta = 0) in a batch larger than the
+    persistent grids of the dense fallback kernels: the declined-frame list is walked with
+    grid-stride loops (prep 296 CTAs, map 1184, compact 592)."""
+    monkeypatch.setenv("PNMS_SMALL_PAIRS", "0")
+    monkeypatch.setenv("PNMS_ALGO", "0")
+    x, y, z, s = random_frames(1500, 300, seed=77, frame_w=400, frame_h=300)
+    counts = np.full(1500, 300, np.int32)
+    counts[::7] = 123
+    for theta in (0.0, 0.4):
+        got = _run_batch(x, y, z, s, counts, theta, "paper_faithful", 300)
+        want = c_oracle.run_batch(x, y, z, s, counts, 300, theta)
+        for f in range(1500):
+            assert np.array_equal(got[f], want[f]), (theta, f)
+
+
+@pytest.mark.parametrize("cs", ["8", "16"])
+def test_cluster_path_large_frames(cs, monkeypatch):
+    """Frames of 4097..20000 slots through the thread-block-cluster kernel (both cluster
+    sizes): ragged counts, exact ties, NaN and negative scores with padding, a band-crowded
+    frame and a declined frame (side > 126), both tie policies, vs the C oracle."""
+    monkeypatch.setenv("PNMS_ALGO", "0")
+    monkeypatch.setenv("PNMS_CLUSTER", cs)
+    n = 20000
+    x, y, z, s = random_frames(5, n, seed=41, frame_w=3840, frame_h=2160, duplicate_fraction=0.05)
+    counts = np.array([n, 4097, 12345, 9000, 16384], np.int32)
+    s[1, ::9] = np.nan
+    s[2, 5:40] = -0.5
+    y[3] = y[3] // 6                      # everything in a few cell rows: crowded bands
+    z[4, 17] = 200                        # leaves the narrow7 domain -> dense pipeline
+    for tie in ("paper_faithful", "by_index"):
+        got = _run_batch(x, y, z, s, counts, 0.5, tie, n + 7)
+        for f in range(5):
+            want = c_oracle.run_frame(x[f], y[f], z[f], s[f], int(counts[f]), n + 7, 0.5, tie)
+            assert np.array_equal(got[f], want), (cs, tie, f)
+
+
 def test_binned_key_prefix_collisions(path):
     """Scores whose 64-bit keys share the high 32 bits (the binned kernel's fast gate) — plus
     exact duplicates — force the exact per-row rescan; both tie policies, vs the C oracle."""
@@ -210,11 +247,11 @@ def test_ragged_duplicates_vs_oracle(tie, theta, path):
 
 
 @pytest.mark.parametrize("n", [4097, 6000, 9000, 16384])
-@pytest.mark.parametrize("grid", ["0", "1"])
-def test_chunked_sort_frames_vs_oracle(n, path, grid, monkeypatch):
-    """Frames above one CTA's capacity (cooperative binned kernel when PNMS_GRID=1; chunk sort
-    + merge-rank in the dense pipeline) with exact score ties."""
-    monkeypatch.setenv("PNMS_GRID", grid)
+@pytest.mark.parametrize("cs", ["8", "16"])
+def test_chunked_sort_frames_vs_oracle(n, path, cs, monkeypatch):
+    """Frames above one CTA's capacity (thread-block-cluster binned kernel of cluster size cs;
+    chunk sort + merge-rank in the dense pipeline) with exact score ties."""
+    monkeypatch.setenv("PNMS_CLUSTER", cs)
     x, y, z, s = random_frames(2, n, seed=n, frame_w=3840, frame_h=2160, z_range=(8, 64), duplicate_fraction=0.1)
     s[:, ::7] = 0.5
     for tie in ("paper_faithful", "by_index"):
