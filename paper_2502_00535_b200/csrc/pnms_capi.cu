@@ -21,6 +21,7 @@
 #include "pnms_binned.cuh"
 #include "pnms_validate.cuh"
 #include "pnms_binned_cluster.cuh"
+#include "pnms_binned_pairs.cuh"
 #include "pnms_greedy.cuh"
 #include "pnms_soft.cuh"
 #include "pnms_sort.cuh"
@@ -229,6 +230,29 @@ cudaError_t launch_cluster(const BinArgs& ba, int batch, int n_max, bool by_inde
   if (cs == 16) return per == 1 ? PNMS_CL(16, 1) : (per == 2 ? PNMS_CL(16, 2) : PNMS_CL(16, 4));
   return per == 1 ? PNMS_CL(8, 1) : (per == 2 ? PNMS_CL(8, 2) : PNMS_CL(8, 4));
 #undef PNMS_CL
+}
+
+std::atomic<size_t> g_pairs_smem[8];
+
+template <bool B, bool C, int P>
+cudaError_t launch_pairs_t(const BinArgs& ba, int batch, size_t smem, cudaStream_t st, std::atomic<size_t>& cfg) {
+  cudaError_t e = ensure_smem(pnms_binned_pairs_frame<B, C, P>, smem, cfg);
+  if (e != cudaSuccess) return e;
+  pnms_binned_pairs_frame<B, C, P><<<batch, kPairThreads, smem, st>>>(ba);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pairs(int variant, const BinArgs& ba, int batch, size_t smem, cudaStream_t st) {
+  switch (variant) {
+    case 0: return launch_pairs_t<false, false, 4>(ba, batch, smem, st, g_pairs_smem[0]);
+    case 1: return launch_pairs_t<true, false, 4>(ba, batch, smem, st, g_pairs_smem[1]);
+    case 2: return launch_pairs_t<false, true, 4>(ba, batch, smem, st, g_pairs_smem[2]);
+    case 3: return launch_pairs_t<true, true, 4>(ba, batch, smem, st, g_pairs_smem[3]);
+    case 4: return launch_pairs_t<false, false, 8>(ba, batch, smem, st, g_pairs_smem[4]);
+    case 5: return launch_pairs_t<true, false, 8>(ba, batch, smem, st, g_pairs_smem[5]);
+    case 6: return launch_pairs_t<false, true, 8>(ba, batch, smem, st, g_pairs_smem[6]);
+    default: return launch_pairs_t<true, true, 8>(ba, batch, smem, st, g_pairs_smem[7]);
+  }
 }
 
 cudaError_t launch_binned(int variant, const BinArgs& ba, int batch, size_t smem, cudaStream_t st) {
@@ -530,7 +554,13 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
     const int variant = (tie_break == PNMS_TIE_BY_INDEX ? 1 : 0) + (g_pairs_counter ? 2 : 0) +
                         (binned_per_thread(n_max) == 8 ? 4 : 0);
-    if ((e = launch_binned(variant, ba, batch, smem, st)) != cudaSuccess) return fail_cuda(e);
+    if (env_int("PNMS_BINNED", 0) == 2) {  // cell-pair tiles (pnms_binned_pairs.cuh): opt-in,
+      // measured 4 % slower on BASELINE config 5 (more pair tests without the gate-prefix skip)
+      const size_t psmem = binned_pairs_smem_bytes(binned_npad(n_max));
+      if ((e = launch_pairs(variant, ba, batch, psmem, st)) != cudaSuccess) return fail_cuda(e);
+    } else {                               // per-row scans (pnms_binned.cuh), the default
+      if ((e = launch_binned(variant, ba, batch, smem, st)) != cudaSuccess) return fail_cuda(e);
+    }
     decl_list = ba.decl_list;
     decl_count = ba.decl_count;
     if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);

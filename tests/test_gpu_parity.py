@@ -18,12 +18,14 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda"
 
 
-@pytest.fixture(params=["small", "binned", "dense"])
+@pytest.fixture(params=["small", "binned", "binned_pairs", "dense"])
 def path(request, monkeypatch):
     """Run a test through each device path: the single-launch unsorted kernel, the binned
-    kernel (with the dense pipeline for the frames it declines), and the dense pipeline only."""
+    kernel as per-row scans (default) or as cell-pair tiles (each with the dense pipeline for
+    the frames it declines), and the dense pipeline only."""
     monkeypatch.setenv("PNMS_SMALL_PAIRS", str(1 << 40) if request.param == "small" else "0")
     monkeypatch.setenv("PNMS_ALGO", "1" if request.param == "dense" else "0")
+    monkeypatch.setenv("PNMS_BINNED", "2" if request.param == "binned_pairs" else "0")
     return request.param
 
 
