@@ -92,6 +92,9 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
   const long long fbase = (long long)f * a.n_max;
   const int cnt = frame_count(a.counts, f, a.n_max);
   const int npad = binned_npad(a.n_max);
+  // the fallback kernels over the declined-frame list may launch once every CTA has started
+  // (programmatic dependent launch); they wait for this grid's completion before reading
+  cudaTriggerProgrammaticLaunchCompletion();
   // per-box data stored in cell order (positions [cstart[c], cstart[c+1]) = cell c)
   RecBin* recS = reinterpret_cast<RecBin*>(smem_raw);                         // [npad] records
   uint64_t* keyS = reinterpret_cast<uint64_t*>(recS + npad);                  // [npad] full sort keys

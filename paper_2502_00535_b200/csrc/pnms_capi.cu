@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <utility>
 
 #include "../../include/parnms_b200.h"
 #include "pnms_common.cuh"
@@ -125,6 +126,24 @@ cudaError_t ensure_smem(K kernel, size_t bytes, std::atomic<size_t>& configured)
   return e;
 }
 
+// launch `kernel` with programmatic stream serialization (PDL) when `pdl` is set: it may start
+// while the previous kernel on the stream drains; it calls cudaGridDependencySynchronize()
+template <class... KArgs, class... Args>
+cudaError_t launch_maybe_pdl(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                             Args&&... args) {
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = grid;
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = smem;
+  lc.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = attr;
+  lc.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&lc, kernel, std::forward<Args>(args)...);
+}
+
 std::atomic<size_t> g_sort_frame_smem{0}, g_sort_chunk_smem{0}, g_compact_smem{0};
 std::atomic<size_t> g_map_smem[5];
 
@@ -234,6 +253,8 @@ cudaError_t launch_cluster(const BinArgs& ba, int batch, int n_max, bool by_inde
 
 std::atomic<size_t> g_pairs_smem[8];
 
+
+
 template <bool B, bool C, int P>
 cudaError_t launch_pairs_t(const BinArgs& ba, int batch, size_t smem, cudaStream_t st, std::atomic<size_t>& cfg) {
   cudaError_t e = ensure_smem(pnms_binned_pairs_frame<B, C, P>, smem, cfg);
@@ -329,11 +350,10 @@ MapShape choose_map_shape(int batch, int n_max) {
 }
 
 template <int R>
-cudaError_t launch_map(const MapArgs& ma, long long grid, size_t smem, cudaStream_t st) {
+cudaError_t launch_map(const MapArgs& ma, long long grid, size_t smem, cudaStream_t st, bool pdl) {
   cudaError_t e = ensure_smem(pnms_map_kernel<R>, smem, g_map_smem[R]);
   if (e != cudaSuccess) return e;
-  pnms_map_kernel<R><<<(unsigned)grid, kMapWarps * 32, smem, st>>>(ma);
-  return cudaGetLastError();
+  return launch_maybe_pdl(pdl, pnms_map_kernel<R>, dim3((unsigned)grid), dim3(kMapWarps * 32), smem, st, ma);
 }
 
 }  // namespace
@@ -638,8 +658,9 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
       const size_t smem = sort_frame_smem_bytes(pa.npad);
       if ((e = ensure_smem(pnms_prep_sort_frame, smem, g_sort_frame_smem)) != cudaSuccess) return fail_cuda(e);
       const int pgrid = decl_list ? std::min(nf, 148 * 2) : nf;
-      pnms_prep_sort_frame<<<pgrid, kSortThreads, smem, sort_st>>>(pa);
-      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
+      if ((e = launch_maybe_pdl(decl_list != nullptr, pnms_prep_sort_frame, dim3(pgrid), dim3(kSortThreads), smem,
+                                sort_st, pa)) != cudaSuccess)
+        return fail_cuda(e);
     } else {
       pa.npad = kSortMax;
       pa.nchunks = (n_max + kSortMax - 1) / kSortMax;
@@ -672,9 +693,10 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     const long long grid = decl_list ? std::min<long long>((long long)nf * ipf, 148 * 8) : (long long)nf * ipf;
     if (grid > 0x7FFFFFFFLL) return PNMS_ETOO_LARGE;
     const size_t map_smem = (size_t)ms.chunk * kRecBytes;
-    if (ms.R == 4) e = launch_map<4>(ma, grid, map_smem, st);
-    else if (ms.R == 2) e = launch_map<2>(ma, grid, map_smem, st);
-    else e = launch_map<1>(ma, grid, map_smem, st);
+    const bool pdl = decl_list != nullptr;
+    if (ms.R == 4) e = launch_map<4>(ma, grid, map_smem, st, pdl);
+    else if (ms.R == 2) e = launch_map<2>(ma, grid, map_smem, st, pdl);
+    else e = launch_map<1>(ma, grid, map_smem, st, pdl);
     if (e != cudaSuccess) return fail_cuda(e);
 
     if ((e = mark(events, 2, st)) != cudaSuccess) return fail_cuda(e);
@@ -690,8 +712,9 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     ca.list_count = decl_count;
     const size_t csmem = ((size_t)W32 + 3) / 4 * 16 + 64 * 4;
     if ((e = ensure_smem(pnms_compact, csmem, g_compact_smem)) != cudaSuccess) return fail_cuda(e);
-    pnms_compact<<<decl_list ? std::min(nf, 148 * 4) : nf, kCompactThreads, csmem, st>>>(ca);
-    if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
+    if ((e = launch_maybe_pdl(decl_list != nullptr, pnms_compact, dim3(decl_list ? std::min(nf, 148 * 4) : nf),
+                              dim3(kCompactThreads), csmem, st, ca)) != cudaSuccess)
+      return fail_cuda(e);
   }
   if ((e = mark(events, 3, st)) != cudaSuccess) return fail_cuda(e);
   return PNMS_OK;

@@ -87,6 +87,9 @@ __device__ __forceinline__ void compact_body(const CompactArgs& a, int f, unsign
 __global__ void __launch_bounds__(kCompactThreads) pnms_compact(CompactArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   if (a.list) {
+    // launched programmatically after the binned kernel (PDL): wait for its results
+    cudaGridDependencySynchronize();
+    cudaTriggerProgrammaticLaunchCompletion();
     const int n = *a.list_count;
     for (int li = blockIdx.x; li < n; li += gridDim.x) {
       compact_body(a, a.list[li], smem_raw);

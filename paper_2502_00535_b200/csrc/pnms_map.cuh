@@ -268,6 +268,8 @@ __global__ void __launch_bounds__(kMapWarps * 32) pnms_map_kernel(MapArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bar;
   if (a.list) {
+    cudaGridDependencySynchronize();  // PDL: the previous kernel's results are visible after this
+    cudaTriggerProgrammaticLaunchCompletion();
     const long long n = (long long)*a.list_count * a.items_per_frame;
     for (long long it = blockIdx.x; it < n; it += gridDim.x) {
       map_item<R>(a, a.list[it / a.items_per_frame], (int)(it % a.items_per_frame), smem_raw, bar);

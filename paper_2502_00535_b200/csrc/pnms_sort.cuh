@@ -491,6 +491,9 @@ __device__ __forceinline__ void prep_sort_frame_body(const PrepArgs& a, int f, u
 __global__ void __launch_bounds__(kSortThreads) pnms_prep_sort_frame(PrepArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   if (a.list) {
+    // launched programmatically after the binned kernel (PDL): wait for its results
+    cudaGridDependencySynchronize();
+    cudaTriggerProgrammaticLaunchCompletion();
     const int n = *a.list_count;
     for (int li = blockIdx.x; li < n; li += gridDim.x) {
       prep_sort_frame_body(a, a.list[li], smem_raw);
