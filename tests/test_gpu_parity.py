@@ -195,6 +195,41 @@ def test_cluster_path_large_frames(cs, monkeypatch):
             assert np.array_equal(got[f], want), (cs, tie, f)
 
 
+def test_max_size_frame_cluster_path(monkeypatch):
+    """A 60000-slot frame (the cluster path's largest band layout, 16 CTAs x 3750 slots) vs the
+    C oracle, both tie policies."""
+    monkeypatch.setenv("PNMS_ALGO", "0")
+    n = 60000
+    x, y, z, s = random_frames(1, n, seed=60, frame_w=3840 * 2, frame_h=2160 * 2, duplicate_fraction=0.02)
+    for tie in ("paper_faithful", "by_index"):
+        got = _run_batch(x, y, z, s, np.array([n], np.int32), 0.45, tie, n)
+        want = c_oracle.run_frame(x[0], y[0], z[0], s[0], n, n, 0.45, tie)
+        assert np.array_equal(got[0], want), tie
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_randomized_configurations_all_paths(seed, path):
+    """Fuzz: random batch shapes, counts, theta, tie policy, d_max, frame geometry, side range,
+    duplicates and score ties, through every device path, vs the C oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    B = int(rng.integers(1, 9))
+    n_max = int(rng.choice([1, 7, 64, 255, 1000, 2048, 3000, 4096, 5000]))
+    fw, fh = int(rng.choice([64, 300, 1920])), int(rng.choice([64, 300, 1080]))
+    z_hi = int(min(rng.choice([8, 40, 120]), min(fw, fh) - 1))
+    x, y, z, s = random_frames(B, n_max, seed=seed, frame_w=fw, frame_h=fh, z_range=(1, z_hi),
+                               duplicate_fraction=float(rng.choice([0.0, 0.1])))
+    if rng.random() < 0.5:
+        s = np.round(s, 2)                                     # many exact score ties
+    counts = rng.integers(0, n_max + 1, B).astype(np.int32)
+    theta = float(rng.choice([0.0, 0.05, 0.3, 0.5, 0.77, 1.0]))
+    tie = str(rng.choice(["paper_faithful", "by_index"]))
+    d_max = n_max + int(rng.integers(0, 3))
+    got = _run_batch(x, y, z, s, counts, theta, tie, d_max)
+    for f in range(B):
+        want = c_oracle.run_frame(x[f], y[f], z[f], s[f], int(counts[f]), d_max, theta, tie)
+        assert np.array_equal(got[f], want), (seed, f, B, n_max, theta, tie)
+
+
 def test_binned_key_prefix_collisions(path):
     """Scores whose 64-bit keys share the high 32 bits (the binned kernel's fast gate) — plus
     exact duplicates — force the exact per-row rescan; both tie policies, vs the C oracle."""
