@@ -53,6 +53,7 @@ struct BinArgs {
   uint8_t* fallback;      // [batch] 1 = frame left to the dense pipeline
   int32_t* decl_list;     // declined frames, appended in any order ...
   int* decl_count;        // ... count (zero before the launch)
+  FrameMeta* meta;        // optional: a declined frame's FrameMeta is zeroed (chunked dense path)
   int32_t* keep_idx;
   int32_t* keep_count;
   uint32_t* keep_mask;
@@ -82,6 +83,7 @@ __device__ __forceinline__ int qdiv(int v, uint32_t M) { return (int)__umulhi((u
 
 __device__ __forceinline__ void binned_decline(const BinArgs& a, int f) {
   a.fallback[f] = 1;
+  if (a.meta) a.meta[f] = FrameMeta{};
   a.decl_list[atomicAdd(a.decl_count, 1)] = f;
 }
 

@@ -23,6 +23,7 @@
 #include "pnms_validate.cuh"
 #include "pnms_binned_cluster.cuh"
 #include "pnms_binned_pairs.cuh"
+#include "pnms_binned_tiles.cuh"
 #include "pnms_greedy.cuh"
 #include "pnms_soft.cuh"
 #include "pnms_sort.cuh"
@@ -81,7 +82,7 @@ unsigned long long* g_pairs_counter = nullptr;  // diagnostics: binned pair test
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Layout {
-  size_t rec, perm, lim, supp, meta, sk, idx, dense, list, total;
+  size_t rec, perm, lim, supp, meta, sk, idx, dense, list, tiles, total;
 };
 
 Layout make_layout(int batch, int n_max) {
@@ -97,10 +98,11 @@ Layout make_layout(int batch, int n_max) {
   L.dense = off; off = align_up(off + B, 256);
   L.list = off; off = align_up(off + (B + 1) * 4, 256);  // [0] = count, then frame ids
   if (n_max > kSortMax) {
+    L.tiles = off; off = align_up(off + B * 4 + B * W32 * 4 + 16, 256);  // tile path: decline flags + masks
     L.sk = off;  off = align_up(off + B * N * 8, 256);
     L.idx = off; off = align_up(off + B * N * 4, 256);
   } else {
-    L.sk = L.idx = 0;
+    L.sk = L.idx = L.tiles = 0;
   }
   L.total = off;
   return L;
@@ -570,6 +572,7 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     if ((e = cudaMemsetAsync(ba.decl_count, 0, sizeof(int), st)) != cudaSuccess) return fail_cuda(e);
     ba.keep_idx = keep_idx; ba.keep_count = keep_count; ba.keep_mask = keep_mask;
     ba.pairs_tested = g_pairs_counter;
+    ba.meta = nullptr;  // the frame-level sort rewrites FrameMeta of declined frames
     const size_t smem = binned_smem_bytes(binned_npad(n_max));
     if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
     const int variant = (tie_break == PNMS_TIE_BY_INDEX ? 1 : 0) + (g_pairs_counter ? 2 : 0) +
@@ -592,10 +595,10 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     }
   }
 
-  if (!dense_flags && algo == 0 && gate_pairs == nullptr && n_max > kBinMaxSlots &&
-      cluster_slice(n_max, 16) > 0 && cluster_slice(n_max, cluster_size_for(n_max)) > 0) {
-    // large frames: one thread-block cluster per frame, cell data in distributed shared
-    // memory (pnms_binned_cluster.cuh); declined frames go to the dense pipeline by flag
+  if (!dense_flags && algo == 0 && gate_pairs == nullptr && n_max > kBinMaxSlots) {
+    // large frames: few frames -> kTilesPerFrame independent tile CTAs per frame
+    // (pnms_binned_tiles.cuh, latency); many frames -> one thread-block cluster per frame
+    // (pnms_binned_cluster.cuh, throughput).  Declined frames go to the dense pipeline by list.
     BinArgs ba;
     ba.x = x; ba.y = y; ba.z = z; ba.s = s; ba.counts = counts;
     ba.batch = batch; ba.n_max = n_max; ba.d_max = d_max; ba.tie_break = tie_break; ba.W32 = W32;
@@ -605,13 +608,42 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     ba.decl_list = reinterpret_cast<int32_t*>(ws + L.list) + 1;
     ba.keep_idx = keep_idx; ba.keep_count = keep_count; ba.keep_mask = keep_mask;
     ba.pairs_tested = g_pairs_counter;  // diagnostics: phase trace of the cluster kernel
-    if ((e = cudaMemsetAsync(ba.decl_count, 0, sizeof(int), st)) != cudaSuccess) return fail_cuda(e);
-    if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
-    if ((e = launch_cluster(ba, batch, n_max, tie_break == PNMS_TIE_BY_INDEX, st)) != cudaSuccess) return fail_cuda(e);
-    dense_flags = ws + L.dense;
-    if (events) {
-      ev_local[0] = events[1]; ev_local[1] = events[2]; ev_local[2] = nullptr; ev_local[3] = events[3];
-      events = ev_local;
+    ba.meta = reinterpret_cast<FrameMeta*>(ws + L.meta);  // the chunked sort accumulates into it
+    const int large = env_int("PNMS_LARGE", 0);  // 0 auto, 1 tiles, 2 cluster
+    const bool cluster_ok = cluster_slice(n_max, 16) > 0 && cluster_slice(n_max, cluster_size_for(n_max)) > 0;
+    const bool tiles = n_max <= 65536 && (large == 1 || (large == 0 && (batch <= 2 || !cluster_ok)));
+    if (tiles || cluster_ok) {
+      if ((e = cudaMemsetAsync(ba.decl_count, 0, sizeof(int), st)) != cudaSuccess) return fail_cuda(e);
+      if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
+      if (tiles) {
+        TileArgs ta;
+        ta.b = ba;
+        ta.decline = reinterpret_cast<int*>(ws + L.tiles);
+        ta.mask = reinterpret_cast<uint32_t*>(ws + L.tiles) + batch;
+        if ((e = cudaMemsetAsync(ws + L.tiles, 0, (size_t)batch * 4 + (size_t)batch * W32 * 4, st)) != cudaSuccess)
+          return fail_cuda(e);
+        static std::atomic<size_t> tcfg[2];
+        const size_t tsmem = binned_tiles_smem_bytes();
+        const bool bi = tie_break == PNMS_TIE_BY_INDEX;
+        if ((e = ensure_smem(bi ? pnms_binned_tiles<true> : pnms_binned_tiles<false>, tsmem, tcfg[bi])) != cudaSuccess)
+          return fail_cuda(e);
+        if ((e = launch_maybe_pdl(false, bi ? pnms_binned_tiles<true> : pnms_binned_tiles<false>,
+                                  dim3((unsigned)batch * kTilesPerFrame), dim3(kTileThreads), tsmem, st, ta)) !=
+            cudaSuccess)
+          return fail_cuda(e);
+        if ((e = launch_maybe_pdl(true, pnms_mask_compact, dim3((unsigned)batch), dim3(512), 0, st, ta)) != cudaSuccess)
+          return fail_cuda(e);
+      } else {
+        if ((e = launch_cluster(ba, batch, n_max, tie_break == PNMS_TIE_BY_INDEX, st)) != cudaSuccess)
+          return fail_cuda(e);
+      }
+      decl_list = ba.decl_list;
+      decl_count = ba.decl_count;
+      dense_flags = ws + L.dense;
+      if (events) {
+        ev_local[0] = events[1]; ev_local[1] = events[2]; ev_local[2] = nullptr; ev_local[3] = events[3];
+        events = ev_local;
+      }
     }
   }
 
@@ -664,14 +696,21 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     } else {
       pa.npad = kSortMax;
       pa.nchunks = (n_max + kSortMax - 1) / kSortMax;
-      if ((e = cudaMemsetAsync(pa.meta, 0, sizeof(FrameMeta) * (size_t)nf, sort_st)) != cudaSuccess) return fail_cuda(e);
+      // the declined-frame list path had each frame's FrameMeta zeroed by the decliner
+      if (!decl_list && (e = cudaMemsetAsync(pa.meta, 0, sizeof(FrameMeta) * (size_t)nf, sort_st)) != cudaSuccess)
+        return fail_cuda(e);
       const size_t smem = sort_smem_bytes(kSortMax);
       if ((e = ensure_smem(pnms_prep_sort_chunk, smem, g_sort_chunk_smem)) != cudaSuccess) return fail_cuda(e);
-      pnms_prep_sort_chunk<<<(unsigned)((long long)nf * pa.nchunks), kSortThreads, smem, sort_st>>>(pa);
-      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
+      const long long cgrid = (long long)nf * pa.nchunks;
+      if ((e = launch_maybe_pdl(decl_list != nullptr, pnms_prep_sort_chunk,
+                                dim3((unsigned)(decl_list ? std::min<long long>(cgrid, 148 * 2) : cgrid)),
+                                dim3(kSortThreads), smem, sort_st, pa)) != cudaSuccess)
+        return fail_cuda(e);
       const long long blocks = (long long)nf * ((n_max + 255) / 256);
-      pnms_merge_rank<<<(unsigned)blocks, 256, 0, sort_st>>>(pa);
-      if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
+      if ((e = launch_maybe_pdl(decl_list != nullptr, pnms_merge_rank,
+                                dim3((unsigned)(decl_list ? std::min<long long>(blocks, 148 * 8) : blocks)), dim3(256), 0,
+                                sort_st, pa)) != cudaSuccess)
+        return fail_cuda(e);
     }
     if (chunks > 1) {
       if ((e = cudaEventRecord(side->ev[c], side->s)) != cudaSuccess) return fail_cuda(e);

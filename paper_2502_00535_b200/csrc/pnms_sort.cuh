@@ -507,10 +507,7 @@ __global__ void __launch_bounds__(kSortThreads) pnms_prep_sort_frame(PrepArgs a)
 
 // Chunk mode (n_max > kSortMax), grid = batch * nchunks: sort one kSortMax-slot chunk and
 // publish (sorted key, input index) plus the chunk's statistics (meta is zeroed by the host).
-__global__ void __launch_bounds__(kSortThreads) pnms_prep_sort_chunk(PrepArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int f = blockIdx.x / a.nchunks, c = blockIdx.x % a.nchunks;
-  if (frame_skipped(a.dense, f)) return;
+__device__ __forceinline__ void prep_sort_chunk_body(const PrepArgs& a, int f, int c, unsigned char* smem_raw) {
   const long long fbase = (long long)f * a.n_max;
   const int cnt = frame_count(a.counts, f, a.n_max);
   const int e0 = c * kSortMax;
@@ -542,13 +539,28 @@ __global__ void __launch_bounds__(kSortThreads) pnms_prep_sort_chunk(PrepArgs a)
   }
 }
 
+__global__ void __launch_bounds__(kSortThreads) pnms_prep_sort_chunk(PrepArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (a.list) {
+    // declined-frame list (PDL after the binned kernel; the decliner zeroed each frame's meta)
+    cudaGridDependencySynchronize();
+    cudaTriggerProgrammaticLaunchCompletion();
+    const long long n = (long long)*a.list_count * a.nchunks;
+    for (long long it = blockIdx.x; it < n; it += gridDim.x) {
+      prep_sort_chunk_body(a, a.list[it / a.nchunks], (int)(it % a.nchunks), smem_raw);
+      __syncthreads();
+    }
+    return;
+  }
+  const int f = blockIdx.x / a.nchunks;
+  if (frame_skipped(a.dense, f)) return;
+  prep_sort_chunk_body(a, f, blockIdx.x % a.nchunks, smem_raw);
+}
+
 // Chunk mode, second pass: one thread per slot computes its global sorted position and its
 // column limit by binary search in every chunk, then emits perm / lim / record.
-__global__ void __launch_bounds__(256) pnms_merge_rank(PrepArgs a) {
-  const int blocks_per_frame = (a.n_max + 255) / 256;
-  const int f = blockIdx.x / blocks_per_frame;
-  if (frame_skipped(a.dense, f)) return;
-  const int e = (blockIdx.x % blocks_per_frame) * 256 + threadIdx.x;
+__device__ __forceinline__ void merge_rank_body(const PrepArgs& a, int f, int blk) {
+  const int e = blk * 256 + threadIdx.x;
   const long long fbase = (long long)f * a.n_max;
   const int cnt = frame_count(a.counts, f, a.n_max);
   unsigned long long l = 0;
@@ -578,6 +590,21 @@ __global__ void __launch_bounds__(256) pnms_merge_rank(PrepArgs a) {
   unsigned lo = __reduce_add_sync(0xFFFFFFFFu, (unsigned)(l & 0xFFFFFFFFull));
   unsigned hi = __reduce_add_sync(0xFFFFFFFFu, (unsigned)(l >> 32));
   if ((threadIdx.x & 31) == 0 && (lo | hi)) atomicAdd(&a.meta[f].lim_sum, ((unsigned long long)hi << 32) + lo);
+}
+
+__global__ void __launch_bounds__(256) pnms_merge_rank(PrepArgs a) {
+  const int blocks_per_frame = (a.n_max + 255) / 256;
+  if (a.list) {
+    cudaGridDependencySynchronize();
+    cudaTriggerProgrammaticLaunchCompletion();
+    const long long n = (long long)*a.list_count * blocks_per_frame;
+    for (long long it = blockIdx.x; it < n; it += gridDim.x)
+      merge_rank_body(a, a.list[it / blocks_per_frame], (int)(it % blocks_per_frame));
+    return;
+  }
+  const int f = blockIdx.x / blocks_per_frame;
+  if (frame_skipped(a.dense, f)) return;
+  merge_rank_body(a, f, blockIdx.x % blocks_per_frame);
 }
 
 }  // namespace pnms

@@ -174,13 +174,19 @@ def test_declined_frame_list_grid_stride(monkeypatch):
             assert np.array_equal(got[f], want[f]), (theta, f)
 
 
-@pytest.mark.parametrize("cs", ["8", "16"])
-def test_cluster_path_large_frames(cs, monkeypatch):
-    """Frames of 4097..20000 slots through the thread-block-cluster kernel (both cluster
-    sizes): ragged counts, exact ties, NaN and negative scores with padding, a band-crowded
-    frame and a declined frame (side > 126), both tie policies, vs the C oracle."""
+LARGE_PATHS = {"tiles": ("1", "16"), "cluster8": ("2", "8"), "cluster16": ("2", "16")}
+
+
+@pytest.mark.parametrize("large", list(LARGE_PATHS))
+def test_cluster_path_large_frames(large, monkeypatch):
+    """Frames of 4097..20000 slots through the large-frame binned kernels (independent tile
+    CTAs; one thread-block cluster per frame at both cluster sizes): ragged counts, exact ties,
+    NaN and negative scores with padding, a band-crowded frame and a declined frame (side >
+    126), both tie policies, vs the C oracle."""
     monkeypatch.setenv("PNMS_ALGO", "0")
-    monkeypatch.setenv("PNMS_CLUSTER", cs)
+    monkeypatch.setenv("PNMS_LARGE", LARGE_PATHS[large][0])
+    monkeypatch.setenv("PNMS_CLUSTER", LARGE_PATHS[large][1])
+    cs = large
     n = 20000
     x, y, z, s = random_frames(5, n, seed=41, frame_w=3840, frame_h=2160, duplicate_fraction=0.05)
     counts = np.array([n, 4097, 12345, 9000, 16384], np.int32)
@@ -195,10 +201,13 @@ def test_cluster_path_large_frames(cs, monkeypatch):
             assert np.array_equal(got[f], want), (cs, tie, f)
 
 
-def test_max_size_frame_cluster_path(monkeypatch):
-    """A 60000-slot frame (the cluster path's largest band layout, 16 CTAs x 3750 slots) vs the
-    C oracle, both tie policies."""
+@pytest.mark.parametrize("large", ["tiles", "cluster16"])
+def test_max_size_frame_cluster_path(large, monkeypatch):
+    """A 60000-slot frame (tile kernel; the cluster path's largest band layout, 16 CTAs x 3750
+    slots) vs the C oracle, both tie policies."""
     monkeypatch.setenv("PNMS_ALGO", "0")
+    monkeypatch.setenv("PNMS_LARGE", LARGE_PATHS[large][0])
+    monkeypatch.setenv("PNMS_CLUSTER", LARGE_PATHS[large][1])
     n = 60000
     x, y, z, s = random_frames(1, n, seed=60, frame_w=3840 * 2, frame_h=2160 * 2, duplicate_fraction=0.02)
     for tie in ("paper_faithful", "by_index"):
@@ -284,11 +293,12 @@ def test_ragged_duplicates_vs_oracle(tie, theta, path):
 
 
 @pytest.mark.parametrize("n", [4097, 6000, 9000, 16384])
-@pytest.mark.parametrize("cs", ["8", "16"])
-def test_chunked_sort_frames_vs_oracle(n, path, cs, monkeypatch):
-    """Frames above one CTA's capacity (thread-block-cluster binned kernel of cluster size cs;
-    chunk sort + merge-rank in the dense pipeline) with exact score ties."""
-    monkeypatch.setenv("PNMS_CLUSTER", cs)
+@pytest.mark.parametrize("large", list(LARGE_PATHS))
+def test_chunked_sort_frames_vs_oracle(n, path, large, monkeypatch):
+    """Frames above one CTA's capacity (tile kernel or thread-block-cluster kernel; chunk sort
+    + merge-rank in the dense pipeline) with exact score ties."""
+    monkeypatch.setenv("PNMS_LARGE", LARGE_PATHS[large][0])
+    monkeypatch.setenv("PNMS_CLUSTER", LARGE_PATHS[large][1])
     x, y, z, s = random_frames(2, n, seed=n, frame_w=3840, frame_h=2160, z_range=(8, 64), duplicate_fraction=0.1)
     s[:, ::7] = 0.5
     for tie in ("paper_faithful", "by_index"):
