@@ -35,8 +35,8 @@ constexpr int kBinCellMax = 64;
 // skip = boxes left to the end of the box's cell (<= kBinCellMax).  The pair value
 // d = v*v + w = w_x^2 + skip*2^8 + (z+1) + (w_x*h - T)*2^17 keeps sign(w_x*h - T): the low
 // terms stay below 16129 + 64*256 + 127 < 2^17 (the argument of pair_d).
-// The full keys and input slots live in separate arrays: a column whose high key half equals
-// the row's is resolved by an exact rescan of that row (rare: equal 32-bit prefixes).
+// The full keys and input slots live in separate arrays: a suppressing column whose high key
+// half equals the row's is verified on the full keys (rare: equal 32-bit prefixes).
 struct __align__(16) RecBin {
   uint32_t a, nb;
   int32_t w;
@@ -277,51 +277,43 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
     const int cx0 = qdiv(max(ix - maxz - ox, 0), M), cy0 = qdiv(max(iy - maxz - oy, 0), M);
     const int cx1 = min(GX - 1, qdiv(ix + iz - ox, M)), cy1 = min(GY - 1, qdiv(iy + iz - oy, M));
     const uint32_t pb = (uint32_t)p * (uint32_t)sizeof(RecBin);
-    bool sup = false, tie = false;
+    bool sup = false;
     for (int yy = cy0; yy <= cy1 && !sup; ++yy) {
       // byte offsets of the run's first record and its end
       uint32_t qb = cstart[yy * GX + cx0] * (uint32_t)sizeof(RecBin);
       const uint32_t qe = cstart[yy * GX + cx1 + 1] * (uint32_t)sizeof(RecBin);
-      while (qb < qe) {
-        const uint4 g = *reinterpret_cast<const uint4*>(rbase + qb);  // a, nb, w, k
-        // strict on the high key halves: a subset of the reference's gate; an equal half
-        // (another box) flags the row for the exact rescan below
-        const bool gate = g.w < ri.k;
-        tie |= (g.w == ri.k) & (qb != pb);
-        const uint32_t t1 = __viaddmin_s16x2(ri.a, g.y, zzi);
-        const uint32_t t2 = __viaddmin_s16x2_relu(g.x, ri.nb, t1);
-        const uint32_t v = __vimin_s16x2_relu(t2, __byte_perm(g.z, 0u, 0x4040));
-        if (COUNT && gate) ++tested;
-        if (gate && (int)(v * v) + (int)g.z >= 0) {
+      for (;;) {
+        // gate on the high key halves with <=: a superset of the reference's gate whose
+        // columns still form a prefix of every cell; a suppressor found with an equal half
+        // is verified on the full keys below (outside the hot loop)
+        uint32_t gk = 0;
+        while (qb < qe) {
+          const uint4 g = *reinterpret_cast<const uint4*>(rbase + qb);  // a, nb, w, k
+          const bool gate = g.w <= ri.k;
+          const uint32_t t1 = __viaddmin_s16x2(ri.a, g.y, zzi);
+          const uint32_t t2 = __viaddmin_s16x2_relu(g.x, ri.nb, t1);
+          const uint32_t v = __vimin_s16x2_relu(t2, __byte_perm(g.z, 0u, 0x4040));
+          if (COUNT && gate) ++tested;
+          if (gate && (int)(v * v) + (int)g.z >= 0) {
+            gk = g.w;
+            break;
+          }
+          qb += (gate ? 1u : __byte_perm(g.z, 0u, 0x4441)) * (uint32_t)sizeof(RecBin);
+        }
+        if (qb >= qe) break;
+        if (gk != ri.k) {  // strictly smaller high half: gated
           sup = true;
           break;
         }
-        qb += (gate ? 1u : __byte_perm(g.z, 0u, 0x4441)) * (uint32_t)sizeof(RecBin);
-      }
-    }
-    if (!sup && tie) {
-      // exact rescan of this row: the reference's gate on full keys (and slots for by_index)
-      const uint64_t ki = keyS[p];
-      const int ii = idxS[p];
-      for (int yy = cy0; yy <= cy1 && !sup; ++yy) {
-        int q = cstart[yy * GX + cx0];
-        const int qe = cstart[yy * GX + cx1 + 1];
-        while (q < qe) {
-          const uint64_t kj = keyS[q];
-          const RecBin rj = recS[q];
-          if (kj < ki || (BY_INDEX && kj == ki && (int)idxS[q] < ii)) {
-            const uint32_t t1 = __viaddmin_s16x2(ri.a, rj.nb, zzi);
-            const uint32_t t2 = __viaddmin_s16x2_relu(rj.a, ri.nb, t1);
-            const uint32_t v = __vimin_s16x2_relu(t2, __byte_perm((uint32_t)rj.w, 0u, 0x4040));
-            if ((int)(v * v) + rj.w >= 0) {
-              sup = true;
-              break;
-            }
-            ++q;
-          } else {
-            q += __byte_perm((uint32_t)rj.w, 0u, 0x4441);
+        if (qb != pb) {    // equal halves: the reference's gate on the full key (and slot)
+          const int q = (int)(qb / (uint32_t)sizeof(RecBin));
+          const uint64_t kj = keyS[q], ki = keyS[p];
+          if (kj < ki || (BY_INDEX && kj == ki && idxS[q] < idxS[p])) {
+            sup = true;
+            break;
           }
         }
+        qb += (uint32_t)sizeof(RecBin);  // not gated (or the row itself): keep scanning
       }
     }
     const int i = idxS[p];
