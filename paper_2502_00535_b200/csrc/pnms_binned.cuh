@@ -87,6 +87,42 @@ __device__ __forceinline__ void binned_decline(const BinArgs& a, int f) {
   a.decl_list[atomicAdd(a.decl_count, 1)] = f;
 }
 
+// One row against one contiguous run of cells [qb, qe) (byte offsets of 16 B records in cell
+// order; every cell in (key, slot) order, skip distance in bits 8..14 of w).  Gate on the high
+// key halves with <=: a superset of the reference's gate (engine.py:233-235) whose columns
+// still form a prefix of every cell, so the scan jumps to the cell's end at the first column
+// that fails it; a suppressor found with an equal half (or the row itself, pb) is verified on
+// the full keys and slots outside the hot loop.  Returns true if the row is suppressed.
+template <bool BY_INDEX, bool COUNT>
+__device__ __forceinline__ bool binned_scan_run(const char* rbase, uint32_t qb, uint32_t qe, const RecBin& ri,
+                                                uint32_t zzi, uint32_t pb, const uint64_t* keyS, const uint16_t* idxS,
+                                                int p, unsigned long long& tested) {
+  for (;;) {
+    uint32_t gk = 0;
+    while (qb < qe) {
+      const uint4 g = *reinterpret_cast<const uint4*>(rbase + qb);  // a, nb, w, k
+      const bool gate = g.w <= ri.k;
+      const uint32_t t1 = __viaddmin_s16x2(ri.a, g.y, zzi);
+      const uint32_t t2 = __viaddmin_s16x2_relu(g.x, ri.nb, t1);
+      const uint32_t v = __vimin_s16x2_relu(t2, __byte_perm(g.z, 0u, 0x4040));
+      if (COUNT && gate) ++tested;
+      if (gate && (int)(v * v) + (int)g.z >= 0) {
+        gk = g.w;
+        break;
+      }
+      qb += (gate ? 1u : __byte_perm(g.z, 0u, 0x4441)) * (uint32_t)sizeof(RecBin);
+    }
+    if (qb >= qe) return false;
+    if (gk != ri.k) return true;  // strictly smaller high half: gated
+    if (qb != pb) {               // equal halves: the reference's gate on the full key (and slot)
+      const int q = (int)(qb / (uint32_t)sizeof(RecBin));
+      const uint64_t kj = keyS[q], ki = keyS[p];
+      if (kj < ki || (BY_INDEX && kj == ki && idxS[q] < idxS[p])) return true;
+    }
+    qb += (uint32_t)sizeof(RecBin);  // not gated (or the row itself): keep scanning
+  }
+}
+
 template <bool BY_INDEX, bool COUNT, int PER>
 __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -282,39 +318,7 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
       // byte offsets of the run's first record and its end
       uint32_t qb = cstart[yy * GX + cx0] * (uint32_t)sizeof(RecBin);
       const uint32_t qe = cstart[yy * GX + cx1 + 1] * (uint32_t)sizeof(RecBin);
-      for (;;) {
-        // gate on the high key halves with <=: a superset of the reference's gate whose
-        // columns still form a prefix of every cell; a suppressor found with an equal half
-        // is verified on the full keys below (outside the hot loop)
-        uint32_t gk = 0;
-        while (qb < qe) {
-          const uint4 g = *reinterpret_cast<const uint4*>(rbase + qb);  // a, nb, w, k
-          const bool gate = g.w <= ri.k;
-          const uint32_t t1 = __viaddmin_s16x2(ri.a, g.y, zzi);
-          const uint32_t t2 = __viaddmin_s16x2_relu(g.x, ri.nb, t1);
-          const uint32_t v = __vimin_s16x2_relu(t2, __byte_perm(g.z, 0u, 0x4040));
-          if (COUNT && gate) ++tested;
-          if (gate && (int)(v * v) + (int)g.z >= 0) {
-            gk = g.w;
-            break;
-          }
-          qb += (gate ? 1u : __byte_perm(g.z, 0u, 0x4441)) * (uint32_t)sizeof(RecBin);
-        }
-        if (qb >= qe) break;
-        if (gk != ri.k) {  // strictly smaller high half: gated
-          sup = true;
-          break;
-        }
-        if (qb != pb) {    // equal halves: the reference's gate on the full key (and slot)
-          const int q = (int)(qb / (uint32_t)sizeof(RecBin));
-          const uint64_t kj = keyS[q], ki = keyS[p];
-          if (kj < ki || (BY_INDEX && kj == ki && idxS[q] < idxS[p])) {
-            sup = true;
-            break;
-          }
-        }
-        qb += (uint32_t)sizeof(RecBin);  // not gated (or the row itself): keep scanning
-      }
+      if (binned_scan_run<BY_INDEX, COUNT>(rbase, qb, qe, ri, zzi, pb, keyS, idxS, p, tested)) sup = true;
     }
     const int i = idxS[p];
     // implicit padding gate (engine.py:233 with s_j = 0, z_j = 0): rows with s < 0 drop

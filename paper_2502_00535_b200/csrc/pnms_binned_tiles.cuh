@@ -33,7 +33,7 @@ inline size_t binned_tiles_smem_bytes() {
 }
 
 template <bool BY_INDEX>
-__global__ void __launch_bounds__(kTileThreads, 2) pnms_binned_tiles(TileArgs ta) {
+__global__ void __launch_bounds__(kTileThreads, 1) pnms_binned_tiles(TileArgs ta) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const BinArgs& a = ta.b;
   const int f = blockIdx.x / kTilesPerFrame, t = blockIdx.x % kTilesPerFrame;
@@ -271,49 +271,13 @@ __global__ void __launch_bounds__(kTileThreads, 2) pnms_binned_tiles(TileArgs ta
     const int rx0 = max(qdiv(max(ix - maxz - ox, 0), M), cx0), ry0 = max(qdiv(max(iy - maxz - oy, 0), M), cy0);
     const int rx1 = min(cx1, qdiv(ix + iz - ox, M)), ry1 = min(cy1, qdiv(iy + iz - oy, M));
     const uint32_t pb = (uint32_t)p * (uint32_t)sizeof(RecBin);
-    bool sup = false, tie = false;
+    bool sup = false;
+    unsigned long long tested = 0;
     for (int yy = ry0; yy <= ry1 && !sup; ++yy) {
       const int lr = (yy - cy0) * LW - cx0;
-      uint32_t qb = cstart[lr + rx0] * (uint32_t)sizeof(RecBin);
+      const uint32_t qb = cstart[lr + rx0] * (uint32_t)sizeof(RecBin);
       const uint32_t qe = cstart[lr + rx1 + 1] * (uint32_t)sizeof(RecBin);
-      while (qb < qe) {
-        const uint4 g = *reinterpret_cast<const uint4*>(rbase + qb);
-        const bool gate = g.w < ri.k;
-        tie |= (g.w == ri.k) & (qb != pb);
-        const uint32_t t1 = __viaddmin_s16x2(ri.a, g.y, zzi);
-        const uint32_t t2 = __viaddmin_s16x2_relu(g.x, ri.nb, t1);
-        const uint32_t v = __vimin_s16x2_relu(t2, __byte_perm(g.z, 0u, 0x4040));
-        if (gate && (int)(v * v) + (int)g.z >= 0) {
-          sup = true;
-          break;
-        }
-        qb += (gate ? 1u : __byte_perm(g.z, 0u, 0x4441)) * (uint32_t)sizeof(RecBin);
-      }
-    }
-    if (!sup && tie) {
-      const uint64_t ki = keyS[p];
-      const int ii = idxS[p];
-      for (int yy = ry0; yy <= ry1 && !sup; ++yy) {
-        const int lr = (yy - cy0) * LW - cx0;
-        int q = (int)cstart[lr + rx0];
-        const int qe = (int)cstart[lr + rx1 + 1];
-        while (q < qe) {
-          const uint64_t kj = keyS[q];
-          const RecBin rj = recS[q];
-          if (kj < ki || (BY_INDEX && kj == ki && (int)idxS[q] < ii)) {
-            const uint32_t t1 = __viaddmin_s16x2(ri.a, rj.nb, zzi);
-            const uint32_t t2 = __viaddmin_s16x2_relu(rj.a, ri.nb, t1);
-            const uint32_t v = __vimin_s16x2_relu(t2, __byte_perm((uint32_t)rj.w, 0u, 0x4040));
-            if ((int)(v * v) + rj.w >= 0) {
-              sup = true;
-              break;
-            }
-            ++q;
-          } else {
-            q += __byte_perm((uint32_t)rj.w, 0u, 0x4441);
-          }
-        }
-      }
+      sup = binned_scan_run<BY_INDEX, false>(rbase, qb, qe, ri, zzi, pb, keyS, idxS, p, tested);
     }
     const int i = idxS[p];
     if (!sup && pad_rule && a.s[fbase + i] < 0.0) sup = true;
