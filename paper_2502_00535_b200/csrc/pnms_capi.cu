@@ -352,10 +352,17 @@ MapShape choose_map_shape(int batch, int n_max) {
 }
 
 template <int R>
-cudaError_t launch_map(const MapArgs& ma, long long grid, size_t smem, cudaStream_t st, bool pdl) {
+cudaError_t launch_map(const MapArgs& ma, long long grid, size_t smem, cudaStream_t st, bool list) {
+  if (list) {
+    static std::atomic<size_t> lcfg{0};
+    cudaError_t e = ensure_smem(pnms_map_kernel_list<R>, smem, lcfg);
+    if (e != cudaSuccess) return e;
+    return launch_maybe_pdl(true, pnms_map_kernel_list<R>, dim3((unsigned)grid), dim3(kMapWarps * 32), smem, st, ma);
+  }
   cudaError_t e = ensure_smem(pnms_map_kernel<R>, smem, g_map_smem[R]);
   if (e != cudaSuccess) return e;
-  return launch_maybe_pdl(pdl, pnms_map_kernel<R>, dim3((unsigned)grid), dim3(kMapWarps * 32), smem, st, ma);
+  pnms_map_kernel<R><<<(unsigned)grid, kMapWarps * 32, smem, st>>>(ma);
+  return cudaGetLastError();
 }
 
 }  // namespace
@@ -688,11 +695,17 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
       pa.npad = (n_max + kSortThreads - 1) / kSortThreads * kSortThreads;
       pa.nchunks = 1;
       const size_t smem = sort_frame_smem_bytes(pa.npad);
-      if ((e = ensure_smem(pnms_prep_sort_frame, smem, g_sort_frame_smem)) != cudaSuccess) return fail_cuda(e);
-      const int pgrid = decl_list ? std::min(nf, 148 * 2) : nf;
-      if ((e = launch_maybe_pdl(decl_list != nullptr, pnms_prep_sort_frame, dim3(pgrid), dim3(kSortThreads), smem,
-                                sort_st, pa)) != cudaSuccess)
-        return fail_cuda(e);
+      if (decl_list) {
+        static std::atomic<size_t> lcfg{0};
+        if ((e = ensure_smem(pnms_prep_sort_frame_list, smem, lcfg)) != cudaSuccess) return fail_cuda(e);
+        if ((e = launch_maybe_pdl(true, pnms_prep_sort_frame_list, dim3(std::min(nf, 148 * 2)), dim3(kSortThreads),
+                                  smem, sort_st, pa)) != cudaSuccess)
+          return fail_cuda(e);
+      } else {
+        if ((e = ensure_smem(pnms_prep_sort_frame, smem, g_sort_frame_smem)) != cudaSuccess) return fail_cuda(e);
+        pnms_prep_sort_frame<<<nf, kSortThreads, smem, sort_st>>>(pa);
+        if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
+      }
     } else {
       pa.npad = kSortMax;
       pa.nchunks = (n_max + kSortMax - 1) / kSortMax;

@@ -267,19 +267,24 @@ template <int R>
 __global__ void __launch_bounds__(kMapWarps * 32) pnms_map_kernel(MapArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bar;
-  if (a.list) {
-    cudaGridDependencySynchronize();  // PDL: the previous kernel's results are visible after this
-    cudaTriggerProgrammaticLaunchCompletion();
-    const long long n = (long long)*a.list_count * a.items_per_frame;
-    for (long long it = blockIdx.x; it < n; it += gridDim.x) {
-      map_item<R>(a, a.list[it / a.items_per_frame], (int)(it % a.items_per_frame), smem_raw, bar);
-      __syncthreads();  // every warp is past the barrier wait and done with the column chunk
-    }
-    return;
-  }
   const int f = blockIdx.x / a.items_per_frame;
   if (a.dense && !a.dense[f]) return;
   map_item<R>(a, f, blockIdx.x % a.items_per_frame, smem_raw, bar);
+}
+
+// the same over the binned path's declined-frame list (persistent grid, programmatic
+// dependent launch); a separate kernel so the full-batch one keeps its register budget
+template <int R>
+__global__ void __launch_bounds__(kMapWarps * 32) pnms_map_kernel_list(MapArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bar;
+  cudaGridDependencySynchronize();  // PDL: the previous kernel's results are visible after this
+  cudaTriggerProgrammaticLaunchCompletion();
+  const long long n = (long long)*a.list_count * a.items_per_frame;
+  for (long long it = blockIdx.x; it < n; it += gridDim.x) {
+    map_item<R>(a, a.list[it / a.items_per_frame], (int)(it % a.items_per_frame), smem_raw, bar);
+    __syncthreads();  // every warp is past the barrier wait and done with the column chunk
+  }
 }
 
 }  // namespace pnms

@@ -490,19 +490,22 @@ __device__ __forceinline__ void prep_sort_frame_body(const PrepArgs& a, int f, u
 
 __global__ void __launch_bounds__(kSortThreads) pnms_prep_sort_frame(PrepArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  if (a.list) {
-    // launched programmatically after the binned kernel (PDL): wait for its results
-    cudaGridDependencySynchronize();
-    cudaTriggerProgrammaticLaunchCompletion();
-    const int n = *a.list_count;
-    for (int li = blockIdx.x; li < n; li += gridDim.x) {
-      prep_sort_frame_body(a, a.list[li], smem_raw);
-      __syncthreads();
-    }
-    return;
-  }
   if (frame_skipped(a.dense, blockIdx.x)) return;
   prep_sort_frame_body(a, blockIdx.x, smem_raw);
+}
+
+// the same over the binned path's declined-frame list: a small persistent grid launched
+// programmatically after the binned kernel (kept separate so the full-batch kernel above keeps
+// its register budget)
+__global__ void __launch_bounds__(kSortThreads) pnms_prep_sort_frame_list(PrepArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cudaGridDependencySynchronize();
+  cudaTriggerProgrammaticLaunchCompletion();
+  const int n = *a.list_count;
+  for (int li = blockIdx.x; li < n; li += gridDim.x) {
+    prep_sort_frame_body(a, a.list[li], smem_raw);
+    __syncthreads();
+  }
 }
 
 // Chunk mode (n_max > kSortMax), grid = batch * nchunks: sort one kSortMax-slot chunk and
