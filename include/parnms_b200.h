@@ -158,6 +158,10 @@ int pnms_unpack_box32(const uint32_t* box, int32_t* x, int32_t* y, int32_t* z, l
  * number of pair tests it executes; NULL disables (default).  Process-wide, not reentrant. */
 int pnms_debug_count_pairs(uint64_t* device_counter);
 
+/* Diagnostics: device buffer of >= 256 uint64 that the large-frame kernels fill with global-timer
+ * stamps (CTA r < 16, phase k < 16 at [r*16 + k]); NULL disables (default).  Process-wide. */
+int pnms_debug_trace(uint64_t* device_buffer);
+
 /* Human-readable text for a pnms_status. */
 const char* pnms_strerror(int status);
 

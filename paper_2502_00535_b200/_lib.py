@@ -25,6 +25,7 @@ EXPORTED_SYMBOLS = (
     "pnms_widen_i16",
     "pnms_unpack_box32",
     "pnms_debug_count_pairs",
+    "pnms_debug_trace",
     "pnms_strerror",
     "pnms_last_cuda_error",
     "pnms_version",
@@ -92,6 +93,8 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
     lib.pnms_widen_i16.restype = i32
     lib.pnms_unpack_box32.argtypes = [vp, vp, vp, vp, ctypes.c_longlong, vp]
     lib.pnms_unpack_box32.restype = i32
+    lib.pnms_debug_trace.argtypes = [vp]
+    lib.pnms_debug_trace.restype = i32
     lib.pnms_debug_count_pairs.argtypes = [vp]
     lib.pnms_debug_count_pairs.restype = i32
     lib.pnms_strerror.argtypes = [i32]

@@ -58,6 +58,7 @@ struct BinArgs {
   int32_t* keep_count;
   uint32_t* keep_mask;
   unsigned long long* pairs_tested;  // optional device counter (diagnostics), may be null
+  unsigned long long* trace;         // optional per-CTA phase timestamps (diagnostics), may be null
 };
 
 struct __align__(16) BinStats {
@@ -98,21 +99,25 @@ __device__ __forceinline__ bool binned_scan_run(const char* rbase, uint32_t qb, 
                                                 uint32_t zzi, uint32_t pb, const uint64_t* keyS, const uint16_t* idxS,
                                                 int p, unsigned long long& tested) {
   for (;;) {
+    // branch-free body: the loop exits through its condition only (no break, so no
+    // convergence-barrier bookkeeping per candidate)
     uint32_t gk = 0;
-    while (qb < qe) {
+    bool hit = false;
+    bool go = qb < qe;
+    while (go) {
       const uint4 g = *reinterpret_cast<const uint4*>(rbase + qb);  // a, nb, w, k
       const bool gate = g.w <= ri.k;
       const uint32_t t1 = __viaddmin_s16x2(ri.a, g.y, zzi);
       const uint32_t t2 = __viaddmin_s16x2_relu(g.x, ri.nb, t1);
       const uint32_t v = __vimin_s16x2_relu(t2, __byte_perm(g.z, 0u, 0x4040));
       if (COUNT && gate) ++tested;
-      if (gate && (int)(v * v) + (int)g.z >= 0) {
-        gk = g.w;
-        break;
-      }
-      qb += (gate ? 1u : __byte_perm(g.z, 0u, 0x4441)) * (uint32_t)sizeof(RecBin);
+      hit = gate && (int)(v * v) + (int)g.z >= 0;
+      gk = g.w;
+      const uint32_t nqb = qb + ((gate ? 1u : __byte_perm(g.z, 0u, 0x4441)) << 4);
+      qb = hit ? qb : nqb;
+      go = !hit && nqb < qe;
     }
-    if (qb >= qe) return false;
+    if (!hit) return false;
     if (gk != ri.k) return true;  // strictly smaller high half: gated
     if (qb != pb) {               // equal halves: the reference's gate on the full key (and slot)
       const int q = (int)(qb / (uint32_t)sizeof(RecBin));

@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kClThreads, 1) pnms_binned_cluster(BinArgs a, 
   ClStats* st0 = cl.map_shared_rank(st, 0);
   const int e0 = r * slice;
   const int slice_words = slice / 32;
-  unsigned long long* trace = a.pairs_tested;  // the cluster kernel reuses the diagnostics hook
+  unsigned long long* trace = a.trace;  // diagnostics: phase timestamps (pnms_debug_trace)
 
   if (threadIdx.x == 0) {
     st->mode = kNarrow7; st->minz = 0x7FFFFFFF; st->maxz = 0;

@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) pnms_binned_tiles(TileArgs ta
   const long long fbase = (long long)f * a.n_max;
   const int cnt = frame_count(a.counts, f, a.n_max);
   cudaTriggerProgrammaticLaunchCompletion();  // pnms_mask_compact may launch early (PDL)
-  unsigned long long* trace = a.pairs_tested;   // diagnostics: per-CTA phase timestamps
+  unsigned long long* trace = a.trace;          // diagnostics: per-CTA phase timestamps
 #define PNMS_TILE_TRACE(ph)                                                               \
   do {                                                                                    \
     if (trace && threadIdx.x == 0 && t < 16) {                                            \

@@ -77,7 +77,8 @@ __global__ void __launch_bounds__(256) pnms_unpack_box32_kernel(const uint32_t* 
 namespace {
 
 thread_local int g_last_cuda_error = 0;
-unsigned long long* g_pairs_counter = nullptr;  // diagnostics: binned pair tests (pnms_debug_pairs_counter)
+unsigned long long* g_pairs_counter = nullptr;  // diagnostics: binned pair tests (pnms_debug_count_pairs)
+unsigned long long* g_trace = nullptr;          // diagnostics: phase timestamps (pnms_debug_trace)
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -471,6 +472,11 @@ int pnms_unpack_box32(const uint32_t* box, int32_t* x, int32_t* y, int32_t* z, l
   return e == cudaSuccess ? PNMS_OK : fail_cuda(e);
 }
 
+int pnms_debug_trace(uint64_t* device_buffer) {
+  g_trace = reinterpret_cast<unsigned long long*>(device_buffer);
+  return PNMS_OK;
+}
+
 int pnms_debug_count_pairs(uint64_t* device_counter) {
   g_pairs_counter = reinterpret_cast<unsigned long long*>(device_counter);
   return PNMS_OK;
@@ -579,6 +585,7 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     if ((e = cudaMemsetAsync(ba.decl_count, 0, sizeof(int), st)) != cudaSuccess) return fail_cuda(e);
     ba.keep_idx = keep_idx; ba.keep_count = keep_count; ba.keep_mask = keep_mask;
     ba.pairs_tested = g_pairs_counter;
+    ba.trace = g_trace;
     ba.meta = nullptr;  // the frame-level sort rewrites FrameMeta of declined frames
     const size_t smem = binned_smem_bytes(binned_npad(n_max));
     if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
@@ -614,7 +621,8 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     ba.decl_count = reinterpret_cast<int*>(ws + L.list);
     ba.decl_list = reinterpret_cast<int32_t*>(ws + L.list) + 1;
     ba.keep_idx = keep_idx; ba.keep_count = keep_count; ba.keep_mask = keep_mask;
-    ba.pairs_tested = g_pairs_counter;  // diagnostics: phase trace of the cluster kernel
+    ba.pairs_tested = nullptr;
+    ba.trace = g_trace;
     ba.meta = reinterpret_cast<FrameMeta*>(ws + L.meta);  // the chunked sort accumulates into it
     const int large = env_int("PNMS_LARGE", 0);  // 0 auto, 1 tiles, 2 cluster
     const bool cluster_ok = cluster_slice(n_max, 16) > 0 && cluster_slice(n_max, cluster_size_for(n_max)) > 0;

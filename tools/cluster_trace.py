@@ -14,10 +14,10 @@ x, y, z, s = (torch.from_numpy(np.ascontiguousarray(g[f"C3_{c}"]).reshape(1, -1)
 for _ in range(3):
     batched_nms_keep(x, y, z, s, None, 0.5)
 buf = torch.zeros(16 * 16, dtype=torch.int64, device="cuda")
-_lib.load().pnms_debug_count_pairs(buf.data_ptr())
+_lib.load().pnms_debug_trace(buf.data_ptr())
 batched_nms_keep(x, y, z, s, None, 0.5)
 torch.cuda.synchronize()
-_lib.load().pnms_debug_count_pairs(None)
+_lib.load().pnms_debug_trace(None)
 t = buf.cpu().numpy().reshape(16, 16)
 t0 = t[t > 0].min()
 for r in range(16):
