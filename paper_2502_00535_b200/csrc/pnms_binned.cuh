@@ -88,24 +88,31 @@ __device__ __forceinline__ void binned_decline(const BinArgs& a, int f) {
   a.decl_list[atomicAdd(a.decl_count, 1)] = f;
 }
 
-// One row against one contiguous run of cells [qb, qe) (byte offsets of 16 B records in cell
-// order; every cell in (key, slot) order, skip distance in bits 8..14 of w).  Gate on the high
-// key halves with <=: a superset of the reference's gate (engine.py:233-235) whose columns
-// still form a prefix of every cell, so the scan jumps to the cell's end at the first column
-// that fails it; a suppressor found with an equal half (or the row itself, pb) is verified on
-// the full keys and slots outside the hot loop.  Returns true if the row is suppressed.
+__device__ __forceinline__ uint4 lds128(uint32_t saddr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(saddr));
+  return v;
+}
+
+// One row against one contiguous run of cells [qb, qe) (shared-window byte addresses of 16 B
+// records in cell order; every cell in (key, slot) order, skip distance in bits 8..14 of w).
+// Gate on the high key halves with <=: a superset of the reference's gate (engine.py:233-235)
+// whose columns still form a prefix of every cell, so the scan jumps to the cell's end at the
+// first column that fails it; a suppressor found with an equal half (or the row itself at pb)
+// is verified on the full keys and slots outside the hot loop.  `base` is the address of
+// record 0.  Returns true if the row is suppressed.
 template <bool BY_INDEX, bool COUNT>
-__device__ __forceinline__ bool binned_scan_run(const char* rbase, uint32_t qb, uint32_t qe, const RecBin& ri,
+__device__ __forceinline__ bool binned_scan_run(uint32_t base, uint32_t qb, uint32_t qe, const RecBin& ri,
                                                 uint32_t zzi, uint32_t pb, const uint64_t* keyS, const uint16_t* idxS,
                                                 int p, unsigned long long& tested) {
   for (;;) {
     // branch-free body: the loop exits through its condition only (no break, so no
     // convergence-barrier bookkeeping per candidate)
-    uint32_t gk = 0;
+    uint32_t gk = 0, step = 0;
     bool hit = false;
     bool go = qb < qe;
     while (go) {
-      const uint4 g = *reinterpret_cast<const uint4*>(rbase + qb);  // a, nb, w, k
+      const uint4 g = lds128(qb);  // a, nb, w, k
       const bool gate = g.w <= ri.k;
       const uint32_t t1 = __viaddmin_s16x2(ri.a, g.y, zzi);
       const uint32_t t2 = __viaddmin_s16x2_relu(g.x, ri.nb, t1);
@@ -113,14 +120,15 @@ __device__ __forceinline__ bool binned_scan_run(const char* rbase, uint32_t qb, 
       if (COUNT && gate) ++tested;
       hit = gate && (int)(v * v) + (int)g.z >= 0;
       gk = g.w;
-      const uint32_t nqb = qb + ((gate ? 1u : __byte_perm(g.z, 0u, 0x4441)) << 4);
-      qb = hit ? qb : nqb;
-      go = !hit && nqb < qe;
+      step = (gate ? 1u : __byte_perm(g.z, 0u, 0x4441)) << 4;
+      qb += step;
+      go = !hit && qb < qe;
     }
     if (!hit) return false;
+    qb -= step;                   // back to the suppressor
     if (gk != ri.k) return true;  // strictly smaller high half: gated
     if (qb != pb) {               // equal halves: the reference's gate on the full key (and slot)
-      const int q = (int)(qb / (uint32_t)sizeof(RecBin));
+      const int q = (int)((qb - base) >> 4);
       const uint64_t kj = keyS[q], ki = keyS[p];
       if (kj < ki || (BY_INDEX && kj == ki && idxS[q] < idxS[p])) return true;
     }
@@ -308,7 +316,7 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
   unsigned long long tested = 0;
   const int maxz = st->maxz;
   const bool pad_rule = a.d_max > cnt;
-  const char* rbase = reinterpret_cast<const char*>(recS);
+  const uint32_t rbase = static_cast<uint32_t>(__cvta_generic_to_shared(recS));
   for (int p = threadIdx.x; p < n_act; p += kBinThreads) {
     const RecBin ri = recS[p];
     const uint32_t zzi = __byte_perm((uint32_t)ri.w, 0u, 0x4040);  // (z+1, z+1)
@@ -317,12 +325,12 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
     const int32_t iz = (int32_t)(ri.w & 0xFF) - 1;
     const int cx0 = qdiv(max(ix - maxz - ox, 0), M), cy0 = qdiv(max(iy - maxz - oy, 0), M);
     const int cx1 = min(GX - 1, qdiv(ix + iz - ox, M)), cy1 = min(GY - 1, qdiv(iy + iz - oy, M));
-    const uint32_t pb = (uint32_t)p * (uint32_t)sizeof(RecBin);
+    const uint32_t pb = rbase + (uint32_t)p * (uint32_t)sizeof(RecBin);
     bool sup = false;
     for (int yy = cy0; yy <= cy1 && !sup; ++yy) {
       // byte offsets of the run's first record and its end
-      uint32_t qb = cstart[yy * GX + cx0] * (uint32_t)sizeof(RecBin);
-      const uint32_t qe = cstart[yy * GX + cx1 + 1] * (uint32_t)sizeof(RecBin);
+      const uint32_t qb = rbase + cstart[yy * GX + cx0] * (uint32_t)sizeof(RecBin);
+      const uint32_t qe = rbase + cstart[yy * GX + cx1 + 1] * (uint32_t)sizeof(RecBin);
       if (binned_scan_run<BY_INDEX, COUNT>(rbase, qb, qe, ri, zzi, pb, keyS, idxS, p, tested)) sup = true;
     }
     const int i = idxS[p];

@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) pnms_binned_tiles(TileArgs ta
   const int maxz = st->maxz;
   const bool pad_rule = a.d_max > cnt;
   const int nl = (int)cstart[lcells];
-  const char* rbase = reinterpret_cast<const char*>(recS);
+  const uint32_t rbase = static_cast<uint32_t>(__cvta_generic_to_shared(recS));
   for (int p = threadIdx.x; p < nl; p += kTileThreads) {
     const int lc = cellS[p];
     const int gcx = cx0 + lc % LW, gcy = cy0 + lc / LW;
@@ -270,13 +270,13 @@ __global__ void __launch_bounds__(kTileThreads, 1) pnms_binned_tiles(TileArgs ta
     const int32_t iz = (int32_t)(ri.w & 0xFF) - 1;
     const int rx0 = max(qdiv(max(ix - maxz - ox, 0), M), cx0), ry0 = max(qdiv(max(iy - maxz - oy, 0), M), cy0);
     const int rx1 = min(cx1, qdiv(ix + iz - ox, M)), ry1 = min(cy1, qdiv(iy + iz - oy, M));
-    const uint32_t pb = (uint32_t)p * (uint32_t)sizeof(RecBin);
+    const uint32_t pb = rbase + (uint32_t)p * (uint32_t)sizeof(RecBin);
     bool sup = false;
     unsigned long long tested = 0;
     for (int yy = ry0; yy <= ry1 && !sup; ++yy) {
       const int lr = (yy - cy0) * LW - cx0;
-      const uint32_t qb = cstart[lr + rx0] * (uint32_t)sizeof(RecBin);
-      const uint32_t qe = cstart[lr + rx1 + 1] * (uint32_t)sizeof(RecBin);
+      const uint32_t qb = rbase + cstart[lr + rx0] * (uint32_t)sizeof(RecBin);
+      const uint32_t qe = rbase + cstart[lr + rx1 + 1] * (uint32_t)sizeof(RecBin);
       sup = binned_scan_run<BY_INDEX, false>(rbase, qb, qe, ri, zzi, pb, keyS, idxS, p, tested);
     }
     const int i = idxS[p];
