@@ -266,46 +266,52 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
     if (threadIdx.x == 0) binned_decline(a, f);
     return;
   }
-  // ---- pass 3: scatter records, keys and input slots straight into cell order
+  // ---- pass 3: keys and slots into cell order by arrival; every box then counts the members
+  // of its cell that precede it in (key, slot) order (parallel rank sort, no serial per-cell
+  // insertion sort) and, after a barrier, writes its record, key and slot at the final
+  // position with the distance to its cell's end
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
     if (zc[k] != 0xFFFFFFFFu) {
       const int e = threadIdx.x + k * kBinThreads;
       const uint32_t pos = cstart[zc[k] >> 16] + ((zc[k] >> 8) & 0xFFu);
-      const int32_t xv = (int32_t)(xy[k] & 0xFFFFu), yv = (int32_t)(xy[k] >> 16), zv = (int32_t)(zc[k] & 0xFFu);
-      const RecNarrow rn = make_rec_narrow(xv, yv, zv, a.theta, kNarrow7);
-      const uint64_t key = sort_key(a.s[fbase + e]);
-      RecBin rb;
-      rb.a = rn.a; rb.nb = rn.nb; rb.w = rn.negT | (zv + 1); rb.k = (uint32_t)(key >> 32);
-      recS[pos] = rb;
-      keyS[pos] = key;
+      keyS[pos] = sort_key(a.s[fbase + e]);
       idxS[pos] = (uint16_t)e;
     }
   }
   __syncthreads();
-  // ---- order every cell by (sort key asc == score desc, index asc): insertion sort; every
-  // position learns where its cell ends
-  for (int c = threadIdx.x; c < cells; c += kBinThreads) {
-    const int b = cstart[c], en = cstart[c + 1];
-    for (int i = b + 1; i < en; ++i) {
-      const uint64_t kv = keyS[i];
-      const uint16_t v = idxS[i];
-      const RecBin rv = recS[i];
-      int j = i - 1;
-      while (j >= b) {
-        const uint64_t ku = keyS[j];
-        const uint16_t u = idxS[j];
-        if (ku < kv || (ku == kv && u < v)) break;
-        keyS[j + 1] = ku;
-        idxS[j + 1] = u;
-        recS[j + 1] = recS[j];
-        --j;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    if (zc[k] != 0xFFFFFFFFu) {
+      const int e = threadIdx.x + k * kBinThreads;
+      const int c = (int)(zc[k] >> 16);
+      const int b = (int)cstart[c], en = (int)cstart[c + 1];
+      const uint64_t key = keyS[b + ((zc[k] >> 8) & 0xFFu)];
+      int rank = 0;
+      for (int j = b; j < en; ++j) {
+        const uint64_t kj = keyS[j];
+        rank += kj < key || (kj == key && (int)idxS[j] < e);
       }
-      keyS[j + 1] = kv;
-      idxS[j + 1] = v;
-      recS[j + 1] = rv;
+      zc[k] = (zc[k] & 0xFFFF00FFu) | ((uint32_t)rank << 8);  // rank < kBinCellMax
     }
-    for (int i = b; i < en; ++i) recS[i].w |= (en - i) << 8;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    if (zc[k] != 0xFFFFFFFFu) {
+      const int e = threadIdx.x + k * kBinThreads;
+      const int c = (int)(zc[k] >> 16);
+      const int pos = (int)cstart[c] + (int)((zc[k] >> 8) & 0xFFu);
+      const int en = (int)cstart[c + 1];
+      const int32_t xv = (int32_t)(xy[k] & 0xFFFFu), yv = (int32_t)(xy[k] >> 16), zv = (int32_t)(zc[k] & 0xFFu);
+      const RecNarrow rn = make_rec_narrow(xv, yv, zv, a.theta, kNarrow7);
+      const uint64_t key = sort_key(a.s[fbase + e]);
+      RecBin rb;
+      rb.a = rn.a; rb.nb = rn.nb; rb.w = rn.negT | (zv + 1) | ((en - pos) << 8); rb.k = (uint32_t)(key >> 32);
+      recS[pos] = rb;
+      keyS[pos] = key;
+      idxS[pos] = (uint16_t)e;
+    }
   }
   __syncthreads();
   // ---- scan: each valid box against the gate-passing prefix of every cell its extent can
