@@ -287,10 +287,22 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
       const int c = (int)(zc[k] >> 16);
       const int b = (int)cstart[c], en = (int)cstart[c + 1];
       const uint64_t key = keyS[b + ((zc[k] >> 8) & 0xFFu)];
-      int rank = 0;
+      // count on the high key halves (one 32-bit load per member); members with an equal half
+      // other than the box itself are rare and resolved exactly in a second loop
+      const uint32_t* khi = reinterpret_cast<const uint32_t*>(keyS) + 1;
+      const uint32_t hi = (uint32_t)(key >> 32);
+      int rank = 0, eq = 0;
       for (int j = b; j < en; ++j) {
-        const uint64_t kj = keyS[j];
-        rank += kj < key || (kj == key && (int)idxS[j] < e);
+        const uint32_t hj = khi[2 * j];
+        rank += hj < hi;
+        eq += hj == hi;
+      }
+      if (eq > 1) {
+        rank = 0;
+        for (int j = b; j < en; ++j) {
+          const uint64_t kj = keyS[j];
+          rank += kj < key || (kj == key && (int)idxS[j] < e);
+        }
       }
       zc[k] = (zc[k] & 0xFFFF00FFu) | ((uint32_t)rank << 8);  // rank < kBinCellMax
     }
