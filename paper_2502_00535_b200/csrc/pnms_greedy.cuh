@@ -43,7 +43,7 @@ __host__ __device__ inline int greedy_npad(int n_max) { return (n_max + 127) & ~
 inline size_t greedy_smem_bytes(int n_max) {
   const size_t n = (size_t)greedy_npad(n_max);
   const size_t cells = n < 64 ? 64 : n;
-  return n * (4 * 3 + 8 + 8 + 1 + 2 + 2) + (cells + 4) * 4 + (n / 32 + 4) * 4 + 64 * 4 + 64;
+  return n * (4 * 3 + 8 + 8 + 1 + 1 + 2 + 2) + (cells + 4) * 4 + (n / 32 + 4) * 4 + 64 * 4 + 64;
 }
 
 // covers(cand, ref) of oracles.py:20-29 in exact integer arithmetic; T = ceil(fl64(theta*a))
@@ -78,7 +78,8 @@ __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a
   uint64_t* key = reinterpret_cast<uint64_t*>(sz + npad);
   unsigned long long* thr = reinterpret_cast<unsigned long long*>(key + npad);
   uint8_t* state = reinterpret_cast<uint8_t*>(thr + npad);
-  uint16_t* cellof = reinterpret_cast<uint16_t*>(state + npad);
+  uint8_t* dec = state + npad;  // this round's decisions, applied after a barrier (no read/write race)
+  uint16_t* cellof = reinterpret_cast<uint16_t*>(dec + npad);
   uint16_t* list = cellof + npad;
   uint32_t* cstart = reinterpret_cast<uint32_t*>(list + npad);
   uint32_t* kbits = cstart + max_cells + 4;
@@ -100,6 +101,7 @@ __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a
     key[e] = sort_key(sv);
     thr[e] = greedy_threshold(a.theta, zv);
     state[e] = (sv != sv) ? kKept : kUndecided;  // NaN: unordered, never covers (documented)
+    dec[e] = kUndecided;
     if (xv < 0 || yv < 0 || zv < 0) atomicAnd(&s_stat[5], 0);
     atomicMin(&s_stat[0], xv); atomicMin(&s_stat[1], yv);
     atomicMax(&s_stat[2], xv); atomicMax(&s_stat[3], yv); atomicMax(&s_stat[4], zv);
@@ -195,14 +197,17 @@ __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a
           undec_cov = true;
         }
       }
-      if (kept_cov) state[j] = kRemoved;
-      else if (!undec_cov) state[j] = kKept;
+      if (kept_cov) dec[j] = kRemoved;
+      else if (!undec_cov) dec[j] = kKept;
     }
     __syncthreads();
     if (threadIdx.x == 0) s_stat[7] = 0;
     __syncthreads();
     int und = 0;
-    for (int j = threadIdx.x; j < cnt; j += kGreedyThreads) und += state[j] == kUndecided;
+    for (int j = threadIdx.x; j < cnt; j += kGreedyThreads) {
+      if (dec[j] != kUndecided) { state[j] = dec[j]; dec[j] = kUndecided; }
+      und += state[j] == kUndecided;
+    }
     und = __reduce_add_sync(0xFFFFFFFFu, und);
     if ((threadIdx.x & 31) == 0 && und) atomicAdd(&s_stat[7], und);
     __syncthreads();

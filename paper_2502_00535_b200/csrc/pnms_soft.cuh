@@ -56,7 +56,7 @@ __host__ __device__ inline int soft_npad(int n_max) { return (n_max + 127) & ~12
 inline size_t soft_smem_bytes(int n_max) {
   const size_t n = (size_t)soft_npad(n_max);
   const size_t cells = n < 64 ? 64 : n;
-  return n * (4 * 3 + 8 + 8 + 8 + 1 + 1 + 2 + 2) + (cells + 4) * 4 + 64 * 4 + 64;
+  return n * (4 * 3 + 8 + 8 + 8 + 1 + 1 + 2 + 2 + 2) + (cells + 4) * 4 + 64 * 4 + 64;
 }
 
 // the reference's factor of box b on pending box j (oracles.py:31-34, 115-120); `ovl` is
@@ -87,8 +87,9 @@ struct SoftFrame {
   int32_t *sx, *sy, *sz;
   double *s0, *cur;
   uint64_t* fkey;
-  uint8_t *state, *dirty;
+  uint8_t *state, *mark;   // mark: ready this round (written only by the box's own thread)
   uint16_t *cellof, *list;
+  uint16_t* fround;         // round in which the box became final
   uint32_t* cstart;   // after the scatter: cstart[c] = end(c) = start(c+1), start(0) = 0
   int cnt, GX, GY, S, ox, oy;
   bool bin;
@@ -126,10 +127,11 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
   F.cur = F.s0 + npad;
   F.fkey = reinterpret_cast<uint64_t*>(F.cur + npad);
   F.state = reinterpret_cast<uint8_t*>(F.fkey + npad);
-  F.dirty = F.state + npad;
-  F.cellof = reinterpret_cast<uint16_t*>(F.dirty + npad);
+  F.mark = F.state + npad;
+  F.cellof = reinterpret_cast<uint16_t*>(F.mark + npad);
   F.list = F.cellof + npad;
-  F.cstart = reinterpret_cast<uint32_t*>(F.list + npad);
+  F.fround = F.list + npad;
+  F.cstart = reinterpret_cast<uint32_t*>(F.fround + npad);
   F.cnt = cnt;
   uint32_t* scan_tmp = F.cstart + max_cells + 4;
 
@@ -150,7 +152,7 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
     const double sv = a.s[g];
     F.sx[e] = xv; F.sy[e] = yv; F.sz[e] = zv;
     F.s0[e] = sv; F.cur[e] = sv;
-    F.state[e] = kSoftPending; F.dirty[e] = 0;
+    F.state[e] = kSoftPending; F.mark[e] = 0; F.fround[e] = 0xFFFF;
     if (!(sv > 0.0 && sv <= 1.7976931348623157e308)) atomicOr(&s_stat[8], 1);
     if (xv < 0 || yv < 0 || zv < 0) atomicAnd(&s_stat[5], 0);
     atomicMin(&s_stat[0], xv); atomicMin(&s_stat[1], yv);
@@ -215,33 +217,40 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
 
   const int mode = a.mode;
   const double theta = a.theta, sigma = a.sigma;
-  // ---- rounds
+  // ---- rounds.  Every phase writes only the slots of its own boxes and reads the others'
+  // slots as the previous barrier left them (race-free by construction).
   int round = 0;
   for (;; ++round) {
-    // A: exact tentative scores of pending boxes whose final neighbour set grew:
-    //    s0 times the factors of the final overlapping neighbours in selection order
-    for (int j = threadIdx.x; j < cnt; j += kSoftThreads) {
-      if (F.state[j] != kSoftPending || !F.dirty[j]) continue;
-      F.dirty[j] = 0;
-      const int32_t jx = F.sx[j], jy = F.sy[j], jz = F.sz[j];
-      double t = F.s0[j];
-      uint64_t lk = 0;
-      int li = -1;
-      for (;;) {
-        uint64_t bk = ~0ull;
-        int bi = 0x7FFFFFFF;
+    // A: exact tentative scores of pending boxes with an overlapping neighbour finalized in the
+    //    previous round: s0 times the factors of the final overlapping neighbours, in order
+    if (round > 0) {
+      for (int j = threadIdx.x; j < cnt; j += kSoftThreads) {
+        if (F.state[j] != kSoftPending) continue;
+        const int32_t jx = F.sx[j], jy = F.sy[j], jz = F.sz[j];
+        bool fresh = false;
         F.for_candidates(j, [&](int b) {
-          if (F.state[b] != kSoftFinal) return;
-          const uint64_t kb = F.fkey[b];
-          if (!soft_before(lk, li, kb, b) || !soft_before(kb, b, bk, bi)) return;
-          if (!soft_overlap(jx, jy, jz, F.sx[b], F.sy[b], F.sz[b])) return;
-          bk = kb; bi = b;
+          if (!fresh && F.fround[b] == round - 1 && soft_overlap(jx, jy, jz, F.sx[b], F.sy[b], F.sz[b])) fresh = true;
         });
-        if (bi == 0x7FFFFFFF) break;
-        t = soft_apply(t, jx, jy, jz, F.sx[bi], F.sy[bi], F.sz[bi], mode, theta, sigma);
-        lk = bk; li = bi;
+        if (!fresh) continue;
+        double t = F.s0[j];
+        uint64_t lk = 0;
+        int li = -1;
+        for (;;) {
+          uint64_t bk = ~0ull;
+          int bi = 0x7FFFFFFF;
+          F.for_candidates(j, [&](int b) {
+            if (F.state[b] != kSoftFinal) return;
+            const uint64_t kb = F.fkey[b];
+            if (!soft_before(lk, li, kb, b) || !soft_before(kb, b, bk, bi)) return;
+            if (!soft_overlap(jx, jy, jz, F.sx[b], F.sy[b], F.sz[b])) return;
+            bk = kb; bi = b;
+          });
+          if (bi == 0x7FFFFFFF) break;
+          t = soft_apply(t, jx, jy, jz, F.sx[bi], F.sy[bi], F.sz[bi], mode, theta, sigma);
+          lk = bk; li = bi;
+        }
+        F.cur[j] = t;
       }
-      F.cur[j] = t;
     }
     __syncthreads();
     if (round >= kSoftMaxRounds) break;
@@ -252,27 +261,25 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
       const uint64_t kj = sort_key(F.cur[j]);
       bool ready = true;
       F.for_candidates(j, [&](int n) {
-        if (!ready || n == j || F.state[n] == kSoftFinal) return;
+        if (!ready || n == j || F.state[n] != kSoftPending) return;
         if (!soft_before(sort_key(F.cur[n]), n, kj, j)) return;
         if (soft_overlap(jx, jy, jz, F.sx[n], F.sy[n], F.sz[n])) ready = false;
       });
-      if (ready) F.state[j] = kSoftReady;
-    }
-    __syncthreads();
-    // C: finalize; pending overlapping neighbours must recompute
-    for (int j = threadIdx.x; j < cnt; j += kSoftThreads) {
-      if (F.state[j] != kSoftReady) continue;
-      F.fkey[j] = sort_key(F.cur[j]);
-      F.state[j] = kSoftFinal;
-      const int32_t jx = F.sx[j], jy = F.sy[j], jz = F.sz[j];
-      F.for_candidates(j, [&](int n) {
-        if (F.state[n] == kSoftPending && soft_overlap(jx, jy, jz, F.sx[n], F.sy[n], F.sz[n])) F.dirty[n] = 1;
-      });
+      F.mark[j] = ready ? 1 : 0;
     }
     if (threadIdx.x == 0) s_stat[7] = 0;
     __syncthreads();
+    // C: finalize (own slots only) and count what is still pending
     int pend = 0;
-    for (int j = threadIdx.x; j < cnt; j += kSoftThreads) pend += F.state[j] != kSoftFinal;
+    for (int j = threadIdx.x; j < cnt; j += kSoftThreads) {
+      if (F.state[j] == kSoftPending && F.mark[j]) {
+        F.fkey[j] = sort_key(F.cur[j]);
+        F.fround[j] = (uint16_t)round;
+        F.state[j] = kSoftFinal;
+        F.mark[j] = 0;
+      }
+      pend += F.state[j] != kSoftFinal;
+    }
     pend = __reduce_add_sync(0xFFFFFFFFu, pend);
     if ((threadIdx.x & 31) == 0 && pend) atomicAdd(&s_stat[7], pend);
     __syncthreads();
