@@ -645,3 +645,22 @@ def test_soft_nms_domain_and_argument_errors():
         soft_nms_rescore(vec, "box", 0.3)
     with pytest.raises(ValueError, match="sigma must be positive, got 0"):
         soft_nms_rescore(vec, "gaussian", 0.3, 0)
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
+def test_compute_sanitizer_clean(tool):
+    """Every device path (binned rows / pair tiles, dense, single-launch, tiles, cluster, greedy,
+    Soft-NMS) under compute-sanitizer: no memory errors, no shared-memory races."""
+    import shutil
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    exe = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not Path(exe).exists():
+        pytest.skip("compute-sanitizer not installed")
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([exe, "--tool", tool, "--error-exitcode", "9", sys.executable,
+                        str(root / "tools" / "sanitize_run.py")], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "sanitize run ok" in r.stdout
