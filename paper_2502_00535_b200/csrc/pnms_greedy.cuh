@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a
   // ---- spatial cells (exact for greedy at any theta: zero overlap never covers)
   bool bin = s_stat[5] != 0 && cnt > 0;
   int S = 1, GX = 1, GY = 1;
+  float inv_gx = 1.0f;  // 1/GX: cell row of a cell id without an integer division (exact, ids < 2^12)
   const int ox = s_stat[0], oy = s_stat[1];
   if (bin) {
     S = s_stat[4] + 1;
@@ -151,6 +152,7 @@ __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a
     }
     __syncthreads();
     bin = s_stat[6] <= kGreedyCellMax;
+    inv_gx = 1.0f / (float)GX;
     if (bin) {
       // scatter with cstart as the cursor: afterwards cstart[c] = end(c) = start(c+1)
       for (int e = threadIdx.x; e < cnt; e += kGreedyThreads) {
@@ -169,7 +171,8 @@ __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a
       const int32_t jx = sx[j], jy = sy[j], jz = sz[j];
       bool kept_cov = false, undec_cov = false;
       if (bin) {
-        const int cx = (int)(((long long)jx - ox) / S), cy = (int)(((long long)jy - oy) / S);
+        const int cc = cellof[j];
+        const int cy = (int)(((float)cc + 0.5f) * inv_gx), cx = cc - cy * GX;
         for (int yy = max(0, cy - 1); yy <= min(GY - 1, cy + 1) && !kept_cov; ++yy) {
           for (int xx = max(0, cx - 1); xx <= min(GX - 1, cx + 1) && !kept_cov; ++xx) {
             const int c = yy * GX + xx;

@@ -56,7 +56,7 @@ __host__ __device__ inline int soft_npad(int n_max) { return (n_max + 127) & ~12
 inline size_t soft_smem_bytes(int n_max) {
   const size_t n = (size_t)soft_npad(n_max);
   const size_t cells = n < 64 ? 64 : n;
-  return n * (4 * 3 + 8 + 8 + 8 + 1 + 1 + 2 + 2 + 2) + (cells + 4) * 4 + 64 * 4 + 64;
+  return n * (4 * 3 + 8 + 8 + 8 + 1 + 1 + 2 + 2 + 2 + 2 + 2) + (cells + 4) * 4 + 64 * 4 + 64;
 }
 
 // the reference's factor of box b on pending box j (oracles.py:31-34, 115-120); `ovl` is
@@ -92,13 +92,15 @@ struct SoftFrame {
   uint16_t* fround;         // round in which the box became final
   uint32_t* cstart;   // after the scatter: cstart[c] = end(c) = start(c+1), start(0) = 0
   int cnt, GX, GY, S, ox, oy;
+  float inv_gx;   // 1/GX: cell row of a cell id without an integer division (exact, ids < 2^12)
   bool bin;
 
   // visit every candidate slot that may overlap box j (3x3 cells, or every slot)
   template <class F>
   __device__ __forceinline__ void for_candidates(int j, F&& fn) const {
     if (bin) {
-      const int cx = (int)(((long long)sx[j] - ox) / S), cy = (int)(((long long)sy[j] - oy) / S);
+      const int c = cellof[j];
+      const int cy = (int)(((float)c + 0.5f) * inv_gx), cx = c - cy * GX;
       for (int yy = max(0, cy - 1); yy <= min(GY - 1, cy + 1); ++yy) {
         const int c0 = yy * GX + max(0, cx - 1), c1 = yy * GX + min(GX - 1, cx + 1);
         const int b = c0 == 0 ? 0 : (int)cstart[c0 - 1], en = (int)cstart[c1];
@@ -131,7 +133,8 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
   F.cellof = reinterpret_cast<uint16_t*>(F.mark + npad);
   F.list = F.cellof + npad;
   F.fround = F.list + npad;
-  F.cstart = reinterpret_cast<uint32_t*>(F.fround + npad);
+  uint16_t* plist[2] = {F.fround + npad, F.fround + 2 * npad};  // pending boxes, double-buffered
+  F.cstart = reinterpret_cast<uint32_t*>(F.fround + 3 * npad);
   F.cnt = cnt;
   uint32_t* scan_tmp = F.cstart + max_cells + 4;
 
@@ -206,6 +209,7 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
     }
     __syncthreads();
     F.bin = s_stat[6] <= kSoftCellMax;
+    F.inv_gx = 1.0f / (float)F.GX;
     if (F.bin) {
       for (int e = threadIdx.x; e < cnt; e += kSoftThreads) {
         const uint32_t pos = atomicAdd(&F.cstart[F.cellof[e]], 1u);
@@ -217,46 +221,73 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
 
   const int mode = a.mode;
   const double theta = a.theta, sigma = a.sigma;
-  // ---- rounds.  Every phase writes only the slots of its own boxes and reads the others'
-  // slots as the previous barrier left them (race-free by construction).
-  int round = 0;
+  // ---- rounds over a compacted list of the pending boxes.  Every phase writes only the slots
+  // of its own boxes and reads the others' slots as the previous barrier left them
+  // (race-free by construction).
+  __shared__ int s_npend[2];
+  for (int e = threadIdx.x; e < cnt; e += kSoftThreads) plist[0][e] = (uint16_t)e;
+  if (threadIdx.x == 0) { s_npend[0] = cnt; s_npend[1] = 0; }
+  __syncthreads();
+  int round = 0, cur_list = 0;
   for (;; ++round) {
+    const uint16_t* pl = plist[cur_list];
+    const int npend = s_npend[cur_list];
     // A: exact tentative scores of pending boxes with an overlapping neighbour finalized in the
-    //    previous round: s0 times the factors of the final overlapping neighbours, in order
+    //    previous round: s0 times the factors of the final overlapping neighbours, in the
+    //    reference's selection order (collected and insertion-sorted by (key, slot))
     if (round > 0) {
-      for (int j = threadIdx.x; j < cnt; j += kSoftThreads) {
-        if (F.state[j] != kSoftPending) continue;
+      for (int t = threadIdx.x; t < npend; t += kSoftThreads) {
+        const int j = pl[t];
         const int32_t jx = F.sx[j], jy = F.sy[j], jz = F.sz[j];
+        constexpr int kMaxNb = 24;
+        uint64_t nk[kMaxNb];
+        int nb[kMaxNb];
+        int nn = 0;
         bool fresh = false;
         F.for_candidates(j, [&](int b) {
-          if (!fresh && F.fround[b] == round - 1 && soft_overlap(jx, jy, jz, F.sx[b], F.sy[b], F.sz[b])) fresh = true;
+          if (F.state[b] != kSoftFinal || !soft_overlap(jx, jy, jz, F.sx[b], F.sy[b], F.sz[b])) return;
+          fresh |= F.fround[b] == round - 1;
+          if (nn <= kMaxNb) {
+            if (nn < kMaxNb) {
+              const uint64_t kb = F.fkey[b];
+              int i = nn;
+              while (i > 0 && soft_before(kb, b, nk[i - 1], nb[i - 1])) { nk[i] = nk[i - 1]; nb[i] = nb[i - 1]; --i; }
+              nk[i] = kb; nb[i] = b;
+            }
+            ++nn;
+          }
         });
         if (!fresh) continue;
-        double t = F.s0[j];
-        uint64_t lk = 0;
-        int li = -1;
-        for (;;) {
-          uint64_t bk = ~0ull;
-          int bi = 0x7FFFFFFF;
-          F.for_candidates(j, [&](int b) {
-            if (F.state[b] != kSoftFinal) return;
-            const uint64_t kb = F.fkey[b];
-            if (!soft_before(lk, li, kb, b) || !soft_before(kb, b, bk, bi)) return;
-            if (!soft_overlap(jx, jy, jz, F.sx[b], F.sy[b], F.sz[b])) return;
-            bk = kb; bi = b;
-          });
-          if (bi == 0x7FFFFFFF) break;
-          t = soft_apply(t, jx, jy, jz, F.sx[bi], F.sy[bi], F.sz[bi], mode, theta, sigma);
-          lk = bk; li = bi;
+        double tv = F.s0[j];
+        if (nn <= kMaxNb) {
+          for (int i = 0; i < nn; ++i)
+            tv = soft_apply(tv, jx, jy, jz, F.sx[nb[i]], F.sy[nb[i]], F.sz[nb[i]], mode, theta, sigma);
+        } else {  // many final neighbours (crowds): repeated minimum in key order
+          uint64_t lk = 0;
+          int li = -1;
+          for (;;) {
+            uint64_t bk = ~0ull;
+            int bi = 0x7FFFFFFF;
+            F.for_candidates(j, [&](int b) {
+              if (F.state[b] != kSoftFinal) return;
+              const uint64_t kb = F.fkey[b];
+              if (!soft_before(lk, li, kb, b) || !soft_before(kb, b, bk, bi)) return;
+              if (!soft_overlap(jx, jy, jz, F.sx[b], F.sy[b], F.sz[b])) return;
+              bk = kb; bi = b;
+            });
+            if (bi == 0x7FFFFFFF) break;
+            tv = soft_apply(tv, jx, jy, jz, F.sx[bi], F.sy[bi], F.sz[bi], mode, theta, sigma);
+            lk = bk; li = bi;
+          }
         }
-        F.cur[j] = t;
+        F.cur[j] = tv;
       }
     }
     __syncthreads();
     if (round >= kSoftMaxRounds) break;
     // B: a pending box that precedes every pending overlapping neighbour is final
-    for (int j = threadIdx.x; j < cnt; j += kSoftThreads) {
-      if (F.state[j] != kSoftPending) continue;
+    for (int t = threadIdx.x; t < npend; t += kSoftThreads) {
+      const int j = pl[t];
       const int32_t jx = F.sx[j], jy = F.sy[j], jz = F.sz[j];
       const uint64_t kj = sort_key(F.cur[j]);
       bool ready = true;
@@ -267,24 +298,34 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
       });
       F.mark[j] = ready ? 1 : 0;
     }
-    if (threadIdx.x == 0) s_stat[7] = 0;
+    if (threadIdx.x == 0) s_npend[cur_list ^ 1] = 0;
     __syncthreads();
-    // C: finalize (own slots only) and count what is still pending
-    int pend = 0;
-    for (int j = threadIdx.x; j < cnt; j += kSoftThreads) {
-      if (F.state[j] == kSoftPending && F.mark[j]) {
-        F.fkey[j] = sort_key(F.cur[j]);
-        F.fround[j] = (uint16_t)round;
-        F.state[j] = kSoftFinal;
-        F.mark[j] = 0;
+    // C: finalize (own slots only) and compact the still-pending boxes into the other list
+    uint16_t* nl = plist[cur_list ^ 1];
+    for (int base = 0; base < npend; base += kSoftThreads) {
+      const int t = base + threadIdx.x;
+      bool keep = false;
+      int j = 0;
+      if (t < npend) {
+        j = pl[t];
+        if (F.mark[j]) {
+          F.fkey[j] = sort_key(F.cur[j]);
+          F.fround[j] = (uint16_t)round;
+          F.state[j] = kSoftFinal;
+          F.mark[j] = 0;
+        } else {
+          keep = true;
+        }
       }
-      pend += F.state[j] != kSoftFinal;
+      const unsigned bal = __ballot_sync(0xFFFFFFFFu, keep);
+      int wbase = 0;
+      if ((threadIdx.x & 31) == 0 && bal) wbase = atomicAdd(&s_npend[cur_list ^ 1], __popc(bal));
+      wbase = __shfl_sync(0xFFFFFFFFu, wbase, 0);
+      if (keep) nl[wbase + __popc(bal & lanemask_lt())] = (uint16_t)j;
     }
-    pend = __reduce_add_sync(0xFFFFFFFFu, pend);
-    if ((threadIdx.x & 31) == 0 && pend) atomicAdd(&s_stat[7], pend);
     __syncthreads();
-    if (s_stat[7] == 0) break;
-    __syncthreads();
+    cur_list ^= 1;
+    if (s_npend[cur_list] == 0) break;
   }
   // ---- dense crowds: finish with the reference's loop (cur is exact for every pending box)
   if (round >= kSoftMaxRounds) {
