@@ -43,7 +43,7 @@ __host__ __device__ inline int greedy_npad(int n_max) { return (n_max + 127) & ~
 inline size_t greedy_smem_bytes(int n_max) {
   const size_t n = (size_t)greedy_npad(n_max);
   const size_t cells = n < 64 ? 64 : n;
-  return n * (4 * 3 + 8 + 8 + 1 + 1 + 2 + 2) + (cells + 4) * 4 + (n / 32 + 4) * 4 + 64 * 4 + 64;
+  return n * (4 * 3 + 8 + 8 + 1 + 1 + 2 + 2 + 2 + 2) + (cells + 4) * 4 + (n / 32 + 4) * 4 + 64 * 4 + 64;
 }
 
 // covers(cand, ref) of oracles.py:20-29 in exact integer arithmetic; T = ceil(fl64(theta*a))
@@ -81,7 +81,8 @@ __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a
   uint8_t* dec = state + npad;  // this round's decisions, applied after a barrier (no read/write race)
   uint16_t* cellof = reinterpret_cast<uint16_t*>(dec + npad);
   uint16_t* list = cellof + npad;
-  uint32_t* cstart = reinterpret_cast<uint32_t*>(list + npad);
+  uint16_t* ulist[2] = {list + npad, list + 2 * npad};  // undecided boxes, double-buffered
+  uint32_t* cstart = reinterpret_cast<uint32_t*>(list + 3 * npad);
   uint32_t* kbits = cstart + max_cells + 4;
   uint32_t* scan_tmp = kbits + npad / 32 + 4;
 
@@ -163,10 +164,18 @@ __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a
   }
   __syncthreads();
   // After the scatter, cstart[c] == end(c) == start(c+1); start(0) = 0.
-  // ---- rounds
-  for (;;) {
-    for (int j = threadIdx.x; j < cnt; j += kGreedyThreads) {
-      if (state[j] != kUndecided) continue;
+  // ---- rounds over a compacted list of the undecided boxes; decisions go to dec[] and are
+  // applied after a barrier (every box's slots are written only by its own thread)
+  __shared__ int s_nund[2];
+  for (int e = threadIdx.x; e < cnt; e += kGreedyThreads) ulist[0][e] = (uint16_t)e;
+  if (threadIdx.x == 0) { s_nund[0] = cnt; s_nund[1] = 0; }
+  __syncthreads();
+  for (int cur = 0;; cur ^= 1) {
+    const uint16_t* ul = ulist[cur];
+    const int nund = s_nund[cur];
+    for (int t = threadIdx.x; t < nund; t += kGreedyThreads) {
+      const int j = ul[t];
+      if (state[j] != kUndecided) continue;  // NaN rows start kept
       const uint64_t kj = key[j];
       const int32_t jx = sx[j], jy = sy[j], jz = sz[j];
       bool kept_cov = false, undec_cov = false;
@@ -203,19 +212,26 @@ __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a
       if (kept_cov) dec[j] = kRemoved;
       else if (!undec_cov) dec[j] = kKept;
     }
+    if (threadIdx.x == 0) s_nund[cur ^ 1] = 0;
     __syncthreads();
-    if (threadIdx.x == 0) s_stat[7] = 0;
-    __syncthreads();
-    int und = 0;
-    for (int j = threadIdx.x; j < cnt; j += kGreedyThreads) {
-      if (dec[j] != kUndecided) { state[j] = dec[j]; dec[j] = kUndecided; }
-      und += state[j] == kUndecided;
+    uint16_t* nl = ulist[cur ^ 1];
+    for (int base = 0; base < nund; base += kGreedyThreads) {
+      const int t = base + threadIdx.x;
+      bool keep = false;
+      int j = 0;
+      if (t < nund) {
+        j = ul[t];
+        if (dec[j] != kUndecided) { state[j] = dec[j]; dec[j] = kUndecided; }
+        keep = state[j] == kUndecided;
+      }
+      const unsigned bal = __ballot_sync(0xFFFFFFFFu, keep);
+      int wbase = 0;
+      if ((threadIdx.x & 31) == 0 && bal) wbase = atomicAdd(&s_nund[cur ^ 1], __popc(bal));
+      wbase = __shfl_sync(0xFFFFFFFFu, wbase, 0);
+      if (keep) nl[wbase + __popc(bal & lanemask_lt())] = (uint16_t)j;
     }
-    und = __reduce_add_sync(0xFFFFFFFFu, und);
-    if ((threadIdx.x & 31) == 0 && und) atomicAdd(&s_stat[7], und);
     __syncthreads();
-    if (s_stat[7] == 0) break;
-    __syncthreads();
+    if (s_nund[cur ^ 1] == 0) break;
   }
   // ---- compaction of the kept boxes (ascending input order, oracles.py:84)
   for (int j = threadIdx.x; j < cnt; j += kGreedyThreads)
