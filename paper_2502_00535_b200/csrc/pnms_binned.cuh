@@ -69,8 +69,8 @@ __host__ __device__ inline int binned_max_cells(int npad) { return npad < 64 ? 6
 // npad is a multiple of 128, so every region below starts 16-byte aligned
 __host__ __device__ inline int binned_npad(int n_max) { return (n_max + 127) & ~127; }
 inline size_t binned_smem_bytes(int npad) {
-  return (size_t)npad * (sizeof(RecBin) + 8 + 2) + (size_t)(binned_max_cells(npad) + 4) * 4 + (size_t)(npad / 32 + 4) * 4 +
-         64 * 4 + sizeof(BinStats) + 64;
+  return (size_t)npad * (sizeof(RecBin) + 8 + 2 + 2) + (size_t)(binned_max_cells(npad) + 4) * 4 +
+         (size_t)(npad / 32 + 4) * 4 + 64 * 4 + sizeof(BinStats) + 64;
 }
 // boxes each thread keeps in registers between the load, binning and scatter passes
 inline int binned_per_thread(int n_max) { return n_max <= 4 * kBinThreads ? 4 : 8; }
@@ -155,6 +155,7 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
   uint32_t* kbits = cstart + max_cells + 4;                                   // [npad/32] survivors
   uint32_t* scan_tmp = kbits + npad / 32 + 4;                                 // [64]
   BinStats* st = reinterpret_cast<BinStats*>(scan_tmp + 64);
+  uint16_t* cpos = reinterpret_cast<uint16_t*>(st + 1);  // [npad] cell, then rank, of arrival position p
 
   if (threadIdx.x == 0) {
     st->mode = kNarrow7; st->minz = 0x7FFFFFFF; st->maxz = 0;
@@ -266,10 +267,11 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
     if (threadIdx.x == 0) binned_decline(a, f);
     return;
   }
-  // ---- pass 3: keys and slots into cell order by arrival; every box then counts the members
-  // of its cell that precede it in (key, slot) order (parallel rank sort, no serial per-cell
-  // insertion sort) and, after a barrier, writes its record, key and slot at the final
-  // position with the distance to its cell's end
+  // ---- pass 3: keys, slots and cells into cell order by arrival; then one thread per arrival
+  // position counts the members of its cell that precede it in (key, slot) order — a parallel
+  // rank sort whose adjacent lanes share a cell (uniform trip counts) — and after a barrier
+  // every box writes its record, key and slot at the final position with the distance to its
+  // cell's end
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
     if (zc[k] != 0xFFFFFFFFu) {
@@ -277,20 +279,18 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
       const uint32_t pos = cstart[zc[k] >> 16] + ((zc[k] >> 8) & 0xFFu);
       keyS[pos] = sort_key(a.s[fbase + e]);
       idxS[pos] = (uint16_t)e;
+      cpos[pos] = (uint16_t)(zc[k] >> 16);
     }
   }
   __syncthreads();
-#pragma unroll
-  for (int k = 0; k < PER; ++k) {
-    if (zc[k] != 0xFFFFFFFFu) {
-      const int e = threadIdx.x + k * kBinThreads;
-      const int c = (int)(zc[k] >> 16);
+  {
+    // high key halves (one 32-bit load per member); members with an equal half other than the
+    // box itself are rare and resolved exactly in a second loop
+    const uint32_t* khi = reinterpret_cast<const uint32_t*>(keyS) + 1;
+    for (int p = threadIdx.x; p < n_act; p += kBinThreads) {
+      const int c = cpos[p];
       const int b = (int)cstart[c], en = (int)cstart[c + 1];
-      const uint64_t key = keyS[b + ((zc[k] >> 8) & 0xFFu)];
-      // count on the high key halves (one 32-bit load per member); members with an equal half
-      // other than the box itself are rare and resolved exactly in a second loop
-      const uint32_t* khi = reinterpret_cast<const uint32_t*>(keyS) + 1;
-      const uint32_t hi = (uint32_t)(key >> 32);
+      const uint32_t hi = khi[2 * p];
       int rank = 0, eq = 0;
       for (int j = b; j < en; ++j) {
         const uint32_t hj = khi[2 * j];
@@ -298,13 +298,15 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
         eq += hj == hi;
       }
       if (eq > 1) {
+        const uint64_t key = keyS[p];
+        const int e = idxS[p];
         rank = 0;
         for (int j = b; j < en; ++j) {
           const uint64_t kj = keyS[j];
           rank += kj < key || (kj == key && (int)idxS[j] < e);
         }
       }
-      zc[k] = (zc[k] & 0xFFFF00FFu) | ((uint32_t)rank << 8);  // rank < kBinCellMax
+      cpos[p] = (uint16_t)rank;  // own slot; < kBinCellMax
     }
   }
   __syncthreads();
@@ -313,7 +315,8 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
     if (zc[k] != 0xFFFFFFFFu) {
       const int e = threadIdx.x + k * kBinThreads;
       const int c = (int)(zc[k] >> 16);
-      const int pos = (int)cstart[c] + (int)((zc[k] >> 8) & 0xFFu);
+      const int b = (int)cstart[c];
+      const int pos = b + (int)cpos[b + ((zc[k] >> 8) & 0xFFu)];
       const int en = (int)cstart[c + 1];
       const int32_t xv = (int32_t)(xy[k] & 0xFFFFu), yv = (int32_t)(xy[k] >> 16), zv = (int32_t)(zc[k] & 0xFFu);
       const RecNarrow rn = make_rec_narrow(xv, yv, zv, a.theta, kNarrow7);
