@@ -33,3 +33,28 @@ for n in (1, 2, 4, 8):
     print(f"N={n}: {F} frames/rank {ms:.3f} ms -> {8192 / ms * 1e3 / 1e6:.2f} M frames/s, "
           f"efficiency {base / (n * ms):.2f}")
     del eng
+
+# phase split of one shard call (binned kernel vs the fallback chain) at N = 8
+import ctypes  # noqa: E402
+
+from paper_2502_00535_b200 import _lib  # noqa: E402
+
+F = 1024
+eng = NmsEngine(F, 2048, 0.5, device=dev)
+lib = _lib.load()
+st = torch.cuda.current_stream(dev)
+evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+for e in evs:
+    e.record()
+torch.cuda.synchronize()
+h = (ctypes.c_void_p * 4)(*[e.cuda_event for e in evs])
+p = lambda t: t.data_ptr()  # noqa: E731
+res = []
+for _ in range(10):
+    flush.zero_()
+    lib.pnms_run_profiled(p(x), p(y), p(z), p(s), None, F, 2048, 2048, 0.5, 0, p(eng.keep_idx), p(eng.keep_count),
+                          None, None, p(eng.ws_full), eng.ws_full.numel(), st.cuda_stream, h)
+    evs[3].synchronize()
+    res.append((evs[0].elapsed_time(evs[1]), evs[1].elapsed_time(evs[3])))
+res.sort()
+print(f"N=8 shard: binned kernel {res[5][0] * 1e3:.1f} us, fallback chain {res[5][1] * 1e3:.1f} us (profiled, events between)")
