@@ -309,7 +309,11 @@ def main():
     x, y, z, s = shard
     F = x.shape[0]
     dx, dy, dz, ds = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (x, y, z, s))
-    eng = NmsEngine(F, BOXES, THETA, TIE, BOXES, device=dev, chunks=8)
+    # pipeline depth of the end-to-end path by shard size (measured on B200, tools/e2e_probe.py:
+    # ~1000 frames per chunk amortise the per-chunk copy and launch latency; small shards need a
+    # few chunks for overlap)
+    e2e_chunks = 4 if F <= 1024 else max(2, min(8, F // 1024))
+    eng = NmsEngine(F, BOXES, THETA, TIE, BOXES, device=dev, chunks=e2e_chunks)
     lib = _lib.load()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -484,7 +488,7 @@ def main():
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d_bytes,
                     "d2h_bytes_per_step": int(F * eng.W32 * 4 + F * 4), "matches_device_run": ok,
                     "input_format": "packed 32-bit boxes (pack_box32) + float64 s planes, unpacked on device",
-                    "pipeline": "8 chunks over 2 streams (H2D, unpack, NMS, D2H of masks + counts)",
+                    "pipeline": f"{e2e_chunks} chunks over 2 streams (H2D, unpack, NMS, D2H of masks + counts)",
                     "h2d_link_gbs": h2d_gbs, "link_bound_frames_per_s": world * F / (copy_ms / 1e3),
                     "frac_of_link_bound": e2e_value / (world * F / (copy_ms / 1e3)),
                     "link_bound_basis": "the step's input planes copied host->device alone (no compute), best of 5"},

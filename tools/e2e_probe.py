@@ -42,7 +42,7 @@ h16 = [torch.from_numpy(a.astype(np.int16)).pin_memory() for a in (x, y, z)]
 hb = torch.from_numpy(pack_box32(x, y, z)).pin_memory()
 ms = timeit(lambda: (d[: F * N * 8].view(torch.float64).view(F, N).copy_(hs, non_blocking=True)))
 print(f"raw H2D of the score plane: {F * N * 8 / ms / 1e6:.1f} GB/s")
-for chunks in (4, 8, 16):
+for chunks in ((2, 4, 8) if F <= 2048 else (6, 8, 12, 16)):
     eng = NmsEngine(F, N, 0.5, chunks=chunks, device=dev)
     om = torch.empty((F, eng.W32), dtype=torch.int32).pin_memory()
     oc = torch.empty((F,), dtype=torch.int32).pin_memory()
