@@ -73,7 +73,7 @@ inline size_t binned_smem_bytes(int npad) {
          (size_t)(npad / 32 + 4) * 4 + 64 * 4 + sizeof(BinStats) + 64;
 }
 // boxes each thread keeps in registers between the load, binning and scatter passes
-inline int binned_per_thread(int n_max) { return n_max <= 4 * kBinThreads ? 4 : 8; }
+inline int binned_per_thread(int n_max, int threads) { return n_max <= 2 * threads ? 2 : (n_max <= 4 * threads ? 4 : 8); }
 
 // floor(v / S) for 0 <= v < 2^16 as one IMAD.HI: M = floor(2^32 / S) + 1 is exact there
 // (v * (M*S - 2^32) < 2^32).  S >= 2^15 makes every quotient 0 (M = 0).
@@ -136,8 +136,10 @@ __device__ __forceinline__ bool binned_scan_run(uint32_t base, uint32_t qb, uint
   }
 }
 
-template <bool BY_INDEX, bool COUNT, int PER>
-__global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
+// THREADS = 512 (three CTAs per SM: throughput) or 1024 (one CTA per SM, half the rows per
+// thread: latency, for batches that fit one wave)
+template <bool BY_INDEX, bool COUNT, int PER, int THREADS>
+__global__ void __launch_bounds__(THREADS, (THREADS == 512 ? 3 : 1)) pnms_binned_frame(BinArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int f = blockIdx.x;
   const long long fbase = (long long)f * a.n_max;
@@ -162,9 +164,9 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
     st->minx = st->miny = 0x7FFFFFFF; st->maxx = st->maxy = -0x7FFFFFFF;
     st->big = 0; st->n_act = 0;
   }
-  for (int w = threadIdx.x; w < npad / 32; w += kBinThreads) kbits[w] = 0u;
+  for (int w = threadIdx.x; w < npad / 32; w += THREADS) kbits[w] = 0u;
   __syncthreads();
-  if (a.n_max > PER * kBinThreads) {
+  if (a.n_max > PER * THREADS) {
     if (threadIdx.x == 0) binned_decline(a, f);
     return;
   }
@@ -177,7 +179,7 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
     int minx = 0x7FFFFFFF, miny = 0x7FFFFFFF, maxx = -0x7FFFFFFF, maxy = -0x7FFFFFFF;
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
-      const int e = threadIdx.x + k * kBinThreads;
+      const int e = threadIdx.x + k * THREADS;
       xy[k] = 0u; zc[k] = 0xFFFFFFFFu;  // 0xFFFFFFFF = no box (slot >= count, or NaN score)
       if (e < cnt) {
         const long long g = fbase + e;
@@ -231,7 +233,7 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
   }
   const uint32_t M = div_magic(S);
   const int cells = GX * GY;
-  for (int c = threadIdx.x; c < cells + 1; c += kBinThreads) cstart[c] = 0u;
+  for (int c = threadIdx.x; c < cells + 1; c += THREADS) cstart[c] = 0u;
   __syncthreads();
   // ---- pass 2: histogram; the atomic's return value is the box's rank inside its cell
 #pragma unroll
@@ -246,7 +248,7 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
   __syncthreads();
   // exclusive scan of the cell counts (+ largest cell)
   {
-    const int per = (cells + 1 + kBinThreads - 1) / kBinThreads;
+    const int per = (cells + 1 + THREADS - 1) / THREADS;
     const int b0 = threadIdx.x * per;
     uint32_t sum = 0, big = 0;
     for (int t = 0; t < per; ++t) {
@@ -275,7 +277,7 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
     if (zc[k] != 0xFFFFFFFFu) {
-      const int e = threadIdx.x + k * kBinThreads;
+      const int e = threadIdx.x + k * THREADS;
       const uint32_t pos = cstart[zc[k] >> 16] + ((zc[k] >> 8) & 0xFFu);
       keyS[pos] = sort_key(a.s[fbase + e]);
       idxS[pos] = (uint16_t)e;
@@ -287,7 +289,7 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
     // high key halves (one 32-bit load per member); members with an equal half other than the
     // box itself are rare and resolved exactly in a second loop
     const uint32_t* khi = reinterpret_cast<const uint32_t*>(keyS) + 1;
-    for (int p = threadIdx.x; p < n_act; p += kBinThreads) {
+    for (int p = threadIdx.x; p < n_act; p += THREADS) {
       const int c = cpos[p];
       const int b = (int)cstart[c], en = (int)cstart[c + 1];
       const uint32_t hi = khi[2 * p];
@@ -313,7 +315,7 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
     if (zc[k] != 0xFFFFFFFFu) {
-      const int e = threadIdx.x + k * kBinThreads;
+      const int e = threadIdx.x + k * THREADS;
       const int c = (int)(zc[k] >> 16);
       const int b = (int)cstart[c];
       const int pos = b + (int)cpos[b + ((zc[k] >> 8) & 0xFFu)];
@@ -338,7 +340,7 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
   const int maxz = st->maxz;
   const bool pad_rule = a.d_max > cnt;
   const uint32_t rbase = static_cast<uint32_t>(__cvta_generic_to_shared(recS));
-  for (int p = threadIdx.x; p < n_act; p += kBinThreads) {
+  for (int p = threadIdx.x; p < n_act; p += THREADS) {
     const RecBin ri = recS[p];
     const uint32_t zzi = __byte_perm((uint32_t)ri.w, 0u, 0x4040);  // (z+1, z+1)
     // corner and side back from the packed record: nb = (-x, -y)
@@ -365,7 +367,7 @@ __global__ void __launch_bounds__(kBinThreads, 3) pnms_binned_frame(BinArgs a) {
   }
   __syncthreads();
   // ---- compaction (engine.py:284-293)
-  const int words_per_thread = (a.W32 + kBinThreads - 1) / kBinThreads;
+  const int words_per_thread = (a.W32 + THREADS - 1) / THREADS;
   const int w0 = threadIdx.x * words_per_thread, w1 = min(w0 + words_per_thread, a.W32);
   uint32_t local = 0;
   for (int w = w0; w < w1; ++w) {

@@ -116,6 +116,18 @@ long long env_ll(const char* name, long long dflt) {
 }
 int env_int(const char* name, int dflt) { return (int)env_ll(name, dflt); }
 
+// streaming multiprocessors of the current device (cached per process)
+int sm_count() {
+  static std::atomic<int> cached{0};
+  int v = cached.load();
+  if (v > 0) return v;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    v = 148;
+  cached.store(v);
+  return v;
+}
+
 int fail_cuda(cudaError_t e) {
   g_last_cuda_error = (int)e;
   return PNMS_ECUDA;
@@ -171,13 +183,13 @@ SideStream* side_stream() {
   return &ss;
 }
 std::atomic<size_t> g_small_smem[8];
-std::atomic<size_t> g_binned_smem[8];
+std::atomic<size_t> g_binned_smem[16];
 
-template <bool B, bool C, int P>
+template <bool B, bool C, int P, int T>
 cudaError_t launch_binned_t(const BinArgs& ba, int batch, size_t smem, cudaStream_t st, std::atomic<size_t>& cfg) {
-  cudaError_t e = ensure_smem(pnms_binned_frame<B, C, P>, smem, cfg);
+  cudaError_t e = ensure_smem(pnms_binned_frame<B, C, P, T>, smem, cfg);
   if (e != cudaSuccess) return e;
-  pnms_binned_frame<B, C, P><<<batch, kBinThreads, smem, st>>>(ba);
+  pnms_binned_frame<B, C, P, T><<<batch, T, smem, st>>>(ba);
   return cudaGetLastError();
 }
 
@@ -279,16 +291,26 @@ cudaError_t launch_pairs(int variant, const BinArgs& ba, int batch, size_t smem,
   }
 }
 
-cudaError_t launch_binned(int variant, const BinArgs& ba, int batch, size_t smem, cudaStream_t st) {
+// variant bits: 1 by_index, 2 count pairs, 4 eight boxes per thread; `latency` picks 1024-thread
+// CTAs (one per SM, two boxes per thread) for batches that fit one wave
+cudaError_t launch_binned(int variant, const BinArgs& ba, int batch, size_t smem, cudaStream_t st, bool latency) {
+  if (latency) {
+    switch (variant & 3) {
+      case 0: return launch_binned_t<false, false, 2, 1024>(ba, batch, smem, st, g_binned_smem[8]);
+      case 1: return launch_binned_t<true, false, 2, 1024>(ba, batch, smem, st, g_binned_smem[9]);
+      case 2: return launch_binned_t<false, true, 2, 1024>(ba, batch, smem, st, g_binned_smem[10]);
+      default: return launch_binned_t<true, true, 2, 1024>(ba, batch, smem, st, g_binned_smem[11]);
+    }
+  }
   switch (variant) {
-    case 0: return launch_binned_t<false, false, 4>(ba, batch, smem, st, g_binned_smem[0]);
-    case 1: return launch_binned_t<true, false, 4>(ba, batch, smem, st, g_binned_smem[1]);
-    case 2: return launch_binned_t<false, true, 4>(ba, batch, smem, st, g_binned_smem[2]);
-    case 3: return launch_binned_t<true, true, 4>(ba, batch, smem, st, g_binned_smem[3]);
-    case 4: return launch_binned_t<false, false, 8>(ba, batch, smem, st, g_binned_smem[4]);
-    case 5: return launch_binned_t<true, false, 8>(ba, batch, smem, st, g_binned_smem[5]);
-    case 6: return launch_binned_t<false, true, 8>(ba, batch, smem, st, g_binned_smem[6]);
-    default: return launch_binned_t<true, true, 8>(ba, batch, smem, st, g_binned_smem[7]);
+    case 0: return launch_binned_t<false, false, 4, kBinThreads>(ba, batch, smem, st, g_binned_smem[0]);
+    case 1: return launch_binned_t<true, false, 4, kBinThreads>(ba, batch, smem, st, g_binned_smem[1]);
+    case 2: return launch_binned_t<false, true, 4, kBinThreads>(ba, batch, smem, st, g_binned_smem[2]);
+    case 3: return launch_binned_t<true, true, 4, kBinThreads>(ba, batch, smem, st, g_binned_smem[3]);
+    case 4: return launch_binned_t<false, false, 8, kBinThreads>(ba, batch, smem, st, g_binned_smem[4]);
+    case 5: return launch_binned_t<true, false, 8, kBinThreads>(ba, batch, smem, st, g_binned_smem[5]);
+    case 6: return launch_binned_t<false, true, 8, kBinThreads>(ba, batch, smem, st, g_binned_smem[6]);
+    default: return launch_binned_t<true, true, 8, kBinThreads>(ba, batch, smem, st, g_binned_smem[7]);
   }
 }
 
@@ -590,13 +612,16 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     const size_t smem = binned_smem_bytes(binned_npad(n_max));
     if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
     const int variant = (tie_break == PNMS_TIE_BY_INDEX ? 1 : 0) + (g_pairs_counter ? 2 : 0) +
-                        (binned_per_thread(n_max) == 8 ? 4 : 0);
+                        (binned_per_thread(n_max, kBinThreads) == 8 ? 4 : 0);
+    // one wave of 1024-thread CTAs (two boxes per thread) when the batch fits the SMs
+    const int lat_env = env_int("PNMS_BINNED_LATENCY", -1);
+    const bool latency = n_max <= 2048 && (lat_env >= 0 ? lat_env == 1 : batch <= sm_count());
     if (env_int("PNMS_BINNED", 0) == 2) {  // cell-pair tiles (pnms_binned_pairs.cuh): opt-in,
       // measured 4 % slower on BASELINE config 5 (more pair tests without the gate-prefix skip)
       const size_t psmem = binned_pairs_smem_bytes(binned_npad(n_max));
       if ((e = launch_pairs(variant, ba, batch, psmem, st)) != cudaSuccess) return fail_cuda(e);
     } else {                               // per-row scans (pnms_binned.cuh), the default
-      if ((e = launch_binned(variant, ba, batch, smem, st)) != cudaSuccess) return fail_cuda(e);
+      if ((e = launch_binned(variant, ba, batch, smem, st, latency)) != cudaSuccess) return fail_cuda(e);
     }
     decl_list = ba.decl_list;
     decl_count = ba.decl_count;

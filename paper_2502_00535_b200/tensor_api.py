@@ -346,12 +346,31 @@ class NmsEngine:
                     d[a:b].copy_(h[a:b], non_blocking=True)
         self._pipeline(stage, hs, hcounts, out_mask, out_count)
 
-    def run_host_box32(self, hbox, hs, hcounts, out_mask, out_count):
+    def run_host_box32(self, hbox, hs, hcounts, out_mask, out_count, graph: bool = False):
         """run_host with the packed 32-bit box format of `pack_box32` (x | y<<12 | z<<24 in an
         int32 plane [B, n_max]): 4 B of geometry per box on the wire, 12 B with the score;
-        unpacked on the device by pnms_unpack_box32."""
+        unpacked on the device by pnms_unpack_box32.
+
+        graph=True replays the whole pipeline (copies, kernels, read-back) as one CUDA graph,
+        captured on the first call for this set of host buffers: no per-chunk host launch
+        overhead on the critical path.  The buffers must then stay allocated and be refilled
+        in place between calls."""
         if hbox.dtype != torch.int32 or hbox.shape != (self.batch, self.n_max):
             raise ValueError("hbox must be an int32 [batch, n_max] plane of pack_box32 words")
+        if graph:
+            key = tuple(t.data_ptr() for t in (hbox, hs, hcounts, out_mask, out_count))
+            if getattr(self, "_graph_key", None) != key:
+                self._run_box32(hbox, hs, hcounts, out_mask, out_count)  # warm-up: attributes, buffers
+                torch.cuda.synchronize(self.device)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._run_box32(hbox, hs, hcounts, out_mask, out_count)
+                self._graph, self._graph_key = g, key
+            self._graph.replay()
+            return
+        self._run_box32(hbox, hs, hcounts, out_mask, out_count)
+
+    def _run_box32(self, hbox, hs, hcounts, out_mask, out_count):
         dx, dy, dz, _, _ = self._device_inputs()
         lib = _lib.load()
         if getattr(self, "_dev32", None) is None:

@@ -540,6 +540,18 @@ def test_engine_run_host_int16_and_int32_agree():
     eng.run_host_box32(hb, hs, hc, om, oc)
     torch.cuda.synchronize()
     assert torch.equal(om, ref_mask.cpu()) and torch.equal(oc, ref_cnt.cpu())
+    # the same pipeline captured and replayed as one CUDA graph; new inputs refilled in place
+    for rep in range(3):
+        om.zero_(); oc.zero_()
+        eng.run_host_box32(hb, hs, hc, om, oc, graph=True)
+        torch.cuda.synchronize()
+        assert torch.equal(om, ref_mask.cpu()) and torch.equal(oc, ref_cnt.cpu()), rep
+    x2, y2, z2, s2 = random_frames(37, 500, seed=13)
+    hb.copy_(torch.from_numpy(pack_box32(x2, y2, z2))); hs.copy_(torch.from_numpy(s2))
+    eng.run_host_box32(hb, hs, hc, om, oc, graph=True)
+    torch.cuda.synchronize()
+    eng.run_device(*[torch.from_numpy(a).to(DEV) for a in (x2, y2, z2, s2)], want_mask=True)
+    assert torch.equal(om, eng.keep_mask.cpu()) and torch.equal(oc, eng.keep_count.cpu())
 
 
 def test_unpack_box32_extremes():
