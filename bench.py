@@ -249,6 +249,27 @@ def variants_suite(torch, dev, frames: int = 256, n: int = 1024, iters: int = 10
 
     res = {"workload": f"{frames} frames x {n} boxes (random_frame distribution), theta 0.5 / soft theta 0.3, "
                        f"sigma 0.5", "unit": "frames/s"}
+    # device-side ingest validation (detections.py:60-85) of the config-5 stream: an HBM stream
+    from paper_2502_00535_b200 import validate_batch
+    from paper_2502_00535_b200.synth import random_frames as rf
+
+    from paper_2502_00535_b200 import _lib
+
+    big = [torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in rf(8192, 2048, seed=65, **GEN)]
+    validate_batch(*big)  # the public call (raises on an invalid detection); timed below: its kernel
+    first = torch.empty(8192, dtype=torch.int32, device=dev)
+    why = torch.empty(8192, dtype=torch.int32, device=dev)
+    lib = _lib.load()
+    st_ = torch.cuda.current_stream(dev).cuda_stream
+    vrate, _ = dev_rate(lambda: lib.pnms_validate(*(t.data_ptr() for t in big), None, 8192, 2048, first.data_ptr(),
+                                                   why.data_ptr(), st_))
+    vbytes = 8192 * 2048 * 20
+    mp = ROOT / "MEASURED_PEAKS.json"
+    peak = float(json.loads(mp.read_text()).get("hbm_gbs", 6650.0)) if mp.exists() else 6650.0
+    vsec = frames / vrate  # dev_rate reports `frames` per call
+    res["validate_c5"] = {"ms": vsec * 1e3, "gbs": vbytes / vsec / 1e9, "hbm_frac": vbytes / vsec / 1e9 / peak,
+                          "note": "pnms_validate over 8192 x 2048 slots (20 B each), device time per call"}
+    del big
     rate, (ki, kc) = dev_rate(lambda: greedy_nms_keep(x, y, z, s, None, THETA))
     crate, want = cpu_rate(lambda f: c_oracle.greedy_frame(*(a[f] for a in arrs), n, THETA), 4)  # want = frame 3
     res["greedy"] = {"value": rate, "cpu_port_1core": crate,

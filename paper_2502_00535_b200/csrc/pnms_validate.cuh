@@ -47,7 +47,23 @@ __global__ void __launch_bounds__(256) pnms_validate_kernel(const int32_t* x, co
   const int cnt = frame_count(counts, f, n_max);
   if (threadIdx.x == 0) s_first = 0x7FFFFFFF;
   __syncthreads();
-  for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+  // 16 B vector loads when the frame's slots are 16 B aligned (HBM streaming), else scalar
+  const bool vec = ((fbase & 3) == 0) && ((((uintptr_t)x) | ((uintptr_t)y) | ((uintptr_t)z) | ((uintptr_t)s)) & 15) == 0;
+  const int nv = vec ? cnt / 4 : 0;
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    const long long g = fbase + 4LL * v;
+    const int4 X = *reinterpret_cast<const int4*>(x + g), Y = *reinterpret_cast<const int4*>(y + g);
+    const int4 Z = *reinterpret_cast<const int4*>(z + g);
+    const double2 S0 = *reinterpret_cast<const double2*>(s + g), S1 = *reinterpret_cast<const double2*>(s + g + 2);
+    // the smallest invalid slot of the four (atomicMin keeps the frame's smallest overall)
+    int bad = 0x7FFFFFFF;
+    if (validate_one(X.w, Y.w, Z.w, S1.y) != kValid) bad = 4 * v + 3;
+    if (validate_one(X.z, Y.z, Z.z, S1.x) != kValid) bad = 4 * v + 2;
+    if (validate_one(X.y, Y.y, Z.y, S0.y) != kValid) bad = 4 * v + 1;
+    if (validate_one(X.x, Y.x, Z.x, S0.x) != kValid) bad = 4 * v;
+    if (bad != 0x7FFFFFFF) atomicMin(&s_first, bad);
+  }
+  for (int e = 4 * nv + threadIdx.x; e < cnt; e += blockDim.x) {
     const long long g = fbase + e;
     if (validate_one(x[g], y[g], z[g], s[g]) != kValid) atomicMin(&s_first, e);
   }
