@@ -228,7 +228,8 @@ cudaError_t launch_cluster_t(const BinArgs& ba, int batch, int slice, cudaStream
 
 // cluster size: 16 CTAs (non-portable; one GPC) when the device can co-schedule them, else 8
 int cluster_size_for(int n_max) {
-  static int cs16 = -1;
+  static std::atomic<int> cs16_cached{-1};  // probed once per process (benign if two threads race)
+  int cs16 = cs16_cached.load();
   if (cs16 < 0) {
     int n = 0;
     cudaLaunchConfig_t lc = {};
@@ -249,6 +250,7 @@ int cluster_size_for(int n_max) {
               cudaOccupancyMaxActiveClusters(&n, fn, &lc) == cudaSuccess && n > 0;
     cudaGetLastError();
     cs16 = ok ? 1 : 0;
+    cs16_cached.store(cs16);
   }
   const int want = env_int("PNMS_CLUSTER", 0);
   if (want == 8 || want == 16) return (want == 16 && !cs16) ? 8 : want;
