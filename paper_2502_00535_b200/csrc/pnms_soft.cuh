@@ -240,6 +240,9 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
         const int j = pl[t];
         const int32_t jx = F.sx[j], jy = F.sy[j], jz = F.sz[j];
         constexpr int kMaxNb = 24;
+        // sorted (key, slot) list of the final overlapping neighbours; entries [0, nn) are
+        // always written before they are read (insertion sort)
+#pragma nv_diag_suppress 549
         uint64_t nk[kMaxNb];
         int nb[kMaxNb];
         int nn = 0;
@@ -257,6 +260,7 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
             ++nn;
           }
         });
+#pragma nv_diag_default 549
         if (!fresh) continue;
         double tv = F.s0[j];
         if (nn <= kMaxNb) {
