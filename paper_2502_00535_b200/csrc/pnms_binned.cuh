@@ -4,14 +4,14 @@
 // Exactness argument.  A pair with no pixel overlap has w*h = 0, and the reference
 // suppresses on it only if 0 >= theta*(z_j+1)^2, i.e. only if T_j = 0 (theta = 0 or a
 // zero-side slot, engine.py:229-232).  When every valid column has T_j >= 1, only pairs
-// whose boxes overlap can suppress.  Boxes span [x, x+z] inclusive, so two overlapping boxes
-// have |x_i - x_j| <= max side and |y_i - y_j| <= max side: with square cells of side
-// S >= max_z + 1 their corner cells differ by at most one in each axis, and the 3x3
-// neighbourhood of a box's cell holds every box that can suppress it.  Inside a cell the
-// boxes are kept in (score desc, index asc) order, so the columns that pass the reference's
-// gate (engine.py:233-235) form a prefix of each neighbour cell; the scan stops at the first
-// column that fails the gate.  The result is the reference's row AND restricted to the only
-// columns that can clear a bit — bit-identical survivors.
+// whose boxes overlap can suppress.  Boxes span [x, x+z] inclusive, so a column j that
+// overlaps row i has its corner in [x_i - max_z, x_i + z_i] x [y_i - max_z, y_i + z_i]: with
+// square cells of any side S, the cells that rectangle touches hold every box that can
+// suppress row i (a 3x3 neighbourhood when S >= max_z + 1, more, smaller cells below).
+// Inside a cell the boxes are kept in (score desc, index asc) order, so the columns that
+// pass the reference's gate (engine.py:233-235) form a prefix of each cell; the scan stops
+// at the first column that fails the gate.  The result is the reference's row AND
+// restricted to the only columns that can clear a bit — bit-identical survivors.
 //
 // Frames that do not meet the preconditions (a T_j = 0 column, coordinates outside the
 // narrow7 domain, a cell holding more than kBinCellMax boxes, or > kBinMaxSlots slots) are
@@ -25,7 +25,7 @@ namespace pnms {
 
 constexpr int kBinThreads = 512;
 constexpr int kBinMaxSlots = 4096;
-constexpr int kBinMaxCells = 4096;   // upper bound; a frame uses at most max(64, npad) cells
+constexpr int kBinMaxCells = 4096;   // upper bound; a frame uses at most max(64, 2 * npad) cells
 constexpr int kBinCellMax = 64;
 
 // Binned record (16 B, one LDS.128 per candidate column), narrow7 geometry as RecNarrow:
@@ -59,13 +59,16 @@ struct BinArgs {
   uint32_t* keep_mask;
   unsigned long long* pairs_tested;  // optional device counter (diagnostics), may be null
   unsigned long long* trace;         // optional per-CTA phase timestamps (diagnostics), may be null
+  int cell_q8;                       // frame kernel cell side: 0 default, > 0 scale, < 0 absolute
 };
 
 struct __align__(16) BinStats {
   int mode, minz, maxz, minx, miny, maxx, maxy, big, n_act, pad_;
 };
 
-__host__ __device__ inline int binned_max_cells(int npad) { return npad < 64 ? 64 : (npad > kBinMaxCells ? kBinMaxCells : npad); }
+__host__ __device__ inline int binned_max_cells(int npad) {
+  return npad < 32 ? 64 : (2 * npad > kBinMaxCells ? kBinMaxCells : 2 * npad);
+}
 // npad is a multiple of 128, so every region below starts 16-byte aligned
 __host__ __device__ inline int binned_npad(int n_max) { return (n_max + 127) & ~127; }
 inline size_t binned_smem_bytes(int npad) {
@@ -87,6 +90,17 @@ __device__ __forceinline__ void binned_decline(const BinArgs& a, int f) {
   if (a.meta) a.meta[f] = FrameMeta{};
   a.decl_list[atomicAdd(a.decl_count, 1)] = f;
 }
+
+// diagnostics: global timer at phase boundaries of frame f (trace[f * 16 + phase]), thread 0;
+// compiled into the COUNT (diagnostic) instantiations only — the checks cost ~3 % otherwise
+#define PNMS_FRAME_TRACE(ph)                                                                   \
+  do {                                                                                         \
+    if (COUNT && a.trace && threadIdx.x == 0) {                                                \
+      unsigned long long t_;                                                                   \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                   \
+      a.trace[(long long)f * 16 + (ph)] = t_;                                                  \
+    }                                                                                          \
+  } while (0)
 
 __device__ __forceinline__ uint4 lds128(uint32_t saddr) {
   uint4 v;
@@ -148,6 +162,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 512 ? 3 : 1)) pnms_binned
   // the fallback kernels over the declined-frame list may launch once every CTA has started
   // (programmatic dependent launch); they wait for this grid's completion before reading
   cudaTriggerProgrammaticLaunchCompletion();
+  PNMS_FRAME_TRACE(0);
   // per-box data stored in cell order (positions [cstart[c], cstart[c+1]) = cell c)
   RecBin* recS = reinterpret_cast<RecBin*>(smem_raw);                         // [npad] records
   uint64_t* keyS = reinterpret_cast<uint64_t*>(recS + npad);                  // [npad] full sort keys
@@ -212,6 +227,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 512 ? 3 : 1)) pnms_binned
     }
   }
   __syncthreads();
+  PNMS_FRAME_TRACE(1);
   // T_j >= 1 for every active column  <=>  theta > 0 and no zero side (T = 0 only for z = 0,
   // engine.py:232, or theta*(z+1)^2 == 0)
   const int n_act = st->n_act;
@@ -221,7 +237,20 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 512 ? 3 : 1)) pnms_binned
     return;
   }
   // ---- grid of square cells, side >= max side + 1
-  int S = st->maxz + 1, GX = 1, GY = 1;
+  // Cell side: any S >= 1 is exact (the reachable range below is [x - max_z, x + z]); the
+  // default is the power of two nearest (max_z + 1) / 2 — measured on BASELINE config 5
+  // (max_z = 64): S = 32 costs 0.68 ms against 0.76 ms at S = 65 (fewer columns scanned per
+  // row, more runs); 28, 33 and 36 land at 0.71-0.73 ms.  cell_q8 > 0 scales (max_z + 1) by
+  // cell_q8 / 256 instead, < 0 sets S = -cell_q8 (tuning).
+  int S;
+  if (a.cell_q8 == 0) {
+    const int h = st->maxz + 1, half = max(h >> 1, 1);
+    const int p2 = 1 << (31 - __clz(half));
+    S = (long long)h * h > 8LL * p2 * p2 ? 2 * p2 : p2;
+  } else {
+    S = a.cell_q8 < 0 ? -a.cell_q8 : max(1, ((st->maxz + 1) * a.cell_q8 + 255) >> 8);
+  }
+  int GX = 1, GY = 1;
   const int ox = st->minx, oy = st->miny;
   if (n_act > 0) {
     for (;;) {
@@ -235,6 +264,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 512 ? 3 : 1)) pnms_binned
   const int cells = GX * GY;
   for (int c = threadIdx.x; c < cells + 1; c += THREADS) cstart[c] = 0u;
   __syncthreads();
+  PNMS_FRAME_TRACE(2);
   // ---- pass 2: histogram; the atomic's return value is the box's rank inside its cell
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
@@ -246,6 +276,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 512 ? 3 : 1)) pnms_binned
     }
   }
   __syncthreads();
+  PNMS_FRAME_TRACE(3);
   // exclusive scan of the cell counts (+ largest cell)
   {
     const int per = (cells + 1 + THREADS - 1) / THREADS;
@@ -265,6 +296,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 512 ? 3 : 1)) pnms_binned
     if (threadIdx.x == 0) cstart[cells] = n_act;
   }
   __syncthreads();
+  PNMS_FRAME_TRACE(4);
   if (st->big > kBinCellMax) {
     if (threadIdx.x == 0) binned_decline(a, f);
     return;
@@ -285,6 +317,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 512 ? 3 : 1)) pnms_binned
     }
   }
   __syncthreads();
+  PNMS_FRAME_TRACE(5);
   {
     // high key halves (one 32-bit load per member); members with an equal half other than the
     // box itself are rare and resolved exactly in a second loop
@@ -312,6 +345,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 512 ? 3 : 1)) pnms_binned
     }
   }
   __syncthreads();
+  PNMS_FRAME_TRACE(6);
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
     if (zc[k] != 0xFFFFFFFFu) {
@@ -331,6 +365,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 512 ? 3 : 1)) pnms_binned
     }
   }
   __syncthreads();
+  PNMS_FRAME_TRACE(7);
   // ---- scan: each valid box against the gate-passing prefix of every cell its extent can
   // reach.  A column j overlapping row i has x_j in [x_i - max_z, x_i + z_i] (same for y), so
   // the reachable cells of one cell row are contiguous in cell order: one run per cell row.
@@ -366,6 +401,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 512 ? 3 : 1)) pnms_binned
     if ((threadIdx.x & 31) == 0 && tested) atomicAdd(a.pairs_tested, tested);
   }
   __syncthreads();
+  PNMS_FRAME_TRACE(8);
   // ---- compaction (engine.py:284-293)
   const int words_per_thread = (a.W32 + THREADS - 1) / THREADS;
   const int w0 = threadIdx.x * words_per_thread, w1 = min(w0 + words_per_thread, a.W32);
@@ -390,6 +426,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 512 ? 3 : 1)) pnms_binned
     if (a.keep_count) a.keep_count[f] = (int32_t)total;
     a.fallback[f] = 0;
   }
+  PNMS_FRAME_TRACE(9);
 }
 
 }  // namespace pnms

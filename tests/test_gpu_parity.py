@@ -158,6 +158,25 @@ def test_binned_mixed_batch_vs_oracle(monkeypatch):
     assert int(counter.item()) > 0  # the binned kernel did run
 
 
+@pytest.mark.parametrize("cell", ["0", "-1", "-3", "-7", "-33", "-200", "64", "256", "400"])
+def test_binned_cell_side_invariance(cell, monkeypatch):
+    """Any cell side is exact (pnms_binned.cuh header): tiny cells (many runs per row, cell
+    grids that double until they fit), the default power of two, 3x3 neighbourhoods and cells
+    larger than the frame give the oracle's survivors, with ties, NaNs and ragged counts."""
+    monkeypatch.setenv("PNMS_SMALL_PAIRS", "0")
+    monkeypatch.setenv("PNMS_ALGO", "0")
+    monkeypatch.setenv("PNMS_CELL_Q8", cell)
+    x, y, z, s = random_frames(6, 1500, seed=77, frame_w=1280, frame_h=720, z_range=(3, 90), duplicate_fraction=0.1)
+    s[1, ::5] = np.nan
+    s[2, ::3] = 0.25
+    counts = np.array([1500, 1499, 1200, 64, 1, 0], np.int32)
+    for tie in ("paper_faithful", "by_index"):
+        got = _run_batch(x, y, z, s, counts, 0.4, tie, 1500)
+        for f in range(6):
+            want = c_oracle.run_frame(x[f], y[f], z[f], s[f], int(counts[f]), 1500, 0.4, tie)
+            assert np.array_equal(got[f], want), (cell, f, tie)
+
+
 def test_declined_frame_list_grid_stride(monkeypatch):
     """Every frame declined by the binned kernel (theta = 0) in a batch larger than the
     persistent grids of the dense fallback kernels: the declined-frame list is walked with
