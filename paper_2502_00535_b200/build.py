@@ -33,7 +33,8 @@ def _nvcc() -> str:
 
 
 def sources() -> list[Path]:
-    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + [REPO_DIR / "include" / "parnms_b200.h"]
+    return (sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h"))
+            + [REPO_DIR / "include" / "parnms_b200.h"])
 
 
 def needs_build() -> bool:
@@ -47,12 +48,29 @@ def build(force: bool = False, verbose: bool = False, extra: list[str] | None = 
     """Compile csrc/*.cu into the in-tree shared library; returns its path."""
     if not force and not needs_build():
         return LIB_PATH
-    cmd = [_nvcc(), *NVCC_FLAGS, *(extra or []), "-shared", "-o", str(LIB_PATH) + ".tmp",
-           str(CSRC / "pnms_capi.cu")]
+    # two units: pnms_devchain.cu with relocatable device code (device-side launches of the
+    # binned path's fallback chain), pnms_capi.cu whole-program (its kernels keep their
+    # register budgets); nvcc device-links the relocatable object into the shared library
+    tmp = LIB_PATH.parent / "build_tmp"
+    tmp.mkdir(exist_ok=True)
+    steps = [
+        [_nvcc(), *NVCC_FLAGS, *(extra or []), "-rdc=true", "-c", "-o", str(tmp / "devchain.o"),
+         str(CSRC / "pnms_devchain.cu")],
+        [_nvcc(), *NVCC_FLAGS, *(extra or []), "-c", "-o", str(tmp / "capi.o"), str(CSRC / "pnms_capi.cu")],
+        [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static", "-shared",
+         "-o", str(LIB_PATH) + ".tmp", str(tmp / "capi.o"), str(tmp / "devchain.o"), "-lcudadevrt"],
+    ]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+        for cmd in steps:
+            cmd.insert(1, "-Xptxas=-v")
+            print(" ".join(cmd), file=sys.stderr)
+    compiles = [subprocess.Popen(cmd) for cmd in steps[:2]]  # the two units compile in parallel
+    for cmd, proc in zip(steps[:2], compiles):
+        if proc.wait() != 0:
+            raise subprocess.CalledProcessError(proc.returncode, cmd)
+    subprocess.run(steps[2], check=True)
+    for obj in ("devchain.o", "capi.o"):
+        (tmp / obj).unlink(missing_ok=True)
     os.replace(str(LIB_PATH) + ".tmp", LIB_PATH)
     return LIB_PATH
 

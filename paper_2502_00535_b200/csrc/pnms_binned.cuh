@@ -153,7 +153,8 @@ __device__ __forceinline__ bool binned_scan_run(uint32_t base, uint32_t qb, uint
 // THREADS = 512 (three CTAs per SM: throughput) or 1024 (one CTA per SM, half the rows per
 // thread: latency, for batches that fit one wave)
 template <bool BY_INDEX, bool COUNT, int PER, int THREADS>
-__global__ void __launch_bounds__(THREADS, (THREADS == 512 ? 3 : 1)) pnms_binned_frame(BinArgs a) {
+// returns true when the frame was declined (appended to the list for the dense pipeline)
+__device__ __forceinline__ bool binned_frame_body(const BinArgs& a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int f = blockIdx.x;
   const long long fbase = (long long)f * a.n_max;
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 512 ? 3 : 1)) pnms_binned
   const int npad = binned_npad(a.n_max);
   // the fallback kernels over the declined-frame list may launch once every CTA has started
   // (programmatic dependent launch); they wait for this grid's completion before reading
-  cudaTriggerProgrammaticLaunchCompletion();
+  pdl_trigger();
   PNMS_FRAME_TRACE(0);
   // per-box data stored in cell order (positions [cstart[c], cstart[c+1]) = cell c)
   RecBin* recS = reinterpret_cast<RecBin*>(smem_raw);                         // [npad] records
@@ -183,7 +184,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 512 ? 3 : 1)) pnms_binned
   __syncthreads();
   if (a.n_max > PER * THREADS) {
     if (threadIdx.x == 0) binned_decline(a, f);
-    return;
+    return true;
   }
   // ---- pass 1: the frame is read from HBM once; each thread keeps its PER boxes in
   // registers (xy packed as two 16-bit halves — exact for every frame that stays on this
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 512 ? 3 : 1)) pnms_binned
   const bool eligible = st->mode == kNarrow7 && (n_act == 0 || (a.theta > 0.0 && st->minz >= 1));
   if (!eligible) {
     if (threadIdx.x == 0) binned_decline(a, f);
-    return;
+    return true;
   }
   // ---- grid of square cells, side >= max side + 1
   // Cell side: any S >= 1 is exact (the reachable range below is [x - max_z, x + z]); the
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 512 ? 3 : 1)) pnms_binned
   PNMS_FRAME_TRACE(4);
   if (st->big > kBinCellMax) {
     if (threadIdx.x == 0) binned_decline(a, f);
-    return;
+    return true;
   }
   // ---- pass 3: keys, slots and cells into cell order by arrival; then one thread per arrival
   // position counts the members of its cell that precede it in (key, slot) order — a parallel
@@ -427,6 +428,12 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 512 ? 3 : 1)) pnms_binned
     a.fallback[f] = 0;
   }
   PNMS_FRAME_TRACE(9);
+  return false;
+}
+
+template <bool BY_INDEX, bool COUNT, int PER, int THREADS>
+__global__ void __launch_bounds__(THREADS, (THREADS == 512 ? 3 : 1)) pnms_binned_frame(BinArgs a) {
+  binned_frame_body<BY_INDEX, COUNT, PER, THREADS>(a);
 }
 
 }  // namespace pnms

@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(kPairThreads, (PER == 4 ? 3 : 1)) pnms_binned_
   const int npad = binned_npad(a.n_max);
   // the fallback kernels over the declined-frame list may launch once every CTA has started
   // (programmatic dependent launch); they wait for this grid's completion before reading
-  cudaTriggerProgrammaticLaunchCompletion();
+  pdl_trigger();
   RecPair* recS = reinterpret_cast<RecPair*>(smem_raw);                    // [npad] cell order
   uint64_t* keyS = reinterpret_cast<uint64_t*>(recS + npad);               // [npad] sort keys
   const int max_cells = binned_max_cells(npad);

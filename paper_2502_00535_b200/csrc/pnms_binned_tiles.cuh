@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) pnms_binned_tiles(TileArgs ta
   const int f = blockIdx.x / kTilesPerFrame, t = blockIdx.x % kTilesPerFrame;
   const long long fbase = (long long)f * a.n_max;
   const int cnt = frame_count(a.counts, f, a.n_max);
-  cudaTriggerProgrammaticLaunchCompletion();  // pnms_mask_compact may launch early (PDL)
+  pdl_trigger();  // pnms_mask_compact may launch early (PDL)
   unsigned long long* trace = a.trace;          // diagnostics: per-CTA phase timestamps
 #define PNMS_TILE_TRACE(ph)                                                               \
   do {                                                                                    \
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) pnms_binned_tiles(TileArgs ta
 // survivor mask -> ascending keep indices, count and mask output (engine.py:284-293); one CTA
 // per frame; frames flagged in `decline` are left to the dense pipeline
 __global__ void __launch_bounds__(512) pnms_mask_compact(TileArgs ta) {
-  cudaGridDependencySynchronize();  // PDL: the tile kernel's mask is complete after this
+  pdl_wait();  // PDL: the tile kernel's mask is complete after this
   const BinArgs& a = ta.b;
   const int f = blockIdx.x;
   __shared__ uint32_t scan_tmp[64];

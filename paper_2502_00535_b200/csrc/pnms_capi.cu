@@ -20,6 +20,8 @@
 #include "pnms_reflayout.cuh"
 #include "pnms_small.cuh"
 #include "pnms_binned.cuh"
+#include "pnms_devchain.h"
+#include "pnms_fallback.cuh"
 #include "pnms_validate.cuh"
 #include "pnms_binned_cluster.cuh"
 #include "pnms_binned_pairs.cuh"
@@ -142,7 +144,7 @@ cudaError_t ensure_smem(K kernel, size_t bytes, std::atomic<size_t>& configured)
 }
 
 // launch `kernel` with programmatic stream serialization (PDL) when `pdl` is set: it may start
-// while the previous kernel on the stream drains; it calls cudaGridDependencySynchronize()
+// while the previous kernel on the stream drains; it calls pdl_wait()
 template <class... KArgs, class... Args>
 cudaError_t launch_maybe_pdl(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                              Args&&... args) {
@@ -183,6 +185,8 @@ SideStream* side_stream() {
   return &ss;
 }
 std::atomic<size_t> g_small_smem[8];
+
+
 std::atomic<size_t> g_binned_smem[16];
 
 template <bool B, bool C, int P, int T>
@@ -375,6 +379,12 @@ MapShape choose_map_shape(int batch, int n_max) {
   m.RB = kMapWarps * 32 * m.R;
   return m;
 }
+
+// the binned path's declined-frame count lives in the persistent zeroed scratch
+// (pnms_workspace_init), after the small path's words; every call leaves it zero
+constexpr size_t kDeclCountOffset = kSmallMaxWords * 4 + kSmallMaxFrames * 4 + kSmallMaxFrames * 8;
+static_assert(kDeclCountOffset + 4 <= kSmallScratchBytes, "scratch");
+
 
 template <int R>
 cudaError_t launch_map(const MapArgs& ma, long long grid, size_t smem, cudaStream_t st, bool list) {
@@ -591,6 +601,53 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     return PNMS_OK;
   }
 
+  // arguments of the dense pipeline (prep+sort -> map -> compact) for frames [f0, f0 + nf)
+  const MapShape ms = choose_map_shape(batch, n_max);
+  auto chain_args = [&](int f0, int nf, const uint8_t* dense, const int32_t* list, const int* list_count,
+                        PrepArgs& pa, MapArgs& ma, CompactArgs& ca) {
+    const size_t fo = (size_t)f0 * n_max;
+    pa.x = x + fo; pa.y = y + fo; pa.z = z + fo; pa.s = s + fo; pa.counts = counts ? counts + f0 : nullptr;
+    pa.batch = nf; pa.n_max = n_max; pa.tie_break = tie_break; pa.W32 = W32;
+    pa.theta = theta;
+    pa.rec = ws + L.rec + fo * kRecBytes;
+    pa.perm = reinterpret_cast<int32_t*>(ws + L.perm) + fo;
+    pa.lim = reinterpret_cast<int32_t*>(ws + L.lim) + fo;
+    pa.supp = reinterpret_cast<uint32_t*>(ws + L.supp) + (size_t)f0 * W32;
+    pa.meta = reinterpret_cast<FrameMeta*>(ws + L.meta) + f0;
+    pa.sk_scratch = L.sk ? reinterpret_cast<uint64_t*>(ws + L.sk) + fo : nullptr;
+    pa.idx_scratch = L.idx ? reinterpret_cast<int32_t*>(ws + L.idx) + fo : nullptr;
+    pa.dense = dense ? dense + f0 : nullptr;
+    pa.list = list;          // chunks == 1 whenever the list is set
+    pa.list_count = list_count;
+    if (n_max <= kSortMax) {
+      pa.npad = (n_max + kSortThreads - 1) / kSortThreads * kSortThreads;
+      pa.nchunks = 1;
+    } else {
+      pa.npad = kSortMax;
+      pa.nchunks = (n_max + kSortMax - 1) / kSortMax;
+    }
+    ma.rec = pa.rec; ma.lim = pa.lim; ma.supp = pa.supp; ma.meta = pa.meta;
+    ma.batch = nf; ma.n_max = n_max; ma.W32 = W32;
+    ma.rows_per_block = ms.RB;
+    ma.chunk = ms.chunk;
+    ma.n_rb = (n_max + ms.RB - 1) / ms.RB;
+    ma.items_per_frame = items_per_frame(n_max, ms.RB, ms.chunk);
+    ma.dense = pa.dense;
+    ma.list = list;
+    ma.list_count = list_count;
+    ca.s = pa.s; ca.counts = pa.counts; ca.perm = pa.perm; ca.supp = pa.supp; ca.meta = pa.meta;
+    ca.batch = nf; ca.n_max = n_max; ca.W32 = W32; ca.d_max = d_max; ca.tie_break = tie_break;
+    ca.keep_idx = keep_idx ? keep_idx + fo : nullptr;
+    ca.keep_count = keep_count ? keep_count + f0 : nullptr;
+    ca.keep_mask = keep_mask ? keep_mask + (size_t)f0 * W32 : nullptr;
+    ca.gate_pairs = gate_pairs ? reinterpret_cast<unsigned long long*>(gate_pairs) + f0 : nullptr;
+    ca.dense = pa.dense;
+    ca.list = list;
+    ca.list_count = list_count;
+  };
+  const size_t compact_smem = ((size_t)W32 + 3) / 4 * 16 + 64 * 4;
+  const size_t map_smem = (size_t)ms.chunk * kRecBytes;
+
   // ---- binned path (sparse frames): exact, one CTA per frame; declined frames fall through
   // to the dense pipeline below, which then only processes those frames.
   const uint8_t* dense_flags = nullptr;
@@ -599,14 +656,19 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
   void* ev_local[4];
   const long long algo = env_ll("PNMS_ALGO", 0);  // 0 auto, 1 dense only
   if (algo == 0 && gate_pairs == nullptr && n_max <= kBinMaxSlots) {
-    BinArgs ba;
+    const bool pairs = env_int("PNMS_BINNED", 0) == 2;
+    BinArgs ba{};
     ba.x = x; ba.y = y; ba.z = z; ba.s = s; ba.counts = counts;
     ba.batch = batch; ba.n_max = n_max; ba.d_max = d_max; ba.tie_break = tie_break; ba.W32 = W32;
     ba.theta = theta;
     ba.fallback = ws + L.dense;
-    ba.decl_count = reinterpret_cast<int*>(ws + L.list);
     ba.decl_list = reinterpret_cast<int32_t*>(ws + L.list) + 1;
-    if ((e = cudaMemsetAsync(ba.decl_count, 0, sizeof(int), st)) != cudaSuccess) return fail_cuda(e);
+    if (pairs) {  // the cell-pair kernel leaves the count for the host chain: zero it per call
+      ba.decl_count = reinterpret_cast<int*>(ws + L.list);
+      if ((e = cudaMemsetAsync(ba.decl_count, 0, sizeof(int), st)) != cudaSuccess) return fail_cuda(e);
+    } else {      // count in the zeroed scratch, left zero by the dispatcher (pnms_fallback.cuh)
+      ba.decl_count = reinterpret_cast<int*>(ws + kDeclCountOffset);
+    }
     ba.keep_idx = keep_idx; ba.keep_count = keep_count; ba.keep_mask = keep_mask;
     ba.pairs_tested = g_pairs_counter;
     ba.trace = g_trace;
@@ -619,7 +681,7 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     // one wave of 1024-thread CTAs (two boxes per thread) when the batch fits the SMs
     const int lat_env = env_int("PNMS_BINNED_LATENCY", -1);
     const bool latency = n_max <= 2048 && (lat_env >= 0 ? lat_env == 1 : batch <= sm_count());
-    if (env_int("PNMS_BINNED", 0) == 2) {  // cell-pair tiles (pnms_binned_pairs.cuh): opt-in,
+    if (pairs) {                           // cell-pair tiles (pnms_binned_pairs.cuh): opt-in,
       // measured 4 % slower on BASELINE config 5 (more pair tests without the gate-prefix skip)
       const size_t psmem = binned_pairs_smem_bytes(binned_npad(n_max));
       if ((e = launch_pairs(variant, ba, batch, psmem, st)) != cudaSuccess) return fail_cuda(e);
@@ -629,6 +691,26 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     decl_list = ba.decl_list;
     decl_count = ba.decl_count;
     if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
+    if (!pairs) {
+      // one-CTA dispatcher: snapshots and zeroes the count and, when frames were declined,
+      // tail-launches the dense chain over them (unless the host launches it: profiled calls)
+      FallbackPlan plan{};
+      int* snap = reinterpret_cast<int*>(ws + L.list);
+      chain_args(0, batch, ws + L.dense, ba.decl_list, snap, plan.pa, plan.ma, plan.ca);
+      plan.map_R = ms.R;
+      plan.sort_smem = (int)sort_frame_smem_bytes(plan.pa.npad);
+      plan.map_smem = (int)map_smem;
+      plan.compact_smem = (int)compact_smem;
+      plan.enabled = events == nullptr && env_int("PNMS_DEVCHAIN", 1) != 0;  // 0: host chain (debug)
+      static const bool same_layout = pnms_devchain_plan_size() == sizeof(FallbackPlan);
+      if (!same_layout) return fail_cuda(cudaErrorInvalidValue);
+      if (plan.enabled &&
+          (e = pnms_devchain_prepare(ms.R, plan.sort_smem, map_smem, compact_smem)) != cudaSuccess)
+        return fail_cuda(e);
+      if ((e = pnms_devchain_dispatch(&plan, ba.decl_count, snap, st)) != cudaSuccess) return fail_cuda(e);
+      if (plan.enabled) return PNMS_OK;
+      decl_count = snap;
+    }
     dense_flags = ws + L.dense;
     if (events) {
       // phases become: [0,1) binned kernel, [1,2) dense prep of declined frames, [2,3) their map+compact
@@ -641,7 +723,7 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     // large frames: few frames -> kTilesPerFrame independent tile CTAs per frame
     // (pnms_binned_tiles.cuh, latency); many frames -> one thread-block cluster per frame
     // (pnms_binned_cluster.cuh, throughput).  Declined frames go to the dense pipeline by list.
-    BinArgs ba;
+    BinArgs ba{};
     ba.x = x; ba.y = y; ba.z = z; ba.s = s; ba.counts = counts;
     ba.batch = batch; ba.n_max = n_max; ba.d_max = d_max; ba.tie_break = tie_break; ba.W32 = W32;
     ba.theta = theta;
@@ -694,7 +776,6 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
   // ---- sorted pipeline: prep+sort -> map -> compact, per frame chunk --------------------
   // Large batches are cut into chunks whose sort runs on an internal side stream while the
   // previous chunk's map runs on the caller's stream, so the sort hides behind the map.
-  const MapShape ms = choose_map_shape(batch, n_max);
   int chunks = 1;
   if (!events && !decl_list && n_max <= kSortMax && batch >= 512) {
     chunks = std::max(1, std::min(32, env_int("PNMS_OVERLAP_CHUNKS", 1)));
@@ -711,26 +792,13 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     const int f0 = (int)((long long)batch * c / chunks), f1 = (int)((long long)batch * (c + 1) / chunks);
     const int nf = f1 - f0;
     if (nf <= 0) continue;
-    const size_t fo = (size_t)f0 * n_max;
     cudaStream_t sort_st = chunks > 1 ? side->s : st;
     PrepArgs pa;
-    pa.x = x + fo; pa.y = y + fo; pa.z = z + fo; pa.s = s + fo; pa.counts = counts ? counts + f0 : nullptr;
-    pa.batch = nf; pa.n_max = n_max; pa.tie_break = tie_break; pa.W32 = W32;
-    pa.theta = theta;
-    pa.rec = ws + L.rec + fo * kRecBytes;
-    pa.perm = reinterpret_cast<int32_t*>(ws + L.perm) + fo;
-    pa.lim = reinterpret_cast<int32_t*>(ws + L.lim) + fo;
-    pa.supp = reinterpret_cast<uint32_t*>(ws + L.supp) + (size_t)f0 * W32;
-    pa.meta = reinterpret_cast<FrameMeta*>(ws + L.meta) + f0;
-    pa.sk_scratch = L.sk ? reinterpret_cast<uint64_t*>(ws + L.sk) + fo : nullptr;
-    pa.idx_scratch = L.idx ? reinterpret_cast<int32_t*>(ws + L.idx) + fo : nullptr;
-    pa.dense = dense_flags ? dense_flags + f0 : nullptr;
-    pa.list = decl_list;          // chunks == 1 whenever the list is set
-    pa.list_count = decl_count;
+    MapArgs ma;
+    CompactArgs ca;
+    chain_args(f0, nf, dense_flags, decl_list, decl_count, pa, ma, ca);
 
     if (n_max <= kSortMax) {
-      pa.npad = (n_max + kSortThreads - 1) / kSortThreads * kSortThreads;
-      pa.nchunks = 1;
       const size_t smem = sort_frame_smem_bytes(pa.npad);
       if (decl_list) {
         static std::atomic<size_t> lcfg{0};
@@ -744,8 +812,6 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
         if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
       }
     } else {
-      pa.npad = kSortMax;
-      pa.nchunks = (n_max + kSortMax - 1) / kSortMax;
       // the declined-frame list path had each frame's FrameMeta zeroed by the decliner
       if (!decl_list && (e = cudaMemsetAsync(pa.meta, 0, sizeof(FrameMeta) * (size_t)nf, sort_st)) != cudaSuccess)
         return fail_cuda(e);
@@ -768,20 +834,9 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     }
 
     if ((e = mark(events, 1, st)) != cudaSuccess) return fail_cuda(e);
-    MapArgs ma;
-    ma.rec = pa.rec; ma.lim = pa.lim; ma.supp = pa.supp; ma.meta = pa.meta;
-    ma.batch = nf; ma.n_max = n_max; ma.W32 = W32;
-    ma.rows_per_block = ms.RB;
-    ma.chunk = ms.chunk;
-    ma.n_rb = (n_max + ms.RB - 1) / ms.RB;
-    const int ipf = items_per_frame(n_max, ms.RB, ms.chunk);
-    ma.items_per_frame = ipf;
-    ma.dense = pa.dense;
-    ma.list = decl_list;
-    ma.list_count = decl_count;
+    const int ipf = ma.items_per_frame;
     const long long grid = decl_list ? std::min<long long>((long long)nf * ipf, 148 * 8) : (long long)nf * ipf;
     if (grid > 0x7FFFFFFFLL) return PNMS_ETOO_LARGE;
-    const size_t map_smem = (size_t)ms.chunk * kRecBytes;
     const bool pdl = decl_list != nullptr;
     if (ms.R == 4) e = launch_map<4>(ma, grid, map_smem, st, pdl);
     else if (ms.R == 2) e = launch_map<2>(ma, grid, map_smem, st, pdl);
@@ -789,20 +844,9 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     if (e != cudaSuccess) return fail_cuda(e);
 
     if ((e = mark(events, 2, st)) != cudaSuccess) return fail_cuda(e);
-    CompactArgs ca;
-    ca.s = pa.s; ca.counts = pa.counts; ca.perm = pa.perm; ca.supp = pa.supp; ca.meta = pa.meta;
-    ca.batch = nf; ca.n_max = n_max; ca.W32 = W32; ca.d_max = d_max; ca.tie_break = tie_break;
-    ca.keep_idx = keep_idx ? keep_idx + fo : nullptr;
-    ca.keep_count = keep_count ? keep_count + f0 : nullptr;
-    ca.keep_mask = keep_mask ? keep_mask + (size_t)f0 * W32 : nullptr;
-    ca.gate_pairs = gate_pairs ? reinterpret_cast<unsigned long long*>(gate_pairs) + f0 : nullptr;
-    ca.dense = pa.dense;
-    ca.list = decl_list;
-    ca.list_count = decl_count;
-    const size_t csmem = ((size_t)W32 + 3) / 4 * 16 + 64 * 4;
-    if ((e = ensure_smem(pnms_compact, csmem, g_compact_smem)) != cudaSuccess) return fail_cuda(e);
+    if ((e = ensure_smem(pnms_compact, compact_smem, g_compact_smem)) != cudaSuccess) return fail_cuda(e);
     if ((e = launch_maybe_pdl(decl_list != nullptr, pnms_compact, dim3(decl_list ? std::min(nf, 148 * 4) : nf),
-                              dim3(kCompactThreads), csmem, st, ca)) != cudaSuccess)
+                              dim3(kCompactThreads), compact_smem, st, ca)) != cudaSuccess)
       return fail_cuda(e);
   }
   if ((e = mark(events, 3, st)) != cudaSuccess) return fail_cuda(e);

@@ -14,6 +14,24 @@
 
 namespace pnms {
 
+// programmatic dependent launch as inline PTX (the runtime wrappers become calls in
+// relocatable device code): wait for the preceding grid's completion and memory flush / let
+// the dependent grid start launching.  Both are no-ops without a programmatic launch.
+#ifdef PNMS_DEVICE_CHAIN
+// pnms_devchain.cu: the list kernels there are only tail-launched by the binned kernel, after
+// it completed; waiting on the launching grid from a tail launch would never return
+__device__ __forceinline__ void pdl_wait() {}
+#else
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#endif
+#ifdef PNMS_DEVICE_CHAIN
+// ... and a grid that tail-launches must not trigger its dependents early: measured on B200,
+// griddepcontrol.launch_dependents in the parent keeps a tail launch from ever starting
+__device__ __forceinline__ void pdl_trigger() {}
+#else
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#endif
+
 constexpr int kSortMax = 4096;        // frames up to this many slots sort inside one CTA
 constexpr int kSortThreads = 512;     // 16 warps
 constexpr int kSortWarps = kSortThreads / 32;

@@ -88,8 +88,8 @@ __global__ void __launch_bounds__(kCompactThreads) pnms_compact(CompactArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   if (a.list) {
     // launched programmatically after the binned kernel (PDL): wait for its results
-    cudaGridDependencySynchronize();
-    cudaTriggerProgrammaticLaunchCompletion();
+    pdl_wait();
+    pdl_trigger();
     const int n = *a.list_count;
     for (int li = blockIdx.x; li < n; li += gridDim.x) {
       compact_body(a, a.list[li], smem_raw);

@@ -164,7 +164,7 @@ __device__ __forceinline__ bool suppress_wide(const RecWide& ri, const RecWide& 
 }
 
 template <int R>
-__device__ __noinline__ void warp_scan_wide(const RecWide* scol, const RecWide* rec_frame, int c0, int c1, int pw,
+static __device__ __noinline__ void warp_scan_wide(const RecWide* scol, const RecWide* rec_frame, int c0, int c1, int pw,
                                             int p_end, const int32_t* lim_frame, bool (&hit)[R],
                                             const bool (&pre)[R]) {
   const int lane = threadIdx.x & 31;
@@ -278,8 +278,8 @@ template <int R>
 __global__ void __launch_bounds__(kMapWarps * 32) pnms_map_kernel_list(MapArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bar;
-  cudaGridDependencySynchronize();  // PDL: the previous kernel's results are visible after this
-  cudaTriggerProgrammaticLaunchCompletion();
+  pdl_wait();  // PDL: the previous kernel's results are visible after this
+  pdl_trigger();
   const long long n = (long long)*a.list_count * a.items_per_frame;
   for (long long it = blockIdx.x; it < n; it += gridDim.x) {
     map_item<R>(a, a.list[it / a.items_per_frame], (int)(it % a.items_per_frame), smem_raw, bar);

@@ -499,8 +499,8 @@ __global__ void __launch_bounds__(kSortThreads) pnms_prep_sort_frame(PrepArgs a)
 // its register budget)
 __global__ void __launch_bounds__(kSortThreads) pnms_prep_sort_frame_list(PrepArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  cudaGridDependencySynchronize();
-  cudaTriggerProgrammaticLaunchCompletion();
+  pdl_wait();
+  pdl_trigger();
   const int n = *a.list_count;
   for (int li = blockIdx.x; li < n; li += gridDim.x) {
     prep_sort_frame_body(a, a.list[li], smem_raw);
@@ -546,8 +546,8 @@ __global__ void __launch_bounds__(kSortThreads) pnms_prep_sort_chunk(PrepArgs a)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   if (a.list) {
     // declined-frame list (PDL after the binned kernel; the decliner zeroed each frame's meta)
-    cudaGridDependencySynchronize();
-    cudaTriggerProgrammaticLaunchCompletion();
+    pdl_wait();
+    pdl_trigger();
     const long long n = (long long)*a.list_count * a.nchunks;
     for (long long it = blockIdx.x; it < n; it += gridDim.x) {
       prep_sort_chunk_body(a, a.list[it / a.nchunks], (int)(it % a.nchunks), smem_raw);
@@ -598,8 +598,8 @@ __device__ __forceinline__ void merge_rank_body(const PrepArgs& a, int f, int bl
 __global__ void __launch_bounds__(256) pnms_merge_rank(PrepArgs a) {
   const int blocks_per_frame = (a.n_max + 255) / 256;
   if (a.list) {
-    cudaGridDependencySynchronize();
-    cudaTriggerProgrammaticLaunchCompletion();
+    pdl_wait();
+    pdl_trigger();
     const long long n = (long long)*a.list_count * blocks_per_frame;
     for (long long it = blockIdx.x; it < n; it += gridDim.x)
       merge_rank_body(a, a.list[it / blocks_per_frame], (int)(it % blocks_per_frame));
