@@ -23,8 +23,8 @@ constexpr int kTileCells = 1024;     // cells of tile + halo a CTA may hold
 
 struct TileArgs {
   BinArgs b;
-  uint32_t* mask;        // [batch][W32] survivor bits, zeroed before the launch
-  int* decline;          // [batch] set by any CTA of a frame that must go to the dense path
+  uint32_t* mask;        // [batch][W32] survivor bits: zero at entry, zeroed again by pnms_mask_compact
+  int* decline;          // [batch] set by any CTA of a frame that must go to the dense path (ditto)
 };
 
 inline size_t binned_tiles_smem_bytes() {
@@ -289,20 +289,28 @@ __global__ void __launch_bounds__(kTileThreads, 1) pnms_binned_tiles(TileArgs ta
 }
 
 // survivor mask -> ascending keep indices, count and mask output (engine.py:284-293); one CTA
-// per frame; frames flagged in `decline` are left to the dense pipeline
+// per frame; frames flagged in `decline` are left to the dense pipeline.  The mask and flag
+// live in the caller's persistent zeroed scratch: every word is zeroed again by the thread
+// that read it last, so the next call needs no memset.
 __global__ void __launch_bounds__(512) pnms_mask_compact(TileArgs ta) {
   pdl_wait();  // PDL: the tile kernel's mask is complete after this
   const BinArgs& a = ta.b;
   const int f = blockIdx.x;
   __shared__ uint32_t scan_tmp[64];
-  if (ta.decline[f]) {
-    if (threadIdx.x == 0) binned_decline(a, f);
+  uint32_t* m = ta.mask + (long long)f * a.W32;
+  const int wpt = (a.W32 + 511) / 512;
+  const int w0 = threadIdx.x * wpt, w1 = min(w0 + wpt, a.W32);
+  const int declined = ta.decline[f];
+  __syncthreads();  // every thread has the flag before thread 0 clears it
+  if (declined) {
+    for (int w = w0; w < w1; ++w) m[w] = 0u;
+    if (threadIdx.x == 0) {
+      ta.decline[f] = 0;
+      binned_decline(a, f);
+    }
     return;
   }
   const long long fbase = (long long)f * a.n_max;
-  const uint32_t* m = ta.mask + (long long)f * a.W32;
-  const int wpt = (a.W32 + 511) / 512;
-  const int w0 = threadIdx.x * wpt, w1 = min(w0 + wpt, a.W32);
   uint32_t local = 0;
   for (int w = w0; w < w1; ++w) {
     const uint32_t bits = m[w];
@@ -311,9 +319,10 @@ __global__ void __launch_bounds__(512) pnms_mask_compact(TileArgs ta) {
   }
   uint32_t total;
   uint32_t pos = block_exclusive_scan(local, scan_tmp, &total);
-  if (a.keep_idx) {
-    for (int w = w0; w < w1; ++w) {
-      uint32_t bits = m[w];
+  for (int w = w0; w < w1; ++w) {
+    uint32_t bits = m[w];
+    m[w] = 0u;
+    if (a.keep_idx) {
       while (bits) {
         a.keep_idx[fbase + pos++] = w * 32 + __ffs(bits) - 1;
         bits &= bits - 1;

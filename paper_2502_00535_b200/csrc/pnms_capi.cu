@@ -384,6 +384,9 @@ MapShape choose_map_shape(int batch, int n_max) {
 // (pnms_workspace_init), after the small path's words; every call leaves it zero
 constexpr size_t kDeclCountOffset = kSmallMaxWords * 4 + kSmallMaxFrames * 4 + kSmallMaxFrames * 8;
 static_assert(kDeclCountOffset + 4 <= kSmallScratchBytes, "scratch");
+// the tile path's decline flags and survivor masks, re-zeroed by pnms_mask_compact
+constexpr size_t kTilesScratchOffset = 32 * 1024;
+static_assert(kDeclCountOffset + 4 <= kTilesScratchOffset, "scratch");
 
 
 template <int R>
@@ -647,6 +650,27 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
   };
   const size_t compact_smem = ((size_t)W32 + 3) / 4 * 16 + 64 * 4;
   const size_t map_smem = (size_t)ms.chunk * kRecBytes;
+  // one-CTA dispatcher behind a declining kernel (pnms_fallback.cuh): snapshots the declined
+  // count into `snap`, zeroes it and, when frames were declined, tail-launches the dense chain
+  // over them; `*host_chain` is set when the host must launch the chain itself (profiled calls)
+  auto dispatch_fallback = [&](const int32_t* list, int* count, int* snap, bool* host_chain) -> cudaError_t {
+    FallbackPlan plan{};
+    chain_args(0, batch, ws + L.dense, list, snap, plan.pa, plan.ma, plan.ca);
+    plan.chunked = n_max > kSortMax;
+    plan.map_R = ms.R;
+    plan.sort_smem = (int)(plan.chunked ? sort_smem_bytes(kSortMax) : sort_frame_smem_bytes(plan.pa.npad));
+    plan.map_smem = (int)map_smem;
+    plan.compact_smem = (int)compact_smem;
+    plan.enabled = events == nullptr && env_int("PNMS_DEVCHAIN", 1) != 0;  // 0: host chain (debug)
+    static const bool same_layout = pnms_devchain_plan_size() == sizeof(FallbackPlan);
+    if (!same_layout) return cudaErrorInvalidValue;
+    cudaError_t err;
+    if (plan.enabled &&
+        (err = pnms_devchain_prepare(plan.chunked, ms.R, plan.sort_smem, map_smem, compact_smem)) != cudaSuccess)
+      return err;
+    *host_chain = !plan.enabled;
+    return pnms_devchain_dispatch(&plan, count, snap, st);
+  };
 
   // ---- binned path (sparse frames): exact, one CTA per frame; declined frames fall through
   // to the dense pipeline below, which then only processes those frames.
@@ -692,23 +716,10 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     decl_count = ba.decl_count;
     if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
     if (!pairs) {
-      // one-CTA dispatcher: snapshots and zeroes the count and, when frames were declined,
-      // tail-launches the dense chain over them (unless the host launches it: profiled calls)
-      FallbackPlan plan{};
       int* snap = reinterpret_cast<int*>(ws + L.list);
-      chain_args(0, batch, ws + L.dense, ba.decl_list, snap, plan.pa, plan.ma, plan.ca);
-      plan.map_R = ms.R;
-      plan.sort_smem = (int)sort_frame_smem_bytes(plan.pa.npad);
-      plan.map_smem = (int)map_smem;
-      plan.compact_smem = (int)compact_smem;
-      plan.enabled = events == nullptr && env_int("PNMS_DEVCHAIN", 1) != 0;  // 0: host chain (debug)
-      static const bool same_layout = pnms_devchain_plan_size() == sizeof(FallbackPlan);
-      if (!same_layout) return fail_cuda(cudaErrorInvalidValue);
-      if (plan.enabled &&
-          (e = pnms_devchain_prepare(ms.R, plan.sort_smem, map_smem, compact_smem)) != cudaSuccess)
-        return fail_cuda(e);
-      if ((e = pnms_devchain_dispatch(&plan, ba.decl_count, snap, st)) != cudaSuccess) return fail_cuda(e);
-      if (plan.enabled) return PNMS_OK;
+      bool host_chain = false;
+      if ((e = dispatch_fallback(ba.decl_list, ba.decl_count, snap, &host_chain)) != cudaSuccess) return fail_cuda(e);
+      if (!host_chain) return PNMS_OK;
       decl_count = snap;
     }
     dense_flags = ws + L.dense;
@@ -728,7 +739,7 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     ba.batch = batch; ba.n_max = n_max; ba.d_max = d_max; ba.tie_break = tie_break; ba.W32 = W32;
     ba.theta = theta;
     ba.fallback = ws + L.dense;
-    ba.decl_count = reinterpret_cast<int*>(ws + L.list);
+    ba.decl_count = reinterpret_cast<int*>(ws + kDeclCountOffset);  // zeroed scratch (dispatcher)
     ba.decl_list = reinterpret_cast<int32_t*>(ws + L.list) + 1;
     ba.keep_idx = keep_idx; ba.keep_count = keep_count; ba.keep_mask = keep_mask;
     ba.pairs_tested = nullptr;
@@ -739,15 +750,19 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     const bool cluster_ok = cluster_slice(n_max, 16) > 0 && cluster_slice(n_max, cluster_size_for(n_max)) > 0;
     const bool tiles = n_max <= 65536 && (large == 1 || (large == 0 && (batch <= 2 || !cluster_ok)));
     if (tiles || cluster_ok) {
-      if ((e = cudaMemsetAsync(ba.decl_count, 0, sizeof(int), st)) != cudaSuccess) return fail_cuda(e);
       if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
       if (tiles) {
         TileArgs ta;
         ta.b = ba;
-        ta.decline = reinterpret_cast<int*>(ws + L.tiles);
-        ta.mask = reinterpret_cast<uint32_t*>(ws + L.tiles) + batch;
-        if ((e = cudaMemsetAsync(ws + L.tiles, 0, (size_t)batch * 4 + (size_t)batch * W32 * 4, st)) != cudaSuccess)
-          return fail_cuda(e);
+        // decline flags and survivor masks in the zeroed scratch (pnms_mask_compact re-zeroes
+        // them) when they fit — the latency case, <= 2 frames — else zeroed per call
+        const size_t fbytes = ((size_t)batch * 4 + 15) / 16 * 16;
+        const size_t tbytes = fbytes + (size_t)batch * W32 * 4;
+        const bool in_scratch = kTilesScratchOffset + tbytes <= kSmallScratchBytes;
+        uint8_t* tbase = in_scratch ? ws + kTilesScratchOffset : ws + L.tiles;
+        ta.decline = reinterpret_cast<int*>(tbase);
+        ta.mask = reinterpret_cast<uint32_t*>(tbase + fbytes);
+        if (!in_scratch && (e = cudaMemsetAsync(tbase, 0, tbytes, st)) != cudaSuccess) return fail_cuda(e);
         static std::atomic<size_t> tcfg[2];
         const size_t tsmem = binned_tiles_smem_bytes();
         const bool bi = tie_break == PNMS_TIE_BY_INDEX;
@@ -764,7 +779,11 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
           return fail_cuda(e);
       }
       decl_list = ba.decl_list;
-      decl_count = ba.decl_count;
+      int* snap = reinterpret_cast<int*>(ws + L.list);
+      bool host_chain = false;
+      if ((e = dispatch_fallback(ba.decl_list, ba.decl_count, snap, &host_chain)) != cudaSuccess) return fail_cuda(e);
+      if (!host_chain) return PNMS_OK;
+      decl_count = snap;
       dense_flags = ws + L.dense;
       if (events) {
         ev_local[0] = events[1]; ev_local[1] = events[2]; ev_local[2] = nullptr; ev_local[3] = events[3];

@@ -24,9 +24,10 @@ cudaError_t ensure_smem_dc(Kernel kernel, size_t bytes, std::atomic<size_t>& con
 
 size_t pnms_devchain_plan_size() { return sizeof(pnms_dc::FallbackPlan); }
 
-cudaError_t pnms_devchain_prepare(int map_R, int sort_smem, size_t map_smem, size_t compact_smem) {
-  static std::atomic<size_t> scfg{0}, mcfg[5], ccfg{0};
-  cudaError_t e = ensure_smem_dc(pnms_dc::pnms_prep_sort_frame_list, (size_t)sort_smem, scfg);
+cudaError_t pnms_devchain_prepare(int chunked, int map_R, int sort_smem, size_t map_smem, size_t compact_smem) {
+  static std::atomic<size_t> scfg{0}, kcfg{0}, mcfg[5], ccfg{0};
+  cudaError_t e = chunked ? ensure_smem_dc(pnms_dc::pnms_prep_sort_chunk, (size_t)sort_smem, kcfg)
+                          : ensure_smem_dc(pnms_dc::pnms_prep_sort_frame_list, (size_t)sort_smem, scfg);
   if (e != cudaSuccess) return e;
   if (map_R == 4) e = ensure_smem_dc(pnms_dc::pnms_map_kernel_list<4>, map_smem, mcfg[4]);
   else if (map_R == 2) e = ensure_smem_dc(pnms_dc::pnms_map_kernel_list<2>, map_smem, mcfg[2]);

@@ -9,7 +9,8 @@
 
 PNMS_INTERNAL size_t pnms_devchain_plan_size();
 // dynamic shared memory limits of the list kernels the dispatcher may tail-launch
-PNMS_INTERNAL cudaError_t pnms_devchain_prepare(int map_R, int sort_smem, size_t map_smem, size_t compact_smem);
+PNMS_INTERNAL cudaError_t pnms_devchain_prepare(int chunked, int map_R, int sort_smem, size_t map_smem,
+                                                size_t compact_smem);
 // pnms_fallback_dispatch<<<1, 32>>> behind the binned kernel (programmatic dependent launch);
 // `plan` points at a FallbackPlan
 PNMS_INTERNAL cudaError_t pnms_devchain_dispatch(const void* plan, int* decl_count, int* count_snap,

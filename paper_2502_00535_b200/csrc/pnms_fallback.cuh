@@ -30,6 +30,7 @@ struct FallbackPlan {
   CompactArgs ca;
   int map_R;        // 1, 2 or 4 rows per lane (choose_map_shape)
   int sort_smem, map_smem, compact_smem;
+  int chunked;      // frames > kSortMax slots: chunk sorts + merge rank instead of the frame sort
   int enabled;      // 0: the host launches the chain itself (profiled calls), reading the snapshot
 };
 
@@ -45,7 +46,14 @@ __global__ void __launch_bounds__(32) pnms_fallback_dispatch(FallbackPlan plan, 
   *decl_count = 0;
   *count_snap = c;
   if (c == 0 || !plan.enabled) return;
-  pnms_prep_sort_frame_list<<<min(c, 148 * 2), kSortThreads, plan.sort_smem, cudaStreamTailLaunch>>>(plan.pa);
+  if (plan.chunked) {
+    const long long chunks = (long long)c * plan.pa.nchunks;
+    pnms_prep_sort_chunk<<<(int)min(chunks, 148LL * 2), kSortThreads, plan.sort_smem, cudaStreamTailLaunch>>>(plan.pa);
+    const long long blocks = (long long)c * ((plan.pa.n_max + 255) / 256);
+    pnms_merge_rank<<<(int)min(blocks, 148LL * 8), 256, 0, cudaStreamTailLaunch>>>(plan.pa);
+  } else {
+    pnms_prep_sort_frame_list<<<min(c, 148 * 2), kSortThreads, plan.sort_smem, cudaStreamTailLaunch>>>(plan.pa);
+  }
   const int map_grid = (int)min((long long)c * plan.ma.items_per_frame, 148LL * 8);
   if (plan.map_R == 4)
     pnms_map_kernel_list<4><<<map_grid, kMapWarps * 32, plan.map_smem, cudaStreamTailLaunch>>>(plan.ma);
