@@ -514,7 +514,9 @@ def main():
                     "h2d_link_gbs": h2d_gbs, "link_bound_frames_per_s": world * F / (copy_ms / 1e3),
                     "frac_of_link_bound": e2e_value / (world * F / (copy_ms / 1e3)),
                     "link_bound_basis": "the step's input planes copied host->device alone (no compute), best of 5"},
-            "gpu_launches": 4 * args.steps,  # binned kernel + 3 fallback kernels over the declined list
+            # binned kernel + the one-CTA fallback dispatcher (the dense chain is tail-launched from the
+            # device only for declined frames; none in this workload)
+            "gpu_launches": 2 * args.steps,
             # the dominant kernel against the HBM roofline: algorithmic bytes per launch (SURVEY.md
             # §8d) = 20 B per slot read (x, y, z int32 + s float64) + 4 B per survivor index written
             "roofline": {"bound": "hbm", "achieved": hbm_bytes / b_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
