@@ -679,7 +679,13 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
   const int* decl_count = nullptr;
   void* ev_local[4];
   const long long algo = env_ll("PNMS_ALGO", 0);  // 0 auto, 1 dense only
-  if (algo == 0 && gate_pairs == nullptr && n_max <= kBinMaxSlots) {
+  // calls of <= 2 frames of 2049..4096 slots that the single-launch path did not take run on
+  // the multi-CTA tile path instead of one CTA per frame (measured, tools/single_frame_paths.py:
+  // a 4096-box random frame 22 us on tiles against 52 us on one CTA; PNMS_TILES_SMALL = the
+  // slot threshold, 0 disables)
+  const int tiles_small_env = env_int("PNMS_TILES_SMALL", 2048);
+  const bool tiles_small = tiles_small_env > 0 && batch <= 2 && n_max > tiles_small_env && n_max <= kBinMaxSlots;
+  if (algo == 0 && gate_pairs == nullptr && n_max <= kBinMaxSlots && !tiles_small) {
     const bool pairs = env_int("PNMS_BINNED", 0) == 2;
     BinArgs ba{};
     ba.x = x; ba.y = y; ba.z = z; ba.s = s; ba.counts = counts;
@@ -730,7 +736,7 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     }
   }
 
-  if (!dense_flags && algo == 0 && gate_pairs == nullptr && n_max > kBinMaxSlots) {
+  if (!dense_flags && algo == 0 && gate_pairs == nullptr && (n_max > kBinMaxSlots || tiles_small)) {
     // large frames: few frames -> kTilesPerFrame independent tile CTAs per frame
     // (pnms_binned_tiles.cuh, latency); many frames -> one thread-block cluster per frame
     // (pnms_binned_cluster.cuh, throughput).  Declined frames go to the dense pipeline by list.
@@ -748,7 +754,8 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     ba.meta = reinterpret_cast<FrameMeta*>(ws + L.meta);  // the chunked sort accumulates into it
     const int large = env_int("PNMS_LARGE", 0);  // 0 auto, 1 tiles, 2 cluster
     const bool cluster_ok = cluster_slice(n_max, 16) > 0 && cluster_slice(n_max, cluster_size_for(n_max)) > 0;
-    const bool tiles = n_max <= 65536 && (large == 1 || (large == 0 && (batch <= 2 || !cluster_ok)));
+    const bool tiles = tiles_small ||
+                       (n_max <= 65536 && (large == 1 || (large == 0 && (batch <= 2 || !cluster_ok))));
     if (tiles || cluster_ok) {
       if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
       if (tiles) {

@@ -27,6 +27,7 @@ def path(request, monkeypatch):
     monkeypatch.setenv("PNMS_SMALL_PAIRS", str(1 << 40) if request.param == "small" else "0")
     monkeypatch.setenv("PNMS_ALGO", "1" if request.param == "dense" else "0")
     monkeypatch.setenv("PNMS_BINNED", "2" if request.param == "binned_pairs" else "0")
+    monkeypatch.setenv("PNMS_TILES_SMALL", "0")  # one CTA per frame (the tile path has its own tests)
     return request.param
 
 
@@ -157,6 +158,31 @@ def test_binned_mixed_batch_vs_oracle(monkeypatch):
     finally:
         _lib.load().pnms_debug_count_pairs(None)
     assert int(counter.item()) > 0  # the binned kernel did run
+
+
+@pytest.mark.parametrize("tie", ["paper_faithful", "by_index"])
+def test_tile_path_small_calls_vs_oracle(golden_configs, tie, monkeypatch):
+    """Calls of <= 2 frames of 2049..4096 slots that skip the single-launch path run on the
+    multi-CTA tile path (default PNMS_TILES_SMALL): golden C2, random and ragged pairs, a
+    declined frame (crowded cell) finished by the device-side fallback."""
+    monkeypatch.setenv("PNMS_SMALL_PAIRS", "0")
+    monkeypatch.delenv("PNMS_TILES_SMALL", raising=False)
+    g = golden_configs["C2"]
+    n = len(g["x"])
+    if tie == "paper_faithful":
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a).reshape(1, n)).to(DEV)  # noqa: E731
+        ki, kc = batched_nms_keep(t(g["x"]), t(g["y"]), t(g["z"]), t(g["s"]), None, 0.5)
+        assert np.array_equal(ki[0, : int(kc.item())].cpu().numpy(), g["keep"])
+    for n, counts in ((2049, [2049]), (3000, [3000, 2500]), (4096, [4096, 4096])):
+        B = len(counts)
+        x, y, z, s = random_frames(B, n, seed=n, z_range=(4, 80), duplicate_fraction=0.05)
+        if B == 2 and n == 4096:
+            x[1, :500] = 30; y[1, :500] = 40   # a crowded cell: declined, dense fallback
+        cnt = np.array(counts, np.int32)
+        got = _run_batch(x, y, z, s, cnt, 0.45, tie, n)
+        for f in range(B):
+            want = c_oracle.run_frame(x[f], y[f], z[f], s[f], int(cnt[f]), n, 0.45, tie)
+            assert np.array_equal(got[f], want), (n, f, tie)
 
 
 @pytest.mark.parametrize("cell", ["0", "-1", "-3", "-7", "-33", "-200", "64", "256", "400"])

@@ -19,9 +19,16 @@ top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", str(ROOT / "paper_2502_00535_b200" / "libparnms_b200.so")], cwd=tmp,
                capture_output=True)
-cubin = glob.glob(tmp + "/*.cubin")[0]
-dis = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout.splitlines()
-start = [i for i, l in enumerate(dis) if l.startswith("//---") and fun in l][0]
+# the library holds several device modules (whole-program unit, relocatable unit): find the one
+# with the kernel
+for cubin in sorted(glob.glob(tmp + "/*.cubin")):
+    dis = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout.splitlines()
+    hits = [i for i, l in enumerate(dis) if l.startswith("//---") and fun in l]
+    if hits:
+        start = hits[0]
+        break
+else:
+    sys.exit(f"{fun} not found in the library's device modules")
 cur, seq = None, []
 for l in dis[start + 1:]:
     if l.startswith("//---"):
