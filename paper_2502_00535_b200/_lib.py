@@ -7,9 +7,12 @@ point raises — there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libparnms_b200.so"
+# PNMS_LIB selects another build of the library (diagnostics: the no-dynamic-parallelism
+# variant build_tmp/libparnms_b200_nocdp.so for compute-sanitizer's racecheck/synccheck/initcheck)
+LIB_PATH = Path(os.environ.get("PNMS_LIB") or Path(__file__).resolve().parent / "libparnms_b200.so")
 
 # every symbol include/parnms_b200.h declares
 EXPORTED_SYMBOLS = (

@@ -16,6 +16,7 @@ REPO_DIR = PKG_DIR.parent
 CSRC = PKG_DIR / "csrc"
 LIB_NAME = "libparnms_b200.so"
 LIB_PATH = PKG_DIR / LIB_NAME
+NOCDP_PATH = PKG_DIR / "build_tmp" / "libparnms_b200_nocdp.so"  # diagnostics only (see build())
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -38,7 +39,7 @@ def sources() -> list[Path]:
 
 
 def needs_build() -> bool:
-    if not LIB_PATH.exists():
+    if not LIB_PATH.exists() or not NOCDP_PATH.exists():
         return True
     built = LIB_PATH.stat().st_mtime
     return any(p.stat().st_mtime > built for p in sources())
@@ -53,23 +54,32 @@ def build(force: bool = False, verbose: bool = False, extra: list[str] | None = 
     # register budgets); nvcc device-links the relocatable object into the shared library
     tmp = LIB_PATH.parent / "build_tmp"
     tmp.mkdir(exist_ok=True)
-    steps = [
+    # (+ a diagnostic variant without the relocatable unit, NOCDP_PATH: compute-sanitizer's
+    # racecheck / synccheck / initcheck do not support dynamic parallelism)
+    compiles = [
         [_nvcc(), *NVCC_FLAGS, *(extra or []), "-rdc=true", "-c", "-o", str(tmp / "devchain.o"),
          str(CSRC / "pnms_devchain.cu")],
         [_nvcc(), *NVCC_FLAGS, *(extra or []), "-c", "-o", str(tmp / "capi.o"), str(CSRC / "pnms_capi.cu")],
+        [_nvcc(), *NVCC_FLAGS, *(extra or []), "-DPNMS_NO_DEVCHAIN", "-c", "-o", str(tmp / "capi_nocdp.o"),
+         str(CSRC / "pnms_capi.cu")],
+    ]
+    links = [
         [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static", "-shared",
          "-o", str(LIB_PATH) + ".tmp", str(tmp / "capi.o"), str(tmp / "devchain.o"), "-lcudadevrt"],
+        [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static", "-shared",
+         "-o", str(NOCDP_PATH), str(tmp / "capi_nocdp.o")],
     ]
     if verbose:
-        for cmd in steps:
+        for cmd in compiles + links:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), file=sys.stderr)
-    compiles = [subprocess.Popen(cmd) for cmd in steps[:2]]  # the two units compile in parallel
-    for cmd, proc in zip(steps[:2], compiles):
+    procs = [subprocess.Popen(cmd) for cmd in compiles]  # the units compile in parallel
+    for cmd, proc in zip(compiles, procs):
         if proc.wait() != 0:
             raise subprocess.CalledProcessError(proc.returncode, cmd)
-    subprocess.run(steps[2], check=True)
-    for obj in ("devchain.o", "capi.o"):
+    for cmd in links:
+        subprocess.run(cmd, check=True)
+    for obj in ("devchain.o", "capi.o", "capi_nocdp.o"):
         (tmp / obj).unlink(missing_ok=True)
     os.replace(str(LIB_PATH) + ".tmp", LIB_PATH)
     return LIB_PATH

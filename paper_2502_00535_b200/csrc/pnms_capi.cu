@@ -380,6 +380,16 @@ MapShape choose_map_shape(int batch, int n_max) {
   return m;
 }
 
+// when the host launches the fallback chain (profiled calls, PNMS_DEVCHAIN=0): the declined
+// count is snapshotted for the chain and zeroed for the next call, as the dispatcher does
+__global__ void pnms_count_snapshot(int* count, int* snap) {
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    *snap = *count;
+    *count = 0;
+  }
+}
+
 // the binned path's declined-frame count lives in the persistent zeroed scratch
 // (pnms_workspace_init), after the small path's words; every call leaves it zero
 constexpr size_t kDeclCountOffset = kSmallMaxWords * 4 + kSmallMaxFrames * 4 + kSmallMaxFrames * 8;
@@ -661,15 +671,23 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     plan.sort_smem = (int)(plan.chunked ? sort_smem_bytes(kSortMax) : sort_frame_smem_bytes(plan.pa.npad));
     plan.map_smem = (int)map_smem;
     plan.compact_smem = (int)compact_smem;
+#ifdef PNMS_NO_DEVCHAIN  // diagnostic build without the relocatable unit (sanitizer tools)
+    plan.enabled = 0;
+#else
     plan.enabled = events == nullptr && env_int("PNMS_DEVCHAIN", 1) != 0;  // 0: host chain (debug)
+#endif
+    *host_chain = !plan.enabled;
+    if (!plan.enabled)  // snapshot + zero only; the host launches the chain over `snap`
+      return launch_maybe_pdl(true, pnms_count_snapshot, dim3(1), dim3(32), 0, st, count, snap);
+#ifndef PNMS_NO_DEVCHAIN
     static const bool same_layout = pnms_devchain_plan_size() == sizeof(FallbackPlan);
     if (!same_layout) return cudaErrorInvalidValue;
-    cudaError_t err;
-    if (plan.enabled &&
-        (err = pnms_devchain_prepare(plan.chunked, ms.R, plan.sort_smem, map_smem, compact_smem)) != cudaSuccess)
-      return err;
-    *host_chain = !plan.enabled;
+    cudaError_t err = pnms_devchain_prepare(plan.chunked, ms.R, plan.sort_smem, map_smem, compact_smem);
+    if (err != cudaSuccess) return err;
     return pnms_devchain_dispatch(&plan, count, snap, st);
+#else
+    return cudaSuccess;
+#endif
   };
 
   // ---- binned path (sparse frames): exact, one CTA per frame; declined frames fall through
