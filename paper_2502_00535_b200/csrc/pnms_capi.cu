@@ -382,10 +382,10 @@ MapShape choose_map_shape(int batch, int n_max) {
 
 // when the host launches the fallback chain (profiled calls, PNMS_DEVCHAIN=0): the declined
 // count is snapshotted for the chain and zeroed for the next call, as the dispatcher does
-__global__ void pnms_count_snapshot(int* count, int* snap) {
+__global__ void pnms_count_snapshot(int* count, int* snap, int batch) {
   pdl_wait();
   if (threadIdx.x == 0) {
-    *snap = *count;
+    *snap = min(max(*count, 0), batch);
     *count = 0;
   }
 }
@@ -678,7 +678,7 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
 #endif
     *host_chain = !plan.enabled;
     if (!plan.enabled)  // snapshot + zero only; the host launches the chain over `snap`
-      return launch_maybe_pdl(true, pnms_count_snapshot, dim3(1), dim3(32), 0, st, count, snap);
+      return launch_maybe_pdl(true, pnms_count_snapshot, dim3(1), dim3(32), 0, st, count, snap, batch);
 #ifndef PNMS_NO_DEVCHAIN
     static const bool same_layout = pnms_devchain_plan_size() == sizeof(FallbackPlan);
     if (!same_layout) return cudaErrorInvalidValue;

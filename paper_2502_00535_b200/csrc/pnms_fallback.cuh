@@ -42,8 +42,8 @@ struct FallbackPlan {
 __global__ void __launch_bounds__(32) pnms_fallback_dispatch(FallbackPlan plan, int* decl_count, int* count_snap) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the binned grid is complete and flushed
   if (threadIdx.x != 0) return;
-  const int c = *decl_count;
-  *decl_count = 0;
+  const int c = min(max(*decl_count, 0), plan.pa.batch);  // a workspace that was not zeroed
+  *decl_count = 0;                                          // cannot send the chain out of range
   *count_snap = c;
   if (c == 0 || !plan.enabled) return;
   if (plan.chunked) {
