@@ -60,6 +60,7 @@ struct BinArgs {
   unsigned long long* pairs_tested;  // optional device counter (diagnostics), may be null
   unsigned long long* trace;         // optional per-CTA phase timestamps (diagnostics), may be null
   int cell_q8;                       // frame kernel cell side: 0 default, > 0 scale, < 0 absolute
+  int cell_sx;                       // frame kernel: > 0 overrides the cell width
 };
 
 struct __align__(16) BinStats {
@@ -237,31 +238,38 @@ __device__ __forceinline__ bool binned_frame_body(const BinArgs& a) {
     if (threadIdx.x == 0) binned_decline(a, f);
     return true;
   }
-  // ---- grid of square cells, side >= max side + 1
-  // Cell side: any S >= 1 is exact (the reachable range below is [x - max_z, x + z]); the
-  // default is the power of two nearest (max_z + 1) / 2 — measured on BASELINE config 5
-  // (max_z = 64): S = 32 costs 0.68 ms against 0.76 ms at S = 65 (fewer columns scanned per
-  // row, more runs); 28, 33 and 36 land at 0.71-0.73 ms.  cell_q8 > 0 scales (max_z + 1) by
-  // cell_q8 / 256 instead, < 0 sets S = -cell_q8 (tuning).
-  int S;
+  // ---- grid of cells, Sx wide and Sy tall.  Any sides are exact (a column that can suppress
+  // row i has its corner in [x_i - max_z, x_i + z_i] x [y_i - max_z, y_i + z_i]).  A row scans
+  // one contiguous run of cells per cell row it reaches, so narrow cells tighten the x range at
+  // no cost in runs while tall cells cut the runs per row.  Default: Sy = the power of two
+  // nearest max_z + 1, Sx = Sy / 4 — measured on BASELINE config 5 (max_z = 64, 2048 boxes of
+  // 1920x1080): 16 x 64 cells 0.65 ms, 12 x 64 0.645, 24 x 64 0.66, 16 x 48 0.70, 16 x 80 0.74,
+  // 32 x 32 0.68, 65 x 65 (3x3 neighbourhoods) 0.76 (tools/env_sweep.py PNMS_CELL_SX ...).
+  // Tuning: cell_q8 < 0 sets square cells of side -cell_q8, > 0 scales (max_z + 1) by
+  // cell_q8 / 256 for both; cell_sx > 0 then overrides the width.
+  int Sx, Sy;
   if (a.cell_q8 == 0) {
-    const int h = st->maxz + 1, half = max(h >> 1, 1);
-    const int p2 = 1 << (31 - __clz(half));
-    S = (long long)h * h > 8LL * p2 * p2 ? 2 * p2 : p2;
+    const int h = st->maxz + 1;
+    const int p2 = 1 << (31 - __clz(h));
+    Sy = (long long)h * h > 2LL * p2 * p2 ? 2 * p2 : p2;
+    Sx = max(Sy >> 2, 1);
   } else {
-    S = a.cell_q8 < 0 ? -a.cell_q8 : max(1, ((st->maxz + 1) * a.cell_q8 + 255) >> 8);
+    Sy = a.cell_q8 < 0 ? -a.cell_q8 : max(1, ((st->maxz + 1) * a.cell_q8 + 255) >> 8);
+    Sx = Sy;
   }
+  if (a.cell_sx > 0) Sx = a.cell_sx;
   int GX = 1, GY = 1;
   const int ox = st->minx, oy = st->miny;
   if (n_act > 0) {
     for (;;) {
-      GX = (st->maxx - ox) / S + 1;
-      GY = (st->maxy - oy) / S + 1;
+      GX = (st->maxx - ox) / Sx + 1;
+      GY = (st->maxy - oy) / Sy + 1;
       if ((long long)GX * GY <= max_cells) break;
-      S *= 2;
+      if (Sx < Sy) Sx *= 2;  // too many cells: widen first, then grow both
+      else { Sx *= 2; Sy *= 2; }
     }
   }
-  const uint32_t M = div_magic(S);
+  const uint32_t Mx = div_magic(Sx), My = div_magic(Sy);
   const int cells = GX * GY;
   for (int c = threadIdx.x; c < cells + 1; c += THREADS) cstart[c] = 0u;
   __syncthreads();
@@ -271,7 +279,7 @@ __device__ __forceinline__ bool binned_frame_body(const BinArgs& a) {
   for (int k = 0; k < PER; ++k) {
     if (zc[k] != 0xFFFFFFFFu) {
       const int ex = (int)(xy[k] & 0xFFFFu), ey = (int)(xy[k] >> 16);
-      const int c = qdiv(ey - oy, M) * GX + qdiv(ex - ox, M);
+      const int c = qdiv(ey - oy, My) * GX + qdiv(ex - ox, Mx);
       const uint32_t r = atomicAdd(&cstart[c], 1u);
       zc[k] |= ((uint32_t)c << 16) | (min(r, 255u) << 8);
     }
@@ -382,8 +390,8 @@ __device__ __forceinline__ bool binned_frame_body(const BinArgs& a) {
     // corner and side back from the packed record: nb = (-x, -y)
     const int32_t ix = -(int32_t)(int16_t)(ri.nb & 0xFFFFu), iy = -(int32_t)(int16_t)(ri.nb >> 16);
     const int32_t iz = (int32_t)(ri.w & 0xFF) - 1;
-    const int cx0 = qdiv(max(ix - maxz - ox, 0), M), cy0 = qdiv(max(iy - maxz - oy, 0), M);
-    const int cx1 = min(GX - 1, qdiv(ix + iz - ox, M)), cy1 = min(GY - 1, qdiv(iy + iz - oy, M));
+    const int cx0 = qdiv(max(ix - maxz - ox, 0), Mx), cy0 = qdiv(max(iy - maxz - oy, 0), My);
+    const int cx1 = min(GX - 1, qdiv(ix + iz - ox, Mx)), cy1 = min(GY - 1, qdiv(iy + iz - oy, My));
     const uint32_t pb = rbase + (uint32_t)p * (uint32_t)sizeof(RecBin);
     bool sup = false;
     for (int yy = cy0; yy <= cy1 && !sup; ++yy) {

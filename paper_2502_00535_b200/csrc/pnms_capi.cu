@@ -721,6 +721,7 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     ba.pairs_tested = g_pairs_counter;
     ba.trace = g_trace;
     ba.cell_q8 = env_int("PNMS_CELL_Q8", 0);
+    ba.cell_sx = env_int("PNMS_CELL_SX", 0);
     ba.meta = nullptr;  // the frame-level sort rewrites FrameMeta of declined frames
     const size_t smem = binned_smem_bytes(binned_npad(n_max));
     if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
@@ -769,6 +770,7 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     ba.pairs_tested = nullptr;
     ba.trace = g_trace;
     ba.cell_q8 = env_int("PNMS_CELL_Q8", 0);
+    ba.cell_sx = env_int("PNMS_CELL_SX", 0);
     ba.meta = reinterpret_cast<FrameMeta*>(ws + L.meta);  // the chunked sort accumulates into it
     const int large = env_int("PNMS_LARGE", 0);  // 0 auto, 1 tiles, 2 cluster
     const bool cluster_ok = cluster_slice(n_max, 16) > 0 && cluster_slice(n_max, cluster_size_for(n_max)) > 0;

@@ -185,14 +185,18 @@ def test_tile_path_small_calls_vs_oracle(golden_configs, tie, monkeypatch):
             assert np.array_equal(got[f], want), (n, f, tie)
 
 
-@pytest.mark.parametrize("cell", ["0", "-1", "-3", "-7", "-33", "-200", "64", "256", "400"])
+@pytest.mark.parametrize("cell", ["0", "-1", "-3", "-7", "-33", "-200", "64", "256", "400",
+                                  "-64/16", "-32/5", "-8/128", "-1/2", "0/1"])
 def test_binned_cell_side_invariance(cell, monkeypatch):
-    """Any cell side is exact (pnms_binned.cuh header): tiny cells (many runs per row, cell
-    grids that double until they fit), the default power of two, 3x3 neighbourhoods and cells
-    larger than the frame give the oracle's survivors, with ties, NaNs and ragged counts."""
+    """Any cell shape is exact (pnms_binned.cuh): tiny cells (many runs per row, cell grids
+    that grow until they fit), the default 16 x 64, squares, wide and tall rectangles and cells
+    larger than the frame give the oracle's survivors, with ties, NaNs and ragged counts.
+    `cell` is PNMS_CELL_Q8[/PNMS_CELL_SX]."""
     monkeypatch.setenv("PNMS_SMALL_PAIRS", "0")
     monkeypatch.setenv("PNMS_ALGO", "0")
-    monkeypatch.setenv("PNMS_CELL_Q8", cell)
+    q8, _, sx = cell.partition("/")
+    monkeypatch.setenv("PNMS_CELL_Q8", q8)
+    monkeypatch.setenv("PNMS_CELL_SX", sx or "0")
     x, y, z, s = random_frames(6, 1500, seed=77, frame_w=1280, frame_h=720, z_range=(3, 90), duplicate_fraction=0.1)
     s[1, ::5] = np.nan
     s[2, ::3] = 0.25
