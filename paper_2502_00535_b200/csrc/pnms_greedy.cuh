@@ -110,26 +110,30 @@ __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a
   __syncthreads();
   // ---- spatial cells (exact for greedy at any theta: zero overlap never covers)
   bool bin = s_stat[5] != 0 && cnt > 0;
-  int S = 1, GX = 1, GY = 1;
-  float inv_gx = 1.0f;  // 1/GX: cell row of a cell id without an integer division (exact, ids < 2^12)
-  const int ox = s_stat[0], oy = s_stat[1];
+  // cells Sx wide and Sy tall (any shape is exact: a box's coverers have their corner in
+  // [x - max_z, x + z] x [y - max_z, y + z]); narrow cells tighten the x range of a scan,
+  // tall ones keep the cell rows per scan few (as in pnms_binned.cuh)
+  int Sx = 1, Sy = 1, GX = 1, GY = 1;
+  const int ox = s_stat[0], oy = s_stat[1], maxz = s_stat[4];
   if (bin) {
-    S = s_stat[4] + 1;
-    if (S <= 0) bin = false;  // z = INT_MAX
+    Sy = s_stat[4] + 1;
+    if (Sy <= 0) bin = false;  // z = INT_MAX
+    Sx = max(Sy >> 2, 1);
   }
   if (bin) {
     for (;;) {
-      GX = (int)(((long long)s_stat[2] - ox) / S + 1);
-      GY = (int)(((long long)s_stat[3] - oy) / S + 1);
+      GX = (int)(((long long)s_stat[2] - ox) / Sx + 1);
+      GY = (int)(((long long)s_stat[3] - oy) / Sy + 1);
       if ((long long)GX * GY <= max_cells) break;
-      if (S > (1 << 29)) { GX = GY = 1; break; }
-      S *= 2;
+      if (Sy > (1 << 29)) { GX = GY = 1; break; }
+      if (Sx < Sy) Sx *= 2;
+      else { Sx *= 2; Sy *= 2; }
     }
     const int cells = GX * GY;
     for (int c = threadIdx.x; c <= cells; c += kGreedyThreads) cstart[c] = 0u;
     __syncthreads();
     for (int e = threadIdx.x; e < cnt; e += kGreedyThreads) {
-      const int c = (int)(((long long)sy[e] - oy) / S) * GX + (int)(((long long)sx[e] - ox) / S);
+      const int c = (int)(((long long)sy[e] - oy) / Sy) * GX + (int)(((long long)sx[e] - ox) / Sx);
       cellof[e] = (uint16_t)c;
       atomicAdd(&cstart[c], 1u);
     }
@@ -153,7 +157,6 @@ __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a
     }
     __syncthreads();
     bin = s_stat[6] <= kGreedyCellMax;
-    inv_gx = 1.0f / (float)GX;
     if (bin) {
       // scatter with cstart as the cursor: afterwards cstart[c] = end(c) = start(c+1)
       for (int e = threadIdx.x; e < cnt; e += kGreedyThreads) {
@@ -180,22 +183,23 @@ __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a
       const int32_t jx = sx[j], jy = sy[j], jz = sz[j];
       bool kept_cov = false, undec_cov = false;
       if (bin) {
-        const int cc = cellof[j];
-        const int cy = (int)(((float)cc + 0.5f) * inv_gx), cx = cc - cy * GX;
-        for (int yy = max(0, cy - 1); yy <= min(GY - 1, cy + 1) && !kept_cov; ++yy) {
-          for (int xx = max(0, cx - 1); xx <= min(GX - 1, cx + 1) && !kept_cov; ++xx) {
-            const int c = yy * GX + xx;
-            const int b = c == 0 ? 0 : (int)cstart[c - 1], en = (int)cstart[c];
-            for (int q = b; q < en; ++q) {
-              const int i = list[q];
-              const uint8_t si = state[i];
-              if (si == kRemoved) continue;
-              const uint64_t ki = key[i];
-              if (!(ki < kj || (ki == kj && i < j))) continue;
-              if (!greedy_covers(jx, jy, jz, sx[i], sy[i], sz[i], thr[i])) continue;
-              if (si == kKept) { kept_cov = true; break; }
-              undec_cov = true;
-            }
+        // the cells the coverers' corners can lie in; one contiguous run per cell row
+        const int cx0 = (int)(max(0LL, (long long)jx - maxz - ox) / Sx);
+        const int cy0 = (int)(max(0LL, (long long)jy - maxz - oy) / Sy);
+        const int cx1 = (int)min((long long)GX - 1, ((long long)jx + jz - ox) / Sx);
+        const int cy1 = (int)min((long long)GY - 1, ((long long)jy + jz - oy) / Sy);
+        for (int yy = cy0; yy <= cy1 && !kept_cov; ++yy) {
+          const int c0 = yy * GX + cx0, c1 = yy * GX + cx1;
+          const int b = c0 == 0 ? 0 : (int)cstart[c0 - 1], en = (int)cstart[c1];
+          for (int q = b; q < en; ++q) {
+            const int i = list[q];
+            const uint8_t si = state[i];
+            if (si == kRemoved) continue;
+            const uint64_t ki = key[i];
+            if (!(ki < kj || (ki == kj && i < j))) continue;
+            if (!greedy_covers(jx, jy, jz, sx[i], sy[i], sz[i], thr[i])) continue;
+            if (si == kKept) { kept_cov = true; break; }
+            undec_cov = true;
           }
         }
       } else {

@@ -91,18 +91,21 @@ struct SoftFrame {
   uint16_t *cellof, *list;
   uint16_t* fround;         // round in which the box became final
   uint32_t* cstart;   // after the scatter: cstart[c] = end(c) = start(c+1), start(0) = 0
-  int cnt, GX, GY, S, ox, oy;
-  float inv_gx;   // 1/GX: cell row of a cell id without an integer division (exact, ids < 2^12)
+  int cnt, GX, GY, Sx, Sy, ox, oy, maxz;
   bool bin;
 
-  // visit every candidate slot that may overlap box j (3x3 cells, or every slot)
+  // visit every candidate slot that may overlap box j: the cells its overlapping boxes'
+  // corners can lie in ([x - max_z, x + z] x [y - max_z, y + z]; cells Sx wide and Sy tall,
+  // one contiguous run per cell row), or every slot
   template <class F>
   __device__ __forceinline__ void for_candidates(int j, F&& fn) const {
     if (bin) {
-      const int c = cellof[j];
-      const int cy = (int)(((float)c + 0.5f) * inv_gx), cx = c - cy * GX;
-      for (int yy = max(0, cy - 1); yy <= min(GY - 1, cy + 1); ++yy) {
-        const int c0 = yy * GX + max(0, cx - 1), c1 = yy * GX + min(GX - 1, cx + 1);
+      const long long jx = sx[j], jy = sy[j], jz = sz[j];
+      const int cx0 = (int)(max(0LL, jx - maxz - ox) / Sx), cy0 = (int)(max(0LL, jy - maxz - oy) / Sy);
+      const int cx1 = (int)min((long long)GX - 1, (jx + jz - ox) / Sx);
+      const int cy1 = (int)min((long long)GY - 1, (jy + jz - oy) / Sy);
+      for (int yy = cy0; yy <= cy1; ++yy) {
+        const int c0 = yy * GX + cx0, c1 = yy * GX + cx1;
         const int b = c0 == 0 ? 0 : (int)cstart[c0 - 1], en = (int)cstart[c1];
         for (int q = b; q < en; ++q) fn((int)list[q]);
       }
@@ -168,25 +171,27 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
   }
   // ---- spatial cells (exact: zero overlap leaves a score unchanged)
   F.bin = s_stat[5] != 0 && cnt > 0;
-  F.S = 1; F.GX = 1; F.GY = 1;
-  F.ox = s_stat[0]; F.oy = s_stat[1];
-  if (F.bin) {
-    F.S = s_stat[4] + 1;
-    if (F.S <= 0) F.bin = false;
+  F.Sx = F.Sy = 1; F.GX = 1; F.GY = 1;
+  F.ox = s_stat[0]; F.oy = s_stat[1]; F.maxz = s_stat[4];
+  if (F.bin) {  // cells Sx wide, Sy tall, as pnms_greedy.cuh
+    F.Sy = s_stat[4] + 1;
+    if (F.Sy <= 0) F.bin = false;
+    F.Sx = max(F.Sy >> 2, 1);
   }
   if (F.bin) {
     for (;;) {
-      F.GX = (int)(((long long)s_stat[2] - F.ox) / F.S + 1);
-      F.GY = (int)(((long long)s_stat[3] - F.oy) / F.S + 1);
+      F.GX = (int)(((long long)s_stat[2] - F.ox) / F.Sx + 1);
+      F.GY = (int)(((long long)s_stat[3] - F.oy) / F.Sy + 1);
       if ((long long)F.GX * F.GY <= max_cells) break;
-      if (F.S > (1 << 29)) { F.GX = F.GY = 1; break; }
-      F.S *= 2;
+      if (F.Sy > (1 << 29)) { F.GX = F.GY = 1; break; }
+      if (F.Sx < F.Sy) F.Sx *= 2;
+      else { F.Sx *= 2; F.Sy *= 2; }
     }
     const int cells = F.GX * F.GY;
     for (int c = threadIdx.x; c <= cells; c += kSoftThreads) F.cstart[c] = 0u;
     __syncthreads();
     for (int e = threadIdx.x; e < cnt; e += kSoftThreads) {
-      const int c = (int)(((long long)F.sy[e] - F.oy) / F.S) * F.GX + (int)(((long long)F.sx[e] - F.ox) / F.S);
+      const int c = (int)(((long long)F.sy[e] - F.oy) / F.Sy) * F.GX + (int)(((long long)F.sx[e] - F.ox) / F.Sx);
       F.cellof[e] = (uint16_t)c;
       atomicAdd(&F.cstart[c], 1u);
     }
@@ -209,7 +214,6 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
     }
     __syncthreads();
     F.bin = s_stat[6] <= kSoftCellMax;
-    F.inv_gx = 1.0f / (float)F.GX;
     if (F.bin) {
       for (int e = threadIdx.x; e < cnt; e += kSoftThreads) {
         const uint32_t pos = atomicAdd(&F.cstart[F.cellof[e]], 1u);
