@@ -651,6 +651,44 @@ def test_device_fallback_chain_direct_and_graph(chunks, monkeypatch):
     assert torch.equal(oc, want_c) and torch.equal(om, want_m)
 
 
+def test_one_workspace_across_paths_and_shapes(monkeypatch):
+    """The persistent scratch head is shared by the single-launch path (suppression words,
+    tickets), the binned and tile paths (declined count, tile masks and flags): calls of every
+    path and shape, with and without declined frames, interleaved on ONE workspace, each
+    against the oracle — every call must leave the head zero for the next."""
+    from paper_2502_00535_b200 import _lib
+
+    ws = torch.zeros(_lib.workspace_bytes(64, 9000), dtype=torch.uint8, device=DEV)
+    rng = np.random.default_rng(5)
+    cases = []
+    for (B, n, env) in ((3, 700, {}),                                              # single launch
+                        (20, 900, {"PNMS_SMALL_PAIRS": "0"}),                      # binned
+                        (1, 3000, {"PNMS_SMALL_PAIRS": "0"}),                      # tiles (small call)
+                        (2, 9000, {}),                                             # tiles
+                        (3, 9000, {"PNMS_LARGE": "2"}),                            # cluster
+                        (40, 1200, {"PNMS_SMALL_PAIRS": "0"})):                    # binned again
+        x, y, z, s = random_frames(B, n, seed=int(rng.integers(1 << 30)), frame_w=2000, frame_h=1500,
+                                   z_range=(4, 70))
+        if B > 1:
+            x[1, :300] = 50; y[1, :300] = 60    # a crowded cell: declined on the cell paths
+        cases.append((x, y, z, s, env))
+    for rep in range(2):
+        for x, y, z, s, env in cases:
+            for k in ("PNMS_SMALL_PAIRS", "PNMS_LARGE"):
+                monkeypatch.delenv(k, raising=False)
+            for k, v in env.items():
+                monkeypatch.setenv(k, v)
+            B, n = x.shape
+            t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)  # noqa: E731
+            ki, kc = batched_nms_keep(t(x), t(y), t(z), t(s), None, 0.5, "by_index", n, workspace=ws)
+            ki, kc = ki.cpu().numpy(), kc.cpu().numpy()
+            for f in range(B):
+                want = c_oracle.run_frame(x[f], y[f], z[f], s[f], n, n, 0.5, "by_index")
+                assert np.array_equal(ki[f, : kc[f]], want), (rep, B, n, env, f)
+    torch.cuda.synchronize()
+    assert int(ws[: 64 * 1024].count_nonzero().item()) == 0  # the persistent head is clean
+
+
 def test_unpack_box32_extremes():
     """pnms_unpack_box32 round-trips the packable domain edges, ragged lengths included."""
     from paper_2502_00535_b200 import _lib, pack_box32
