@@ -198,17 +198,20 @@ __global__ void __launch_bounds__(kClThreads, 1) pnms_binned_cluster(BinArgs a, 
     if (r == 0 && threadIdx.x == 0) binned_decline(a, f);
     return;
   }
-  // ---- cells of side >= max side + 1, cell rows split into CS balanced bands
-  int S = g_maxz + 1, GX = 1, GY = 1;
+  // ---- cells Sy >= max side + 1 tall (a row reaches one cell row beyond its own band) and
+  // Sx = Sy / 4 wide (the x reach is range-based: narrow cells tighten it, pnms_binned.cuh),
+  // cell rows split into CS balanced bands
+  int Sy = g_maxz + 1, Sx = max(Sy >> 2, 1), GX = 1, GY = 1;
   if (n_act > 0) {
     for (;;) {
-      GX = (g_maxx - ox) / S + 1;
-      GY = (g_maxy - oy) / S + 1;
+      GX = (g_maxx - ox) / Sx + 1;
+      GY = (g_maxy - oy) / Sy + 1;
       if ((long long)GX * ((GY + CS - 1) / CS) + 1 <= kClCells) break;
-      S *= 2;
+      if (Sx < Sy) Sx *= 2;
+      else { Sx *= 2; Sy *= 2; }
     }
   }
-  const uint32_t M = div_magic(S);
+  const uint32_t Mx = div_magic(Sx), My = div_magic(Sy);
   // band o holds cell rows [rb(o), rb(o+1)), rb(o) = ceil(o*GY/CS); owner(cy) = cy*CS/GY
   auto band_lo = [&](int o) { return (o * GY + CS - 1) / CS; };
   auto owner = [&](int cy) { return (cy * CS) / GY; };
@@ -218,7 +221,7 @@ __global__ void __launch_bounds__(kClThreads, 1) pnms_binned_cluster(BinArgs a, 
   for (int k = 0; k < PER; ++k) {
     if (zc[k] != 0xFFFFFFFFu) {
       const int ex = (int)(xy[k] & 0xFFFFu), ey = (int)(xy[k] >> 16);
-      const int cy = qdiv(ey - oy, M), cx = qdiv(ex - ox, M);
+      const int cy = qdiv(ey - oy, My), cx = qdiv(ex - ox, Mx);
       const int o = owner(cy);
       const int lc = (cy - band_lo(o)) * GX + cx;
       const uint32_t rk = atomicAdd(cl.map_shared_rank(cstart, o) + lc, 1u);
@@ -265,7 +268,7 @@ __global__ void __launch_bounds__(kClThreads, 1) pnms_binned_cluster(BinArgs a, 
       const int el = threadIdx.x + k * kClThreads;
       const int e = e0 + el;
       const int32_t xv = (int32_t)(xy[k] & 0xFFFFu), yv = (int32_t)(xy[k] >> 16), zv = (int32_t)(zc[k] & 0xFFu);
-      const int o = owner(qdiv(yv - oy, M));
+      const int o = owner(qdiv(yv - oy, My));
       const uint32_t lc = zc[k] >> 16;
       const uint32_t pos = cl.map_shared_rank(cstart, o)[lc] + ((zc[k] >> 8) & 0xFFu);
       const RecNarrow rn = make_rec_narrow(xv, yv, zv, a.theta, kNarrow7);
@@ -364,8 +367,8 @@ __global__ void __launch_bounds__(kClThreads, 1) pnms_binned_cluster(BinArgs a, 
     const RecBin ri = recS[p];
     const int32_t ix = -(int32_t)(int16_t)(ri.nb & 0xFFFFu), iy = -(int32_t)(int16_t)(ri.nb >> 16);
     const int32_t iz = (int32_t)(ri.w & 0xFF) - 1;
-    const int cx0 = qdiv(max(ix - g_maxz - ox, 0), M), cy0 = qdiv(max(iy - g_maxz - oy, 0), M);
-    const int cx1 = min(GX - 1, qdiv(ix + iz - ox, M)), cy1 = min(GY - 1, qdiv(iy + iz - oy, M));
+    const int cx0 = qdiv(max(ix - g_maxz - ox, 0), Mx), cy0 = qdiv(max(iy - g_maxz - oy, 0), My);
+    const int cx1 = min(GX - 1, qdiv(ix + iz - ox, Mx)), cy1 = min(GY - 1, qdiv(iy + iz - oy, My));
     bool sup;
     if (ext_ok) {
       sup = cluster_row_scan<BY_INDEX>(ri, p + own_off, cx0, cx1, cy0, cy1, [&](int yy) { return (yy - R0) * GX; },
