@@ -651,6 +651,30 @@ def test_device_fallback_chain_direct_and_graph(chunks, monkeypatch):
     assert torch.equal(oc, want_c) and torch.equal(om, want_m)
 
 
+@pytest.mark.parametrize("crowd", [100, 127, 128])
+@pytest.mark.parametrize("where", ["binned", "tiles", "cluster"])
+def test_crowded_cells_at_the_cell_limit(crowd, where, monkeypatch):
+    """Cells of up to kBinCellMax = 127 boxes stay on the culling paths (skip distance and
+    in-cell ranks at their field limits); 128 is declined to the dense pipeline — exact either
+    way, with equal scores inside the crowd."""
+    monkeypatch.setenv("PNMS_SMALL_PAIRS", "0")
+    if where == "binned":
+        B, n = 3, 1500
+    else:
+        B, n = (1, 6000) if where == "tiles" else (3, 6000)
+        monkeypatch.setenv("PNMS_LARGE", "1" if where == "tiles" else "2")
+    x, y, z, s = random_frames(B, n, seed=crowd, frame_w=1800, frame_h=1000, z_range=(4, 60))
+    f = B - 1
+    x[f, :crowd] = 300 + np.arange(crowd) % 3     # one 16 x 64 cell
+    y[f, :crowd] = 200 + np.arange(crowd) % 5
+    s[f, : crowd // 2] = 0.75                     # ties inside the crowd
+    for tie in ("paper_faithful", "by_index"):
+        got = _run_batch(x, y, z, s, np.full(B, n, np.int32), 0.5, tie, n)
+        for g in range(B):
+            want = c_oracle.run_frame(x[g], y[g], z[g], s[g], n, n, 0.5, tie)
+            assert np.array_equal(got[g], want), (crowd, where, tie, g)
+
+
 def test_one_workspace_across_paths_and_shapes(monkeypatch):
     """The persistent scratch head is shared by the single-launch path (suppression words,
     tickets), the binned and tile paths (declined count, tile masks and flags): calls of every
