@@ -26,7 +26,7 @@ namespace pnms {
 constexpr int kBinThreads = 512;
 constexpr int kBinMaxSlots = 4096;
 constexpr int kBinMaxCells = 4096;   // upper bound; a frame uses at most max(64, 2 * npad) cells
-constexpr int kBinCellMax = 127;  // skip (bits 8..14 of RecBin::w) and the rank fields hold it
+constexpr int kBinCellMax = 255;  // skip (byte 1 of RecBin::w) and the 8-bit rank fields hold it
 
 // Binned record (16 B, one LDS.128 per candidate column), narrow7 geometry as RecNarrow:
 //   a  = (x+z+1, y+z+1), nb = (-x, -y)                       packed s16x2
@@ -34,7 +34,7 @@ constexpr int kBinCellMax = 127;  // skip (bits 8..14 of RecBin::w) and the rank
 //   k  = high 32 bits of the 64-bit sort key (ascending == score descending)
 // skip = boxes left to the end of the box's cell (<= kBinCellMax).  The pair value
 // d = v*v + w = w_x^2 + skip*2^8 + (z+1) + (w_x*h - T)*2^17 keeps sign(w_x*h - T): the low
-// terms stay below 16129 + 127*256 + 127 < 2^17 (the argument of pair_d).
+// terms stay below 16129 + 255*256 + 127 < 2^17 (the argument of pair_d).
 // The full keys and input slots live in separate arrays: a suppressing column whose high key
 // half equals the row's is verified on the full keys (rare: equal 32-bit prefixes).
 struct __align__(16) RecBin {

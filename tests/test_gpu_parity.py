@@ -651,12 +651,12 @@ def test_device_fallback_chain_direct_and_graph(chunks, monkeypatch):
     assert torch.equal(oc, want_c) and torch.equal(om, want_m)
 
 
-@pytest.mark.parametrize("crowd", [100, 127, 128])
+@pytest.mark.parametrize("crowd", [100, 255, 256])
 @pytest.mark.parametrize("where", ["binned", "tiles", "cluster"])
 def test_crowded_cells_at_the_cell_limit(crowd, where, monkeypatch):
-    """Cells of up to kBinCellMax = 127 boxes stay on the culling paths (skip distance and
-    in-cell ranks at their field limits); 128 is declined to the dense pipeline — exact either
-    way, with equal scores inside the crowd."""
+    """Cells of up to kBinCellMax = 255 boxes stay on the culling paths (skip distance and
+    in-cell ranks at their 8-bit field limits); 256 is declined to the dense pipeline — exact
+    either way, with equal scores inside the crowd."""
     monkeypatch.setenv("PNMS_SMALL_PAIRS", "0")
     if where == "binned":
         B, n = 3, 1500
