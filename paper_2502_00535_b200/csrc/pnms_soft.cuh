@@ -55,7 +55,7 @@ struct SoftArgs {
 __host__ __device__ inline int soft_npad(int n_max) { return (n_max + 127) & ~127; }
 inline size_t soft_smem_bytes(int n_max) {
   const size_t n = (size_t)soft_npad(n_max);
-  const size_t cells = n < 64 ? 64 : n;
+  const size_t cells = n < 32 ? 64 : 2 * n;  // rectangular cells: up to two per box
   return n * (4 * 3 + 8 + 8 + 8 + 1 + 1 + 2 + 2 + 2 + 2 + 2) + (cells + 4) * 4 + 64 * 4 + 64;
 }
 
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
   const long long fbase = (long long)f * a.n_max;
   const int cnt = frame_count(a.counts, f, a.n_max);
   const int npad = soft_npad(a.n_max);
-  const int max_cells = npad < 64 ? 64 : npad;
+  const int max_cells = npad < 32 ? 64 : 2 * npad;
   SoftFrame F;
   F.sx = reinterpret_cast<int32_t*>(smem_raw);
   F.sy = F.sx + npad;
