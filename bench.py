@@ -8,22 +8,30 @@ Headline workload (BASELINE.json config 5): a stream of 8192 frames x 2048 synth
 paper_faithful ties, sharded contiguously over the N ranks (one process per GPU, no
 collective on the data path).  One step = every frame of the rank's shard through one
 batched pnms_run.  `value` = frames of all ranks per second of the slowest rank, with inputs
-resident in HBM; `e2e` = the same through NmsEngine.run_host from pinned host buffers
-(H2D inputs + D2H survivor masks inside the timed region).  Rank 0 also reports the
-single-frame latencies of configs 1-3 (the reference's own frames, tests/golden) and the
-256-frame batch of config 4.
+resident in HBM; `e2e` = the same through the public NmsEngine.run_host from pinned host
+buffers in the C ABI's own input layout (int32 x, y, z + float64 s planes, 20 B per box) to
+pinned host keep indices (H2D inputs + D2H indices and counts inside the timed region).
+Rank 0 also reports the single-frame latencies of configs 1-3 (the reference's own frames,
+tests/golden; device time and host-to-host through nms_keep / run_nms), the 256-frame batch
+of config 4, an oracle check of a sample of the timed frames, and the reference's greedy /
+Soft-NMS variants.
 
---impl reference times the reference algorithm's CPU implementation (the numpy port in
-oracle/parnms_oracle.py, all host cores) on bounded samples of the same workload.
+--gpus N without a torchrun environment re-launches itself under torch.distributed.run
+with N ranks (NCCL when the box has N GPUs; gloo with the ranks sharing the GPUs otherwise).
+
+--impl reference times the reference's own CPU implementation (parnms.engine.run_nms from
+baseline/_ref, one process per host core, one frame per task; the numpy port in
+oracle/parnms_oracle.py when baseline/_ref is absent) on bounded samples of the same workload.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -33,6 +41,7 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+REF_DIR = ROOT / "baseline" / "_ref"
 
 METRIC = "NMS latency/frame at N=1024 boxes (µs) and batched frames/sec at 1/2/4/8 B200"
 FRAMES, BOXES, THETA, TIE = 8192, 2048, 0.5, "paper_faithful"
@@ -40,6 +49,7 @@ GEN = dict(frame_w=1920, frame_h=1080, z_range=(8, 64))
 WORKLOAD = (f"config 5: stream of {FRAMES} frames x {BOXES} boxes (random_frame distribution 1920x1080, "
             f"z 8..64), theta {THETA}, {TIE}, sharded contiguously over the GPUs")
 SEED = 20250200
+DTYPE = "int32+f64"  # int32 geometry and products, float64 thresholds and score order (exact)
 
 
 from paper_2502_00535_b200.sharding import gather_survivors, shard_bounds  # noqa: E402
@@ -56,77 +66,130 @@ def make_shard(rank: int, world: int):
     return [c[off: off + (b - a)] for c in cat]
 
 
+def host_cpu():
+    """Host CPU model, logical cores and nominal clock (the CPU baseline's hardware)."""
+    model, mhz = None, None
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name") and model is None:
+                model = ln.split(":", 1)[1].strip()
+            if ln.startswith("cpu MHz") and mhz is None:
+                mhz = float(ln.split(":", 1)[1])
+    except OSError:
+        pass
+    return {"model": model, "logical_cores": os.cpu_count(), "mhz": mhz}
+
+
 # --------------------------------------------------------------------- CPU reference leg
-def _cpu_frame(args):
-    sys.path.insert(0, str(ROOT / "oracle"))
+_W: dict = {}  # per worker process: the sample frames, prebuilt before any timing
+
+
+def _ref_importable() -> bool:
+    if not (REF_DIR / "parnms" / "engine.py").exists():
+        return False
+    sys.path.insert(0, str(REF_DIR))
+    try:
+        import parnms.engine  # noqa: F401
+        return True
+    except Exception:
+        return False
+
+
+def _pool_init(kind: str, x, y, z, s):
+    """Worker initializer: build the frames once (the reference's DetectionVector construction
+    is a Python loop, detections.py:125-129, and is not part of run_nms)."""
+    _W["kind"] = kind
+    if kind == "reference":
+        sys.path.insert(0, str(REF_DIR))
+        from parnms.detections import Detection, DetectionVector
+        from parnms.engine import NmsConfig
+
+        _W["cfg"] = NmsConfig(theta=THETA, d_max=x.shape[1], k=32, workers=1, tie_break=TIE)
+        _W["vecs"] = [DetectionVector(map(Detection, x[f].tolist(), y[f].tolist(), z[f].tolist(), s[f].tolist()),
+                                      x.shape[1], validate=False) for f in range(x.shape[0])]
+    else:
+        sys.path.insert(0, str(ROOT / "oracle"))
+        _W["arrays"] = (x, y, z, s)
+
+
+def _pool_frame(f: int) -> int:
+    if _W["kind"] == "reference":
+        from parnms.engine import run_nms
+
+        res, _ = run_nms(_W["vecs"][f], _W["cfg"])
+        return len(res.survivors)
     import parnms_oracle
 
-    x, y, z, s = args
-    keep, _ = parnms_oracle.run_nms_oracle(x, y, z, s, x.shape[0], x.shape[0], THETA, TIE)
+    x, y, z, s = _W["arrays"]
+    keep, _ = parnms_oracle.run_nms_oracle(x[f], y[f], z[f], s[f], x.shape[1], x.shape[1], THETA, TIE)
     return len(keep)
 
 
-def cpu_reference_rate(shard, budget_s: float = 8.0, max_frames: int = 4096, pool=None):
-    """Frames/s of the numpy port of engine.run_nms over all host cores (bounded sample)."""
-    import multiprocessing as mp
+class CpuReference:
+    """The reference's CPU path on every host core: a process pool (fork), one frame per task
+    (BASELINE.md §3), each worker running the single-threaded run_nms on pre-built frames."""
 
-    cores = os.cpu_count() or 1
-    own = pool is None
-    if own:
-        pool = mp.get_context("fork").Pool(cores)
-    x, y, z, s = shard
-    done, t0, f = 0, time.perf_counter(), 0
-    try:
-        pool.map(_cpu_frame, [(x[i], y[i], z[i], s[i]) for i in range(min(cores, x.shape[0]))])  # warm
+    def __init__(self, shard, kind: str | None = None, sample: int | None = None):
+        import multiprocessing as mp
+
+        self.kind = kind or ("reference" if _ref_importable() else "port")
+        self.cores = os.cpu_count() or 1
+        n = sample or 2 * self.cores
+        self.frames = n
+        x, y, z, s = (np.ascontiguousarray(a[:n]) for a in shard)
+        self.pool = mp.get_context("fork").Pool(self.cores, initializer=_pool_init, initargs=(self.kind, x, y, z, s))
+        self.pool.map(_pool_frame, range(self.cores), chunksize=1)  # warm every worker
+
+    def step(self, base: int) -> float:
+        """One timed step: `cores` frames (one per core) through run_nms; returns seconds."""
+        idx = [(base + i) % self.frames for i in range(self.cores)]
         t0 = time.perf_counter()
-        while time.perf_counter() - t0 < budget_s and done < max_frames:
-            batch = [((x[(f + i) % x.shape[0]], y[(f + i) % x.shape[0]], z[(f + i) % x.shape[0]],
-                       s[(f + i) % x.shape[0]])) for i in range(cores)]
-            pool.map(_cpu_frame, batch)
-            f += cores
-            done += cores
-        el = time.perf_counter() - t0
-    finally:
-        if own:
-            pool.close()
-            pool.join()
-    return done / el, cores, done, el
+        self.pool.map(_pool_frame, idx, chunksize=1)
+        return time.perf_counter() - t0
+
+    def rate(self, budget_s: float) -> tuple[float, int, float]:
+        done, el, k = 0, 0.0, 0
+        while el < budget_s:
+            el += self.step(k * self.cores)
+            done += self.cores
+            k += 1
+        return done / el, done, el
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+    def describe(self) -> str:
+        what = ("parnms.engine.run_nms of the unmodified reference (baseline/_ref)" if self.kind == "reference"
+                else "numpy port of engine.run_nms (oracle/parnms_oracle.py; baseline/_ref absent)")
+        return f"{what}, workers=1, one process per host core, one frame per task"
 
 
 def run_reference_impl(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import multiprocessing as mp
-
     shard = make_shard(0, 1)
-    cores = os.cpu_count() or 1
-    pool = mp.get_context("fork").Pool(cores)
+    ref = CpuReference(shard)
     per_step = []
-    x, y, z, s = shard
     try:
         for step in range(args.warmup + args.steps):
-            base = (step * cores) % FRAMES
-            batch = [(x[(base + i) % FRAMES], y[(base + i) % FRAMES], z[(base + i) % FRAMES], s[(base + i) % FRAMES])
-                     for i in range(cores)]
-            t0 = time.perf_counter()
-            pool.map(_cpu_frame, batch)
-            el = time.perf_counter() - t0
+            el = ref.step(step * ref.cores)
             if step >= args.warmup:
                 per_step.append(el)
     finally:
-        pool.close()
-        pool.join()
+        ref.close()
     tot = sum(per_step)
-    value = cores * len(per_step) / tot
-    sample = f"{cores} frames of the workload per step (one per host core), numpy port of engine.run_nms"
+    value = ref.cores * len(per_step) / tot
+    sample = f"{ref.cores} frames of the workload per step (one per host core); {ref.describe()}"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(per_step),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32+f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": DTYPE,
         "data": "synthetic", "config": {"workload": WORKLOAD, "frames": FRAMES, "boxes_per_frame": BOXES,
                                         "theta": THETA, "tie_break": TIE},
-        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": ref.cores, "kind": ref.kind, "sample": sample,
+                         "host_cpu": host_cpu()},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -185,11 +248,12 @@ class ClockSampler:
 
 # --------------------------------------------------------------------- GPU leg
 def latency_suite(torch, dev, iters: int = 50):
-    """Median single-call device latency (CUDA events, device-resident inputs) of configs 1-4.
-
-    A spin kernel is queued ahead of the start event so the events bracket only device time
-    (first kernel start to last kernel end), not the host's enqueue time."""
-    from paper_2502_00535_b200 import batched_nms_keep
+    """Single-call latency of configs 1-4: device time (CUDA events, device-resident inputs; a
+    spin kernel queued ahead of the start event so the events bracket device time only), and
+    host to host for configs 1-3 through the public calls — nms_keep (device tensors in, host-
+    synchronised keep indices out) and the reference-facing engine.run_nms (a host
+    DetectionVector in, NmsResult + WorkCounters out) — as wall-clock medians."""
+    from paper_2502_00535_b200 import DetectionVector, LaunchConfig, NmsConfig, batched_nms_keep, nms_keep, run_nms
     from paper_2502_00535_b200.synth import random_frames
 
     g = np.load(ROOT / "tests" / "golden" / "configs.npz")
@@ -201,8 +265,9 @@ def latency_suite(torch, dev, iters: int = 50):
         B, n = x.shape
         ki = torch.empty((B, n), dtype=torch.int32, device=dev)
         kc = torch.empty((B,), dtype=torch.int32, device=dev)
+        lc = LaunchConfig()
         for _ in range(5):
-            batched_nms_keep(x, y, z, s, None, THETA, TIE, n, keep_idx=ki, keep_count=kc)
+            batched_nms_keep(x, y, z, s, None, THETA, TIE, n, keep_idx=ki, keep_count=kc, launch=lc)
         ts = []
         for _ in range(iters):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -212,18 +277,47 @@ def latency_suite(torch, dev, iters: int = 50):
             b.record()
             b.synchronize()
             ts.append(a.elapsed_time(b) * 1e3)
-        out[nm] = {"frames": B, "boxes": n, "median_us": statistics.median(ts), "min_us": min(ts)}
+        rec = {"frames": B, "boxes": n, "path": lc.path_taken, "device_median_us": statistics.median(ts),
+               "device_min_us": min(ts)}
+        if B == 1:
+            boxes = torch.stack([x[0], y[0], z[0]], 1).contiguous()
+            scores = s[0].contiguous()
+            for _ in range(5):
+                nms_keep(boxes, scores, THETA)
+            hs = []
+            for _ in range(iters):
+                t0 = time.perf_counter()
+                nms_keep(boxes, scores, THETA)
+                hs.append((time.perf_counter() - t0) * 1e6)
+            rec["nms_keep_host_to_host_median_us"] = statistics.median(hs)
+            vec = DetectionVector.from_arrays(arrs[0][0], arrs[1][0], arrs[2][0], arrs[3][0], n, validate=False)
+            cfg = NmsConfig(theta=THETA, d_max=n, k=1, tie_break=TIE)
+            for _ in range(5):
+                run_nms(vec, cfg)
+            hs = []
+            for _ in range(iters):
+                t0 = time.perf_counter()
+                res, ctr = run_nms(vec, cfg)
+                hs.append((time.perf_counter() - t0) * 1e6)
+            rec["run_nms_host_to_host_median_us"] = statistics.median(hs)
+            rec["run_nms_survivors"] = len(res.survivors)
+            rec["matches_golden"] = bool(np.array_equal(
+                np.array([d.x for d in res.survivors]), arrs[0][0][g[f"{nm}_keep"]]))
+        out[nm] = rec
+    out["note"] = ("device_*: CUDA events around one call with the host enqueue hidden; *_host_to_host: "
+                   "wall clock of the whole public call (H2D, kernels, D2H, synchronisation; run_nms also "
+                   "builds the reference's Detection tuple)")
     return out
 
 
 def variants_suite(torch, dev, frames: int = 256, n: int = 1024, iters: int = 10):
     """The reference's sequential NMS variants (oracles.py:64-123) on a config-4-shaped batch:
     device frames/s of greedy NMS and Soft-NMS (linear, gaussian) next to the C restatement of
-    the same algorithm on one host core, plus a parity spot check of frame 0."""
+    the same algorithm on one host core, plus a parity spot check of one frame."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import c_oracle
 
-    from paper_2502_00535_b200 import greedy_nms_keep, soft_nms_rescore_batched
+    from paper_2502_00535_b200 import _lib, greedy_nms_keep, soft_nms_rescore_batched, validate_batch
     from paper_2502_00535_b200.synth import random_frames
 
     arrs = random_frames(frames, n, seed=64, **GEN)
@@ -250,12 +344,7 @@ def variants_suite(torch, dev, frames: int = 256, n: int = 1024, iters: int = 10
     res = {"workload": f"{frames} frames x {n} boxes (random_frame distribution), theta 0.5 / soft theta 0.3, "
                        f"sigma 0.5", "unit": "frames/s"}
     # device-side ingest validation (detections.py:60-85) of the config-5 stream: an HBM stream
-    from paper_2502_00535_b200 import validate_batch
-    from paper_2502_00535_b200.synth import random_frames as rf
-
-    from paper_2502_00535_b200 import _lib
-
-    big = [torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in rf(8192, 2048, seed=65, **GEN)]
+    big = [torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in random_frames(8192, 2048, seed=65, **GEN)]
     validate_batch(*big)  # the public call (raises on an invalid detection); timed below: its kernel
     first = torch.empty(8192, dtype=torch.int32, device=dev)
     why = torch.empty(8192, dtype=torch.int32, device=dev)
@@ -278,10 +367,42 @@ def variants_suite(torch, dev, frames: int = 256, n: int = 1024, iters: int = 10
         rate, (out, st) = dev_rate(lambda: soft_nms_rescore_batched(x, y, z, s, None, mode, 0.3, 0.5))
         crate, want = cpu_rate(lambda f: c_oracle.soft_frame(*(a[f] for a in arrs), n, mode, 0.3, 0.5), 2)  # frame 1
         got = out[1].cpu().numpy()
-        same = (np.array_equal(got.view(np.uint64), want.view(np.uint64)) if mode == "linear"
-                else bool(np.allclose(got, want, rtol=1e-13, atol=0)))
-        res[f"soft_{mode}"] = {"value": rate, "cpu_port_1core": crate, "frame1_matches_oracle": same}
+        res[f"soft_{mode}"] = {"value": rate, "cpu_port_1core": crate,
+                               "frame1_matches_oracle": bool(np.array_equal(got.view(np.uint64), want.view(np.uint64)))}
     return res
+
+
+def oracle_check(shard, keep_idx, keep_count, sample: int = 64):
+    """Parity of the timed run itself: keep indices and counts of `sample` frames spread over
+    the shard, from the last timed step's device outputs, against the C restatement of
+    engine.run_nms (test infrastructure, outside every timed region)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import c_oracle
+
+    x, y, z, s = shard
+    F = x.shape[0]
+    idx = np.unique(np.linspace(0, F - 1, min(sample, F)).astype(int))
+    counts = np.full(len(idx), BOXES, np.int32)
+    want = c_oracle.run_batch(x[idx], y[idx], z[idx], s[idx], counts, BOXES, THETA, TIE)
+    ki, kc = keep_idx[idx].cpu().numpy(), keep_count[idx].cpu().numpy()
+    bad = [int(f) for j, f in enumerate(idx) if not np.array_equal(ki[j, :kc[j]], want[j])]
+    return {"frames_checked": len(idx), "mismatched_frames": bad, "all_match": not bad,
+            "survivors_checked": int(sum(len(w) for w in want)), "oracle": "oracle/nms_oracle.c (C restatement)"}
+
+
+def _free_port() -> int:
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N outside torchrun: re-launch this script under torch.distributed.run with N ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -296,17 +417,31 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_impl(args)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE {world}; reporting {world} ranks", file=sys.stderr)
     shard = make_shard(rank, world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, cores, nfr, el = cpu_reference_rate(shard)
-        cpu = {"value": rate, "unit": "frames/s", "cores": cores, "kind": "port",
-               "sample": f"{nfr} frames of the workload in {el:.1f} s, numpy port of engine.run_nms "
-                         f"(oracle/parnms_oracle.py), one process per core"}
+        # about 10-25 s of host work: the reference itself, then the numpy port as a cross-check
+        ref = CpuReference(shard)
+        rate, nfr, el = ref.rate(10.0)
+        ref.close()
+        cpu = {"value": rate, "unit": "frames/s", "cores": ref.cores, "kind": ref.kind,
+               "sample": f"{nfr} frames of the workload in {el:.1f} s; {ref.describe()}", "host_cpu": host_cpu()}
+        if ref.kind == "reference":
+            port = CpuReference(shard, kind="port")
+            prate, pn, pel = port.rate(4.0)
+            port.close()
+            cpu["port_cross_check"] = {"value": prate, "unit": "frames/s", "sample": f"{pn} frames in {pel:.1f} s",
+                                       "what": port.describe()}
+
+    import ctypes
 
     import torch
 
@@ -317,16 +452,18 @@ def main():
     torch.cuda.set_device(dev_index)
     dev = torch.device("cuda", dev_index)
     dist = None
+    backend = None
     if world > 1:
         import torch.distributed as dist
 
-        # NCCL over NVLink/NVSwitch; PNMS_DIST_BACKEND=gloo lets several ranks share one GPU
-        # (used to exercise the multi-rank path on a single-GPU box)
-        backend = os.environ.get("PNMS_DIST_BACKEND", "nccl")
+        # NCCL over NVLink/NVSwitch with one GPU per rank; when the box has fewer GPUs than
+        # ranks, the ranks share them and the exchange runs over gloo (NCCL refuses two ranks
+        # on one device)
+        backend = "nccl" if ndev >= world else "gloo"
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
-            dist.init_process_group(backend)
+            dist.init_process_group("gloo")
     x, y, z, s = shard
     F = x.shape[0]
     dx, dy, dz, ds = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (x, y, z, s))
@@ -338,21 +475,40 @@ def main():
     lib = _lib.load()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
+    launch = {"auto": _lib.LaunchConfigC(), "dense": _lib.LaunchConfigC(path=_lib.PATHS["dense"])}
+    cur_launch = ["auto"]
+    paths_seen = set()
 
     def step(evs=None):
         ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
-        handles = (__import__("ctypes").c_void_p * 4)(*[e.cuda_event for e in evs]) if evs else None
-        st = lib.pnms_run_profiled(ptr(dx), ptr(dy), ptr(dz), ptr(ds), None, F, BOXES, BOXES, THETA, 0,
-                                   ptr(eng.keep_idx), ptr(eng.keep_count), None, None, ptr(eng.ws_full),
-                                   eng.ws_full.numel(), stream.cuda_stream, handles)
-        _lib.check(st, "pnms_run_profiled")
+        handles = (ctypes.c_void_p * 4)(*[e.cuda_event for e in evs]) if evs else None
+        info = _lib.RunInfoC(0)
+        st = lib.pnms_run_ex(ptr(dx), ptr(dy), ptr(dz), ptr(ds), None, F, BOXES, BOXES, THETA, 0,
+                             ptr(eng.keep_idx), ptr(eng.keep_count), None, None, ptr(eng.ws_full),
+                             eng.ws_full.numel(), stream.cuda_stream, ctypes.byref(launch[cur_launch[0]]),
+                             ctypes.byref(info), handles)
+        _lib.check(st, "pnms_run_ex")
+        paths_seen.add(_lib.PATH_NAMES[info.path])
+
+    def max_over_ranks(v: float) -> float:
+        t = torch.tensor([v], dtype=torch.float64, device=dev if backend != "gloo" else "cpu")
+        if dist:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def all_ranks(v: float) -> list:
+        if not dist:
+            return [v]
+        out = [None] * world
+        dist.all_gather_object(out, v)
+        return out
 
     def timed(algo: str):
-        """Warm-up, then K timed steps with PNMS_ALGO=algo (one event pair around each call, so
-        the library's programmatic dependent launches overlap as in production), then K
+        """Warm-up, then K timed steps on launch path `algo` (one event pair around each call,
+        so the library's programmatic dependent launches overlap as in production), then K
         profiled steps (phase events inside the call) for the per-kernel breakdown.  Returns
-        (per-step phase times, total ms of the K timed steps max over ranks, clock sampler)."""
-        os.environ["PNMS_ALGO"] = algo
+        (per-step phase times, total ms of the K timed steps of this rank, clock sampler)."""
+        cur_launch[0] = algo
         for _ in range(args.warmup):
             step()
         torch.cuda.synchronize(dev)
@@ -372,6 +528,8 @@ def main():
                 step()
                 outer[k][1].record(stream)
             torch.cuda.synchronize(dev)
+            if dist:
+                dist.barrier()
             for k in range(args.steps):
                 flush.zero_()
                 step(evs[k])
@@ -381,20 +539,23 @@ def main():
         ph = [[r[0].elapsed_time(r[1]), r[1].elapsed_time(r[2]), r[2].elapsed_time(r[3]), r[0].elapsed_time(r[3])]
               for r in evs]
         total_ms = sum(o[0].elapsed_time(o[1]) for o in outer)
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        if dist:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return ph, float(t.item()), clk
+        return ph, total_ms, clk
 
-    # headline: the default algorithm (binned kernel; declined frames fall back to dense)
-    ph, max_total_ms, clk = timed("0")
+    # headline: the library's default path (binned kernel; declined frames fall back to dense)
+    ph, rank_total_ms, clk = timed("auto")
+    max_total_ms = max_over_ranks(rank_total_ms)
+    per_rank_ms = all_ranks(rank_total_ms / args.steps)
     value = FRAMES * args.steps / (max_total_ms / 1e3)
+    default_paths = sorted(paths_seen)
     binned_ms = [p[0] for p in ph]
     fallback_ms = [p[1] + p[2] for p in ph]
+    # the timed stream's own result against the oracle (a sample of frames, outside the timing)
+    check = oracle_check(shard, eng.keep_idx, eng.keep_count)
     # dense sorted pipeline on the same workload (roofline of the N x N map kernel)
-    ph_d, max_total_d, clk_d = timed("1")
+    ph_d, rank_total_d, clk_d = timed("dense")
+    max_total_d = max_over_ranks(rank_total_d)
     value_dense = FRAMES * args.steps / (max_total_d / 1e3)
-    os.environ["PNMS_ALGO"] = "0"
+    cur_launch[0] = "auto"
     # executed pair tests of the binned kernel (one extra untimed step)
     counter = torch.zeros(1, dtype=torch.int64, device=dev)
     lib.pnms_debug_count_pairs(counter.data_ptr())
@@ -403,70 +564,82 @@ def main():
     lib.pnms_debug_count_pairs(None)
     pairs_executed = int(counter.item())
 
-    # ---- end to end through the public API: pinned host in -> pinned host out
-    # the workload's pixel coordinates fit the public API's packed 32-bit box format
-    # (pack_box32: x | y<<12 | z<<24), 12 B per box on the wire with the float64 score
-    from paper_2502_00535_b200 import pack_box32
-
-    hb = torch.from_numpy(pack_box32(x, y, z)).pin_memory()
+    # ---- end to end through the public API, in the C ABI's own input layout: pinned int32
+    # x, y, z + float64 s planes (20 B per box) in, pinned int32 keep indices + counts out
+    hx, hy, hz = (torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in (x, y, z))
     hs = torch.from_numpy(np.ascontiguousarray(s)).pin_memory()
     hc = torch.full((F,), BOXES, dtype=torch.int32).pin_memory()
-    om = torch.empty((F, eng.W32), dtype=torch.int32).pin_memory()
+    oi = torch.empty((F, BOXES), dtype=torch.int32).pin_memory()
     oc = torch.empty((F,), dtype=torch.int32).pin_memory()
-    # the link bound of this path: the same input bytes copied host -> device with no compute
-    # (pinned box32 + score planes into the engine's device buffers), best of 5
-    db = torch.empty_like(hb, device=dev)
-    ds_ = torch.empty_like(hs, device=dev)
-    link_ms = []
-    for it in range(7):
-        l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        l0.record(stream)
-        db.copy_(hb, non_blocking=True)
-        ds_.copy_(hs, non_blocking=True)
-        l1.record(stream)
+
+    def link_bound(host_bufs):
+        """The same input bytes copied host -> device alone (no compute), best of 5."""
+        devs = [torch.empty_like(h, device=dev) for h in host_bufs]
+        ts = []
+        for it in range(7):
+            l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            l0.record(stream)
+            for d_, h_ in zip(devs, host_bufs):
+                d_.copy_(h_, non_blocking=True)
+            l1.record(stream)
+            torch.cuda.synchronize(dev)
+            if it >= 2:
+                ts.append(l0.elapsed_time(l1))
+        nbytes = sum(h_.numel() * h_.element_size() for h_ in host_bufs)
+        return min(ts), nbytes / (min(ts) / 1e3) / 1e9
+
+    def e2e_time(run):
+        for _ in range(args.warmup):
+            run()
         torch.cuda.synchronize(dev)
-        if it >= 2:
-            link_ms.append(l0.elapsed_time(l1))
-    copy_ms = min(link_ms)
-    h2d_gbs = (hb.numel() * 4 + hs.numel() * 8) / (copy_ms / 1e3) / 1e9
-    del db, ds_
-    for _ in range(args.warmup):
-        eng.run_host_box32(hb, hs, hc, om, oc, graph=True)
-    torch.cuda.synchronize(dev)
-    if dist:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        eng.run_host_box32(hb, hs, hc, om, oc, graph=True)
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    e2e_ms = e0.elapsed_time(e1)
-    t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.barrier()
-    e2e_value = FRAMES * args.steps / (float(t.item()) / 1e3)
-    # correctness spot check of the e2e output against the device-resident run
-    ok = bool(torch.equal(oc.to(dev), eng.keep_count))
+        if dist:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            run()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return max_over_ranks(e0.elapsed_time(e1))
+
+    copy_ms, h2d_gbs = link_bound([hx, hy, hz, hs])
+    e2e_ms = e2e_time(lambda: eng.run_host(hx, hy, hz, hs, hc, out_count=oc, out_idx=oi, graph=True))
+    e2e_value = FRAMES * args.steps / (e2e_ms / 1e3)
+    e2e_ok = bool(torch.equal(oc.to(dev), eng.keep_count) and torch.equal(oi[:4], eng.keep_idx[:4].cpu()))
+
+    # the compact ingest format (pack_box32: x | y<<12 | z<<24, 12 B per box with the score) and
+    # survivor masks out, with the host-side packing cost measured separately
+    from paper_2502_00535_b200 import pack_box32
+
+    t0 = time.perf_counter()
+    packed = pack_box32(x, y, z)
+    pack_ms = (time.perf_counter() - t0) * 1e3
+    hb = torch.from_numpy(packed).pin_memory()
+    om = torch.empty((F, eng.W32), dtype=torch.int32).pin_memory()
+    oc2 = torch.empty((F,), dtype=torch.int32).pin_memory()
+    copy32_ms, _ = link_bound([hb, hs])
+    e2e32_ms = e2e_time(lambda: eng.run_host_box32(hb, hs, hc, om, oc2, graph=True))
+    e2e32_value = FRAMES * args.steps / (e2e32_ms / 1e3)
 
     # optional exchange step (not part of `value`): gather every rank's survivor masks and
-    # counts on rank 0 over NCCL (NVLink/NVSwitch), timed on the device, max over ranks
+    # counts on rank 0 (NCCL over NVLink/NVSwitch), timed on the device, max over ranks
     gather_ms = None
     if dist:
         dmask = om.to(dev)
+        dcnt = oc2.to(dev)
+        if backend == "gloo":
+            dmask, dcnt = dmask.cpu(), dcnt.cpu()
         for _ in range(2):
-            gather_survivors(dmask, eng.keep_count, FRAMES)
+            gather_survivors(dmask, dcnt, FRAMES)
         torch.cuda.synchronize(dev)
         dist.barrier()
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         g0.record(stream)
-        gather_survivors(dmask, eng.keep_count, FRAMES)
+        t0 = time.perf_counter()
+        gather_survivors(dmask, dcnt, FRAMES)
         g1.record(stream)
         torch.cuda.synchronize(dev)
-        t = torch.tensor([g0.elapsed_time(g1)], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        gather_ms = float(t.item())
+        gather_ms = max_over_ranks(g0.elapsed_time(g1) if backend == "nccl" else (time.perf_counter() - t0) * 1e3)
 
     lat = None
     if rank == 0 and not args.no_latency:
@@ -497,23 +670,42 @@ def main():
         achieved = ops / b_s / 1e12
         map_d = statistics.mean(p[1] for p in ph_d) / 1e3
         achieved_d = ops / map_d / 1e12
-        h2d_bytes = int(F * BOXES * 12 + F * 4)
+        h2d_bytes = int(F * BOXES * 20 + F * 4)
+        d2h_bytes = int(F * BOXES * 4 + F * 4)
+        call_ms = max_total_ms / args.steps
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": max_total_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "warmup": args.warmup, "ms_per_step": call_ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": DTYPE, "data": "synthetic",
             "config": {"workload": WORKLOAD, "frames": FRAMES, "frames_per_gpu": F, "boxes_per_frame": BOXES,
-                       "theta": THETA, "tie_break": TIE, "parallelism": f"frames sharded over {world} GPU(s)",
+                       "theta": THETA, "tie_break": TIE, "parallelism": f"frames sharded over {world} rank(s)",
                        "algorithm": "binned (exact spatial culling) with dense fallback",
                        "l2": "flushed (256 MiB write) between timed steps"},
+            "ranks": {"world": world, "devices": min(ndev, world), "dist_backend": backend,
+                      "per_rank_ms_per_step": per_rank_ms,
+                      "note": ("one GPU per rank" if ndev >= world else
+                               f"{world} ranks share {ndev} GPU(s): the ranks run concurrently on the same device")},
+            "paths": {"default": default_paths, "declined_fallback_ms": statistics.mean(fallback_ms)},
+            "oracle_check": check,
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d_bytes,
-                    "d2h_bytes_per_step": int(F * eng.W32 * 4 + F * 4), "matches_device_run": ok,
-                    "input_format": "packed 32-bit boxes (pack_box32) + float64 s planes, unpacked on device",
-                    "pipeline": f"{e2e_chunks} chunks over 2 streams (H2D, unpack, NMS, D2H of masks + counts), "
+                    "d2h_bytes_per_step": d2h_bytes, "matches_device_run": e2e_ok,
+                    "input_format": "the C ABI's int32 x, y, z + float64 s planes (20 B per box), pinned host",
+                    "output": "int32 keep indices [F, 2048] + counts [F], pinned host",
+                    "api": "NmsEngine.run_host(out_idx=..., graph=True)",
+                    "pipeline": f"{e2e_chunks} chunks over 2 streams (H2D, NMS, D2H of keep indices + counts), "
                                 "replayed as one CUDA graph",
                     "h2d_link_gbs": h2d_gbs, "link_bound_frames_per_s": world * F / (copy_ms / 1e3),
                     "frac_of_link_bound": e2e_value / (world * F / (copy_ms / 1e3)),
                     "link_bound_basis": "the step's input planes copied host->device alone (no compute), best of 5"},
+            "e2e_box32": {"value": e2e32_value, "unit": "frames/s", "h2d_bytes_per_step": int(F * BOXES * 12 + F * 4),
+                          "d2h_bytes_per_step": int(F * eng.W32 * 4 + F * 4),
+                          "input_format": "packed 32-bit boxes (pack_box32: x | y<<12 | z<<24) + float64 s",
+                          "output": "survivor masks + counts",
+                          "host_pack_ms_per_step": pack_ms,
+                          "value_with_host_pack": world * F / (e2e32_ms / args.steps / 1e3 + pack_ms / 1e3),
+                          "pack_note": "pack_box32 (numpy, one host thread) of the rank's frames, outside the timed "
+                                       "region; value_with_host_pack adds it serially to every step",
+                          "link_bound_frames_per_s": world * F / (copy32_ms / 1e3)},
             # binned kernel + the one-CTA fallback dispatcher (the dense chain is tail-launched from the
             # device only for declined frames; none in this workload)
             "gpu_launches": 2 * args.steps,
@@ -524,8 +716,8 @@ def main():
                          "kernel": "pnms_binned_frame", "bytes_per_launch": hbm_bytes,
                          "peak_basis": ("of measured (MEASURED_PEAKS.json hbm_gbs)" if hbm_meas
                                         else "of fallback (B200_PROFILING.md)"),
-                         "note": "issue-bound (ncu issue ~80 %, divergent per-row candidate loops), not "
-                                 "bandwidth-bound: the input is read once (traffic ~= algorithmic bytes)"},
+                         "note": "issue-bound (divergent per-row candidate loops), not bandwidth-bound: the input "
+                                 "is read once (traffic ~= algorithmic bytes)"},
             # the same kernel on the integer-op basis of SURVEY.md §8d (one unordered pair test = 8 int
             # ops, dense-equivalent count); the binned kernel culls pairs that cannot overlap, so this
             # fraction exceeds 1 — the executed-pair fraction is the one that measures its ALU use
@@ -536,7 +728,11 @@ def main():
                              "pair_tests_executed_per_launch": pairs_executed,
                              "pair_tests_dense_per_launch": int(BOXES * (BOXES - 1) // 2 * F),
                              "peak_basis": peak_basis},
-            "phase_ms": {"binned": statistics.mean(binned_ms), "dense_fallback": statistics.mean(fallback_ms)},
+            "phase_ms": {"binned": statistics.mean(binned_ms), "dense_fallback": statistics.mean(fallback_ms),
+                         "call": call_ms, "dispatcher_overhead": call_ms - statistics.mean(binned_ms),
+                         "note": "binned = culling kernel + count snapshot (profiled steps); call = the default "
+                                 "call (culling kernel + device-side dispatcher); the difference is the "
+                                 "dispatcher's cost on the timeline"},
             "dense_path": {"value": value_dense, "unit": "frames/s", "ms_per_step": max_total_d / args.steps,
                            "phase_ms": {"sort": statistics.mean(p[0] for p in ph_d),
                                         "map": statistics.mean(p[1] for p in ph_d),

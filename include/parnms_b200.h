@@ -95,6 +95,53 @@ int pnms_run_profiled(const int32_t* x, const int32_t* y, const int32_t* z, cons
                       int32_t* keep_idx, int32_t* keep_count, uint32_t* keep_mask, uint64_t* gate_pairs,
                       void* workspace, size_t workspace_bytes, void* stream, void* const* phase_events);
 
+/* Device paths of pnms_run (every path gives the same, reference-identical result):
+ *   SMALL        single launch, unsorted full pair matrix (tiny calls)
+ *   BINNED       exact spatial culling, one 512-thread CTA per frame (frames <= 4096 slots)
+ *   BINNED_WIDE  the same kernel with one 1024-thread CTA per SM (frames <= 2048 slots)
+ *   TILES        128 independent tile CTAs per frame (latency of large single frames)
+ *   CLUSTER      one thread-block cluster per frame (frames of 4097..65536 slots, batches)
+ *   DENSE        sorted N x N map (prep+sort -> map -> compact), any frame
+ * The culling paths decline frames outside their exactness preconditions (a zero side or
+ * theta = 0, coordinates outside the 15-bit domain, a crowded cell); the device finishes those
+ * frames on the dense pipeline. */
+#define PNMS_PATH_AUTO 0
+#define PNMS_PATH_SMALL 1
+#define PNMS_PATH_BINNED 2
+#define PNMS_PATH_BINNED_WIDE 3
+#define PNMS_PATH_TILES 4
+#define PNMS_PATH_CLUSTER 5
+#define PNMS_PATH_DENSE 6
+
+/* Launch configuration (all fields 0 = the measured defaults).  Tests, tools and the
+ * benchmark use it to pin a path or a decomposition; production callers pass NULL.
+ * It replaces the reference's per-call ThreadPoolExecutor shape (engine.py:156-173,
+ * NmsConfig.k/workers), which never changes the result. */
+typedef struct pnms_launch_config {
+  int path;            /* PNMS_PATH_*; a path that cannot take the call falls back to AUTO */
+  int cluster_size;    /* CLUSTER: 8 or 16 CTAs per frame (0 = 16 when co-schedulable)     */
+  int cell_q8;         /* binned cells: < 0 square side -cell_q8 px, > 0 (max_z+1)*q8/256  */
+  int cell_sx;         /* binned cells: > 0 overrides the cell width                       */
+  int map_rows;        /* DENSE map: rows per lane 1, 2 or 4                               */
+  int map_chunk;       /* DENSE map: column chunk, a multiple of 32 in [32, 4096]           */
+  int small_col_tiles; /* SMALL: column tiles per frame                                    */
+  int host_chain;      /* 1: the host launches the fallback chain for declined frames      */
+  int32_t* declined;   /* device int32[1] or NULL: frames the culling kernel declined      */
+} pnms_launch_config;
+
+/* Path report of one pnms_run_ex call (host memory). */
+typedef struct pnms_run_info {
+  int path;            /* PNMS_PATH_* that ran (declined frames additionally ran DENSE)    */
+} pnms_run_info;
+
+/* pnms_run with an explicit launch configuration (may be NULL), a path report (may be NULL)
+ * and optional phase events (as pnms_run_profiled; may be NULL). */
+int pnms_run_ex(const int32_t* x, const int32_t* y, const int32_t* z, const double* s,
+                const int32_t* counts, int batch, int n_max, int d_max, double theta, int tie_break,
+                int32_t* keep_idx, int32_t* keep_count, uint32_t* keep_mask, uint64_t* gate_pairs,
+                void* workspace, size_t workspace_bytes, void* stream, const pnms_launch_config* config,
+                pnms_run_info* info, void* const* phase_events);
+
 /* Reference-layout map phase (engine.py:176-250): writes the full d_max x d_max
  * SuppressionMatrix — row-major, rows padded to 64-bit words, bit (i,j) at word j/64 bit
  * j%64 (= byte j/8 bit j%8, little endian, engine.py:74-111), pad bits set to 1 — for ONE

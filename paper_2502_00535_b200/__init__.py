@@ -37,7 +37,7 @@ __version__ = "0.1.0"
 def __getattr__(name):
     # torch-dependent entry points load lazily so the host-only API imports without CUDA
     if name in ("batched_nms_keep", "nms_keep", "NmsEngine", "validate_batch", "greedy_nms_keep", "pack_box32",
-                "soft_nms_rescore_batched"):
+                "soft_nms_rescore_batched", "LaunchConfig", "launch_override"):
         from . import tensor_api
 
         return getattr(tensor_api, name)
@@ -49,5 +49,5 @@ __all__ = [
     "DetectionVector", "NmsConfig", "NmsResult", "ParseError", "SuppressionMatrix", "SurvivorMask",
     "ValidationError", "WorkCounters", "map_phase", "mask_survivors", "reduce_phase", "run_nms",
     "batched_nms_keep", "nms_keep", "NmsEngine", "validate_batch", "greedy_nms", "greedy_nms_keep", "pack_box32",
-    "soft_nms_rescore", "soft_nms_rescore_batched",
+    "soft_nms_rescore", "soft_nms_rescore_batched", "LaunchConfig", "launch_override",
 ]

@@ -20,6 +20,7 @@ EXPORTED_SYMBOLS = (
     "pnms_workspace_init",
     "pnms_run",
     "pnms_run_profiled",
+    "pnms_run_ex",
     "pnms_map_reference_layout",
     "pnms_reduce_rows",
     "pnms_validate",
@@ -46,6 +47,24 @@ PNMS_EINVAL_K = -8
 
 TIE_CODES = {"paper_faithful": 0, "by_index": 1}
 MAX_SLOTS = 65536
+
+# PNMS_PATH_* (include/parnms_b200.h)
+PATHS = {"auto": 0, "small": 1, "binned": 2, "binned_wide": 3, "tiles": 4, "cluster": 5, "dense": 6}
+PATH_NAMES = {v: k for k, v in PATHS.items()}
+
+
+class LaunchConfigC(ctypes.Structure):
+    """struct pnms_launch_config"""
+
+    _fields_ = [("path", ctypes.c_int), ("cluster_size", ctypes.c_int), ("cell_q8", ctypes.c_int),
+                ("cell_sx", ctypes.c_int), ("map_rows", ctypes.c_int), ("map_chunk", ctypes.c_int),
+                ("small_col_tiles", ctypes.c_int), ("host_chain", ctypes.c_int), ("declined", ctypes.c_void_p)]
+
+
+class RunInfoC(ctypes.Structure):
+    """struct pnms_run_info"""
+
+    _fields_ = [("path", ctypes.c_int)]
 
 _lib = None
 
@@ -82,6 +101,9 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
     lib.pnms_run.restype = i32
     lib.pnms_run_profiled.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, f64, i32, vp, vp, vp, vp, vp, sz, vp, vp]
     lib.pnms_run_profiled.restype = i32
+    lib.pnms_run_ex.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, f64, i32, vp, vp, vp, vp, vp, sz, vp,
+                                ctypes.POINTER(LaunchConfigC), ctypes.POINTER(RunInfoC), vp]
+    lib.pnms_run_ex.restype = i32
     lib.pnms_map_reference_layout.argtypes = [vp, vp, vp, vp, i32, f64, i32, vp, vp, vp]
     lib.pnms_map_reference_layout.restype = i32
     lib.pnms_reduce_rows.argtypes = [vp, i32, i32, vp, vp]

@@ -80,16 +80,21 @@ inline size_t binned_smem_bytes(int npad) {
 inline int binned_per_thread(int n_max, int threads) { return n_max <= 2 * threads ? 2 : (n_max <= 4 * threads ? 4 : 8); }
 
 // floor(v / S) for 0 <= v < 2^16 as one IMAD.HI: M = floor(2^32 / S) + 1 is exact there
-// (v * (M*S - 2^32) < 2^32).  S >= 2^15 makes every quotient 0 (M = 0).
+// (v * (M*S - 2^32) < 2^32) for 2 <= S < 2^15; S >= 2^15 makes every quotient 0 (M = 0).
+// S = 1 has no 32-bit magic (2^32 + 1): callers keep every cell side >= 2 (kMinCellSide).
+constexpr int kMinCellSide = 2;
 __device__ __forceinline__ uint32_t div_magic(int S) {
-  return S >= 32768 ? 0u : (uint32_t)(0xFFFFFFFFu / (uint32_t)S) + 1u;
+  return S >= 32768 ? 0u : (uint32_t)(0xFFFFFFFFu / (uint32_t)max(S, kMinCellSide)) + 1u;
 }
 __device__ __forceinline__ int qdiv(int v, uint32_t M) { return (int)__umulhi((uint32_t)v, M); }
 
 __device__ __forceinline__ void binned_decline(const BinArgs& a, int f) {
   a.fallback[f] = 1;
   if (a.meta) a.meta[f] = FrameMeta{};
-  a.decl_list[atomicAdd(a.decl_count, 1)] = f;
+  // the count starts at zero (workspace head); the bound keeps a workspace whose head was not
+  // zeroed from writing past the list (the dispatcher clamps the count it reads)
+  const int slot = atomicAdd(a.decl_count, 1);
+  if (slot >= 0 && slot < a.batch) a.decl_list[slot] = f;
 }
 
 // diagnostics: global timer at phase boundaries of frame f (trace[f * 16 + phase]), thread 0;
@@ -252,12 +257,14 @@ __device__ __forceinline__ bool binned_frame_body(const BinArgs& a) {
     const int h = st->maxz + 1;
     const int p2 = 1 << (31 - __clz(h));
     Sy = (long long)h * h > 2LL * p2 * p2 ? 2 * p2 : p2;
-    Sx = max(Sy >> 2, 1);
+    Sx = Sy >> 2;
   } else {
-    Sy = a.cell_q8 < 0 ? -a.cell_q8 : max(1, ((st->maxz + 1) * a.cell_q8 + 255) >> 8);
+    Sy = a.cell_q8 < 0 ? -a.cell_q8 : ((st->maxz + 1) * a.cell_q8 + 255) >> 8;
     Sx = Sy;
   }
   if (a.cell_sx > 0) Sx = a.cell_sx;
+  Sx = max(Sx, kMinCellSide);  // div_magic needs sides >= 2
+  Sy = max(Sy, kMinCellSide);
   int GX = 1, GY = 1;
   const int ox = st->minx, oy = st->miny;
   if (n_act > 0) {

@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kClThreads, 1) pnms_binned_cluster(BinArgs a, 
   // ---- cells Sy >= max side + 1 tall (a row reaches one cell row beyond its own band) and
   // Sx = Sy / 4 wide (the x reach is range-based: narrow cells tighten it, pnms_binned.cuh),
   // cell rows split into CS balanced bands
-  int Sy = g_maxz + 1, Sx = max(Sy >> 2, 1), GX = 1, GY = 1;
+  int Sy = max(g_maxz + 1, kMinCellSide), Sx = max(Sy >> 2, kMinCellSide), GX = 1, GY = 1;
   if (n_act > 0) {
     for (;;) {
       GX = (g_maxx - ox) / Sx + 1;

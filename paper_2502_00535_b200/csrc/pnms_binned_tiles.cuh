@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) pnms_binned_tiles(TileArgs ta
   if (n_act == 0) return;
   // ---- cells Sy = max_z + 1 tall and Sx = Sy / 4 wide (as pnms_binned.cuh: fewer runs per
   // row, tight x ranges) and a tile layout of at most kTilesPerFrame tiles, square in pixels
-  const int Sy = st->maxz + 1, Sx = max(Sy >> 2, 1), ox = st->minx, oy = st->miny;
+  const int Sy = max(st->maxz + 1, kMinCellSide), Sx = max(Sy >> 2, kMinCellSide), ox = st->minx, oy = st->miny;
   const uint32_t Mx = div_magic(Sx), My = div_magic(Sy);
   const int GX = (st->maxx - ox) / Sx + 1, GY = (st->maxy - oy) / Sy + 1;
   const int hx = (st->maxz + Sx - 1) / Sx;  // halo columns: a row reaches max_z pixels either way

@@ -9,7 +9,6 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
-#include <cstdlib>
 #include <cstring>
 #include <utility>
 
@@ -24,8 +23,8 @@
 #include "pnms_fallback.cuh"
 #include "pnms_validate.cuh"
 #include "pnms_binned_cluster.cuh"
-#include "pnms_binned_pairs.cuh"
 #include "pnms_binned_tiles.cuh"
+#include "pnms_gate.cuh"
 #include "pnms_greedy.cuh"
 #include "pnms_soft.cuh"
 #include "pnms_sort.cuh"
@@ -111,36 +110,43 @@ Layout make_layout(int batch, int n_max) {
   return L;
 }
 
-long long env_ll(const char* name, long long dflt) {
-  const char* v = std::getenv(name);
-  if (!v || !*v) return dflt;
-  return std::strtoll(v, nullptr, 10);
-}
-int env_int(const char* name, int dflt) { return (int)env_ll(name, dflt); }
+// ---- per-device caches (attributes and properties are per device: a process may drive several)
+constexpr int kMaxDevices = 64;
 
-// streaming multiprocessors of the current device (cached per process)
+inline int current_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+  return d;
+}
+
+// the largest dynamic shared memory a kernel has been opened up to, per device
+struct SmemCache {
+  std::atomic<size_t> v[kMaxDevices];
+};
+
+template <typename K>
+cudaError_t ensure_smem(K kernel, size_t bytes, SmemCache& c) {
+  std::atomic<size_t>& slot = c.v[current_device()];
+  if (bytes <= 48 * 1024 || slot.load(std::memory_order_relaxed) >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) slot.store(bytes, std::memory_order_relaxed);
+  return e;
+}
+
+// streaming multiprocessors of the current device
 int sm_count() {
-  static std::atomic<int> cached{0};
-  int v = cached.load();
+  static std::atomic<int> cached[kMaxDevices];
+  const int dev = current_device();
+  int v = cached[dev].load();
   if (v > 0) return v;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-    v = 148;
-  cached.store(v);
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+  cached[dev].store(v);
   return v;
 }
 
 int fail_cuda(cudaError_t e) {
   g_last_cuda_error = (int)e;
   return PNMS_ECUDA;
-}
-
-template <typename K>
-cudaError_t ensure_smem(K kernel, size_t bytes, std::atomic<size_t>& configured) {
-  if (bytes <= 48 * 1024 || configured.load(std::memory_order_relaxed) >= bytes) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e == cudaSuccess) configured.store(bytes, std::memory_order_relaxed);
-  return e;
 }
 
 // launch `kernel` with programmatic stream serialization (PDL) when `pdl` is set: it may start
@@ -161,36 +167,14 @@ cudaError_t launch_maybe_pdl(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3
   return cudaLaunchKernelEx(&lc, kernel, std::forward<Args>(args)...);
 }
 
-std::atomic<size_t> g_sort_frame_smem{0}, g_sort_chunk_smem{0}, g_compact_smem{0};
-std::atomic<size_t> g_map_smem[5];
-
-// Internal side stream + events used to overlap a chunk's sort with the previous chunk's
-// map.  One set per host thread and device, created on first use and kept for the process
-// lifetime, so concurrent callers on different threads never share event state.
-struct SideStream {
-  cudaStream_t s = nullptr;
-  cudaEvent_t fork = nullptr;
-  cudaEvent_t ev[32] = {};
-};
-SideStream* side_stream() {
-  thread_local SideStream cache[64];
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  SideStream& ss = cache[dev];
-  if (!ss.s) {
-    if (cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) != cudaSuccess) { ss.s = nullptr; return nullptr; }
-    cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming);
-    for (auto& ev : ss.ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-  }
-  return &ss;
-}
-std::atomic<size_t> g_small_smem[8];
-
-
-std::atomic<size_t> g_binned_smem[16];
+SmemCache g_sort_frame_smem, g_sort_chunk_smem, g_compact_smem, g_sort_list_smem;
+SmemCache g_map_smem[5], g_map_list_smem[5];
+SmemCache g_small_smem[8];
+SmemCache g_binned_smem[8];
+SmemCache g_tiles_smem[2];
 
 template <bool B, bool C, int P, int T>
-cudaError_t launch_binned_t(const BinArgs& ba, int batch, size_t smem, cudaStream_t st, std::atomic<size_t>& cfg) {
+cudaError_t launch_binned_t(const BinArgs& ba, int batch, size_t smem, cudaStream_t st, SmemCache& cfg) {
   cudaError_t e = ensure_smem(pnms_binned_frame<B, C, P, T>, smem, cfg);
   if (e != cudaSuccess) return e;
   pnms_binned_frame<B, C, P, T><<<batch, T, smem, st>>>(ba);
@@ -205,15 +189,16 @@ int cluster_slice(int n_max, int cs) {
 
 template <bool B, int CS, int P>
 cudaError_t launch_cluster_t(const BinArgs& ba, int batch, int slice, cudaStream_t st) {
-  static std::atomic<size_t> cfg{0};
-  static std::atomic<int> nonportable{0};
+  static SmemCache cfg;
+  static std::atomic<int> nonportable[kMaxDevices];
   const size_t smem = binned_cluster_smem_bytes();
   cudaError_t e = ensure_smem(pnms_binned_cluster<B, CS, P>, smem, cfg);
   if (e != cudaSuccess) return e;
-  if (CS > 8 && !nonportable.load()) {
+  std::atomic<int>& np = nonportable[current_device()];
+  if (CS > 8 && !np.load()) {
     e = cudaFuncSetAttribute(pnms_binned_cluster<B, CS, P>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
-    nonportable.store(1);
+    np.store(1);
   }
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3((unsigned)batch * CS);
@@ -230,11 +215,13 @@ cudaError_t launch_cluster_t(const BinArgs& ba, int batch, int slice, cudaStream
   return cudaLaunchKernelEx(&lc, pnms_binned_cluster<B, CS, P>, ba, slice);
 }
 
-// cluster size: 16 CTAs (non-portable; one GPC) when the device can co-schedule them, else 8
-int cluster_size_for(int n_max) {
-  static std::atomic<int> cs16_cached{-1};  // probed once per process (benign if two threads race)
-  int cs16 = cs16_cached.load();
-  if (cs16 < 0) {
+// whether the current device can co-schedule a 16-CTA cluster of the cluster kernel (probed
+// once per device; benign if two threads race)
+bool cluster16_ok() {
+  static std::atomic<int> cached[kMaxDevices] = {};
+  std::atomic<int>& c = cached[current_device()];
+  int v = c.load();
+  if (v == 0) {
     int n = 0;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(16);
@@ -253,17 +240,21 @@ int cluster_size_for(int n_max) {
                   cudaSuccess &&
               cudaOccupancyMaxActiveClusters(&n, fn, &lc) == cudaSuccess && n > 0;
     cudaGetLastError();
-    cs16 = ok ? 1 : 0;
-    cs16_cached.store(cs16);
+    v = ok ? 1 : 2;
+    c.store(v);
   }
-  const int want = env_int("PNMS_CLUSTER", 0);
+  return v == 1;
+}
+
+// cluster size: 16 CTAs (non-portable; one GPC) when the device can co-schedule them and the
+// frame is large, else 8; `want` (8 or 16) pins it
+int cluster_size_for(int n_max, int want) {
+  const bool cs16 = cluster16_ok();
   if (want == 8 || want == 16) return (want == 16 && !cs16) ? 8 : want;
   return (cs16 && n_max > 8 * 1024) ? 16 : 8;
 }
 
-cudaError_t launch_cluster(const BinArgs& ba, int batch, int n_max, bool by_index, cudaStream_t st) {
-  const int cs = cluster_size_for(n_max);
-  const int slice = cluster_slice(n_max, cs);
+cudaError_t launch_cluster(const BinArgs& ba, int batch, int cs, int slice, bool by_index, cudaStream_t st) {
   const int per = slice <= kClThreads ? 1 : (slice <= 2 * kClThreads ? 2 : 4);
 #define PNMS_CL(CS, P) (by_index ? launch_cluster_t<true, CS, P>(ba, batch, slice, st) \
                                  : launch_cluster_t<false, CS, P>(ba, batch, slice, st))
@@ -272,56 +263,37 @@ cudaError_t launch_cluster(const BinArgs& ba, int batch, int n_max, bool by_inde
 #undef PNMS_CL
 }
 
-std::atomic<size_t> g_pairs_smem[8];
-
-
-
-template <bool B, bool C, int P>
-cudaError_t launch_pairs_t(const BinArgs& ba, int batch, size_t smem, cudaStream_t st, std::atomic<size_t>& cfg) {
-  cudaError_t e = ensure_smem(pnms_binned_pairs_frame<B, C, P>, smem, cfg);
-  if (e != cudaSuccess) return e;
-  pnms_binned_pairs_frame<B, C, P><<<batch, kPairThreads, smem, st>>>(ba);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_pairs(int variant, const BinArgs& ba, int batch, size_t smem, cudaStream_t st) {
-  switch (variant) {
-    case 0: return launch_pairs_t<false, false, 4>(ba, batch, smem, st, g_pairs_smem[0]);
-    case 1: return launch_pairs_t<true, false, 4>(ba, batch, smem, st, g_pairs_smem[1]);
-    case 2: return launch_pairs_t<false, true, 4>(ba, batch, smem, st, g_pairs_smem[2]);
-    case 3: return launch_pairs_t<true, true, 4>(ba, batch, smem, st, g_pairs_smem[3]);
-    case 4: return launch_pairs_t<false, false, 8>(ba, batch, smem, st, g_pairs_smem[4]);
-    case 5: return launch_pairs_t<true, false, 8>(ba, batch, smem, st, g_pairs_smem[5]);
-    case 6: return launch_pairs_t<false, true, 8>(ba, batch, smem, st, g_pairs_smem[6]);
-    default: return launch_pairs_t<true, true, 8>(ba, batch, smem, st, g_pairs_smem[7]);
-  }
-}
-
-// variant bits: 1 by_index, 2 count pairs, 4 eight boxes per thread; `latency` picks 1024-thread
+// variant bits: 1 by_index, 2 count pairs, 4 eight boxes per thread; `wide` picks 1024-thread
 // CTAs (one per SM, two boxes per thread) for batches that fit one wave
-cudaError_t launch_binned(int variant, const BinArgs& ba, int batch, size_t smem, cudaStream_t st, bool latency) {
-  if (latency) {
+cudaError_t launch_binned(int variant, const BinArgs& ba, int batch, size_t smem, cudaStream_t st, bool wide) {
+  if (wide) {
     switch (variant & 3) {
-      case 0: return launch_binned_t<false, false, 2, 1024>(ba, batch, smem, st, g_binned_smem[8]);
-      case 1: return launch_binned_t<true, false, 2, 1024>(ba, batch, smem, st, g_binned_smem[9]);
-      case 2: return launch_binned_t<false, true, 2, 1024>(ba, batch, smem, st, g_binned_smem[10]);
-      default: return launch_binned_t<true, true, 2, 1024>(ba, batch, smem, st, g_binned_smem[11]);
+      case 0: return launch_binned_t<false, false, 2, 1024>(ba, batch, smem, st, g_binned_smem[4]);
+      case 1: return launch_binned_t<true, false, 2, 1024>(ba, batch, smem, st, g_binned_smem[5]);
+      case 2: return launch_binned_t<false, true, 2, 1024>(ba, batch, smem, st, g_binned_smem[6]);
+      default: return launch_binned_t<true, true, 2, 1024>(ba, batch, smem, st, g_binned_smem[7]);
     }
   }
-  switch (variant) {
-    case 0: return launch_binned_t<false, false, 4, kBinThreads>(ba, batch, smem, st, g_binned_smem[0]);
-    case 1: return launch_binned_t<true, false, 4, kBinThreads>(ba, batch, smem, st, g_binned_smem[1]);
-    case 2: return launch_binned_t<false, true, 4, kBinThreads>(ba, batch, smem, st, g_binned_smem[2]);
-    case 3: return launch_binned_t<true, true, 4, kBinThreads>(ba, batch, smem, st, g_binned_smem[3]);
-    case 4: return launch_binned_t<false, false, 8, kBinThreads>(ba, batch, smem, st, g_binned_smem[4]);
-    case 5: return launch_binned_t<true, false, 8, kBinThreads>(ba, batch, smem, st, g_binned_smem[5]);
-    case 6: return launch_binned_t<false, true, 8, kBinThreads>(ba, batch, smem, st, g_binned_smem[6]);
-    default: return launch_binned_t<true, true, 8, kBinThreads>(ba, batch, smem, st, g_binned_smem[7]);
+  switch (variant & 3) {
+    case 0: return launch_binned_t<false, false, 8, kBinThreads>(ba, batch, smem, st, g_binned_smem[0]);
+    case 1: return launch_binned_t<true, false, 8, kBinThreads>(ba, batch, smem, st, g_binned_smem[1]);
+    case 2: return launch_binned_t<false, true, 8, kBinThreads>(ba, batch, smem, st, g_binned_smem[2]);
+    default: return launch_binned_t<true, true, 8, kBinThreads>(ba, batch, smem, st, g_binned_smem[3]);
+  }
+}
+
+cudaError_t launch_binned4(int variant, const BinArgs& ba, int batch, size_t smem, cudaStream_t st) {
+  static SmemCache c[4];
+  switch (variant & 3) {
+    case 0: return launch_binned_t<false, false, 4, kBinThreads>(ba, batch, smem, st, c[0]);
+    case 1: return launch_binned_t<true, false, 4, kBinThreads>(ba, batch, smem, st, c[1]);
+    case 2: return launch_binned_t<false, true, 4, kBinThreads>(ba, batch, smem, st, c[2]);
+    default: return launch_binned_t<true, true, 4, kBinThreads>(ba, batch, smem, st, c[3]);
   }
 }
 
 template <bool B, bool C, int R>
-cudaError_t launch_small_t(const SmallArgs& sa, long long grid, size_t smem, cudaStream_t st, std::atomic<size_t>& cfg) {
+cudaError_t launch_small_t(const SmallArgs& sa, long long grid, size_t smem, cudaStream_t st, SmemCache& cfg) {
   cudaError_t e = ensure_smem(pnms_small_kernel<B, C, R>, smem, cfg);
   if (e != cudaSuccess) return e;
   pnms_small_kernel<B, C, R><<<(unsigned)grid, kSmallThreads, smem, st>>>(sa);
@@ -342,13 +314,42 @@ cudaError_t launch_small(int v, const SmallArgs& sa, long long grid, size_t smem
   }
 }
 
-// Calls with little total work run the single-launch unsorted path (pnms_small.cuh).
-bool use_small_path(int batch, int n_max) {
+// ---- path selection ---------------------------------------------------------------------
+// Calls with little total work run the single-launch unsorted path (pnms_small.cuh): below
+// 24 Mi slot pairs per call (measured: the single launch beats the sort/cull pipelines there)
+constexpr long long kSmallPairs = 24LL << 20;
+// calls of <= 2 frames above this many slots take the multi-CTA tile path (measured,
+// tools/single_frame_paths.py: a 4096-box random frame 22 us on tiles against 52 us on one CTA)
+constexpr int kTilesSmallSlots = 2048;
+
+bool small_fits(int batch, int n_max) {
   const int W32 = (n_max + 31) / 32;
-  if (n_max > kSortMax || batch > kSmallMaxFrames || (long long)batch * W32 > kSmallMaxWords) return false;
-  const long long pairs = (long long)batch * n_max * n_max;
-  const long long limit = env_ll("PNMS_SMALL_PAIRS", 24LL << 20);
-  return pairs <= limit;
+  return n_max <= kSortMax && batch <= kSmallMaxFrames && (long long)batch * W32 <= kSmallMaxWords;
+}
+
+bool cluster_fits(int n_max, int cs) { return cluster_slice(n_max, 16) > 0 && cluster_slice(n_max, cs) > 0; }
+
+bool path_fits(int path, int batch, int n_max, int cs) {
+  switch (path) {
+    case PNMS_PATH_SMALL: return small_fits(batch, n_max);
+    case PNMS_PATH_BINNED: return n_max <= kBinMaxSlots;
+    case PNMS_PATH_BINNED_WIDE: return n_max <= 2048;
+    case PNMS_PATH_TILES: return n_max <= PNMS_MAX_SLOTS;
+    case PNMS_PATH_CLUSTER: return cluster_fits(n_max, cs);
+    case PNMS_PATH_DENSE: return true;
+    default: return false;
+  }
+}
+
+int auto_path(int batch, int n_max, int cs) {
+  if (small_fits(batch, n_max) && (long long)batch * n_max * n_max <= kSmallPairs) return PNMS_PATH_SMALL;
+  if (n_max <= kBinMaxSlots) {
+    if (batch <= 2 && n_max > kTilesSmallSlots) return PNMS_PATH_TILES;
+    // one wave of 1024-thread CTAs (two boxes per thread) when the batch fits the SMs
+    return (n_max <= 2048 && batch <= sm_count()) ? PNMS_PATH_BINNED_WIDE : PNMS_PATH_BINNED;
+  }
+  if (batch <= 2 || !cluster_fits(n_max, cs)) return PNMS_PATH_TILES;
+  return PNMS_PATH_CLUSTER;
 }
 
 struct MapShape {
@@ -363,7 +364,7 @@ int items_per_frame(int n_max, int RB, int chunk) {
 
 // Work-item shape: the largest (rows-per-lane, chunk) whose item count still gives every SM
 // a few items to balance the triangular work (measured on B200 with tools/tune_map.py).
-MapShape choose_map_shape(int batch, int n_max) {
+MapShape choose_map_shape(int batch, int n_max, const pnms_launch_config& lc) {
   static const int cand[][2] = {{4, 1024}, {4, 512}, {2, 512}, {2, 256}, {1, 256}};
   MapShape m{1, kMapWarps * 32, 256};
   for (const auto& c : cand) {
@@ -372,15 +373,13 @@ MapShape choose_map_shape(int batch, int n_max) {
     m.chunk = c[1];
     if (items >= 512) break;
   }
-  const int r_env = env_int("PNMS_MAP_R", 0);
-  if (r_env == 1 || r_env == 2 || r_env == 4) m.R = r_env;
-  const int c_env = env_int("PNMS_MAP_CHUNK", 0);
-  if (c_env >= 32 && c_env <= 4096 && (c_env % 32) == 0) m.chunk = c_env;
+  if (lc.map_rows == 1 || lc.map_rows == 2 || lc.map_rows == 4) m.R = lc.map_rows;
+  if (lc.map_chunk >= 32 && lc.map_chunk <= 4096 && (lc.map_chunk % 32) == 0) m.chunk = lc.map_chunk;
   m.RB = kMapWarps * 32 * m.R;
   return m;
 }
 
-// when the host launches the fallback chain (profiled calls, PNMS_DEVCHAIN=0): the declined
+// when the host launches the fallback chain (profiled calls, host_chain): the declined
 // count is snapshotted for the chain and zeroed for the next call, as the dispatcher does
 __global__ void pnms_count_snapshot(int* count, int* snap, int batch) {
   pdl_wait();
@@ -398,12 +397,10 @@ static_assert(kDeclCountOffset + 4 <= kSmallScratchBytes, "scratch");
 constexpr size_t kTilesScratchOffset = 32 * 1024;
 static_assert(kDeclCountOffset + 4 <= kTilesScratchOffset, "scratch");
 
-
 template <int R>
 cudaError_t launch_map(const MapArgs& ma, long long grid, size_t smem, cudaStream_t st, bool list) {
   if (list) {
-    static std::atomic<size_t> lcfg{0};
-    cudaError_t e = ensure_smem(pnms_map_kernel_list<R>, smem, lcfg);
+    cudaError_t e = ensure_smem(pnms_map_kernel_list<R>, smem, g_map_list_smem[R]);
     if (e != cudaSuccess) return e;
     return launch_maybe_pdl(true, pnms_map_kernel_list<R>, dim3((unsigned)grid), dim3(kMapWarps * 32), smem, st, ma);
   }
@@ -411,6 +408,329 @@ cudaError_t launch_map(const MapArgs& ma, long long grid, size_t smem, cudaStrea
   if (e != cudaSuccess) return e;
   pnms_map_kernel<R><<<(unsigned)grid, kMapWarps * 32, smem, st>>>(ma);
   return cudaGetLastError();
+}
+
+// WorkCounters.map_writes from the scores alone (pnms_gate.cuh), for the culling paths; runs
+// after the call's other kernels and reuses the workspace from the record region on
+cudaError_t launch_gate_pairs(const double* s, const int32_t* counts, int batch, int n_max, int d_max, int tie_break,
+                              uint64_t* gate_pairs, uint8_t* ws, const Layout& L, cudaStream_t st) {
+  GateArgs ga;
+  ga.s = s; ga.counts = counts; ga.batch = batch; ga.n_max = n_max; ga.d_max = d_max; ga.tie_break = tie_break;
+  ga.cap = 2 * n_max;
+  const size_t keys_b = (size_t)batch * ga.cap * 8, mult_b = (size_t)batch * ga.cap * 4;
+  ga.keys = reinterpret_cast<unsigned long long*>(ws + L.rec);
+  ga.mult = reinterpret_cast<uint32_t*>(ws + L.rec + keys_b);
+  ga.acc = reinterpret_cast<unsigned long long*>(ws + L.rec + keys_b + mult_b);  // 8 B aligned
+  ga.gate_pairs = reinterpret_cast<unsigned long long*>(gate_pairs);
+  // keys + multiplicities + accumulators: 24 B per slot + 16 B per frame <= the 40 B per slot
+  // of the record, perm and lim regions that follow each other from L.rec
+  cudaError_t e = cudaMemsetAsync(ws + L.rec, 0, keys_b + mult_b + (size_t)batch * 16, st);
+  if (e != cudaSuccess) return e;
+  pnms_gate_ties<<<dim3((unsigned)((n_max + kGateThreads - 1) / kGateThreads), (unsigned)batch), kGateThreads, 0, st>>>(ga);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  pnms_gate_finalize<<<(unsigned)((batch + kGateThreads - 1) / kGateThreads), kGateThreads, 0, st>>>(ga);
+  return cudaGetLastError();
+}
+
+inline cudaError_t mark(void* const* events, int i, cudaStream_t st) {
+  if (!events || !events[i]) return cudaSuccess;
+  return cudaEventRecord((cudaEvent_t)events[i], st);
+}
+
+int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double* s, const int32_t* counts,
+             int batch, int n_max, int d_max, double theta, int tie_break, int32_t* keep_idx,
+             int32_t* keep_count, uint32_t* keep_mask, uint64_t* gate_pairs, void* workspace,
+             size_t workspace_bytes, void* stream, const pnms_launch_config* config, pnms_run_info* info,
+             void* const* events) {
+  if (!(theta >= 0.0 && theta <= 1.0)) return PNMS_EINVAL_THETA;
+  if (d_max < 1) return PNMS_EINVAL_DMAX;
+  if (tie_break != PNMS_TIE_PAPER_FAITHFUL && tie_break != PNMS_TIE_BY_INDEX) return PNMS_EINVAL_TIE;
+  if (batch < 0 || n_max < 0) return PNMS_EINVAL_ARG;
+  if (n_max > PNMS_MAX_SLOTS) return PNMS_ETOO_LARGE;
+  const pnms_launch_config lc = config ? *config : pnms_launch_config{};
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  if (info) info->path = PNMS_PATH_AUTO;
+  if (lc.declined && (e = cudaMemsetAsync(lc.declined, 0, sizeof(int32_t), st)) != cudaSuccess) return fail_cuda(e);
+  if (batch == 0 || n_max == 0) {
+    if (batch > 0 && keep_count) {
+      e = cudaMemsetAsync(keep_count, 0, sizeof(int32_t) * batch, st);
+      if (e != cudaSuccess) return fail_cuda(e);
+    }
+    if (batch > 0 && gate_pairs) {
+      // all d_max slots are padding (0,0,0,0.0): only by_index gates equal-score pairs
+      // (handled on the host side of the Python layer; here report zero work)
+      e = cudaMemsetAsync(gate_pairs, 0, sizeof(uint64_t) * batch, st);
+      if (e != cudaSuccess) return fail_cuda(e);
+    }
+    return PNMS_OK;
+  }
+  if (!x || !y || !z || !s) return PNMS_EINVAL_ARG;
+  const Layout L = make_layout(batch, n_max);
+  if (!workspace || workspace_bytes < L.total) return PNMS_EWORKSPACE;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  const int W32 = (n_max + 31) / 32;
+  const int cs = cluster_size_for(n_max, lc.cluster_size);
+  int path = lc.path;
+  if (path != PNMS_PATH_AUTO && !path_fits(path, batch, n_max, cs)) path = PNMS_PATH_AUTO;
+  if (path == PNMS_PATH_AUTO) path = auto_path(batch, n_max, cs);
+  if (info) info->path = path;
+
+  if (path == PNMS_PATH_SMALL) {
+    SmallArgs sa;
+    sa.x = x; sa.y = y; sa.z = z; sa.s = s; sa.counts = counts;
+    sa.batch = batch; sa.n_max = n_max; sa.d_max = d_max; sa.tie_break = tie_break; sa.W32 = W32;
+    sa.theta = theta;
+    const int R = ((long long)batch * n_max <= 2048) ? 1 : kSmallRowsMax;  // tiny calls: more CTAs
+    sa.n_rt = (n_max + kSmallThreads * R - 1) / (kSmallThreads * R);
+    const int max_ct = (n_max + 31) / 32;
+    int n_ct = (int)std::min<long long>(max_ct, std::max<long long>(1, (2LL * 148 + (long long)batch * sa.n_rt - 1) /
+                                                                         ((long long)batch * sa.n_rt)));
+    if (lc.small_col_tiles > 0) n_ct = std::min(lc.small_col_tiles, max_ct);
+    sa.cols = ((n_max + n_ct - 1) / n_ct + 31) / 32 * 32;
+    sa.n_ct = (n_max + sa.cols - 1) / sa.cols;
+    sa.supp = reinterpret_cast<uint32_t*>(ws);
+    sa.ticket = reinterpret_cast<unsigned int*>(ws + kSmallMaxWords * 4);
+    sa.gacc = reinterpret_cast<unsigned long long*>(ws + kSmallMaxWords * 4 + kSmallMaxFrames * 4);
+    sa.keep_idx = keep_idx; sa.keep_count = keep_count; sa.keep_mask = keep_mask;
+    sa.gate_pairs = reinterpret_cast<unsigned long long*>(gate_pairs);
+    const size_t smem = (size_t)sa.cols * (8 + sizeof(RecWide));
+    const long long grid = (long long)batch * sa.n_rt * sa.n_ct;
+    if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
+    if ((e = mark(events, 1, st)) != cudaSuccess) return fail_cuda(e);
+    const int variant = (tie_break == PNMS_TIE_BY_INDEX ? 2 : 0) + (gate_pairs != nullptr ? 1 : 0) + (R == 1 ? 4 : 0);
+    if ((e = launch_small(variant, sa, grid, smem, st)) != cudaSuccess) return fail_cuda(e);
+    if ((e = mark(events, 2, st)) != cudaSuccess) return fail_cuda(e);
+    if ((e = mark(events, 3, st)) != cudaSuccess) return fail_cuda(e);
+    return PNMS_OK;
+  }
+
+  // arguments of the dense pipeline (prep+sort -> map -> compact) for frames [f0, f0 + nf)
+  const MapShape ms = choose_map_shape(batch, n_max, lc);
+  const bool culling = path != PNMS_PATH_DENSE;
+  // the culling paths count map_writes from the scores (pnms_gate.cuh); the dense pipeline
+  // counts the gate passes of its own sorted map
+  uint64_t* dense_gate = culling ? nullptr : gate_pairs;
+  auto chain_args = [&](int f0, int nf, const uint8_t* dense, const int32_t* list, const int* list_count,
+                        PrepArgs& pa, MapArgs& ma, CompactArgs& ca) {
+    const size_t fo = (size_t)f0 * n_max;
+    pa.x = x + fo; pa.y = y + fo; pa.z = z + fo; pa.s = s + fo; pa.counts = counts ? counts + f0 : nullptr;
+    pa.batch = nf; pa.n_max = n_max; pa.tie_break = tie_break; pa.W32 = W32;
+    pa.theta = theta;
+    pa.rec = ws + L.rec + fo * kRecBytes;
+    pa.perm = reinterpret_cast<int32_t*>(ws + L.perm) + fo;
+    pa.lim = reinterpret_cast<int32_t*>(ws + L.lim) + fo;
+    pa.supp = reinterpret_cast<uint32_t*>(ws + L.supp) + (size_t)f0 * W32;
+    pa.meta = reinterpret_cast<FrameMeta*>(ws + L.meta) + f0;
+    pa.sk_scratch = L.sk ? reinterpret_cast<uint64_t*>(ws + L.sk) + fo : nullptr;
+    pa.idx_scratch = L.idx ? reinterpret_cast<int32_t*>(ws + L.idx) + fo : nullptr;
+    pa.dense = dense ? dense + f0 : nullptr;
+    pa.list = list;
+    pa.list_count = list_count;
+    if (n_max <= kSortMax) {
+      pa.npad = (n_max + kSortThreads - 1) / kSortThreads * kSortThreads;
+      pa.nchunks = 1;
+    } else {
+      pa.npad = kSortMax;
+      pa.nchunks = (n_max + kSortMax - 1) / kSortMax;
+    }
+    ma.rec = pa.rec; ma.lim = pa.lim; ma.supp = pa.supp; ma.meta = pa.meta;
+    ma.batch = nf; ma.n_max = n_max; ma.W32 = W32;
+    ma.rows_per_block = ms.RB;
+    ma.chunk = ms.chunk;
+    ma.n_rb = (n_max + ms.RB - 1) / ms.RB;
+    ma.items_per_frame = items_per_frame(n_max, ms.RB, ms.chunk);
+    ma.dense = pa.dense;
+    ma.list = list;
+    ma.list_count = list_count;
+    ca.s = pa.s; ca.counts = pa.counts; ca.perm = pa.perm; ca.supp = pa.supp; ca.meta = pa.meta;
+    ca.batch = nf; ca.n_max = n_max; ca.W32 = W32; ca.d_max = d_max; ca.tie_break = tie_break;
+    ca.keep_idx = keep_idx ? keep_idx + fo : nullptr;
+    ca.keep_count = keep_count ? keep_count + f0 : nullptr;
+    ca.keep_mask = keep_mask ? keep_mask + (size_t)f0 * W32 : nullptr;
+    ca.gate_pairs = dense_gate ? reinterpret_cast<unsigned long long*>(dense_gate) + f0 : nullptr;
+    ca.dense = pa.dense;
+    ca.list = list;
+    ca.list_count = list_count;
+  };
+  const size_t compact_smem = ((size_t)W32 + 3) / 4 * 16 + 64 * 4;
+  const size_t map_smem = (size_t)ms.chunk * kRecBytes;
+  // one-CTA dispatcher behind a declining kernel (pnms_fallback.cuh): snapshots the declined
+  // count into `snap`, zeroes it and, when frames were declined, tail-launches the dense chain
+  // over them; `*host_chain` is set when the host must launch the chain itself (profiled calls)
+  auto dispatch_fallback = [&](const int32_t* list, int* count, int* snap, bool* host_chain) -> cudaError_t {
+    FallbackPlan plan{};
+    chain_args(0, batch, ws + L.dense, list, snap, plan.pa, plan.ma, plan.ca);
+    plan.chunked = n_max > kSortMax;
+    plan.map_R = ms.R;
+    plan.sort_smem = (int)(plan.chunked ? sort_smem_bytes(kSortMax) : sort_frame_smem_bytes(plan.pa.npad));
+    plan.map_smem = (int)map_smem;
+    plan.compact_smem = (int)compact_smem;
+#ifdef PNMS_NO_DEVCHAIN  // diagnostic build without the relocatable unit (sanitizer tools)
+    plan.enabled = 0;
+#else
+    plan.enabled = events == nullptr && lc.host_chain == 0;
+#endif
+    *host_chain = !plan.enabled;
+    cudaError_t err;
+    if (!plan.enabled) {  // snapshot + zero only; the host launches the chain over `snap`
+      err = launch_maybe_pdl(true, pnms_count_snapshot, dim3(1), dim3(32), 0, st, count, snap, batch);
+    } else {
+#ifndef PNMS_NO_DEVCHAIN
+      static const bool same_layout = pnms_devchain_plan_size() == sizeof(FallbackPlan);
+      if (!same_layout) return cudaErrorInvalidValue;
+      err = pnms_devchain_prepare(plan.chunked, ms.R, plan.sort_smem, map_smem, compact_smem);
+      if (err == cudaSuccess) err = pnms_devchain_dispatch(&plan, count, snap, st);
+#else
+      err = cudaSuccess;
+#endif
+    }
+    if (err == cudaSuccess && lc.declined)
+      err = cudaMemcpyAsync(lc.declined, snap, sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
+    return err;
+  };
+  // the counter runs behind everything else of the call (stream order includes the
+  // dispatcher's tail launches)
+  auto finish = [&]() -> int {
+    if (culling && gate_pairs) {
+      cudaError_t err = launch_gate_pairs(s, counts, batch, n_max, d_max, tie_break, gate_pairs, ws, L, st);
+      if (err != cudaSuccess) return fail_cuda(err);
+    }
+    return PNMS_OK;
+  };
+
+  const uint8_t* dense_flags = nullptr;
+  const int32_t* decl_list = nullptr;  // culling paths: the declined frames, read on the device
+  const int* decl_count = nullptr;
+  void* ev_local[4];
+  BinArgs ba{};
+  ba.x = x; ba.y = y; ba.z = z; ba.s = s; ba.counts = counts;
+  ba.batch = batch; ba.n_max = n_max; ba.d_max = d_max; ba.tie_break = tie_break; ba.W32 = W32;
+  ba.theta = theta;
+  ba.fallback = ws + L.dense;
+  ba.decl_count = reinterpret_cast<int*>(ws + kDeclCountOffset);  // zeroed scratch, left zero by the dispatcher
+  ba.decl_list = reinterpret_cast<int32_t*>(ws + L.list) + 1;
+  ba.keep_idx = keep_idx; ba.keep_count = keep_count; ba.keep_mask = keep_mask;
+  ba.trace = g_trace;
+  ba.cell_q8 = lc.cell_q8;
+  ba.cell_sx = lc.cell_sx;
+  if (culling) {
+    if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
+    if (path == PNMS_PATH_BINNED || path == PNMS_PATH_BINNED_WIDE) {
+      // ---- exact spatial culling, one CTA per frame (pnms_binned.cuh)
+      ba.pairs_tested = g_pairs_counter;
+      ba.meta = nullptr;  // the frame-level sort rewrites FrameMeta of declined frames
+      const size_t smem = binned_smem_bytes(binned_npad(n_max));
+      const int variant = (tie_break == PNMS_TIE_BY_INDEX ? 1 : 0) + (g_pairs_counter ? 2 : 0);
+      const int per = binned_per_thread(n_max, kBinThreads);
+      if (path == PNMS_PATH_BINNED_WIDE) e = launch_binned(variant, ba, batch, smem, st, true);
+      else if (per <= 4) e = launch_binned4(variant, ba, batch, smem, st);
+      else e = launch_binned(variant, ba, batch, smem, st, false);
+      if (e != cudaSuccess) return fail_cuda(e);
+    } else if (path == PNMS_PATH_TILES) {
+      // ---- large single frames: kTilesPerFrame independent tile CTAs per frame (pnms_binned_tiles.cuh)
+      ba.pairs_tested = nullptr;
+      ba.meta = reinterpret_cast<FrameMeta*>(ws + L.meta);  // the chunked sort accumulates into it
+      TileArgs ta;
+      ta.b = ba;
+      // decline flags and survivor masks in the zeroed scratch (pnms_mask_compact re-zeroes
+      // them) when they fit — the latency case, <= 2 frames — else zeroed per call
+      const size_t fbytes = ((size_t)batch * 4 + 15) / 16 * 16;
+      const size_t tbytes = fbytes + (size_t)batch * W32 * 4;
+      const bool in_scratch = kTilesScratchOffset + tbytes <= kSmallScratchBytes;
+      uint8_t* tbase = in_scratch ? ws + kTilesScratchOffset : (L.tiles ? ws + L.tiles : ws + L.rec);
+      ta.decline = reinterpret_cast<int*>(tbase);
+      ta.mask = reinterpret_cast<uint32_t*>(tbase + fbytes);
+      if (!in_scratch && (e = cudaMemsetAsync(tbase, 0, tbytes, st)) != cudaSuccess) return fail_cuda(e);
+      const size_t tsmem = binned_tiles_smem_bytes();
+      const bool bi = tie_break == PNMS_TIE_BY_INDEX;
+      if ((e = ensure_smem(bi ? pnms_binned_tiles<true> : pnms_binned_tiles<false>, tsmem, g_tiles_smem[bi])) != cudaSuccess)
+        return fail_cuda(e);
+      if ((e = launch_maybe_pdl(false, bi ? pnms_binned_tiles<true> : pnms_binned_tiles<false>,
+                                dim3((unsigned)batch * kTilesPerFrame), dim3(kTileThreads), tsmem, st, ta)) != cudaSuccess)
+        return fail_cuda(e);
+      if ((e = launch_maybe_pdl(true, pnms_mask_compact, dim3((unsigned)batch), dim3(512), 0, st, ta)) != cudaSuccess)
+        return fail_cuda(e);
+    } else {
+      // ---- large frames in batches: one thread-block cluster per frame (pnms_binned_cluster.cuh)
+      ba.pairs_tested = nullptr;
+      ba.meta = reinterpret_cast<FrameMeta*>(ws + L.meta);
+      if ((e = launch_cluster(ba, batch, cs, cluster_slice(n_max, cs), tie_break == PNMS_TIE_BY_INDEX, st)) !=
+          cudaSuccess)
+        return fail_cuda(e);
+    }
+    // declined frames: the dense pipeline, tail-launched from the device by the dispatcher
+    decl_list = ba.decl_list;
+    int* snap = reinterpret_cast<int*>(ws + L.list);
+    bool host_chain = false;
+    if ((e = dispatch_fallback(ba.decl_list, ba.decl_count, snap, &host_chain)) != cudaSuccess) return fail_cuda(e);
+    if (!host_chain) {
+      if ((e = mark(events, 3, st)) != cudaSuccess) return fail_cuda(e);
+      return finish();
+    }
+    decl_count = snap;
+    dense_flags = ws + L.dense;
+    if (events) {
+      // phases become: [0,1) culling kernel, [1,2) dense prep of declined frames, [2,3) their map+compact
+      ev_local[0] = events[1]; ev_local[1] = events[2]; ev_local[2] = nullptr; ev_local[3] = events[3];
+      events = ev_local;
+    }
+  }
+
+  // ---- sorted pipeline: prep+sort -> map -> compact (every frame, or the declined list)
+  {
+    const int nf = batch;
+    PrepArgs pa;
+    MapArgs ma;
+    CompactArgs ca;
+    chain_args(0, nf, dense_flags, decl_list, decl_count, pa, ma, ca);
+    if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
+    if (n_max <= kSortMax) {
+      const size_t smem = sort_frame_smem_bytes(pa.npad);
+      if (decl_list) {
+        if ((e = ensure_smem(pnms_prep_sort_frame_list, smem, g_sort_list_smem)) != cudaSuccess) return fail_cuda(e);
+        if ((e = launch_maybe_pdl(true, pnms_prep_sort_frame_list, dim3(std::min(nf, 148 * 2)), dim3(kSortThreads),
+                                  smem, st, pa)) != cudaSuccess)
+          return fail_cuda(e);
+      } else {
+        if ((e = ensure_smem(pnms_prep_sort_frame, smem, g_sort_frame_smem)) != cudaSuccess) return fail_cuda(e);
+        pnms_prep_sort_frame<<<nf, kSortThreads, smem, st>>>(pa);
+        if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
+      }
+    } else {
+      // the declined-frame list path had each frame's FrameMeta zeroed by the decliner
+      if (!decl_list && (e = cudaMemsetAsync(pa.meta, 0, sizeof(FrameMeta) * (size_t)nf, st)) != cudaSuccess)
+        return fail_cuda(e);
+      const size_t smem = sort_smem_bytes(kSortMax);
+      if ((e = ensure_smem(pnms_prep_sort_chunk, smem, g_sort_chunk_smem)) != cudaSuccess) return fail_cuda(e);
+      const long long cgrid = (long long)nf * pa.nchunks;
+      if ((e = launch_maybe_pdl(decl_list != nullptr, pnms_prep_sort_chunk,
+                                dim3((unsigned)(decl_list ? std::min<long long>(cgrid, 148 * 2) : cgrid)),
+                                dim3(kSortThreads), smem, st, pa)) != cudaSuccess)
+        return fail_cuda(e);
+      const long long blocks = (long long)nf * ((n_max + 255) / 256);
+      if ((e = launch_maybe_pdl(decl_list != nullptr, pnms_merge_rank,
+                                dim3((unsigned)(decl_list ? std::min<long long>(blocks, 148 * 8) : blocks)), dim3(256), 0,
+                                st, pa)) != cudaSuccess)
+        return fail_cuda(e);
+    }
+    if ((e = mark(events, 1, st)) != cudaSuccess) return fail_cuda(e);
+    const int ipf = ma.items_per_frame;
+    const long long grid = decl_list ? std::min<long long>((long long)nf * ipf, 148 * 8) : (long long)nf * ipf;
+    if (grid > 0x7FFFFFFFLL) return PNMS_ETOO_LARGE;
+    const bool pdl = decl_list != nullptr;
+    if (ms.R == 4) e = launch_map<4>(ma, grid, map_smem, st, pdl);
+    else if (ms.R == 2) e = launch_map<2>(ma, grid, map_smem, st, pdl);
+    else e = launch_map<1>(ma, grid, map_smem, st, pdl);
+    if (e != cudaSuccess) return fail_cuda(e);
+    if ((e = mark(events, 2, st)) != cudaSuccess) return fail_cuda(e);
+    if ((e = ensure_smem(pnms_compact, compact_smem, g_compact_smem)) != cudaSuccess) return fail_cuda(e);
+    if ((e = launch_maybe_pdl(decl_list != nullptr, pnms_compact, dim3(decl_list ? std::min(nf, 148 * 4) : nf),
+                              dim3(kCompactThreads), compact_smem, st, ca)) != cudaSuccess)
+      return fail_cuda(e);
+  }
+  if ((e = mark(events, 3, st)) != cudaSuccess) return fail_cuda(e);
+  return finish();
 }
 
 }  // namespace
@@ -464,7 +784,7 @@ int pnms_greedy_run(const int32_t* x, const int32_t* y, const int32_t* z, const 
   ga.x = x; ga.y = y; ga.z = z; ga.s = s; ga.counts = counts;
   ga.batch = batch; ga.n_max = n_max; ga.W32 = (n_max + 31) / 32; ga.theta = theta;
   ga.keep_idx = keep_idx; ga.keep_count = keep_count; ga.keep_mask = keep_mask;
-  static std::atomic<size_t> cfg{0};
+  static SmemCache cfg;
   const size_t smem = greedy_smem_bytes(n_max);
   if ((e = ensure_smem(pnms_greedy_frame, smem, cfg)) != cudaSuccess) return fail_cuda(e);
   pnms_greedy_frame<<<batch, kGreedyThreads, smem, st>>>(ga);
@@ -492,7 +812,7 @@ int pnms_soft_rescore(const int32_t* x, const int32_t* y, const int32_t* z, cons
   sa.x = x; sa.y = y; sa.z = z; sa.s = s; sa.counts = counts;
   sa.batch = batch; sa.n_max = n_max; sa.mode = mode; sa.theta = theta; sa.sigma = sigma;
   sa.out_s = out_s; sa.status = status; sa.rounds = rounds;
-  static std::atomic<size_t> cfg{0};
+  static SmemCache cfg;
   const size_t smem = soft_smem_bytes(n_max);
   if ((e = ensure_smem(pnms_soft_frame, smem, cfg)) != cudaSuccess) return fail_cuda(e);
   pnms_soft_frame<<<batch, kSoftThreads, smem, st>>>(sa);
@@ -544,363 +864,6 @@ int pnms_workspace_bytes(int batch, int n_max, size_t* out_bytes) {
 
 }  // extern "C"
 
-namespace {
-
-inline cudaError_t mark(void* const* events, int i, cudaStream_t st) {
-  if (!events || !events[i]) return cudaSuccess;
-  return cudaEventRecord((cudaEvent_t)events[i], st);
-}
-
-int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double* s, const int32_t* counts,
-             int batch, int n_max, int d_max, double theta, int tie_break, int32_t* keep_idx,
-             int32_t* keep_count, uint32_t* keep_mask, uint64_t* gate_pairs, void* workspace,
-             size_t workspace_bytes, void* stream, void* const* events) {
-  if (!(theta >= 0.0 && theta <= 1.0)) return PNMS_EINVAL_THETA;
-  if (d_max < 1) return PNMS_EINVAL_DMAX;
-  if (tie_break != PNMS_TIE_PAPER_FAITHFUL && tie_break != PNMS_TIE_BY_INDEX) return PNMS_EINVAL_TIE;
-  if (batch < 0 || n_max < 0) return PNMS_EINVAL_ARG;
-  if (n_max > PNMS_MAX_SLOTS) return PNMS_ETOO_LARGE;
-  if (batch == 0 || n_max == 0) {
-    cudaStream_t st0 = (cudaStream_t)stream;
-    if (batch > 0 && keep_count) {
-      cudaError_t e = cudaMemsetAsync(keep_count, 0, sizeof(int32_t) * batch, st0);
-      if (e != cudaSuccess) return fail_cuda(e);
-    }
-    if (batch > 0 && gate_pairs) {
-      // all d_max slots are padding (0,0,0,0.0): only by_index gates equal-score pairs
-      // (handled on the host side of the Python layer; here report zero work)
-      cudaError_t e = cudaMemsetAsync(gate_pairs, 0, sizeof(uint64_t) * batch, st0);
-      if (e != cudaSuccess) return fail_cuda(e);
-    }
-    return PNMS_OK;
-  }
-  if (!x || !y || !z || !s) return PNMS_EINVAL_ARG;
-  const Layout L = make_layout(batch, n_max);
-  if (!workspace || workspace_bytes < L.total) return PNMS_EWORKSPACE;
-  cudaStream_t st = (cudaStream_t)stream;
-  uint8_t* ws = static_cast<uint8_t*>(workspace);
-  const int W32 = (n_max + 31) / 32;
-  cudaError_t e;
-
-  if (use_small_path(batch, n_max)) {
-    SmallArgs sa;
-    sa.x = x; sa.y = y; sa.z = z; sa.s = s; sa.counts = counts;
-    sa.batch = batch; sa.n_max = n_max; sa.d_max = d_max; sa.tie_break = tie_break; sa.W32 = W32;
-    sa.theta = theta;
-    const int R = ((long long)batch * n_max <= 2048) ? 1 : kSmallRowsMax;  // tiny calls: more CTAs
-    sa.n_rt = (n_max + kSmallThreads * R - 1) / (kSmallThreads * R);
-    const int max_ct = (n_max + 31) / 32;
-    int n_ct = (int)std::min<long long>(max_ct, std::max<long long>(1, (2LL * 148 + (long long)batch * sa.n_rt - 1) /
-                                                                         ((long long)batch * sa.n_rt)));
-    const int ct_env = env_int("PNMS_SMALL_CT", 0);
-    if (ct_env > 0) n_ct = std::min(ct_env, max_ct);
-    sa.cols = ((n_max + n_ct - 1) / n_ct + 31) / 32 * 32;
-    sa.n_ct = (n_max + sa.cols - 1) / sa.cols;
-    sa.supp = reinterpret_cast<uint32_t*>(ws);
-    sa.ticket = reinterpret_cast<unsigned int*>(ws + kSmallMaxWords * 4);
-    sa.gacc = reinterpret_cast<unsigned long long*>(ws + kSmallMaxWords * 4 + kSmallMaxFrames * 4);
-    sa.keep_idx = keep_idx; sa.keep_count = keep_count; sa.keep_mask = keep_mask;
-    sa.gate_pairs = reinterpret_cast<unsigned long long*>(gate_pairs);
-    const size_t smem = (size_t)sa.cols * (8 + sizeof(RecWide));
-    const long long grid = (long long)batch * sa.n_rt * sa.n_ct;
-    if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
-    if ((e = mark(events, 1, st)) != cudaSuccess) return fail_cuda(e);
-    const int variant = (tie_break == PNMS_TIE_BY_INDEX ? 2 : 0) + (gate_pairs != nullptr ? 1 : 0) + (R == 1 ? 4 : 0);
-    e = launch_small(variant, sa, grid, smem, st);
-    if (e != cudaSuccess) return fail_cuda(e);
-    if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
-    if ((e = mark(events, 2, st)) != cudaSuccess) return fail_cuda(e);
-    if ((e = mark(events, 3, st)) != cudaSuccess) return fail_cuda(e);
-    return PNMS_OK;
-  }
-
-  // arguments of the dense pipeline (prep+sort -> map -> compact) for frames [f0, f0 + nf)
-  const MapShape ms = choose_map_shape(batch, n_max);
-  auto chain_args = [&](int f0, int nf, const uint8_t* dense, const int32_t* list, const int* list_count,
-                        PrepArgs& pa, MapArgs& ma, CompactArgs& ca) {
-    const size_t fo = (size_t)f0 * n_max;
-    pa.x = x + fo; pa.y = y + fo; pa.z = z + fo; pa.s = s + fo; pa.counts = counts ? counts + f0 : nullptr;
-    pa.batch = nf; pa.n_max = n_max; pa.tie_break = tie_break; pa.W32 = W32;
-    pa.theta = theta;
-    pa.rec = ws + L.rec + fo * kRecBytes;
-    pa.perm = reinterpret_cast<int32_t*>(ws + L.perm) + fo;
-    pa.lim = reinterpret_cast<int32_t*>(ws + L.lim) + fo;
-    pa.supp = reinterpret_cast<uint32_t*>(ws + L.supp) + (size_t)f0 * W32;
-    pa.meta = reinterpret_cast<FrameMeta*>(ws + L.meta) + f0;
-    pa.sk_scratch = L.sk ? reinterpret_cast<uint64_t*>(ws + L.sk) + fo : nullptr;
-    pa.idx_scratch = L.idx ? reinterpret_cast<int32_t*>(ws + L.idx) + fo : nullptr;
-    pa.dense = dense ? dense + f0 : nullptr;
-    pa.list = list;          // chunks == 1 whenever the list is set
-    pa.list_count = list_count;
-    if (n_max <= kSortMax) {
-      pa.npad = (n_max + kSortThreads - 1) / kSortThreads * kSortThreads;
-      pa.nchunks = 1;
-    } else {
-      pa.npad = kSortMax;
-      pa.nchunks = (n_max + kSortMax - 1) / kSortMax;
-    }
-    ma.rec = pa.rec; ma.lim = pa.lim; ma.supp = pa.supp; ma.meta = pa.meta;
-    ma.batch = nf; ma.n_max = n_max; ma.W32 = W32;
-    ma.rows_per_block = ms.RB;
-    ma.chunk = ms.chunk;
-    ma.n_rb = (n_max + ms.RB - 1) / ms.RB;
-    ma.items_per_frame = items_per_frame(n_max, ms.RB, ms.chunk);
-    ma.dense = pa.dense;
-    ma.list = list;
-    ma.list_count = list_count;
-    ca.s = pa.s; ca.counts = pa.counts; ca.perm = pa.perm; ca.supp = pa.supp; ca.meta = pa.meta;
-    ca.batch = nf; ca.n_max = n_max; ca.W32 = W32; ca.d_max = d_max; ca.tie_break = tie_break;
-    ca.keep_idx = keep_idx ? keep_idx + fo : nullptr;
-    ca.keep_count = keep_count ? keep_count + f0 : nullptr;
-    ca.keep_mask = keep_mask ? keep_mask + (size_t)f0 * W32 : nullptr;
-    ca.gate_pairs = gate_pairs ? reinterpret_cast<unsigned long long*>(gate_pairs) + f0 : nullptr;
-    ca.dense = pa.dense;
-    ca.list = list;
-    ca.list_count = list_count;
-  };
-  const size_t compact_smem = ((size_t)W32 + 3) / 4 * 16 + 64 * 4;
-  const size_t map_smem = (size_t)ms.chunk * kRecBytes;
-  // one-CTA dispatcher behind a declining kernel (pnms_fallback.cuh): snapshots the declined
-  // count into `snap`, zeroes it and, when frames were declined, tail-launches the dense chain
-  // over them; `*host_chain` is set when the host must launch the chain itself (profiled calls)
-  auto dispatch_fallback = [&](const int32_t* list, int* count, int* snap, bool* host_chain) -> cudaError_t {
-    FallbackPlan plan{};
-    chain_args(0, batch, ws + L.dense, list, snap, plan.pa, plan.ma, plan.ca);
-    plan.chunked = n_max > kSortMax;
-    plan.map_R = ms.R;
-    plan.sort_smem = (int)(plan.chunked ? sort_smem_bytes(kSortMax) : sort_frame_smem_bytes(plan.pa.npad));
-    plan.map_smem = (int)map_smem;
-    plan.compact_smem = (int)compact_smem;
-#ifdef PNMS_NO_DEVCHAIN  // diagnostic build without the relocatable unit (sanitizer tools)
-    plan.enabled = 0;
-#else
-    plan.enabled = events == nullptr && env_int("PNMS_DEVCHAIN", 1) != 0;  // 0: host chain (debug)
-#endif
-    *host_chain = !plan.enabled;
-    if (!plan.enabled)  // snapshot + zero only; the host launches the chain over `snap`
-      return launch_maybe_pdl(true, pnms_count_snapshot, dim3(1), dim3(32), 0, st, count, snap, batch);
-#ifndef PNMS_NO_DEVCHAIN
-    static const bool same_layout = pnms_devchain_plan_size() == sizeof(FallbackPlan);
-    if (!same_layout) return cudaErrorInvalidValue;
-    cudaError_t err = pnms_devchain_prepare(plan.chunked, ms.R, plan.sort_smem, map_smem, compact_smem);
-    if (err != cudaSuccess) return err;
-    return pnms_devchain_dispatch(&plan, count, snap, st);
-#else
-    return cudaSuccess;
-#endif
-  };
-
-  // ---- binned path (sparse frames): exact, one CTA per frame; declined frames fall through
-  // to the dense pipeline below, which then only processes those frames.
-  const uint8_t* dense_flags = nullptr;
-  const int32_t* decl_list = nullptr;  // binned path: the declined frames, read on the device
-  const int* decl_count = nullptr;
-  void* ev_local[4];
-  const long long algo = env_ll("PNMS_ALGO", 0);  // 0 auto, 1 dense only
-  // calls of <= 2 frames of 2049..4096 slots that the single-launch path did not take run on
-  // the multi-CTA tile path instead of one CTA per frame (measured, tools/single_frame_paths.py:
-  // a 4096-box random frame 22 us on tiles against 52 us on one CTA; PNMS_TILES_SMALL = the
-  // slot threshold, 0 disables)
-  const int tiles_small_env = env_int("PNMS_TILES_SMALL", 2048);
-  const bool tiles_small = tiles_small_env > 0 && batch <= 2 && n_max > tiles_small_env && n_max <= kBinMaxSlots;
-  if (algo == 0 && gate_pairs == nullptr && n_max <= kBinMaxSlots && !tiles_small) {
-    const bool pairs = env_int("PNMS_BINNED", 0) == 2;
-    BinArgs ba{};
-    ba.x = x; ba.y = y; ba.z = z; ba.s = s; ba.counts = counts;
-    ba.batch = batch; ba.n_max = n_max; ba.d_max = d_max; ba.tie_break = tie_break; ba.W32 = W32;
-    ba.theta = theta;
-    ba.fallback = ws + L.dense;
-    ba.decl_list = reinterpret_cast<int32_t*>(ws + L.list) + 1;
-    if (pairs) {  // the cell-pair kernel leaves the count for the host chain: zero it per call
-      ba.decl_count = reinterpret_cast<int*>(ws + L.list);
-      if ((e = cudaMemsetAsync(ba.decl_count, 0, sizeof(int), st)) != cudaSuccess) return fail_cuda(e);
-    } else {      // count in the zeroed scratch, left zero by the dispatcher (pnms_fallback.cuh)
-      ba.decl_count = reinterpret_cast<int*>(ws + kDeclCountOffset);
-    }
-    ba.keep_idx = keep_idx; ba.keep_count = keep_count; ba.keep_mask = keep_mask;
-    ba.pairs_tested = g_pairs_counter;
-    ba.trace = g_trace;
-    ba.cell_q8 = env_int("PNMS_CELL_Q8", 0);
-    ba.cell_sx = env_int("PNMS_CELL_SX", 0);
-    ba.meta = nullptr;  // the frame-level sort rewrites FrameMeta of declined frames
-    const size_t smem = binned_smem_bytes(binned_npad(n_max));
-    if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
-    const int variant = (tie_break == PNMS_TIE_BY_INDEX ? 1 : 0) + (g_pairs_counter ? 2 : 0) +
-                        (binned_per_thread(n_max, kBinThreads) == 8 ? 4 : 0);
-    // one wave of 1024-thread CTAs (two boxes per thread) when the batch fits the SMs
-    const int lat_env = env_int("PNMS_BINNED_LATENCY", -1);
-    const bool latency = n_max <= 2048 && (lat_env >= 0 ? lat_env == 1 : batch <= sm_count());
-    if (pairs) {                           // cell-pair tiles (pnms_binned_pairs.cuh): opt-in,
-      // measured 4 % slower on BASELINE config 5 (more pair tests without the gate-prefix skip)
-      const size_t psmem = binned_pairs_smem_bytes(binned_npad(n_max));
-      if ((e = launch_pairs(variant, ba, batch, psmem, st)) != cudaSuccess) return fail_cuda(e);
-    } else {                               // per-row scans (pnms_binned.cuh), the default
-      if ((e = launch_binned(variant, ba, batch, smem, st, latency)) != cudaSuccess) return fail_cuda(e);
-    }
-    decl_list = ba.decl_list;
-    decl_count = ba.decl_count;
-    if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
-    if (!pairs) {
-      int* snap = reinterpret_cast<int*>(ws + L.list);
-      bool host_chain = false;
-      if ((e = dispatch_fallback(ba.decl_list, ba.decl_count, snap, &host_chain)) != cudaSuccess) return fail_cuda(e);
-      if (!host_chain) return PNMS_OK;
-      decl_count = snap;
-    }
-    dense_flags = ws + L.dense;
-    if (events) {
-      // phases become: [0,1) binned kernel, [1,2) dense prep of declined frames, [2,3) their map+compact
-      ev_local[0] = events[1]; ev_local[1] = events[2]; ev_local[2] = nullptr; ev_local[3] = events[3];
-      events = ev_local;
-    }
-  }
-
-  if (!dense_flags && algo == 0 && gate_pairs == nullptr && (n_max > kBinMaxSlots || tiles_small)) {
-    // large frames: few frames -> kTilesPerFrame independent tile CTAs per frame
-    // (pnms_binned_tiles.cuh, latency); many frames -> one thread-block cluster per frame
-    // (pnms_binned_cluster.cuh, throughput).  Declined frames go to the dense pipeline by list.
-    BinArgs ba{};
-    ba.x = x; ba.y = y; ba.z = z; ba.s = s; ba.counts = counts;
-    ba.batch = batch; ba.n_max = n_max; ba.d_max = d_max; ba.tie_break = tie_break; ba.W32 = W32;
-    ba.theta = theta;
-    ba.fallback = ws + L.dense;
-    ba.decl_count = reinterpret_cast<int*>(ws + kDeclCountOffset);  // zeroed scratch (dispatcher)
-    ba.decl_list = reinterpret_cast<int32_t*>(ws + L.list) + 1;
-    ba.keep_idx = keep_idx; ba.keep_count = keep_count; ba.keep_mask = keep_mask;
-    ba.pairs_tested = nullptr;
-    ba.trace = g_trace;
-    ba.cell_q8 = env_int("PNMS_CELL_Q8", 0);
-    ba.cell_sx = env_int("PNMS_CELL_SX", 0);
-    ba.meta = reinterpret_cast<FrameMeta*>(ws + L.meta);  // the chunked sort accumulates into it
-    const int large = env_int("PNMS_LARGE", 0);  // 0 auto, 1 tiles, 2 cluster
-    const bool cluster_ok = cluster_slice(n_max, 16) > 0 && cluster_slice(n_max, cluster_size_for(n_max)) > 0;
-    const bool tiles = tiles_small ||
-                       (n_max <= 65536 && (large == 1 || (large == 0 && (batch <= 2 || !cluster_ok))));
-    if (tiles || cluster_ok) {
-      if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
-      if (tiles) {
-        TileArgs ta;
-        ta.b = ba;
-        // decline flags and survivor masks in the zeroed scratch (pnms_mask_compact re-zeroes
-        // them) when they fit — the latency case, <= 2 frames — else zeroed per call
-        const size_t fbytes = ((size_t)batch * 4 + 15) / 16 * 16;
-        const size_t tbytes = fbytes + (size_t)batch * W32 * 4;
-        const bool in_scratch = kTilesScratchOffset + tbytes <= kSmallScratchBytes;
-        uint8_t* tbase = in_scratch ? ws + kTilesScratchOffset : ws + L.tiles;
-        ta.decline = reinterpret_cast<int*>(tbase);
-        ta.mask = reinterpret_cast<uint32_t*>(tbase + fbytes);
-        if (!in_scratch && (e = cudaMemsetAsync(tbase, 0, tbytes, st)) != cudaSuccess) return fail_cuda(e);
-        static std::atomic<size_t> tcfg[2];
-        const size_t tsmem = binned_tiles_smem_bytes();
-        const bool bi = tie_break == PNMS_TIE_BY_INDEX;
-        if ((e = ensure_smem(bi ? pnms_binned_tiles<true> : pnms_binned_tiles<false>, tsmem, tcfg[bi])) != cudaSuccess)
-          return fail_cuda(e);
-        if ((e = launch_maybe_pdl(false, bi ? pnms_binned_tiles<true> : pnms_binned_tiles<false>,
-                                  dim3((unsigned)batch * kTilesPerFrame), dim3(kTileThreads), tsmem, st, ta)) !=
-            cudaSuccess)
-          return fail_cuda(e);
-        if ((e = launch_maybe_pdl(true, pnms_mask_compact, dim3((unsigned)batch), dim3(512), 0, st, ta)) != cudaSuccess)
-          return fail_cuda(e);
-      } else {
-        if ((e = launch_cluster(ba, batch, n_max, tie_break == PNMS_TIE_BY_INDEX, st)) != cudaSuccess)
-          return fail_cuda(e);
-      }
-      decl_list = ba.decl_list;
-      int* snap = reinterpret_cast<int*>(ws + L.list);
-      bool host_chain = false;
-      if ((e = dispatch_fallback(ba.decl_list, ba.decl_count, snap, &host_chain)) != cudaSuccess) return fail_cuda(e);
-      if (!host_chain) return PNMS_OK;
-      decl_count = snap;
-      dense_flags = ws + L.dense;
-      if (events) {
-        ev_local[0] = events[1]; ev_local[1] = events[2]; ev_local[2] = nullptr; ev_local[3] = events[3];
-        events = ev_local;
-      }
-    }
-  }
-
-  // ---- sorted pipeline: prep+sort -> map -> compact, per frame chunk --------------------
-  // Large batches are cut into chunks whose sort runs on an internal side stream while the
-  // previous chunk's map runs on the caller's stream, so the sort hides behind the map.
-  int chunks = 1;
-  if (!events && !decl_list && n_max <= kSortMax && batch >= 512) {
-    chunks = std::max(1, std::min(32, env_int("PNMS_OVERLAP_CHUNKS", 1)));
-    chunks = std::min(chunks, batch / 64 > 0 ? batch / 64 : 1);
-  }
-  SideStream* side = chunks > 1 ? side_stream() : nullptr;
-  if (!side) chunks = 1;
-  if (chunks > 1) {
-    if ((e = cudaEventRecord(side->fork, st)) != cudaSuccess) return fail_cuda(e);
-    if ((e = cudaStreamWaitEvent(side->s, side->fork, 0)) != cudaSuccess) return fail_cuda(e);
-  }
-  if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
-  for (int c = 0; c < chunks; ++c) {
-    const int f0 = (int)((long long)batch * c / chunks), f1 = (int)((long long)batch * (c + 1) / chunks);
-    const int nf = f1 - f0;
-    if (nf <= 0) continue;
-    cudaStream_t sort_st = chunks > 1 ? side->s : st;
-    PrepArgs pa;
-    MapArgs ma;
-    CompactArgs ca;
-    chain_args(f0, nf, dense_flags, decl_list, decl_count, pa, ma, ca);
-
-    if (n_max <= kSortMax) {
-      const size_t smem = sort_frame_smem_bytes(pa.npad);
-      if (decl_list) {
-        static std::atomic<size_t> lcfg{0};
-        if ((e = ensure_smem(pnms_prep_sort_frame_list, smem, lcfg)) != cudaSuccess) return fail_cuda(e);
-        if ((e = launch_maybe_pdl(true, pnms_prep_sort_frame_list, dim3(std::min(nf, 148 * 2)), dim3(kSortThreads),
-                                  smem, sort_st, pa)) != cudaSuccess)
-          return fail_cuda(e);
-      } else {
-        if ((e = ensure_smem(pnms_prep_sort_frame, smem, g_sort_frame_smem)) != cudaSuccess) return fail_cuda(e);
-        pnms_prep_sort_frame<<<nf, kSortThreads, smem, sort_st>>>(pa);
-        if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
-      }
-    } else {
-      // the declined-frame list path had each frame's FrameMeta zeroed by the decliner
-      if (!decl_list && (e = cudaMemsetAsync(pa.meta, 0, sizeof(FrameMeta) * (size_t)nf, sort_st)) != cudaSuccess)
-        return fail_cuda(e);
-      const size_t smem = sort_smem_bytes(kSortMax);
-      if ((e = ensure_smem(pnms_prep_sort_chunk, smem, g_sort_chunk_smem)) != cudaSuccess) return fail_cuda(e);
-      const long long cgrid = (long long)nf * pa.nchunks;
-      if ((e = launch_maybe_pdl(decl_list != nullptr, pnms_prep_sort_chunk,
-                                dim3((unsigned)(decl_list ? std::min<long long>(cgrid, 148 * 2) : cgrid)),
-                                dim3(kSortThreads), smem, sort_st, pa)) != cudaSuccess)
-        return fail_cuda(e);
-      const long long blocks = (long long)nf * ((n_max + 255) / 256);
-      if ((e = launch_maybe_pdl(decl_list != nullptr, pnms_merge_rank,
-                                dim3((unsigned)(decl_list ? std::min<long long>(blocks, 148 * 8) : blocks)), dim3(256), 0,
-                                sort_st, pa)) != cudaSuccess)
-        return fail_cuda(e);
-    }
-    if (chunks > 1) {
-      if ((e = cudaEventRecord(side->ev[c], side->s)) != cudaSuccess) return fail_cuda(e);
-      if ((e = cudaStreamWaitEvent(st, side->ev[c], 0)) != cudaSuccess) return fail_cuda(e);
-    }
-
-    if ((e = mark(events, 1, st)) != cudaSuccess) return fail_cuda(e);
-    const int ipf = ma.items_per_frame;
-    const long long grid = decl_list ? std::min<long long>((long long)nf * ipf, 148 * 8) : (long long)nf * ipf;
-    if (grid > 0x7FFFFFFFLL) return PNMS_ETOO_LARGE;
-    const bool pdl = decl_list != nullptr;
-    if (ms.R == 4) e = launch_map<4>(ma, grid, map_smem, st, pdl);
-    else if (ms.R == 2) e = launch_map<2>(ma, grid, map_smem, st, pdl);
-    else e = launch_map<1>(ma, grid, map_smem, st, pdl);
-    if (e != cudaSuccess) return fail_cuda(e);
-
-    if ((e = mark(events, 2, st)) != cudaSuccess) return fail_cuda(e);
-    if ((e = ensure_smem(pnms_compact, compact_smem, g_compact_smem)) != cudaSuccess) return fail_cuda(e);
-    if ((e = launch_maybe_pdl(decl_list != nullptr, pnms_compact, dim3(decl_list ? std::min(nf, 148 * 4) : nf),
-                              dim3(kCompactThreads), compact_smem, st, ca)) != cudaSuccess)
-      return fail_cuda(e);
-  }
-  if ((e = mark(events, 3, st)) != cudaSuccess) return fail_cuda(e);
-  return PNMS_OK;
-}
-
-}  // namespace
-
 extern "C" {
 
 int pnms_run(const int32_t* x, const int32_t* y, const int32_t* z, const double* s, const int32_t* counts,
@@ -908,7 +871,7 @@ int pnms_run(const int32_t* x, const int32_t* y, const int32_t* z, const double*
              int32_t* keep_count, uint32_t* keep_mask, uint64_t* gate_pairs, void* workspace,
              size_t workspace_bytes, void* stream) {
   return run_impl(x, y, z, s, counts, batch, n_max, d_max, theta, tie_break, keep_idx, keep_count, keep_mask,
-                  gate_pairs, workspace, workspace_bytes, stream, nullptr);
+                  gate_pairs, workspace, workspace_bytes, stream, nullptr, nullptr, nullptr);
 }
 
 int pnms_run_profiled(const int32_t* x, const int32_t* y, const int32_t* z, const double* s,
@@ -916,7 +879,15 @@ int pnms_run_profiled(const int32_t* x, const int32_t* y, const int32_t* z, cons
                       int32_t* keep_idx, int32_t* keep_count, uint32_t* keep_mask, uint64_t* gate_pairs,
                       void* workspace, size_t workspace_bytes, void* stream, void* const* phase_events) {
   return run_impl(x, y, z, s, counts, batch, n_max, d_max, theta, tie_break, keep_idx, keep_count, keep_mask,
-                  gate_pairs, workspace, workspace_bytes, stream, phase_events);
+                  gate_pairs, workspace, workspace_bytes, stream, nullptr, nullptr, phase_events);
+}
+
+int pnms_run_ex(const int32_t* x, const int32_t* y, const int32_t* z, const double* s, const int32_t* counts,
+                int batch, int n_max, int d_max, double theta, int tie_break, int32_t* keep_idx, int32_t* keep_count,
+                uint32_t* keep_mask, uint64_t* gate_pairs, void* workspace, size_t workspace_bytes, void* stream,
+                const pnms_launch_config* config, pnms_run_info* info, void* const* phase_events) {
+  return run_impl(x, y, z, s, counts, batch, n_max, d_max, theta, tie_break, keep_idx, keep_count, keep_mask,
+                  gate_pairs, workspace, workspace_bytes, stream, config, info, phase_events);
 }
 
 int pnms_map_reference_layout(const int32_t* x, const int32_t* y, const int32_t* z, const double* s, int d_max,

@@ -12,11 +12,21 @@
 
 namespace {
 
+// the largest dynamic shared memory each list kernel has been opened up to, per device
+// (function attributes are per device)
+constexpr int kMaxDevices = 64;
+struct SmemCache {
+  std::atomic<size_t> v[kMaxDevices];
+};
+
 template <class Kernel>
-cudaError_t ensure_smem_dc(Kernel kernel, size_t bytes, std::atomic<size_t>& configured) {
-  if (bytes <= 48 * 1024 || configured.load(std::memory_order_relaxed) >= bytes) return cudaSuccess;
+cudaError_t ensure_smem_dc(Kernel kernel, size_t bytes, SmemCache& c) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  std::atomic<size_t>& slot = c.v[dev];
+  if (bytes <= 48 * 1024 || slot.load(std::memory_order_relaxed) >= bytes) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e == cudaSuccess) configured.store(bytes, std::memory_order_relaxed);
+  if (e == cudaSuccess) slot.store(bytes, std::memory_order_relaxed);
   return e;
 }
 
@@ -25,7 +35,7 @@ cudaError_t ensure_smem_dc(Kernel kernel, size_t bytes, std::atomic<size_t>& con
 size_t pnms_devchain_plan_size() { return sizeof(pnms_dc::FallbackPlan); }
 
 cudaError_t pnms_devchain_prepare(int chunked, int map_R, int sort_smem, size_t map_smem, size_t compact_smem) {
-  static std::atomic<size_t> scfg{0}, kcfg{0}, mcfg[5], ccfg{0};
+  static SmemCache scfg, kcfg, mcfg[5], ccfg;
   cudaError_t e = chunked ? ensure_smem_dc(pnms_dc::pnms_prep_sort_chunk, (size_t)sort_smem, kcfg)
                           : ensure_smem_dc(pnms_dc::pnms_prep_sort_frame_list, (size_t)sort_smem, scfg);
   if (e != cudaSuccess) return e;

@@ -62,6 +62,9 @@ __global__ void __launch_bounds__(32) pnms_fallback_dispatch(FallbackPlan plan, 
   else
     pnms_map_kernel_list<1><<<map_grid, kMapWarps * 32, plan.map_smem, cudaStreamTailLaunch>>>(plan.ma);
   pnms_compact<<<min(c, 148 * 4), kCompactThreads, plan.compact_smem, cudaStreamTailLaunch>>>(plan.ca);
+  // a chain that could not be launched would leave the declined frames without output: fail
+  // loudly (the stream reports the fault at the caller's next synchronisation)
+  if (cudaGetLastError() != cudaSuccess) __trap();
 }
 #endif
 

@@ -139,38 +139,94 @@ def _frame_columns(d):
     return x, y, z, s
 
 
-def _padding_is_zero(x, y, z, s, count: int) -> bool:
-    if count >= x.shape[0]:
+def _padding_is_zero(d, count: int) -> bool:
+    if count >= len(d):
         return True
-    return not (x[count:].any() or y[count:].any() or z[count:].any() or s[count:].any())
+    return not (np.any(d.xs[count:]) or np.any(d.ys[count:]) or np.any(d.zs[count:]) or np.any(d.ss[count:]))
+
+
+class _FrameStage:
+    """Pinned host <-> device staging of one frame for the reference-facing calls: the frame
+    goes up in ONE host-to-device copy (float64 s plane, then int32 x, y, z planes, 20 B per
+    slot — the casts of engine.py:191-193 happen while filling the pinned buffer) and the
+    result comes back in ONE device-to-host copy of [keep_count, pad, map_writes (int64), keep
+    indices].  One per device, grown on demand."""
+
+    def __init__(self, torch, dev, cap: int):
+        self.cap = cap
+        self.hin = torch.empty(20 * cap, dtype=torch.uint8, pin_memory=True)
+        self.din = torch.empty(20 * cap, dtype=torch.uint8, device=dev)
+        self.hout = torch.empty(4 + cap, dtype=torch.int32, pin_memory=True)
+        self.dout = torch.empty(4 + cap, dtype=torch.int32, device=dev)
+        self.ws = torch.zeros(_lib.workspace_bytes(1, cap), dtype=torch.uint8, device=dev)
+        self.h = self.hin.numpy()
+
+    def run(self, torch, d, n: int, cfg: "NmsConfig"):
+        from .tensor_api import batched_nms_keep
+
+        np.copyto(self.h[: 8 * n].view(np.float64), np.asarray(d.ss[:n], dtype=np.float64))
+        xyz = self.h[8 * n: 20 * n].view(np.int32).reshape(3, n)
+        for r, col in enumerate((d.xs, d.ys, d.zs)):
+            np.copyto(xyz[r], np.asarray(col[:n]), casting="unsafe")  # int32 wrap, engine.py:191-193
+        self.din[: 20 * n].copy_(self.hin[: 20 * n], non_blocking=True)
+        s = self.din[: 8 * n].view(torch.float64).reshape(1, n)
+        dxyz = self.din[8 * n: 20 * n].view(torch.int32).reshape(3, n)
+        x, y, z = (dxyz[r: r + 1] for r in range(3))
+        kc = self.dout[0:1]
+        gp = self.dout[2:4].view(torch.int64)
+        ki = self.dout[4: 4 + n].reshape(1, n)
+        batched_nms_keep(x, y, z, s, None, cfg.theta, cfg.tie_break, cfg.d_max, keep_idx=ki, keep_count=kc,
+                         gate_pairs=gp, workspace=self.ws)
+        self.hout[: 4 + n].copy_(self.dout[: 4 + n], non_blocking=True)
+        torch.cuda.current_stream(s.device).synchronize()
+        out = self.hout.numpy()
+        k = int(out[0])
+        return out[4: 4 + k].astype(np.int64), int(out[2:4].view(np.int64)[0])
+
+
+_STAGES: dict = {}
+
+
+def _stage(torch, dev, n: int) -> _FrameStage:
+    key = dev.index
+    st = _STAGES.get(key)
+    if st is None or st.cap < n:
+        st = _FrameStage(torch, dev, max(n, 1024, st.cap * 2 if st else 0))
+        _STAGES[key] = st
+    return st
+
+
+def _survivors(d, keep: np.ndarray) -> tuple:
+    """The survivors as the reference builds them (d.slot(i), engine.py:291-292); this
+    package's own vectors build the Detection objects from whole columns."""
+    if isinstance(d, DetectionVector):
+        cols = (d.xs[keep].tolist(), d.ys[keep].tolist(), d.zs[keep].tolist(), d.ss[keep].tolist())
+        return tuple(map(Detection, *cols))
+    return tuple(d.slot(int(i)) for i in keep)
 
 
 def run_nms(d: DetectionVector, cfg: NmsConfig) -> tuple[NmsResult, WorkCounters]:
-    """Full pipeline on the GPU; returns (NmsResult, WorkCounters) like engine.py:296-300."""
+    """Full pipeline on the GPU; returns (NmsResult, WorkCounters) like engine.py:296-300.
+
+    Host to host: one pinned upload of the frame, one batched pnms_run (the library picks the
+    device path; map_writes comes from pnms_gate.cuh on the culling paths), one download of
+    [count, map_writes, keep indices], one synchronisation."""
     dim = cfg.d_max
     if len(d) != dim:
         raise ConfigError(f"vector capacity {len(d)} does not match d_max={dim}")
     torch = _torch()
-    from .tensor_api import batched_nms_keep
-
     count = int(d.count)
-    x, y, z, s = _frame_columns(d)
     # Standard vectors carry zero padding, which the device treats implicitly.  A vector
     # whose padding slots hold anything else runs with all d_max slots explicit.
-    n = count if _padding_is_zero(x, y, z, s, count) else dim
+    n = count if _padding_is_zero(d, count) else dim
     dev = torch.device("cuda", torch.cuda.current_device())
     if n == 0:
         keep = np.zeros(0, dtype=np.int64)
         writes = dim * (dim - 1) // 2 if cfg.tie_break == "by_index" else 0
     else:
-        t = lambda a: torch.from_numpy(np.array(a[:n])).reshape(1, n).to(dev)  # noqa: E731
-        gp = torch.empty((1,), dtype=torch.int64, device=dev)
-        idx, cnt = batched_nms_keep(t(x), t(y), t(z), t(s), None, cfg.theta, cfg.tie_break, dim, gate_pairs=gp)
-        k = int(cnt.item())
-        keep = idx[0, :k].cpu().numpy().astype(np.int64)
+        keep, writes = _stage(torch, dev, n).run(torch, d, n, cfg)
         keep = keep[keep < count]
-        writes = int(gp.item())
-    survivors = tuple(d.slot(int(i)) for i in keep)
+    survivors = _survivors(d, keep)
     counters = WorkCounters(map_cells=dim * dim, map_writes=writes, reduce_segments=dim * cfg.k)
     return NmsResult(survivors, count - len(survivors)), counters
 

@@ -12,11 +12,66 @@ score plane s [B, n_max].  PyTorch only provides device memory and streams here.
 
 from __future__ import annotations
 
+import contextlib
+import ctypes
+from dataclasses import dataclass
+
 import torch
 
 from . import _lib
 
 _TIE = _lib.TIE_CODES
+
+
+@dataclass
+class LaunchConfig:
+    """Launch configuration of pnms_run_ex (struct pnms_launch_config, include/parnms_b200.h).
+
+    Every field left at its default takes the library's measured choice.  Tests, tools and the
+    benchmark use it to pin a device path or a decomposition; results never depend on it.
+    After a call, `path_taken` holds the path that ran (declined frames additionally ran
+    "dense"), and `declined` (an int32 CUDA tensor of one element, if given) the number of
+    frames the culling kernel declined.
+
+    path: "auto" | "small" | "binned" | "binned_wide" | "tiles" | "cluster" | "dense"
+    """
+
+    path: str = "auto"
+    cluster_size: int = 0
+    cell_q8: int = 0
+    cell_sx: int = 0
+    map_rows: int = 0
+    map_chunk: int = 0
+    small_col_tiles: int = 0
+    host_chain: bool = False
+    declined: torch.Tensor | None = None
+    path_taken: str | None = None
+
+    def to_c(self) -> _lib.LaunchConfigC:
+        if self.path not in _lib.PATHS:
+            raise ValueError(f"path must be one of {tuple(_lib.PATHS)}, got {self.path!r}")
+        if self.declined is not None:
+            _require_cuda(self.declined, "declined", torch.int32, 1)
+        return _lib.LaunchConfigC(_lib.PATHS[self.path], int(self.cluster_size), int(self.cell_q8),
+                                  int(self.cell_sx), int(self.map_rows), int(self.map_chunk),
+                                  int(self.small_col_tiles), int(bool(self.host_chain)),
+                                  self.declined.data_ptr() if self.declined is not None else None)
+
+
+_DEFAULT_LAUNCH: list[LaunchConfig | None] = [None]
+
+
+@contextlib.contextmanager
+def launch_override(cfg: LaunchConfig | None):
+    """Run every pnms_run call inside the block (including those of engine.run_nms and
+    NmsEngine) with `cfg` unless the call passes its own: how the tests drive the
+    reference-facing API through each device path."""
+    prev = _DEFAULT_LAUNCH[0]
+    _DEFAULT_LAUNCH[0] = cfg
+    try:
+        yield cfg
+    finally:
+        _DEFAULT_LAUNCH[0] = prev
 
 
 def _check_theta(theta: float) -> float:
@@ -45,6 +100,42 @@ def _require_cuda(t: torch.Tensor, name: str, dtype: torch.dtype, ndim: int) -> 
         raise ValueError(f"{name} must be a contiguous {ndim}-D tensor")
 
 
+def _check_out(t: torch.Tensor | None, name: str, dtype: torch.dtype, shape: tuple, dev: torch.device) -> None:
+    if t is None:
+        return
+    _require_cuda(t, name, dtype, len(shape))
+    if tuple(t.shape) != tuple(shape) or t.device != dev:
+        raise ValueError(f"{name} must be {dtype} of shape {list(shape)} on {dev}")
+
+
+def _check_planes(x, y, z, s, counts, keep_mask=None):
+    """The planes of one batched call: int32 x, y, z and float64 s [B, n_max] on one CUDA
+    device, counts int32 [B]; returns (B, n_max)."""
+    _require_cuda(x, "x", torch.int32, 2)
+    B, n_max = x.shape
+    for t, nm in ((y, "y"), (z, "z")):
+        _require_cuda(t, nm, torch.int32, 2)
+        if t.shape != x.shape:
+            raise ValueError(f"{nm} shape {tuple(t.shape)} != x shape {tuple(x.shape)}")
+    _require_cuda(s, "s", torch.float64, 2)
+    if s.shape != x.shape:
+        raise ValueError(f"s shape {tuple(s.shape)} != x shape {tuple(x.shape)}")
+    tensors = [y, z, s]
+    if counts is not None:
+        _require_cuda(counts, "counts", torch.int32, 1)
+        if counts.shape[0] != B:
+            raise ValueError("counts must have one entry per frame")
+        tensors.append(counts)
+    if keep_mask is not None:
+        W32 = (n_max + 31) // 32
+        _require_cuda(keep_mask, "keep_mask", torch.int32, 2)
+        if tuple(keep_mask.shape) != (B, W32):
+            raise ValueError(f"keep_mask must be [{B}, {W32}] int32")
+    if any(t.device != x.device for t in tensors):
+        raise ValueError("all planes must be on the same CUDA device")
+    return B, n_max
+
+
 class _WorkspaceCache:
     """One growing device workspace per (device, stream)."""
 
@@ -69,7 +160,8 @@ def batched_nms_keep(x: torch.Tensor, y: torch.Tensor, z: torch.Tensor, s: torch
                      tie_break: str = "paper_faithful", d_max: int | None = None, *,
                      keep_idx: torch.Tensor | None = None, keep_count: torch.Tensor | None = None,
                      keep_mask: torch.Tensor | None = None, gate_pairs: torch.Tensor | None = None,
-                     workspace: torch.Tensor | None = None, want_idx: bool = True, validate: bool = False):
+                     workspace: torch.Tensor | None = None, want_idx: bool = True, validate: bool = False,
+                     launch: LaunchConfig | None = None):
     """NMS of every frame of a batch; returns (keep_idx [B, n_max] int32, keep_count [B] int32).
 
     Frame f holds counts[f] valid detections in slots [0, counts[f]) of each plane; slots
@@ -79,21 +171,11 @@ def batched_nms_keep(x: torch.Tensor, y: torch.Tensor, z: torch.Tensor, s: torch
     Optional outputs: keep_mask (uint32 [B, ceil(n_max/32)] survivor bits) and gate_pairs
     (int64 [B], the reference's WorkCounters.map_writes).  validate=True first checks every
     valid slot on the device (validate_batch) and raises ValidationError like the reference's
-    DetectionVector construction would.
+    DetectionVector construction would.  `workspace` (optional, uint8) must be zero-filled
+    before its first use (its head is persistent scratch every call leaves zero).  `launch`
+    pins a device path or decomposition (LaunchConfig; default: the library's choice).
     """
-    _require_cuda(x, "x", torch.int32, 2)
-    B, n_max = x.shape
-    for t, nm in ((y, "y"), (z, "z")):
-        _require_cuda(t, nm, torch.int32, 2)
-        if t.shape != x.shape:
-            raise ValueError(f"{nm} shape {tuple(t.shape)} != x shape {tuple(x.shape)}")
-    _require_cuda(s, "s", torch.float64, 2)
-    if s.shape != x.shape:
-        raise ValueError(f"s shape {tuple(s.shape)} != x shape {tuple(x.shape)}")
-    if counts is not None:
-        _require_cuda(counts, "counts", torch.int32, 1)
-        if counts.shape[0] != B:
-            raise ValueError("counts must have one entry per frame")
+    B, n_max = _check_planes(x, y, z, s, counts)
     theta = _check_theta(theta)
     tie = _check_tie(tie_break)
     if validate:
@@ -110,24 +192,29 @@ def batched_nms_keep(x: torch.Tensor, y: torch.Tensor, z: torch.Tensor, s: torch
         keep_idx = torch.empty((B, n_max), dtype=torch.int32, device=dev)
     if keep_count is None:
         keep_count = torch.empty((B,), dtype=torch.int32, device=dev)
-    if keep_mask is not None:
-        _require_cuda(keep_mask, "keep_mask", torch.int32, 2)
-        if tuple(keep_mask.shape) != (B, W32):
-            raise ValueError(f"keep_mask must be [{B}, {W32}] int32")
-    if gate_pairs is not None:
-        _require_cuda(gate_pairs, "gate_pairs", torch.int64, 1)
-    stream = torch.cuda.current_stream(dev)
-    need = _lib.workspace_bytes(B, n_max)
-    if workspace is None:
-        workspace = _WS.get(dev, stream.cuda_stream, need)
-    elif workspace.numel() < need:
-        raise ValueError(f"workspace needs {need} bytes")
-    lib = _lib.load()
-    p = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
-    st = lib.pnms_run(p(x), p(y), p(z), p(s), p(counts), B, n_max, int(d_max), theta, tie,
-                      p(keep_idx), p(keep_count), p(keep_mask), p(gate_pairs), p(workspace),
-                      workspace.numel(), stream.cuda_stream)
-    _lib.check(st, "pnms_run")
+    _check_out(keep_idx, "keep_idx", torch.int32, (B, n_max), dev)
+    _check_out(keep_count, "keep_count", torch.int32, (B,), dev)
+    _check_out(keep_mask, "keep_mask", torch.int32, (B, W32), dev)
+    _check_out(gate_pairs, "gate_pairs", torch.int64, (B,), dev)
+    if launch is None:
+        launch = _DEFAULT_LAUNCH[0]
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        need = _lib.workspace_bytes(B, n_max)
+        if workspace is None:
+            workspace = _WS.get(dev, stream.cuda_stream, need)
+        elif workspace.numel() < need:
+            raise ValueError(f"workspace needs {need} bytes")
+        lib = _lib.load()
+        p = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+        cfg = ctypes.byref(launch.to_c()) if launch is not None else None
+        info = _lib.RunInfoC(0)
+        st = lib.pnms_run_ex(p(x), p(y), p(z), p(s), p(counts), B, n_max, int(d_max), theta, tie,
+                             p(keep_idx), p(keep_count), p(keep_mask), p(gate_pairs), p(workspace),
+                             workspace.numel(), stream.cuda_stream, cfg, ctypes.byref(info), None)
+        _lib.check(st, "pnms_run_ex")
+    if launch is not None:
+        launch.path_taken = _lib.PATH_NAMES.get(info.path, str(info.path))
     return keep_idx, keep_count
 
 
@@ -181,23 +268,20 @@ def greedy_nms_keep(x: torch.Tensor, y: torch.Tensor, z: torch.Tensor, s: torch.
                     keep_mask: torch.Tensor | None = None):
     """Classic greedy NMS of every frame (oracles.greedy_nms, oracles.py:64-85) on the device.
 
-    Same planes and outputs as batched_nms_keep; frames of up to 4096 slots."""
-    _require_cuda(x, "x", torch.int32, 2)
-    B, n_max = x.shape
-    for t, nm in ((y, "y"), (z, "z")):
-        _require_cuda(t, nm, torch.int32, 2)
-    _require_cuda(s, "s", torch.float64, 2)
-    if counts is not None:
-        _require_cuda(counts, "counts", torch.int32, 1)
+    Same planes and outputs as batched_nms_keep."""
+    B, n_max = _check_planes(x, y, z, s, counts, keep_mask)
     theta = _check_theta(theta)
     dev = x.device
     if keep_idx is None:
         keep_idx = torch.empty((B, n_max), dtype=torch.int32, device=dev)
     if keep_count is None:
         keep_count = torch.empty((B,), dtype=torch.int32, device=dev)
+    _check_out(keep_idx, "keep_idx", torch.int32, (B, n_max), dev)
+    _check_out(keep_count, "keep_count", torch.int32, (B,), dev)
     p = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
-    st = _lib.load().pnms_greedy_run(p(x), p(y), p(z), p(s), p(counts), B, n_max, theta, p(keep_idx),
-                                     p(keep_count), p(keep_mask), torch.cuda.current_stream(dev).cuda_stream)
+    with torch.cuda.device(dev):
+        st = _lib.load().pnms_greedy_run(p(x), p(y), p(z), p(s), p(counts), B, n_max, theta, p(keep_idx),
+                                         p(keep_count), p(keep_mask), torch.cuda.current_stream(dev).cuda_stream)
     _lib.check(st, "pnms_greedy_run")
     return keep_idx, keep_count
 
@@ -219,22 +303,24 @@ def soft_nms_rescore_batched(x: torch.Tensor, y: torch.Tensor, z: torch.Tensor, 
                              sigma: float = 0.5, *, out: torch.Tensor | None = None, rounds: torch.Tensor | None = None):
     """Soft-NMS rescoring of every frame (oracles.soft_nms_rescore, oracles.py:88-123) on the
     device.  Returns (scores [B, n_max] float64 in input order, status [B] int32: 0 ok, 1 a
-    score outside the validated domain (finite, > 0)).  Frames of up to 4096 slots."""
+    score outside the validated domain (finite, > 0))."""
     code = _check_soft(mode, sigma)
-    _require_cuda(x, "x", torch.int32, 2)
-    B, n_max = x.shape
-    for t, nm in ((y, "y"), (z, "z")):
-        _require_cuda(t, nm, torch.int32, 2)
-    _require_cuda(s, "s", torch.float64, 2)
-    if counts is not None:
-        _require_cuda(counts, "counts", torch.int32, 1)
+    B, n_max = _check_planes(x, y, z, s, counts)
     dev = x.device
     if out is None:
         out = torch.empty((B, n_max), dtype=torch.float64, device=dev)
     status = torch.empty((B,), dtype=torch.int32, device=dev)
+    if out.shape != x.shape or out.dtype != torch.float64 or not out.is_contiguous() or out.device != dev:
+        raise ValueError(f"out must be a contiguous float64 tensor of shape {tuple(x.shape)} on {dev}")
+    if rounds is not None:
+        _require_cuda(rounds, "rounds", torch.int32, 1)
+        if rounds.shape[0] != B:
+            raise ValueError("rounds must have one entry per frame")
     p = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
-    st = _lib.load().pnms_soft_rescore(p(x), p(y), p(z), p(s), p(counts), B, n_max, code, float(theta), float(sigma),
-                                       p(out), p(status), p(rounds), torch.cuda.current_stream(dev).cuda_stream)
+    with torch.cuda.device(dev):
+        st = _lib.load().pnms_soft_rescore(p(x), p(y), p(z), p(s), p(counts), B, n_max, code, float(theta),
+                                           float(sigma), p(out), p(status), p(rounds),
+                                           torch.cuda.current_stream(dev).cuda_stream)
     _lib.check(st, "pnms_soft_rescore")
     return out, status
 
@@ -281,9 +367,9 @@ class NmsEngine:
     """Reusable batched engine bound to one device: workspace, outputs and pinned staging.
 
     run_device(...)  device-resident planes -> (keep_idx, keep_count) on the device
-    run_host(...)    pinned host planes -> H2D -> NMS -> D2H of survivor masks + counts,
-                     pipelined over `chunks` slices of the batch on two streams so copies
-                     overlap the kernels (the end-to-end path bench.py times)
+    run_host(...)    pinned host planes -> H2D -> NMS -> D2H of keep indices (or survivor
+                     masks) + counts, pipelined over `chunks` slices of the batch on two
+                     streams so copies overlap the kernels (the end-to-end path bench.py times)
     """
 
     def __init__(self, batch: int, n_max: int, theta: float = 0.5, tie_break: str = "paper_faithful",
@@ -306,6 +392,7 @@ class NmsEngine:
         self.ws_full = torch.zeros(_lib.workspace_bytes(self.batch, self.n_max), dtype=torch.uint8, device=dev)
         self.streams = [torch.cuda.Stream(device=dev) for _ in range(min(2, self.chunks))]
         self._dev_in = None
+        self._graphs: dict = {}
 
     def run_device(self, x, y, z, s, counts=None, want_idx: bool = True, want_mask: bool = False):
         return batched_nms_keep(x, y, z, s, counts, self.theta, self.tie_break, self.d_max,
@@ -321,11 +408,18 @@ class NmsEngine:
                             torch.empty((self.batch,), dtype=torch.int32, device=dev))
         return self._dev_in
 
-    def run_host(self, hx, hy, hz, hs, hcounts, out_mask, out_count):
-        """Pinned host planes in, pinned host survivor masks [B, W32] int32 + counts [B] out.
+    def run_host(self, hx, hy, hz, hs, hcounts, out_mask=None, out_count=None, out_idx=None, graph: bool = False):
+        """Pinned host planes in -> pinned host results out: survivor masks [B, W32] int32
+        (out_mask) and/or ascending keep indices [B, n_max] int32 (out_idx, first out_count[f]
+        valid), and counts [B] int32 (out_count).
 
-        x/y/z may be int32 or int16 planes (int16: pixel coordinates < 32768, 6 B per box on
-        the wire instead of 12; widened on the device by pnms_widen_i16)."""
+        x/y/z are the C ABI's int32 planes (20 B per box on the wire with the float64 score) or
+        int16 planes (pixel coordinates < 32768, 14 B per box; widened on the device by
+        pnms_widen_i16).  graph=True replays the whole pipeline (copies, kernels, read-back) as
+        one CUDA graph captured on the first call for this set of host buffers, which must then
+        stay allocated and be refilled in place between calls."""
+        if out_count is None:
+            raise ValueError("out_count is required")
         dx, dy, dz, _, _ = self._device_inputs()
         lib = _lib.load()
         if hx.dtype == torch.int16:
@@ -344,33 +438,17 @@ class NmsEngine:
             def stage(a, b, st):
                 for d, h in ((dx, hx), (dy, hy), (dz, hz)):
                     d[a:b].copy_(h[a:b], non_blocking=True)
-        self._pipeline(stage, hs, hcounts, out_mask, out_count)
+        run = lambda: self._pipeline(stage, hs, hcounts, out_mask, out_count, out_idx)  # noqa: E731
+        self._maybe_graph(graph, (hx, hy, hz, hs, hcounts, out_mask, out_count, out_idx), run)
 
-    def run_host_box32(self, hbox, hs, hcounts, out_mask, out_count, graph: bool = False):
+    def run_host_box32(self, hbox, hs, hcounts, out_mask=None, out_count=None, graph: bool = False, out_idx=None):
         """run_host with the packed 32-bit box format of `pack_box32` (x | y<<12 | z<<24 in an
         int32 plane [B, n_max]): 4 B of geometry per box on the wire, 12 B with the score;
-        unpacked on the device by pnms_unpack_box32.
-
-        graph=True replays the whole pipeline (copies, kernels, read-back) as one CUDA graph,
-        captured on the first call for this set of host buffers: no per-chunk host launch
-        overhead on the critical path.  The buffers must then stay allocated and be refilled
-        in place between calls."""
+        unpacked on the device by pnms_unpack_box32."""
         if hbox.dtype != torch.int32 or hbox.shape != (self.batch, self.n_max):
             raise ValueError("hbox must be an int32 [batch, n_max] plane of pack_box32 words")
-        if graph:
-            key = tuple(t.data_ptr() for t in (hbox, hs, hcounts, out_mask, out_count))
-            if getattr(self, "_graph_key", None) != key:
-                self._run_box32(hbox, hs, hcounts, out_mask, out_count)  # warm-up: attributes, buffers
-                torch.cuda.synchronize(self.device)
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
-                    self._run_box32(hbox, hs, hcounts, out_mask, out_count)
-                self._graph, self._graph_key = g, key
-            self._graph.replay()
-            return
-        self._run_box32(hbox, hs, hcounts, out_mask, out_count)
-
-    def _run_box32(self, hbox, hs, hcounts, out_mask, out_count):
+        if out_count is None:
+            raise ValueError("out_count is required")
         dx, dy, dz, _, _ = self._device_inputs()
         lib = _lib.load()
         if getattr(self, "_dev32", None) is None:
@@ -382,9 +460,25 @@ class NmsEngine:
             _lib.check(lib.pnms_unpack_box32(db[a:b].data_ptr(), dx[a:b].data_ptr(), dy[a:b].data_ptr(),
                                              dz[a:b].data_ptr(), (b - a) * self.n_max, st.cuda_stream),
                        "pnms_unpack_box32")
-        self._pipeline(stage, hs, hcounts, out_mask, out_count)
+        run = lambda: self._pipeline(stage, hs, hcounts, out_mask, out_count, out_idx)  # noqa: E731
+        self._maybe_graph(graph, (hbox, hs, hcounts, out_mask, out_count, out_idx), run)
 
-    def _pipeline(self, stage, hs, hcounts, out_mask, out_count):
+    def _maybe_graph(self, graph: bool, bufs, run):
+        if not graph:
+            run()
+            return
+        key = tuple(t.data_ptr() if t is not None else 0 for t in bufs)
+        g = self._graphs.get(key)
+        if g is None:
+            run()  # warm-up: attributes, buffers
+            torch.cuda.synchronize(self.device)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                run()
+            self._graphs[key] = g
+        g.replay()
+
+    def _pipeline(self, stage, hs, hcounts, out_mask, out_count, out_idx=None):
         dx, dy, dz, ds, dc = self._device_inputs()
         cur = torch.cuda.current_stream(self.device)
         for k, (a, b) in enumerate(self.bounds):
@@ -395,13 +489,14 @@ class NmsEngine:
                 ds[a:b].copy_(hs[a:b], non_blocking=True)
                 dc[a:b].copy_(hcounts[a:b], non_blocking=True)
                 batched_nms_keep(dx[a:b], dy[a:b], dz[a:b], ds[a:b], dc[a:b], self.theta, self.tie_break,
-                                 self.d_max, keep_idx=None, keep_count=self.keep_count[a:b],
-                                 keep_mask=self.keep_mask[a:b], workspace=self.ws[k % len(self.ws)],
-                                 want_idx=False)
-                out_mask[a:b].copy_(self.keep_mask[a:b], non_blocking=True)
+                                 self.d_max, keep_idx=self.keep_idx[a:b] if out_idx is not None else None,
+                                 keep_count=self.keep_count[a:b],
+                                 keep_mask=self.keep_mask[a:b] if out_mask is not None else None,
+                                 workspace=self.ws[k % len(self.ws)], want_idx=out_idx is not None)
+                if out_mask is not None:
+                    out_mask[a:b].copy_(self.keep_mask[a:b], non_blocking=True)
+                if out_idx is not None:
+                    out_idx[a:b].copy_(self.keep_idx[a:b], non_blocking=True)
                 out_count[a:b].copy_(self.keep_count[a:b], non_blocking=True)
         for st in self.streams:
             cur.wait_stream(st)
-
-    def launches_per_call(self) -> int:
-        return 3 if self.n_max <= 4096 else 4

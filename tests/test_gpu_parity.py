@@ -11,24 +11,30 @@ torch = pytest.importorskip("torch")
 
 import c_oracle  # noqa: E402
 from paper_2502_00535_b200 import (  # noqa: E402
-    DetectionVector, NmsConfig, batched_nms_keep, map_phase, nms_keep, reduce_phase, run_nms,
+    DetectionVector, LaunchConfig, NmsConfig, batched_nms_keep, launch_override, map_phase, nms_keep,
+    reduce_phase, run_nms,
 )
 from paper_2502_00535_b200.synth import random_frames  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 DEV = "cuda"
+PATHS = ["small", "binned", "binned_wide", "tiles", "cluster", "dense"]
 
 
-@pytest.fixture(params=["small", "binned", "binned_pairs", "dense"])
-def path(request, monkeypatch):
-    """Run a test through each device path: the single-launch unsorted kernel, the binned
-    kernel as per-row scans (default) or as cell-pair tiles (each with the dense pipeline for
-    the frames it declines), and the dense pipeline only."""
-    monkeypatch.setenv("PNMS_SMALL_PAIRS", str(1 << 40) if request.param == "small" else "0")
-    monkeypatch.setenv("PNMS_ALGO", "1" if request.param == "dense" else "0")
-    monkeypatch.setenv("PNMS_BINNED", "2" if request.param == "binned_pairs" else "0")
-    monkeypatch.setenv("PNMS_TILES_SMALL", "0")  # one CTA per frame (the tile path has its own tests)
-    return request.param
+@pytest.fixture(params=PATHS)
+def path(request):
+    """Run a test through each device path — the single-launch unsorted kernel, the binned
+    kernel (512- and 1024-thread CTAs), the tile and cluster kernels (each with the dense
+    pipeline for the frames it declines) and the dense pipeline only — by pinning it for every
+    pnms_run call inside the test (a call the path cannot take runs the library's choice)."""
+    with launch_override(LaunchConfig(path=request.param)):
+        yield request.param
+
+
+def _path_fits(path, B, n):
+    """Mirror of path_fits (pnms_capi.cu): whether a pinned path can take a B x n call."""
+    return {"small": n <= 4096 and B <= 1024 and B * ((n + 31) // 32) <= 4096, "binned": n <= 4096,
+            "binned_wide": n <= 2048, "tiles": True, "cluster": n <= 16 * 4096, "dense": True}[path]
 
 
 def _vec(c):
@@ -94,46 +100,99 @@ def test_map_phase_bits_match_reference(golden_cases):
     assert n > 300
 
 
-@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4f0", "C4f3", "C5f0", "C5f1", "C5f2", "C5f3"])
+CONFIG_FRAMES = ["C1", "C2", "C3", "C4f0", "C4f1", "C4f2", "C4f3", "C4f4", "C4f5", "C4f6", "C4f7",
+                 "C5f0", "C5f1", "C5f2", "C5f3"]
+
+
+@pytest.mark.parametrize("name", CONFIG_FRAMES)
 def test_config_frames_match_reference(golden_configs, name, path):
+    """The reference's own BASELINE config frames (golden keep indices and map_writes of
+    engine.run_nms) through every device path, with the path that ran asserted and no frame
+    declined to the dense fallback by the culling kernels."""
     g = golden_configs[name]
     n = len(g["x"])
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a).reshape(1, n)).to(DEV)  # noqa: E731
     gp = torch.empty(1, dtype=torch.int64, device=DEV)
+    declined = torch.full((1,), -1, dtype=torch.int32, device=DEV)
+    lc = LaunchConfig(path=path, declined=declined)
     ki, kc = batched_nms_keep(t(g["x"]), t(g["y"]), t(g["z"]), t(g["s"]), None, 0.5, "paper_faithful", n,
-                              gate_pairs=gp)
+                              gate_pairs=gp, launch=lc)
     k = int(kc.item())
     assert np.array_equal(ki[0, :k].cpu().numpy(), g["keep"])
     assert int(gp.item()) == int(g["writes"][0])
+    if _path_fits(path, 1, n):
+        assert lc.path_taken == path
+    assert int(declined.item()) == 0
 
 
-@pytest.mark.parametrize("shape", [(1, 128), (1, 256), (2, 256), (4, 512), (1, 512)])
-def test_launch_shape_invariance(golden_configs, shape, monkeypatch):
-    """Results are independent of the map decomposition (R rows/lane, chunk width)."""
-    monkeypatch.setenv("PNMS_SMALL_PAIRS", "0")
+@pytest.mark.parametrize("path_name", ["binned", "binned_wide", "tiles", "cluster", "small", "dense"])
+def test_config_batches_match_reference(golden_configs, path_name):
+    """The golden C4 and C5 frames as one batch each (the throughput launch shapes) through
+    each path, path asserted, nothing declined."""
+    for prefix in ("C4f", "C5f"):
+        names = sorted(k for k in golden_configs if k.startswith(prefix))
+        n = len(golden_configs[names[0]]["x"])
+        planes = [np.stack([golden_configs[k][c] for k in names]) for c in "xyzs"]
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)  # noqa: E731
+        declined = torch.full((1,), -1, dtype=torch.int32, device=DEV)
+        gp = torch.empty(len(names), dtype=torch.int64, device=DEV)
+        lc = LaunchConfig(path=path_name, declined=declined)
+        ki, kc = batched_nms_keep(*(t(a) for a in planes), None, 0.5, "paper_faithful", n, gate_pairs=gp, launch=lc)
+        ki, kc, gp = ki.cpu().numpy(), kc.cpu().numpy(), gp.cpu().numpy()
+        for f, k in enumerate(names):
+            assert np.array_equal(ki[f, :kc[f]], golden_configs[k]["keep"]), (k, path_name)
+            assert gp[f] == int(golden_configs[k]["writes"][0]), k
+        if _path_fits(path_name, len(names), n):
+            assert lc.path_taken == path_name
+        assert int(declined.item()) == 0
+
+
+def test_default_paths_of_the_configs(golden_configs):
+    """Which path the library picks for each BASELINE config shape (the ones bench.py times)."""
+    want = {"C1": "small", "C2": "small", "C3": "tiles"}
+    for name, p in want.items():
+        g = golden_configs[name]
+        n = len(g["x"])
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a).reshape(1, n)).to(DEV)  # noqa: E731
+        lc = LaunchConfig()
+        ki, kc = batched_nms_keep(t(g["x"]), t(g["y"]), t(g["z"]), t(g["s"]), None, 0.5, launch=lc)
+        assert lc.path_taken == p, name
+        assert np.array_equal(ki[0, : int(kc.item())].cpu().numpy(), g["keep"])
+    for (B, n), p in {(256, 1024): "binned", (100, 1024): "binned_wide", (400, 2048): "binned",
+                      (2, 4000): "tiles", (3, 9000): "cluster"}.items():
+        x, y, z, s = random_frames(B, n, seed=B, frame_w=3840, frame_h=2160)
+        lc = LaunchConfig()
+        ki, kc = batched_nms_keep(*(torch.from_numpy(a).to(DEV) for a in (x, y, z, s)), None, 0.5, launch=lc)
+        assert lc.path_taken == p, (B, n)
+        f = B - 1
+        want = c_oracle.run_frame(x[f], y[f], z[f], s[f], n, n, 0.5)
+        assert np.array_equal(ki[f, : int(kc[f])].cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("shape", [(1, 128), (1, 256), (2, 256), (4, 512), (1, 512), (4, 1024)])
+def test_launch_shape_invariance(golden_configs, shape):
+    """Results are independent of the dense map decomposition (R rows/lane, chunk width)."""
     g = golden_configs["C2"]
     n = len(g["x"])
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a).reshape(1, n)).to(DEV)  # noqa: E731
-    os.environ["PNMS_MAP_R"], os.environ["PNMS_MAP_CHUNK"] = str(shape[0]), str(shape[1])
-    try:
-        ki, kc = batched_nms_keep(t(g["x"]), t(g["y"]), t(g["z"]), t(g["s"]), None, 0.5)
-    finally:
-        del os.environ["PNMS_MAP_R"], os.environ["PNMS_MAP_CHUNK"]
+    lc = LaunchConfig(path="dense", map_rows=shape[0], map_chunk=shape[1])
+    ki, kc = batched_nms_keep(t(g["x"]), t(g["y"]), t(g["z"]), t(g["s"]), None, 0.5, launch=lc)
+    assert lc.path_taken == "dense"
     assert np.array_equal(ki[0, : int(kc.item())].cpu().numpy(), g["keep"])
 
 
-def _run_batch(x, y, z, s, counts, theta, tie, d_max=None):
+def _run_batch(x, y, z, s, counts, theta, tie, d_max=None, launch=None):
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)  # noqa: E731
-    ki, kc = batched_nms_keep(t(x), t(y), t(z), t(s), t(counts), theta, tie, d_max)
+    ki, kc = batched_nms_keep(t(x), t(y), t(z), t(s), t(counts), theta, tie, d_max, launch=launch)
     ki, kc = ki.cpu().numpy(), kc.cpu().numpy()
     return [ki[f, : kc[f]] for f in range(x.shape[0])]
 
 
-def test_binned_mixed_batch_vs_oracle(monkeypatch):
+@pytest.mark.parametrize("host_chain", [False, True])
+def test_binned_mixed_batch_vs_oracle(host_chain):
     """A batch where the binned kernel takes some frames and declines others (z > 126, a
-    zero side, a crowded cell, NaN scores, theta-independent ties) — all must be exact."""
-    monkeypatch.setenv("PNMS_SMALL_PAIRS", "0")
-    monkeypatch.setenv("PNMS_ALGO", "0")
+    zero side, a crowded cell, NaN scores, theta-independent ties) — all must be exact, with
+    the declined frames finished by the device-launched or the host-launched dense chain."""
     from paper_2502_00535_b200 import _lib
 
     x, y, z, s = random_frames(12, 900, seed=123, frame_w=800, frame_h=600, z_range=(4, 60), duplicate_fraction=0.1)
@@ -147,11 +206,14 @@ def test_binned_mixed_batch_vs_oracle(monkeypatch):
     counts[7] = 1
     counts[8] = 0
     counter = torch.zeros(1, dtype=torch.int64, device=DEV)
+    declined = torch.zeros(1, dtype=torch.int32, device=DEV)
     _lib.load().pnms_debug_count_pairs(counter.data_ptr())
     try:
         for tie in ("paper_faithful", "by_index"):
             for theta in (0.3, 0.5, 1.0):
-                got = _run_batch(x, y, z, s, counts, theta, tie, 950)
+                lc = LaunchConfig(path="binned", host_chain=host_chain, declined=declined)
+                got = _run_batch(x, y, z, s, counts, theta, tie, 950, launch=lc)
+                assert lc.path_taken == "binned" and int(declined.item()) >= 4
                 for f in range(12):
                     want = c_oracle.run_frame(x[f], y[f], z[f], s[f], int(counts[f]), 950, theta, tie)
                     assert np.array_equal(got[f], want), (f, tie, theta)
@@ -161,17 +223,16 @@ def test_binned_mixed_batch_vs_oracle(monkeypatch):
 
 
 @pytest.mark.parametrize("tie", ["paper_faithful", "by_index"])
-def test_tile_path_small_calls_vs_oracle(golden_configs, tie, monkeypatch):
-    """Calls of <= 2 frames of 2049..4096 slots that skip the single-launch path run on the
-    multi-CTA tile path (default PNMS_TILES_SMALL): golden C2, random and ragged pairs, a
-    declined frame (crowded cell) finished by the device-side fallback."""
-    monkeypatch.setenv("PNMS_SMALL_PAIRS", "0")
-    monkeypatch.delenv("PNMS_TILES_SMALL", raising=False)
+def test_tile_path_small_calls_vs_oracle(golden_configs, tie):
+    """Calls of <= 2 frames of 2049..4096 slots on the multi-CTA tile path: golden C2, random
+    and ragged pairs, a declined frame (crowded cell) finished by the device-side fallback."""
     g = golden_configs["C2"]
     n = len(g["x"])
     if tie == "paper_faithful":
         t = lambda a: torch.from_numpy(np.ascontiguousarray(a).reshape(1, n)).to(DEV)  # noqa: E731
-        ki, kc = batched_nms_keep(t(g["x"]), t(g["y"]), t(g["z"]), t(g["s"]), None, 0.5)
+        lc = LaunchConfig(path="tiles")
+        ki, kc = batched_nms_keep(t(g["x"]), t(g["y"]), t(g["z"]), t(g["s"]), None, 0.5, launch=lc)
+        assert lc.path_taken == "tiles"
         assert np.array_equal(ki[0, : int(kc.item())].cpu().numpy(), g["keep"])
     for n, counts in ((2049, [2049]), (3000, [3000, 2500]), (4096, [4096, 4096])):
         B = len(counts)
@@ -179,7 +240,7 @@ def test_tile_path_small_calls_vs_oracle(golden_configs, tie, monkeypatch):
         if B == 2 and n == 4096:
             x[1, :500] = 30; y[1, :500] = 40   # a crowded cell: declined, dense fallback
         cnt = np.array(counts, np.int32)
-        got = _run_batch(x, y, z, s, cnt, 0.45, tie, n)
+        got = _run_batch(x, y, z, s, cnt, 0.45, tie, n, launch=LaunchConfig(path="tiles"))
         for f in range(B):
             want = c_oracle.run_frame(x[f], y[f], z[f], s[f], int(cnt[f]), n, 0.45, tie)
             assert np.array_equal(got[f], want), (n, f, tie)
@@ -187,55 +248,56 @@ def test_tile_path_small_calls_vs_oracle(golden_configs, tie, monkeypatch):
 
 @pytest.mark.parametrize("cell", ["0", "-1", "-3", "-7", "-33", "-200", "64", "256", "400",
                                   "-64/16", "-32/5", "-8/128", "-1/2", "0/1"])
-def test_binned_cell_side_invariance(cell, monkeypatch):
+def test_binned_cell_side_invariance(cell):
     """Any cell shape is exact (pnms_binned.cuh): tiny cells (many runs per row, cell grids
     that grow until they fit), the default 16 x 64, squares, wide and tall rectangles and cells
     larger than the frame give the oracle's survivors, with ties, NaNs and ragged counts.
-    `cell` is PNMS_CELL_Q8[/PNMS_CELL_SX]."""
-    monkeypatch.setenv("PNMS_SMALL_PAIRS", "0")
-    monkeypatch.setenv("PNMS_ALGO", "0")
+    `cell` is cell_q8[/cell_sx] of the LaunchConfig."""
     q8, _, sx = cell.partition("/")
-    monkeypatch.setenv("PNMS_CELL_Q8", q8)
-    monkeypatch.setenv("PNMS_CELL_SX", sx or "0")
     x, y, z, s = random_frames(6, 1500, seed=77, frame_w=1280, frame_h=720, z_range=(3, 90), duplicate_fraction=0.1)
     s[1, ::5] = np.nan
     s[2, ::3] = 0.25
     counts = np.array([1500, 1499, 1200, 64, 1, 0], np.int32)
     for tie in ("paper_faithful", "by_index"):
-        got = _run_batch(x, y, z, s, counts, 0.4, tie, 1500)
+        lc = LaunchConfig(path="binned", cell_q8=int(q8), cell_sx=int(sx or 0))
+        got = _run_batch(x, y, z, s, counts, 0.4, tie, 1500, launch=lc)
+        assert lc.path_taken == "binned"
         for f in range(6):
             want = c_oracle.run_frame(x[f], y[f], z[f], s[f], int(counts[f]), 1500, 0.4, tie)
             assert np.array_equal(got[f], want), (cell, f, tie)
 
 
-def test_declined_frame_list_grid_stride(monkeypatch):
+def test_declined_frame_list_grid_stride():
     """Every frame declined by the binned kernel (theta = 0) in a batch larger than the
     persistent grids of the dense fallback kernels: the declined-frame list is walked with
     grid-stride loops (prep 296 CTAs, map 1184, compact 592)."""
-    monkeypatch.setenv("PNMS_SMALL_PAIRS", "0")
-    monkeypatch.setenv("PNMS_ALGO", "0")
     x, y, z, s = random_frames(1500, 300, seed=77, frame_w=400, frame_h=300)
     counts = np.full(1500, 300, np.int32)
     counts[::7] = 123
     for theta in (0.0, 0.4):
-        got = _run_batch(x, y, z, s, counts, theta, "paper_faithful", 300)
+        declined = torch.zeros(1, dtype=torch.int32, device=DEV)
+        got = _run_batch(x, y, z, s, counts, theta, "paper_faithful", 300,
+                         launch=LaunchConfig(path="binned", declined=declined))
+        assert int(declined.item()) == (1500 if theta == 0.0 else 0)
         want = c_oracle.run_batch(x, y, z, s, counts, 300, theta)
         for f in range(1500):
             assert np.array_equal(got[f], want[f]), (theta, f)
 
 
-LARGE_PATHS = {"tiles": ("1", "16"), "cluster8": ("2", "8"), "cluster16": ("2", "16")}
+LARGE_PATHS = {"tiles": ("tiles", 0), "cluster8": ("cluster", 8), "cluster16": ("cluster", 16)}
+
+
+def _large(large):
+    p, cs = LARGE_PATHS[large]
+    return LaunchConfig(path=p, cluster_size=cs)
 
 
 @pytest.mark.parametrize("large", list(LARGE_PATHS))
-def test_cluster_path_large_frames(large, monkeypatch):
+def test_cluster_path_large_frames(large):
     """Frames of 4097..20000 slots through the large-frame binned kernels (independent tile
     CTAs; one thread-block cluster per frame at both cluster sizes): ragged counts, exact ties,
     NaN and negative scores with padding, a band-crowded frame and a declined frame (side >
     126), both tie policies, vs the C oracle."""
-    monkeypatch.setenv("PNMS_ALGO", "0")
-    monkeypatch.setenv("PNMS_LARGE", LARGE_PATHS[large][0])
-    monkeypatch.setenv("PNMS_CLUSTER", LARGE_PATHS[large][1])
     cs = large
     n = 20000
     x, y, z, s = random_frames(5, n, seed=41, frame_w=3840, frame_h=2160, duplicate_fraction=0.05)
@@ -245,23 +307,22 @@ def test_cluster_path_large_frames(large, monkeypatch):
     y[3] = y[3] // 6                      # everything in a few cell rows: crowded bands
     z[4, 17] = 200                        # leaves the narrow7 domain -> dense pipeline
     for tie in ("paper_faithful", "by_index"):
-        got = _run_batch(x, y, z, s, counts, 0.5, tie, n + 7)
+        lc = _large(large)
+        got = _run_batch(x, y, z, s, counts, 0.5, tie, n + 7, launch=lc)
+        assert lc.path_taken == LARGE_PATHS[large][0]
         for f in range(5):
             want = c_oracle.run_frame(x[f], y[f], z[f], s[f], int(counts[f]), n + 7, 0.5, tie)
             assert np.array_equal(got[f], want), (cs, tie, f)
 
 
 @pytest.mark.parametrize("large", ["tiles", "cluster16"])
-def test_max_size_frame_cluster_path(large, monkeypatch):
+def test_max_size_frame_cluster_path(large):
     """A 60000-slot frame (tile kernel; the cluster path's largest band layout, 16 CTAs x 3750
     slots) vs the C oracle, both tie policies."""
-    monkeypatch.setenv("PNMS_ALGO", "0")
-    monkeypatch.setenv("PNMS_LARGE", LARGE_PATHS[large][0])
-    monkeypatch.setenv("PNMS_CLUSTER", LARGE_PATHS[large][1])
     n = 60000
     x, y, z, s = random_frames(1, n, seed=60, frame_w=3840 * 2, frame_h=2160 * 2, duplicate_fraction=0.02)
     for tie in ("paper_faithful", "by_index"):
-        got = _run_batch(x, y, z, s, np.array([n], np.int32), 0.45, tie, n)
+        got = _run_batch(x, y, z, s, np.array([n], np.int32), 0.45, tie, n, launch=_large(large))
         want = c_oracle.run_frame(x[0], y[0], z[0], s[0], n, n, 0.45, tie)
         assert np.array_equal(got[0], want), tie
 
@@ -343,16 +404,15 @@ def test_ragged_duplicates_vs_oracle(tie, theta, path):
 
 
 @pytest.mark.parametrize("n", [4097, 6000, 9000, 16384])
-@pytest.mark.parametrize("large", list(LARGE_PATHS))
-def test_chunked_sort_frames_vs_oracle(n, path, large, monkeypatch):
+@pytest.mark.parametrize("large", list(LARGE_PATHS) + ["dense"])
+def test_chunked_sort_frames_vs_oracle(n, large):
     """Frames above one CTA's capacity (tile kernel or thread-block-cluster kernel; chunk sort
     + merge-rank in the dense pipeline) with exact score ties."""
-    monkeypatch.setenv("PNMS_LARGE", LARGE_PATHS[large][0])
-    monkeypatch.setenv("PNMS_CLUSTER", LARGE_PATHS[large][1])
     x, y, z, s = random_frames(2, n, seed=n, frame_w=3840, frame_h=2160, z_range=(8, 64), duplicate_fraction=0.1)
     s[:, ::7] = 0.5
     for tie in ("paper_faithful", "by_index"):
-        got = _run_batch(x, y, z, s, np.array([n, n - 3], np.int32), 0.5, tie, n)
+        lc = LaunchConfig(path="dense") if large == "dense" else _large(large)
+        got = _run_batch(x, y, z, s, np.array([n, n - 3], np.int32), 0.5, tie, n, launch=lc)
         for f, c in enumerate((n, n - 3)):
             want = c_oracle.run_frame(x[f], y[f], z[f], s[f], c, n, 0.5, tie)
             assert np.array_equal(got[f], want), (n, f, tie)
@@ -419,15 +479,15 @@ def test_properties_full_size():
         assert set(base[f]).issubset(set(hi[f]))
 
 
-def test_small_path_tile_invariance(golden_configs, monkeypatch):
+def test_small_path_tile_invariance(golden_configs):
     """The single-launch path gives the same survivors for any column tiling."""
-    monkeypatch.setenv("PNMS_SMALL_PAIRS", str(1 << 40))
     g = golden_configs["C2"]
     n = len(g["x"])
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a).reshape(1, n)).to(DEV)  # noqa: E731
     for ct in (1, 3, 16, 128):
-        monkeypatch.setenv("PNMS_SMALL_CT", str(ct))
-        ki, kc = batched_nms_keep(t(g["x"]), t(g["y"]), t(g["z"]), t(g["s"]), None, 0.5)
+        lc = LaunchConfig(path="small", small_col_tiles=ct)
+        ki, kc = batched_nms_keep(t(g["x"]), t(g["y"]), t(g["z"]), t(g["s"]), None, 0.5, launch=lc)
+        assert lc.path_taken == "small"
         assert np.array_equal(ki[0, : int(kc.item())].cpu().numpy(), g["keep"]), ct
 
 
@@ -582,6 +642,17 @@ def test_engine_run_host_int16_and_int32_agree():
         eng.run_host(hx, hy, hz, hs, hc, om, oc)
         torch.cuda.synchronize()
         assert torch.equal(om, ref_mask.cpu()) and torch.equal(oc, ref_cnt.cpu()), dt
+    # the reference layout end to end: int32 planes in, keep indices out, direct and replayed
+    hx, hy, hz = (torch.from_numpy(a).pin_memory() for a in (x, y, z))
+    oi = torch.full((37, 500), -1, dtype=torch.int32).pin_memory()
+    for graph in (False, True, True):
+        oi.fill_(-1); oc.zero_()
+        eng.run_host(hx, hy, hz, hs, hc, out_count=oc, out_idx=oi, graph=graph)
+        torch.cuda.synchronize()
+        assert torch.equal(oc, ref_cnt.cpu())
+        for f in range(0, 37, 6):
+            want = c_oracle.run_frame(x[f], y[f], z[f], s[f], 500, 500, 0.5)
+            assert np.array_equal(oi[f, : int(oc[f])].numpy(), want), (graph, f)
     # packed 32-bit boxes (x | y<<12 | z<<24), 12 B per box with the score
     from paper_2502_00535_b200 import pack_box32
 
@@ -605,13 +676,12 @@ def test_engine_run_host_int16_and_int32_agree():
 
 
 @pytest.mark.parametrize("chunks", [1, 2])
-def test_device_fallback_chain_direct_and_graph(chunks, monkeypatch):
+def test_device_fallback_chain_direct_and_graph(chunks):
     """Frames the binned kernel declines are finished by the dense chain it tail-launches from
     the device (pnms_fallback.cuh) — in direct calls, in repeated calls on one workspace (the
     ticket and count are left zero) and when the call is replayed from a CUDA graph."""
     from paper_2502_00535_b200 import NmsEngine, pack_box32
 
-    monkeypatch.setenv("PNMS_SMALL_PAIRS", "0")
     F, n = 16, 600
     x, y, z, s = random_frames(F, n, seed=21, frame_w=640, frame_h=480, z_range=(4, 40))
     for f in (2, 7, 11):
@@ -635,47 +705,51 @@ def test_device_fallback_chain_direct_and_graph(chunks, monkeypatch):
     om = torch.empty((F, eng.W32), dtype=torch.int32).pin_memory()
     oc = torch.empty((F,), dtype=torch.int32).pin_memory()
     want_m, want_c = expect(x, y, z, s)
-    for graph in (False, False, True, True):
-        om.zero_(); oc.zero_()
-        eng.run_host_box32(hb, hs, hc, om, oc, graph=graph)
+    with launch_override(LaunchConfig(path="binned")):
+        for graph in (False, False, True, True):
+            om.zero_(); oc.zero_()
+            eng.run_host_box32(hb, hs, hc, om, oc, graph=graph)
+            torch.cuda.synchronize()
+            assert torch.equal(oc, want_c) and torch.equal(om, want_m), graph
+        # new inputs with other declined frames, replayed from the captured graph
+        x2, y2, z2, s2 = random_frames(F, n, seed=22, frame_w=640, frame_h=480, z_range=(4, 40))
+        x2[0, :300] = 100; y2[0, :300] = 100
+        x2[15, 100:400] = 9; y2[15, 100:400] = 300
+        hb.copy_(torch.from_numpy(pack_box32(x2, y2, z2))); hs.copy_(torch.from_numpy(s2))
+        eng.run_host_box32(hb, hs, hc, om, oc, graph=True)
         torch.cuda.synchronize()
-        assert torch.equal(oc, want_c) and torch.equal(om, want_m), graph
-    # new inputs with other declined frames, replayed from the captured graph
-    x2, y2, z2, s2 = random_frames(F, n, seed=22, frame_w=640, frame_h=480, z_range=(4, 40))
-    x2[0, :300] = 100; y2[0, :300] = 100
-    x2[15, 100:400] = 9; y2[15, 100:400] = 300
-    hb.copy_(torch.from_numpy(pack_box32(x2, y2, z2))); hs.copy_(torch.from_numpy(s2))
-    eng.run_host_box32(hb, hs, hc, om, oc, graph=True)
-    torch.cuda.synchronize()
     want_m, want_c = expect(x2, y2, z2, s2)
     assert torch.equal(oc, want_c) and torch.equal(om, want_m)
 
 
 @pytest.mark.parametrize("crowd", [100, 255, 256])
 @pytest.mark.parametrize("where", ["binned", "tiles", "cluster"])
-def test_crowded_cells_at_the_cell_limit(crowd, where, monkeypatch):
+def test_crowded_cells_at_the_cell_limit(crowd, where):
     """Cells of up to kBinCellMax = 255 boxes stay on the culling paths (skip distance and
     in-cell ranks at their 8-bit field limits); 256 is declined to the dense pipeline — exact
     either way, with equal scores inside the crowd."""
-    monkeypatch.setenv("PNMS_SMALL_PAIRS", "0")
     if where == "binned":
         B, n = 3, 1500
     else:
         B, n = (1, 6000) if where == "tiles" else (3, 6000)
-        monkeypatch.setenv("PNMS_LARGE", "1" if where == "tiles" else "2")
     x, y, z, s = random_frames(B, n, seed=crowd, frame_w=1800, frame_h=1000, z_range=(4, 60))
     f = B - 1
     x[f, :crowd] = 300 + np.arange(crowd) % 3     # one 16 x 64 cell
     y[f, :crowd] = 200 + np.arange(crowd) % 5
     s[f, : crowd // 2] = 0.75                     # ties inside the crowd
     for tie in ("paper_faithful", "by_index"):
-        got = _run_batch(x, y, z, s, np.full(B, n, np.int32), 0.5, tie, n)
+        declined = torch.zeros(1, dtype=torch.int32, device=DEV)
+        lc = LaunchConfig(path=where, declined=declined)
+        got = _run_batch(x, y, z, s, np.full(B, n, np.int32), 0.5, tie, n, launch=lc)
+        assert lc.path_taken == where
+        if where == "binned" and crowd != 255:  # 255 + a random neighbour may tip the cell over
+            assert int(declined.item()) == (1 if crowd > 255 else 0)
         for g in range(B):
             want = c_oracle.run_frame(x[g], y[g], z[g], s[g], n, n, 0.5, tie)
             assert np.array_equal(got[g], want), (crowd, where, tie, g)
 
 
-def test_one_workspace_across_paths_and_shapes(monkeypatch):
+def test_one_workspace_across_paths_and_shapes():
     """The persistent scratch head is shared by the single-launch path (suppression words,
     tickets), the binned and tile paths (declined count, tile masks and flags): calls of every
     path and shape, with and without declined frames, interleaved on ONE workspace, each
@@ -685,12 +759,8 @@ def test_one_workspace_across_paths_and_shapes(monkeypatch):
     ws = torch.zeros(_lib.workspace_bytes(64, 9000), dtype=torch.uint8, device=DEV)
     rng = np.random.default_rng(5)
     cases = []
-    for (B, n, env) in ((3, 700, {}),                                              # single launch
-                        (20, 900, {"PNMS_SMALL_PAIRS": "0"}),                      # binned
-                        (1, 3000, {"PNMS_SMALL_PAIRS": "0"}),                      # tiles (small call)
-                        (2, 9000, {}),                                             # tiles
-                        (3, 9000, {"PNMS_LARGE": "2"}),                            # cluster
-                        (40, 1200, {"PNMS_SMALL_PAIRS": "0"})):                    # binned again
+    for (B, n, env) in ((3, 700, "small"), (20, 900, "binned"), (1, 3000, "tiles"), (2, 9000, "auto"),
+                        (3, 9000, "cluster"), (40, 1200, "binned"), (5, 800, "binned_wide"), (2, 500, "dense")):
         x, y, z, s = random_frames(B, n, seed=int(rng.integers(1 << 30)), frame_w=2000, frame_h=1500,
                                    z_range=(4, 70))
         if B > 1:
@@ -698,13 +768,14 @@ def test_one_workspace_across_paths_and_shapes(monkeypatch):
         cases.append((x, y, z, s, env))
     for rep in range(2):
         for x, y, z, s, env in cases:
-            for k in ("PNMS_SMALL_PAIRS", "PNMS_LARGE"):
-                monkeypatch.delenv(k, raising=False)
-            for k, v in env.items():
-                monkeypatch.setenv(k, v)
             B, n = x.shape
             t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)  # noqa: E731
-            ki, kc = batched_nms_keep(t(x), t(y), t(z), t(s), None, 0.5, "by_index", n, workspace=ws)
+            lc = LaunchConfig(path=env)
+            gp = torch.empty(B, dtype=torch.int64, device=DEV)
+            ki, kc = batched_nms_keep(t(x), t(y), t(z), t(s), None, 0.5, "by_index", n, workspace=ws, launch=lc,
+                                      gate_pairs=gp)
+            assert env == "auto" or lc.path_taken == env
+            assert (gp.cpu().numpy() == n * (n - 1) // 2).all()  # by_index: every pair gates once
             ki, kc = ki.cpu().numpy(), kc.cpu().numpy()
             for f in range(B):
                 want = c_oracle.run_frame(x[f], y[f], z[f], s[f], n, n, 0.5, "by_index")

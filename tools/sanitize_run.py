@@ -1,6 +1,6 @@
 """Small workloads over every device path, for compute-sanitizer (memcheck / racecheck /
-synccheck) runs: binned, pair tiles, dense, small, tiles, cluster, greedy, Soft-NMS, validation."""
-import os
+synccheck) runs: small, binned (both CTA sizes), tiles, cluster, dense, the declined-frame
+chain, map_writes, greedy, Soft-NMS, validation."""
 import sys
 from pathlib import Path
 
@@ -9,24 +9,22 @@ import torch
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
-from paper_2502_00535_b200 import batched_nms_keep, greedy_nms_keep, soft_nms_rescore_batched  # noqa: E402
+from paper_2502_00535_b200 import (  # noqa: E402
+    LaunchConfig, batched_nms_keep, greedy_nms_keep, soft_nms_rescore_batched, validate_batch,
+)
 from paper_2502_00535_b200.synth import random_frames  # noqa: E402
 
 dev = torch.device("cuda", 0)
 t = lambda arrs: [torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in arrs]  # noqa: E731
 small = t(random_frames(6, 700, seed=1, duplicate_fraction=0.1))
 big = t(random_frames(2, 9000, seed=2, frame_w=3840, frame_h=2160))
-for env in ({"PNMS_SMALL_PAIRS": "0", "PNMS_ALGO": "0"}, {"PNMS_SMALL_PAIRS": "0", "PNMS_ALGO": "0", "PNMS_BINNED": "2"},
-            {"PNMS_SMALL_PAIRS": "0", "PNMS_ALGO": "1"}, {"PNMS_SMALL_PAIRS": str(1 << 40)}):
-    os.environ.update(env)
-    for theta in (0.0, 0.5):
-        batched_nms_keep(*small, None, theta, "by_index")
-    for k in ("PNMS_BINNED",):
-        os.environ.pop(k, None)
-os.environ.update({"PNMS_SMALL_PAIRS": "0", "PNMS_ALGO": "0"})
-for large in ("1", "2"):
-    os.environ["PNMS_LARGE"] = large
-    batched_nms_keep(*big, None, 0.5)
+gp = torch.empty(6, dtype=torch.int64, device=dev)
+for path in ("small", "binned", "binned_wide", "tiles", "cluster", "dense"):
+    for theta in (0.0, 0.5):  # theta 0: every frame declined by the culling kernels
+        batched_nms_keep(*small, None, theta, "by_index", gate_pairs=gp, launch=LaunchConfig(path=path))
+for path in ("tiles", "cluster"):
+    batched_nms_keep(*big, None, 0.5, launch=LaunchConfig(path=path))
+validate_batch(*small)
 greedy_nms_keep(*small, None, 0.5)
 soft_nms_rescore_batched(*small, None, "gaussian", 0.3, 0.5)
 torch.cuda.synchronize()
