@@ -158,29 +158,44 @@ int pnms_map_reference_layout(const int32_t* x, const int32_t* y, const int32_t*
  *  mask  uint8 [ceil(d_max/8)]  packed little-endian (SurvivorMask.bits, engine.py:120-122) */
 int pnms_reduce_rows(const uint64_t* bits, int d_max, int k, uint8_t* mask, void* stream);
 
-/* Classic greedy NMS (oracles.greedy_nms, oracles.py:64-85) for `batch` frames of up to 4096
- * slots: visit valid detections by (score desc, index asc), keep one unless an already-kept
- * detection covers it (positive extents on both axes and w*h >= theta*(z_ref+1)^2,
+/* Classic greedy NMS (oracles.greedy_nms, oracles.py:64-85) for `batch` frames of up to
+ * PNMS_MAX_SLOTS slots: visit valid detections by (score desc, index asc), keep one unless an
+ * already-kept detection covers it (positive extents on both axes and w*h >= theta*(z_ref+1)^2,
  * oracles.py:20-29).  Outputs as pnms_run (keep_idx ascending, keep_count, keep_mask; each
- * may be NULL).  Needs no workspace.  Scores must not be NaN (the reference's ordering is
- * undefined for NaN; here NaN detections are kept and never cover others). */
+ * may be NULL).  Frames of up to 4096 slots need no workspace; larger frames need
+ * pnms_variant_workspace_bytes() bytes (pnms_run without it returns PNMS_ETOO_LARGE for them).
+ * Scores must not be NaN (the reference's ordering is undefined for NaN; here NaN detections
+ * are kept and never cover others). */
 int pnms_greedy_run(const int32_t* x, const int32_t* y, const int32_t* z, const double* s,
                     const int32_t* counts, int batch, int n_max, double theta, int32_t* keep_idx,
                     int32_t* keep_count, uint32_t* keep_mask, void* stream);
+int pnms_greedy_run_ws(const int32_t* x, const int32_t* y, const int32_t* z, const double* s,
+                       const int32_t* counts, int batch, int n_max, double theta, int32_t* keep_idx,
+                       int32_t* keep_count, uint32_t* keep_mask, void* workspace, size_t workspace_bytes,
+                       void* stream);
+
+/* Device scratch the greedy and Soft-NMS kernels need for `batch` frames of stride n_max
+ * (0 up to 4096 slots, where the per-slot state lives in shared memory). */
+int pnms_variant_workspace_bytes(int batch, int n_max, size_t* out_bytes);
 
 /* Soft-NMS rescoring (oracles.soft_nms_rescore, oracles.py:88-123) for `batch` frames of up
- * to 4096 slots: repeatedly select the pending detection with the highest current score
+ * to PNMS_MAX_SLOTS slots (workspace as pnms_greedy_run_ws for frames over 4096 slots):
+ * repeatedly select the pending detection with the highest current score
  * (ties: lowest index) and rescale every pending score by its coverage cov = w*h/(z_sel+1)^2
  * of the selected box: mode 0 (linear) s *= 1 - cov when cov >= theta; mode 1 (gaussian)
  * s *= exp(-cov^2 / sigma).  out_s [batch, n_max] float64 receives the rescored scores in
  * input order (0.0 in padding slots).  status [batch]: 0 ok, 1 a valid score is not finite
  * and > 0 (the validated domain, detections.py:79-84; frame left unwritten).  rounds
- * [batch] (may be NULL): parallel resolution rounds used.  Linear mode is bit-identical to
- * the reference; gaussian mode uses the device exp (<= 1 ulp per factor from libm's).
- * mode not 0/1 or sigma <= 0 -> PNMS_EINVAL_ARG (oracles.py:108-111).  No workspace. */
+ * [batch] (may be NULL): parallel resolution rounds used.  Both modes are bit-identical to
+ * the reference (gaussian: exp restated from the host libm, see pnms_debug_exp).
+ * mode not 0/1 or sigma <= 0 -> PNMS_EINVAL_ARG (oracles.py:108-111). */
 int pnms_soft_rescore(const int32_t* x, const int32_t* y, const int32_t* z, const double* s,
                       const int32_t* counts, int batch, int n_max, int mode, double theta, double sigma,
                       double* out_s, int32_t* status, int32_t* rounds, void* stream);
+int pnms_soft_rescore_ws(const int32_t* x, const int32_t* y, const int32_t* z, const double* s,
+                         const int32_t* counts, int batch, int n_max, int mode, double theta, double sigma,
+                         double* out_s, int32_t* status, int32_t* rounds, void* workspace,
+                         size_t workspace_bytes, void* stream);
 
 /* Device-side ingest validation (detections.py:60-85, Detection.validate): for each frame,
  * first_bad[f] = the smallest slot index in [0, counts[f]) violating the detection invariants
@@ -204,6 +219,10 @@ int pnms_unpack_box32(const uint32_t* box, int32_t* x, int32_t* y, int32_t* z, l
 /* Diagnostics: device counter (uint64) that the binned path atomically increments by the
  * number of pair tests it executes; NULL disables (default).  Process-wide, not reentrant. */
 int pnms_debug_count_pairs(uint64_t* device_counter);
+
+/* Diagnostics: y[i] = exp(x[i]) computed on the device exactly as the host C library does
+ * (pnms_libm.cuh, the exp gaussian Soft-NMS uses); x, y: float64 [n] device arrays. */
+int pnms_debug_exp(const double* x, double* y, long long n, void* stream);
 
 /* Diagnostics: device buffer of >= 256 uint64 that the large-frame kernels fill with global-timer
  * stamps (CTA r < 16, phase k < 16 at [r*16 + k]); NULL disables (default).  Process-wide. */

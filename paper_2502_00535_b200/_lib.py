@@ -25,10 +25,14 @@ EXPORTED_SYMBOLS = (
     "pnms_reduce_rows",
     "pnms_validate",
     "pnms_greedy_run",
+    "pnms_greedy_run_ws",
+    "pnms_variant_workspace_bytes",
     "pnms_soft_rescore",
+    "pnms_soft_rescore_ws",
     "pnms_widen_i16",
     "pnms_unpack_box32",
     "pnms_debug_count_pairs",
+    "pnms_debug_exp",
     "pnms_debug_trace",
     "pnms_strerror",
     "pnms_last_cuda_error",
@@ -112,6 +116,12 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
     lib.pnms_validate.restype = i32
     lib.pnms_greedy_run.argtypes = [vp, vp, vp, vp, vp, i32, i32, f64, vp, vp, vp, vp]
     lib.pnms_greedy_run.restype = i32
+    lib.pnms_greedy_run_ws.argtypes = [vp, vp, vp, vp, vp, i32, i32, f64, vp, vp, vp, vp, sz, vp]
+    lib.pnms_greedy_run_ws.restype = i32
+    lib.pnms_variant_workspace_bytes.argtypes = [i32, i32, ctypes.POINTER(sz)]
+    lib.pnms_variant_workspace_bytes.restype = i32
+    lib.pnms_soft_rescore_ws.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, f64, f64, vp, vp, vp, vp, sz, vp]
+    lib.pnms_soft_rescore_ws.restype = i32
     lib.pnms_soft_rescore.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, f64, f64, vp, vp, vp, vp]
     lib.pnms_soft_rescore.restype = i32
     lib.pnms_widen_i16.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_longlong, vp]
@@ -120,6 +130,8 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
     lib.pnms_unpack_box32.restype = i32
     lib.pnms_debug_trace.argtypes = [vp]
     lib.pnms_debug_trace.restype = i32
+    lib.pnms_debug_exp.argtypes = [vp, vp, ctypes.c_longlong, vp]
+    lib.pnms_debug_exp.restype = i32
     lib.pnms_debug_count_pairs.argtypes = [vp]
     lib.pnms_debug_count_pairs.restype = i32
     lib.pnms_strerror.argtypes = [i32]
@@ -148,6 +160,13 @@ def check(status: int, what: str) -> None:
     if status == PNMS_ECUDA:
         msg += f" (cudaError {load().pnms_last_cuda_error()})"
     raise NativeLibraryError(msg)
+
+
+def variant_workspace_bytes(batch: int, n_max: int) -> int:
+    out = ctypes.c_size_t(0)
+    check(load().pnms_variant_workspace_bytes(int(batch), int(n_max), ctypes.byref(out)),
+          "pnms_variant_workspace_bytes")
+    return int(out.value)
 
 
 def workspace_bytes(batch: int, n_max: int) -> int:

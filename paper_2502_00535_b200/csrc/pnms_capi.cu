@@ -73,6 +73,11 @@ __global__ void __launch_bounds__(256) pnms_unpack_box32_kernel(const uint32_t* 
     }
   }
 }
+// y[i] = glibc_exp(x[i]): the device build of the libm restatement (diagnostics / tests)
+__global__ void __launch_bounds__(256) pnms_exp_kernel(const double* __restrict__ x, double* __restrict__ y, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = glibc_exp(x[i]);
+}
 }  // namespace pnms
 
 namespace {
@@ -766,12 +771,19 @@ int pnms_validate(const int32_t* x, const int32_t* y, const int32_t* z, const do
   return e == cudaSuccess ? PNMS_OK : fail_cuda(e);
 }
 
-int pnms_greedy_run(const int32_t* x, const int32_t* y, const int32_t* z, const double* s, const int32_t* counts,
-                    int batch, int n_max, double theta, int32_t* keep_idx, int32_t* keep_count, uint32_t* keep_mask,
-                    void* stream) {
+int pnms_variant_workspace_bytes(int batch, int n_max, size_t* out_bytes) {
+  if (!out_bytes || batch < 0 || n_max < 0) return PNMS_EINVAL_ARG;
+  if (n_max > PNMS_MAX_SLOTS) return PNMS_ETOO_LARGE;
+  *out_bytes = n_max <= kGreedyMaxSlots ? 0 : (size_t)batch * std::max(greedy_smem_bytes(n_max), soft_smem_bytes(n_max));
+  return PNMS_OK;
+}
+
+int pnms_greedy_run_ws(const int32_t* x, const int32_t* y, const int32_t* z, const double* s, const int32_t* counts,
+                       int batch, int n_max, double theta, int32_t* keep_idx, int32_t* keep_count, uint32_t* keep_mask,
+                       void* workspace, size_t workspace_bytes, void* stream) {
   if (!(theta >= 0.0 && theta <= 1.0)) return PNMS_EINVAL_THETA;
   if (batch < 0 || n_max < 0) return PNMS_EINVAL_ARG;
-  if (n_max > kGreedyMaxSlots) return PNMS_ETOO_LARGE;
+  if (n_max > PNMS_MAX_SLOTS) return PNMS_ETOO_LARGE;
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e;
   if (batch == 0) return PNMS_OK;
@@ -784,21 +796,36 @@ int pnms_greedy_run(const int32_t* x, const int32_t* y, const int32_t* z, const 
   ga.x = x; ga.y = y; ga.z = z; ga.s = s; ga.counts = counts;
   ga.batch = batch; ga.n_max = n_max; ga.W32 = (n_max + 31) / 32; ga.theta = theta;
   ga.keep_idx = keep_idx; ga.keep_count = keep_count; ga.keep_mask = keep_mask;
-  static SmemCache cfg;
-  const size_t smem = greedy_smem_bytes(n_max);
-  if ((e = ensure_smem(pnms_greedy_frame, smem, cfg)) != cudaSuccess) return fail_cuda(e);
-  pnms_greedy_frame<<<batch, kGreedyThreads, smem, st>>>(ga);
+  ga.scratch = static_cast<unsigned char*>(workspace);
+  ga.scratch_stride = greedy_smem_bytes(n_max);
+  if (n_max <= kGreedyMaxSlots) {  // per-slot state in shared memory
+    static SmemCache cfg;
+    const size_t smem = greedy_smem_bytes(n_max);
+    if ((e = ensure_smem(pnms_greedy_frame<false>, smem, cfg)) != cudaSuccess) return fail_cuda(e);
+    pnms_greedy_frame<false><<<batch, kGreedyThreads, smem, st>>>(ga);
+  } else {                         // large frames: the same state in the caller's workspace
+    if (!workspace || workspace_bytes < (size_t)batch * ga.scratch_stride) return PNMS_EWORKSPACE;
+    pnms_greedy_frame<true><<<batch, kGreedyThreads, 0, st>>>(ga);
+  }
   if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
   return PNMS_OK;
 }
 
-int pnms_soft_rescore(const int32_t* x, const int32_t* y, const int32_t* z, const double* s, const int32_t* counts,
-                      int batch, int n_max, int mode, double theta, double sigma, double* out_s, int32_t* status,
-                      int32_t* rounds, void* stream) {
+int pnms_greedy_run(const int32_t* x, const int32_t* y, const int32_t* z, const double* s, const int32_t* counts,
+                    int batch, int n_max, double theta, int32_t* keep_idx, int32_t* keep_count, uint32_t* keep_mask,
+                    void* stream) {
+  if (n_max > kGreedyMaxSlots) return PNMS_ETOO_LARGE;  // larger frames: pnms_greedy_run_ws
+  return pnms_greedy_run_ws(x, y, z, s, counts, batch, n_max, theta, keep_idx, keep_count, keep_mask, nullptr, 0,
+                            stream);
+}
+
+int pnms_soft_rescore_ws(const int32_t* x, const int32_t* y, const int32_t* z, const double* s, const int32_t* counts,
+                         int batch, int n_max, int mode, double theta, double sigma, double* out_s, int32_t* status,
+                         int32_t* rounds, void* workspace, size_t workspace_bytes, void* stream) {
   if (mode != 0 && mode != 1) return PNMS_EINVAL_ARG;
   if (!(sigma > 0.0)) return PNMS_EINVAL_ARG;
   if (batch < 0 || n_max < 0) return PNMS_EINVAL_ARG;
-  if (n_max > kSoftMaxSlots) return PNMS_ETOO_LARGE;
+  if (n_max > PNMS_MAX_SLOTS) return PNMS_ETOO_LARGE;
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e;
   if (batch == 0) return PNMS_OK;
@@ -812,12 +839,27 @@ int pnms_soft_rescore(const int32_t* x, const int32_t* y, const int32_t* z, cons
   sa.x = x; sa.y = y; sa.z = z; sa.s = s; sa.counts = counts;
   sa.batch = batch; sa.n_max = n_max; sa.mode = mode; sa.theta = theta; sa.sigma = sigma;
   sa.out_s = out_s; sa.status = status; sa.rounds = rounds;
-  static SmemCache cfg;
-  const size_t smem = soft_smem_bytes(n_max);
-  if ((e = ensure_smem(pnms_soft_frame, smem, cfg)) != cudaSuccess) return fail_cuda(e);
-  pnms_soft_frame<<<batch, kSoftThreads, smem, st>>>(sa);
+  sa.scratch = static_cast<unsigned char*>(workspace);
+  sa.scratch_stride = soft_smem_bytes(n_max);
+  if (n_max <= kSoftMaxSlots) {
+    static SmemCache cfg;
+    const size_t smem = soft_smem_bytes(n_max);
+    if ((e = ensure_smem(pnms_soft_frame<false>, smem, cfg)) != cudaSuccess) return fail_cuda(e);
+    pnms_soft_frame<false><<<batch, kSoftThreads, smem, st>>>(sa);
+  } else {
+    if (!workspace || workspace_bytes < (size_t)batch * sa.scratch_stride) return PNMS_EWORKSPACE;
+    pnms_soft_frame<true><<<batch, kSoftThreads, 0, st>>>(sa);
+  }
   if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e);
   return PNMS_OK;
+}
+
+int pnms_soft_rescore(const int32_t* x, const int32_t* y, const int32_t* z, const double* s, const int32_t* counts,
+                      int batch, int n_max, int mode, double theta, double sigma, double* out_s, int32_t* status,
+                      int32_t* rounds, void* stream) {
+  if (n_max > kSoftMaxSlots) return PNMS_ETOO_LARGE;  // larger frames: pnms_soft_rescore_ws
+  return pnms_soft_rescore_ws(x, y, z, s, counts, batch, n_max, mode, theta, sigma, out_s, status, rounds, nullptr, 0,
+                              stream);
 }
 
 int pnms_widen_i16(const int16_t* x16, const int16_t* y16, const int16_t* z16, int32_t* x, int32_t* y, int32_t* z,
@@ -835,6 +877,15 @@ int pnms_unpack_box32(const uint32_t* box, int32_t* x, int32_t* y, int32_t* z, l
   if (n == 0) return PNMS_OK;
   const long long blocks = std::min<long long>((n + 1023) / 1024, 148LL * 16);
   pnms_unpack_box32_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(box, x, y, z, n);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? PNMS_OK : fail_cuda(e);
+}
+
+int pnms_debug_exp(const double* x, double* y, long long n, void* stream) {
+  if (n < 0 || (n > 0 && (!x || !y))) return PNMS_EINVAL_ARG;
+  if (n == 0) return PNMS_OK;
+  const long long blocks = std::min<long long>((n + 255) / 256, 148LL * 8);
+  pnms_exp_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x, y, n);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? PNMS_OK : fail_cuda(e);
 }

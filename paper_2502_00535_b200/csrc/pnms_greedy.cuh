@@ -14,8 +14,11 @@
 //
 // Candidates: greedy never covers on zero overlap, so spatial cells of side max_z + 1 (3x3
 // neighbourhood, see pnms_binned.cuh) are exact for every theta; frames with negative
-// coordinates or a crowded cell scan all slots instead.  One CTA per frame, shared memory
-// only; covers() is evaluated in exact 64-bit integer arithmetic against ceil(fl64(theta*a)).
+// coordinates or a crowded cell scan all slots instead.  One CTA per frame; covers() is
+// evaluated in exact 64-bit integer arithmetic against ceil(fl64(theta*a)).  The per-slot
+// state of frames up to kGreedyMaxSlots lives in shared memory; larger frames (up to
+// PNMS_MAX_SLOTS) keep the same layout in a caller-provided global workspace slice (L2-resident:
+// ~46 B per slot), with the same code (GLOBAL template parameter).
 #pragma once
 #include "pnms_common.cuh"
 #include "pnms_sort.cuh"
@@ -23,8 +26,9 @@
 namespace pnms {
 
 constexpr int kGreedyThreads = 512;
-constexpr int kGreedyMaxSlots = 4096;
+constexpr int kGreedyMaxSlots = 4096;   // largest frame whose state fits shared memory
 constexpr int kGreedyCellMax = 64;
+constexpr int kGreedyMaxCells = 65535;  // cell ids are 16-bit
 
 enum GreedyState : uint8_t { kUndecided = 0, kKept = 1, kRemoved = 2 };
 
@@ -37,13 +41,19 @@ struct GreedyArgs {
   int32_t* keep_idx;
   int32_t* keep_count;
   uint32_t* keep_mask;
+  unsigned char* scratch;  // GLOBAL: [batch] slices of scratch_stride bytes (greedy_smem_bytes)
+  size_t scratch_stride;
 };
 
 __host__ __device__ inline int greedy_npad(int n_max) { return (n_max + 127) & ~127; }
 inline size_t greedy_smem_bytes(int n_max) {
   const size_t n = (size_t)greedy_npad(n_max);
   const size_t cells = n < 32 ? 64 : 2 * n;  // rectangular cells: up to two per box
-  return n * (4 * 3 + 8 + 8 + 1 + 1 + 2 + 2 + 2 + 2) + (cells + 4) * 4 + (n / 32 + 4) * 4 + 64 * 4 + 64;
+  return (n * (4 * 3 + 8 + 8 + 1 + 1 + 2 + 2 + 2 + 2) + (cells + 4) * 4 + (n / 32 + 4) * 4 + 64 * 4 + 64 + 255) / 256 * 256;
+}
+__host__ __device__ inline int greedy_max_cells(int npad) {
+  const int c = npad < 32 ? 64 : 2 * npad;
+  return c > kGreedyMaxCells ? kGreedyMaxCells : c;
 }
 
 // covers(cand, ref) of oracles.py:20-29 in exact integer arithmetic; T = ceil(fl64(theta*a))
@@ -64,15 +74,20 @@ __device__ __forceinline__ unsigned long long greedy_threshold(double theta, int
   return c >= 1.8e19 ? ~0ull : (unsigned long long)c;
 }
 
+template <bool GLOBAL>
 __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_stat[8];   // 0 minx 1 miny 2 maxx 3 maxy 4 maxz 5 bin_ok 6 big 7 undecided
+  __shared__ uint32_t scan_tmp[64];
   const int f = blockIdx.x;
   const long long fbase = (long long)f * a.n_max;
   const int cnt = frame_count(a.counts, f, a.n_max);
   const int npad = greedy_npad(a.n_max);
-  const int max_cells = npad < 32 ? 64 : 2 * npad;
-  int32_t* sx = reinterpret_cast<int32_t*>(smem_raw);
+  const int max_cells = greedy_max_cells(npad);
+  unsigned char* base;
+  if constexpr (GLOBAL) base = a.scratch + (size_t)f * a.scratch_stride;
+  else base = smem_raw;
+  int32_t* sx = reinterpret_cast<int32_t*>(base);
   int32_t* sy = sx + npad;
   int32_t* sz = sy + npad;
   uint64_t* key = reinterpret_cast<uint64_t*>(sz + npad);
@@ -84,7 +99,6 @@ __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a
   uint16_t* ulist[2] = {list + npad, list + 2 * npad};  // undecided boxes, double-buffered
   uint32_t* cstart = reinterpret_cast<uint32_t*>(list + 3 * npad);
   uint32_t* kbits = cstart + max_cells + 4;
-  uint32_t* scan_tmp = kbits + npad / 32 + 4;
 
   if (threadIdx.x == 0) {
     s_stat[0] = s_stat[1] = 0x7FFFFFFF;

@@ -1,5 +1,5 @@
 // pnms_soft.cuh — Soft-NMS rescoring (oracles.soft_nms_rescore, oracles.py:88-123) on the
-// device, bit-identical to the reference's sequential loop for linear mode.
+// device, bit-identical to the reference's sequential loop in both modes.
 //
 // Reference semantics: repeatedly select the pending detection with the highest current
 // score (ties: lowest index), remove it from the pending set, and multiply every pending
@@ -25,16 +25,18 @@
 // Candidates come from spatial cells of side max_z + 1 (3x3 neighbourhood, exact because
 // zero overlap never changes a score); frames with negative coordinates or a crowded cell
 // use every slot.  Scores must be finite and > 0 (the validated domain, detections.py:79-84);
-// frames outside it are flagged in `status` and left unwritten.  Gaussian mode uses CUDA's
-// exp (max 1 ulp from the correctly rounded value; the reference uses libm exp), so its
-// scores match the reference within a few ulps rather than bit for bit.
+// frames outside it are flagged in `status` and left unwritten.  Gaussian mode evaluates
+// exp with glibc_exp (pnms_libm.cuh), a restatement of the host libm exp the reference's
+// math.exp calls, so its scores are bit-identical too.
 #pragma once
+#include "pnms_libm.cuh"
 #include "pnms_common.cuh"
 
 namespace pnms {
 
 constexpr int kSoftThreads = 512;
-constexpr int kSoftMaxSlots = 4096;
+constexpr int kSoftMaxSlots = 4096;     // largest frame whose state fits shared memory
+constexpr int kSoftMaxCells = 65535;    // cell ids are 16-bit
 constexpr int kSoftCellMax = 64;
 constexpr int kSoftMaxRounds = 96;
 
@@ -50,13 +52,19 @@ struct SoftArgs {
   double* out_s;   // [batch, n_max] rescored scores (0.0 in padding slots)
   int32_t* status; // [batch] 0 ok, 1 scores outside the domain (frame left unwritten)
   int32_t* rounds; // optional [batch] rounds used (diagnostics)
+  unsigned char* scratch;  // GLOBAL: [batch] slices of scratch_stride bytes (soft_smem_bytes)
+  size_t scratch_stride;
 };
 
 __host__ __device__ inline int soft_npad(int n_max) { return (n_max + 127) & ~127; }
 inline size_t soft_smem_bytes(int n_max) {
   const size_t n = (size_t)soft_npad(n_max);
   const size_t cells = n < 32 ? 64 : 2 * n;  // rectangular cells: up to two per box
-  return n * (4 * 3 + 8 + 8 + 8 + 1 + 1 + 2 + 2 + 2 + 2 + 2) + (cells + 4) * 4 + 64 * 4 + 64;
+  return (n * (4 * 3 + 8 + 8 + 8 + 1 + 1 + 2 + 2 + 2 + 2 + 2) + (cells + 4) * 4 + 64 * 4 + 64 + 255) / 256 * 256;
+}
+__host__ __device__ inline int soft_max_cells(int npad) {
+  const int c = npad < 32 ? 64 : 2 * npad;
+  return c > kSoftMaxCells ? kSoftMaxCells : c;
 }
 
 // the reference's factor of box b on pending box j (oracles.py:31-34, 115-120); `ovl` is
@@ -69,7 +77,7 @@ __device__ __forceinline__ double soft_apply(double sj, int32_t jx, int32_t jy, 
   const long long area = ((long long)bz + 1) * ((long long)bz + 1);
   const double cov = __ddiv_rn(__ll2double_rn(w * h), __ll2double_rn(area));
   if (mode == 0) return cov >= theta ? __dmul_rn(sj, __dsub_rn(1.0, cov)) : sj;
-  return __dmul_rn(sj, exp(__ddiv_rn(-__dmul_rn(cov, cov), sigma)));
+  return __dmul_rn(sj, glibc_exp(__ddiv_rn(-__dmul_rn(cov, cov), sigma)));  // math.exp, bit for bit
 }
 
 __device__ __forceinline__ bool soft_overlap(int32_t ax, int32_t ay, int32_t az, int32_t bx, int32_t by, int32_t bz) {
@@ -115,17 +123,24 @@ struct SoftFrame {
   }
 };
 
+// GLOBAL: the per-slot state lives in a global workspace slice instead of shared memory
+// (frames above kSoftMaxSlots; same layout, same code)
+template <bool GLOBAL>
 __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_stat[10];  // 0 minx 1 miny 2 maxx 3 maxy 4 maxz 5 bin_ok 6 big 7 pending 8 bad 9 arg
   __shared__ unsigned long long s_best[kSoftThreads / 32];
+  __shared__ uint32_t scan_tmp[64];
   const int f = blockIdx.x;
   const long long fbase = (long long)f * a.n_max;
   const int cnt = frame_count(a.counts, f, a.n_max);
   const int npad = soft_npad(a.n_max);
-  const int max_cells = npad < 32 ? 64 : 2 * npad;
+  const int max_cells = soft_max_cells(npad);
+  unsigned char* base;
+  if constexpr (GLOBAL) base = a.scratch + (size_t)f * a.scratch_stride;
+  else base = smem_raw;
   SoftFrame F;
-  F.sx = reinterpret_cast<int32_t*>(smem_raw);
+  F.sx = reinterpret_cast<int32_t*>(base);
   F.sy = F.sx + npad;
   F.sz = F.sy + npad;
   F.s0 = reinterpret_cast<double*>(F.sz + npad);
@@ -139,7 +154,6 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
   uint16_t* plist[2] = {F.fround + npad, F.fround + 2 * npad};  // pending boxes, double-buffered
   F.cstart = reinterpret_cast<uint32_t*>(F.fround + 3 * npad);
   F.cnt = cnt;
-  uint32_t* scan_tmp = F.cstart + max_cells + 4;
 
   if (threadIdx.x == 0) {
     s_stat[0] = s_stat[1] = 0x7FFFFFFF;
@@ -147,10 +161,6 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
     s_stat[4] = 0; s_stat[5] = 1; s_stat[6] = 0; s_stat[7] = 0; s_stat[8] = 0;
   }
   __syncthreads();
-  if (a.n_max > kSoftMaxSlots) {
-    if (threadIdx.x == 0) a.status[f] = 2;
-    return;
-  }
   // ---- load
   for (int e = threadIdx.x; e < cnt; e += kSoftThreads) {
     const long long g = fbase + e;

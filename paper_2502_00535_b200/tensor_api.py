@@ -153,6 +153,13 @@ class _WorkspaceCache:
 
 
 _WS = _WorkspaceCache()
+_VWS = _WorkspaceCache()
+
+
+def _variant_ws(dev, stream: int, B: int, n_max: int):
+    """Scratch of the greedy / Soft-NMS kernels (frames over 4096 slots only)."""
+    need = _lib.variant_workspace_bytes(B, n_max)
+    return _VWS.get(dev, stream, need) if need else None
 
 
 def batched_nms_keep(x: torch.Tensor, y: torch.Tensor, z: torch.Tensor, s: torch.Tensor,
@@ -280,9 +287,12 @@ def greedy_nms_keep(x: torch.Tensor, y: torch.Tensor, z: torch.Tensor, s: torch.
     _check_out(keep_count, "keep_count", torch.int32, (B,), dev)
     p = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
     with torch.cuda.device(dev):
-        st = _lib.load().pnms_greedy_run(p(x), p(y), p(z), p(s), p(counts), B, n_max, theta, p(keep_idx),
-                                         p(keep_count), p(keep_mask), torch.cuda.current_stream(dev).cuda_stream)
-    _lib.check(st, "pnms_greedy_run")
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        ws = _variant_ws(dev, stream, B, n_max)
+        st = _lib.load().pnms_greedy_run_ws(p(x), p(y), p(z), p(s), p(counts), B, n_max, theta, p(keep_idx),
+                                            p(keep_count), p(keep_mask), p(ws), ws.numel() if ws is not None else 0,
+                                            stream)
+    _lib.check(st, "pnms_greedy_run_ws")
     return keep_idx, keep_count
 
 
@@ -318,9 +328,11 @@ def soft_nms_rescore_batched(x: torch.Tensor, y: torch.Tensor, z: torch.Tensor, 
             raise ValueError("rounds must have one entry per frame")
     p = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
     with torch.cuda.device(dev):
-        st = _lib.load().pnms_soft_rescore(p(x), p(y), p(z), p(s), p(counts), B, n_max, code, float(theta),
-                                           float(sigma), p(out), p(status), p(rounds),
-                                           torch.cuda.current_stream(dev).cuda_stream)
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        ws = _variant_ws(dev, stream, B, n_max)
+        st = _lib.load().pnms_soft_rescore_ws(p(x), p(y), p(z), p(s), p(counts), B, n_max, code, float(theta),
+                                              float(sigma), p(out), p(status), p(rounds), p(ws),
+                                              ws.numel() if ws is not None else 0, stream)
     _lib.check(st, "pnms_soft_rescore")
     return out, status
 

@@ -71,3 +71,20 @@ def golden_cases():
 @pytest.fixture(scope="session")
 def golden_configs():
     return load_configs()
+
+
+def load_matrices():
+    """Full-size reference SuppressionMatrix goldens (tests/golden/matrices.npz)."""
+    g = np.load(GOLDEN / "matrices.npz")
+    out = {}
+    for nm in sorted({k.rsplit("_", 1)[0] for k in g.files}):
+        d_max, by_index, writes = (int(v) for v in g[f"{nm}_meta"])
+        out[nm] = dict(x=g[f"{nm}_x"], y=g[f"{nm}_y"], z=g[f"{nm}_z"], s=g[f"{nm}_s"], d_max=d_max,
+                       tie="by_index" if by_index else "paper_faithful", writes=writes,
+                       theta=float(g[f"{nm}_theta"][0]), bits=g[f"{nm}_bits"], mask=g[f"{nm}_mask"])
+    return out
+
+
+@pytest.fixture(scope="session")
+def golden_matrices():
+    return load_matrices()

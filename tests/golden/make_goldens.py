@@ -15,6 +15,7 @@ Writes, next to this script:
   kats.json    SPEC.md known-answer examples evaluated by the reference itself.
   greedy.npz   oracles.greedy_nms keep indices on seeded frames.
   soft.npz     oracles.soft_nms_rescore rescored scores (linear and gaussian) on seeded frames.
+  matrices.npz full-size SuppressionMatrix bytes and reduce masks of config frames (C1, C2).
 The reference is only imported here; nothing at test/bench time reads /root/reference.
 """
 
@@ -308,7 +309,35 @@ def make_kats():
     return k
 
 
+def make_matrices():
+    """Full-size SuppressionMatrix bytes of map_phase (engine.py:176-250) on config frames:
+    C1 (1024 x 1024, paper_faithful, theta 0.5), C1 at d_max 1100 (96 padding slots, by_index,
+    theta 0.3) and C2 (4096 x 4096, theta 0.5) — plus the reduce_phase mask of each."""
+    out = {}
+    c1 = random_frame(1024, seed=0, frame_w=1920, frame_h=1080, z_range=(8, 64))
+    c2 = generate_frame(WorkloadSpec.sized_for(objects=1024, detections_per_object=4, seed=0))
+    for name, vec, d_max, theta, tie in (("C1", c1, 1024, 0.5, "paper_faithful"),
+                                         ("C1pad", c1, 1100, 0.3, "by_index"),
+                                         ("C2", c2, 4096, 0.5, "paper_faithful")):
+        v = vec if vec.d_max == d_max else vec.repadded(d_max)
+        cfg = NmsConfig(theta=theta, d_max=d_max, k=4, workers=8, tie_break=tie)
+        m, ctr = map_phase(v, cfg)
+        mask, _ = reduce_phase(m, cfg)
+        x, y, z, s = valid_arrays(v)
+        out[f"{name}_x"] = x.astype(np.int32); out[f"{name}_y"] = y.astype(np.int32)
+        out[f"{name}_z"] = z.astype(np.int32); out[f"{name}_s"] = s
+        out[f"{name}_meta"] = np.array([d_max, 1 if tie == "by_index" else 0, ctr.map_writes], dtype=np.int64)
+        out[f"{name}_theta"] = np.array([theta])
+        out[f"{name}_bits"] = m.bits.copy()
+        out[f"{name}_mask"] = mask.bits.copy()
+        print(f"matrix {name}: {m.bits.shape} writes={ctr.map_writes}", flush=True)
+    return out
+
+
 def main():
+    if "--only-matrices" in sys.argv:
+        np.savez_compressed(OUT / "matrices.npz", **make_matrices())
+        return
     if "--only-soft" in sys.argv:
         np.savez_compressed(OUT / "soft.npz", **make_soft())
         return
@@ -319,6 +348,7 @@ def main():
     np.savez_compressed(OUT / "configs.npz", **make_configs())
     np.savez_compressed(OUT / "greedy.npz", **make_greedy())
     np.savez_compressed(OUT / "soft.npz", **make_soft())
+    np.savez_compressed(OUT / "matrices.npz", **make_matrices())
 
 
 if __name__ == "__main__":

@@ -100,6 +100,26 @@ def test_map_phase_bits_match_reference(golden_cases):
     assert n > 300
 
 
+@pytest.mark.parametrize("name", ["C1", "C1pad", "C2"])
+def test_full_size_matrices_match_reference(golden_matrices, name, path):
+    """map_phase bytes of the reference's full-size matrices (C1 1024 x 1024, C1 padded to
+    1100 under by_index, C2 4096 x 4096), reduce_phase masks, and run_nms survivors and
+    map_writes of the same frames through every device path."""
+    g = golden_matrices[name]
+    n, d_max = len(g["x"]), g["d_max"]
+    vec = DetectionVector.from_arrays(g["x"], g["y"], g["z"], g["s"], d_max, validate=False)
+    cfg = NmsConfig(theta=g["theta"], d_max=d_max, k=4, tie_break=g["tie"])
+    m, ctr = map_phase(vec, cfg)
+    assert m.bits.shape == g["bits"].shape and np.array_equal(m.bits, g["bits"])
+    assert ctr.map_writes == g["writes"]
+    v, _ = reduce_phase(m, cfg)
+    assert np.array_equal(v.bits, g["mask"])
+    res, rc = run_nms(vec, cfg)
+    keep = np.nonzero(np.unpackbits(g["mask"], count=d_max, bitorder="little")[:n])[0]
+    assert [d.x for d in res.survivors] == [int(g["x"][i]) for i in keep]
+    assert rc.map_writes == g["writes"] and res.suppressed_count == n - len(keep)
+
+
 CONFIG_FRAMES = ["C1", "C2", "C3", "C4f0", "C4f1", "C4f2", "C4f3", "C4f4", "C4f5", "C4f6", "C4f7",
                  "C5f0", "C5f1", "C5f2", "C5f3"]
 
@@ -802,14 +822,31 @@ def test_unpack_box32_extremes():
 
 
 # ---------------------------------------------------------------- Soft-NMS (oracles.py:88-123)
-GAUSS_RTOL = 1e-13   # gaussian mode: device exp vs libm exp (<= 1 ulp per factor); linear is exact
-
-
 def _soft_check(got, want, mode, what):
-    if mode in (0, "linear"):
-        assert np.array_equal(np.asarray(got).view(np.uint64), np.asarray(want).view(np.uint64)), what
-    else:
-        np.testing.assert_allclose(got, want, rtol=GAUSS_RTOL, atol=0, err_msg=str(what))
+    """Both modes bit for bit: gaussian mode's exp is the host libm's, restated on the device
+    (pnms_libm.cuh)."""
+    got, want = np.asarray(got, dtype=np.float64), np.asarray(want, dtype=np.float64)
+    bad = np.nonzero(got.view(np.uint64) != want.view(np.uint64))[0]
+    assert bad.size == 0, (what, mode, [(int(i), float(got[i]).hex(), float(want[i]).hex()) for i in bad[:4]])
+
+
+def test_device_exp_is_the_host_libm_exp():
+    """pnms_debug_exp (the device build of pnms_libm.cuh) against math.exp, bit for bit, over
+    the Soft-NMS domain -cov^2/sigma and every other branch of the algorithm."""
+    import math
+
+    from paper_2502_00535_b200 import _lib
+    from test_libm_exp import exp_ranges
+
+    for x in exp_ranges(400_000, seed=11):
+        xd = torch.from_numpy(np.ascontiguousarray(x)).to(DEV)
+        yd = torch.empty_like(xd)
+        _lib.check(_lib.load().pnms_debug_exp(xd.data_ptr(), yd.data_ptr(), xd.numel(),
+                                              torch.cuda.current_stream().cuda_stream), "pnms_debug_exp")
+        got = yd.cpu().numpy()
+        want = np.fromiter((math.exp(v) for v in x.tolist()), dtype=np.float64, count=x.size)
+        bad = np.nonzero(got.view(np.uint64) != want.view(np.uint64))[0]
+        assert bad.size == 0, [(float(x[i]).hex(), float(want[i]).hex(), float(got[i]).hex()) for i in bad[:5]]
 
 
 def test_soft_nms_matches_reference_goldens():
@@ -924,3 +961,31 @@ def test_compute_sanitizer_clean(tool):
     assert summary, out[-3000:]
     counts = [int(v) for v in re.findall(r"(\d+) (?:errors?|hazards?)", summary[-1])]
     assert counts and counts[0] == 0, summary
+
+
+@pytest.mark.parametrize("n", [4097, 16384])
+def test_variants_large_frames_vs_oracle(n):
+    """Greedy NMS and Soft-NMS (both modes) on frames above one CTA's shared memory (config-3
+    size and the first size past it): the per-slot state in the workspace, vs the C oracle
+    (bit for bit), including exact ties and a crowded region."""
+    from paper_2502_00535_b200 import greedy_nms_keep, soft_nms_rescore_batched
+
+    x, y, z, s = random_frames(2, n, seed=n, frame_w=3840, frame_h=2160, z_range=(8, 64), duplicate_fraction=0.05)
+    s[:, ::11] = 0.5
+    x[1, :300] = 1000 + np.arange(300) % 7; y[1, :300] = 500 + np.arange(300) % 5   # crowd: all-slot scan
+    counts = np.array([n, n - 5], np.int32)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)  # noqa: E731
+    for theta in (0.3, 0.5):
+        ki, kc = greedy_nms_keep(t(x), t(y), t(z), t(s), t(counts), theta)
+        ki, kc = ki.cpu().numpy(), kc.cpu().numpy()
+        for f in range(2):
+            want = c_oracle.greedy_frame(x[f], y[f], z[f], s[f], int(counts[f]), theta)
+            assert np.array_equal(ki[f, : kc[f]], want), (n, f, theta)
+    for mode in ("linear", "gaussian"):
+        out, status = soft_nms_rescore_batched(t(x), t(y), t(z), t(s), t(counts), mode, 0.3, 0.5)
+        out = out.cpu().numpy()
+        assert (status.cpu().numpy() == 0).all()
+        for f in range(2):
+            c = int(counts[f])
+            want = c_oracle.soft_frame(x[f], y[f], z[f], s[f], c, mode, 0.3, 0.5)
+            _soft_check(out[f, :c], want, mode, (n, f))

@@ -99,3 +99,19 @@ def test_c_oracle_soft_nms_matches_reference():
         assert np.array_equal(got.view(np.uint64), g["out"][sl].view(np.uint64)), (n, mode, theta, sigma)
         n_frames += 1
     assert n_frames > 150
+
+
+def test_numpy_oracle_full_size_matrices(golden_matrices):
+    """The numpy restatement of map_phase / reduce_phase against the reference's full-size
+    C1 (plain and padded) and C2 SuppressionMatrix bytes."""
+    import parnms_oracle as po
+
+    assert set(golden_matrices) == {"C1", "C1pad", "C2"}
+    for nm, g in golden_matrices.items():
+        n = len(g["x"])
+        px, py, pz, ps = po.pad_frame(g["x"], g["y"], g["z"], g["s"], n, g["d_max"])
+        bits, writes = po.map_matrix(px, py, pz, ps, g["theta"], g["tie"])
+        assert bits.shape == g["bits"].shape and np.array_equal(bits, g["bits"]), nm
+        assert writes == g["writes"], nm
+        flags = po.reduce_matrix(bits, g["d_max"])
+        assert np.array_equal(np.packbits(flags, bitorder="little"), g["mask"]), nm
