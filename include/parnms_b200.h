@@ -127,6 +127,7 @@ typedef struct pnms_launch_config {
   int small_col_tiles; /* SMALL: column tiles per frame                                    */
   int host_chain;      /* 1: the host launches the fallback chain for declined frames      */
   int32_t* declined;   /* device int32[1] or NULL: frames the culling kernel declined      */
+  int binned_impl;     /* BINNED: 0 default (ranked, balanced rows), 1 first-generation     */
 } pnms_launch_config;
 
 /* Path report of one pnms_run_ex call (host memory). */

@@ -61,6 +61,7 @@ struct BinArgs {
   unsigned long long* trace;         // optional per-CTA phase timestamps (diagnostics), may be null
   int cell_q8;                       // frame kernel cell side: 0 default, > 0 scale, < 0 absolute
   int cell_sx;                       // frame kernel: > 0 overrides the cell width
+  int prefetch_ahead;                // frame kernel: > 0 prefetches frame f + this into L2
 };
 
 struct __align__(16) BinStats {

@@ -19,6 +19,7 @@
 #include "pnms_reflayout.cuh"
 #include "pnms_small.cuh"
 #include "pnms_binned.cuh"
+#include "pnms_binned2.cuh"
 #include "pnms_devchain.h"
 #include "pnms_fallback.cuh"
 #include "pnms_validate.cuh"
@@ -175,7 +176,6 @@ cudaError_t launch_maybe_pdl(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3
 SmemCache g_sort_frame_smem, g_sort_chunk_smem, g_compact_smem, g_sort_list_smem;
 SmemCache g_map_smem[5], g_map_list_smem[5];
 SmemCache g_small_smem[8];
-SmemCache g_binned_smem[8];
 SmemCache g_tiles_smem[2];
 
 template <bool B, bool C, int P, int T>
@@ -268,33 +268,52 @@ cudaError_t launch_cluster(const BinArgs& ba, int batch, int cs, int slice, bool
 #undef PNMS_CL
 }
 
-// variant bits: 1 by_index, 2 count pairs, 4 eight boxes per thread; `wide` picks 1024-thread
-// CTAs (one per SM, two boxes per thread) for batches that fit one wave
-cudaError_t launch_binned(int variant, const BinArgs& ba, int batch, size_t smem, cudaStream_t st, bool wide) {
-  if (wide) {
-    switch (variant & 3) {
-      case 0: return launch_binned_t<false, false, 2, 1024>(ba, batch, smem, st, g_binned_smem[4]);
-      case 1: return launch_binned_t<true, false, 2, 1024>(ba, batch, smem, st, g_binned_smem[5]);
-      case 2: return launch_binned_t<false, true, 2, 1024>(ba, batch, smem, st, g_binned_smem[6]);
-      default: return launch_binned_t<true, true, 2, 1024>(ba, batch, smem, st, g_binned_smem[7]);
-    }
-  }
-  switch (variant & 3) {
-    case 0: return launch_binned_t<false, false, 8, kBinThreads>(ba, batch, smem, st, g_binned_smem[0]);
-    case 1: return launch_binned_t<true, false, 8, kBinThreads>(ba, batch, smem, st, g_binned_smem[1]);
-    case 2: return launch_binned_t<false, true, 8, kBinThreads>(ba, batch, smem, st, g_binned_smem[2]);
-    default: return launch_binned_t<true, true, 8, kBinThreads>(ba, batch, smem, st, g_binned_smem[3]);
-  }
+// variant bits: 1 by_index, 2 count pairs; `wide` picks 1024-thread CTAs (one per SM, two
+// boxes per thread) for batches that fit one wave.  impl 1 = the first-generation kernel
+// (pnms_binned.cuh), kept for measurement; the default is pnms_binned2.cuh.
+template <bool B, bool C, int P, int T, int M = (T == 512 ? 3 : 1)>
+cudaError_t launch_binned2_t(const BinArgs& ba, int batch, size_t smem, cudaStream_t st, SmemCache& cfg) {
+  cudaError_t e = ensure_smem(pnms_binned2_frame<B, C, P, T, M>, smem, cfg);
+  if (e != cudaSuccess) return e;
+  pnms_binned2_frame<B, C, P, T, M><<<batch, T, smem, st>>>(ba);
+  return cudaGetLastError();
 }
 
-cudaError_t launch_binned4(int variant, const BinArgs& ba, int batch, size_t smem, cudaStream_t st) {
-  static SmemCache c[4];
-  switch (variant & 3) {
-    case 0: return launch_binned_t<false, false, 4, kBinThreads>(ba, batch, smem, st, c[0]);
-    case 1: return launch_binned_t<true, false, 4, kBinThreads>(ba, batch, smem, st, c[1]);
-    case 2: return launch_binned_t<false, true, 4, kBinThreads>(ba, batch, smem, st, c[2]);
-    default: return launch_binned_t<true, true, 4, kBinThreads>(ba, batch, smem, st, c[3]);
+cudaError_t launch_binned(int impl, int variant, const BinArgs& ba, int batch, int n_max, cudaStream_t st, bool wide) {
+  const int npad = binned_npad(n_max);
+  if (impl == 1) {
+    const size_t smem = binned_smem_bytes(npad);
+    static SmemCache c1[12];
+    const int per = binned_per_thread(n_max, kBinThreads);
+#define PNMS_B1(P, T, I)                                                                        \
+  switch (variant & 3) {                                                                        \
+    case 0: return launch_binned_t<false, false, P, T>(ba, batch, smem, st, c1[I]);            \
+    case 1: return launch_binned_t<true, false, P, T>(ba, batch, smem, st, c1[I + 1]);         \
+    case 2: return launch_binned_t<false, true, P, T>(ba, batch, smem, st, c1[I + 2]);         \
+    default: return launch_binned_t<true, true, P, T>(ba, batch, smem, st, c1[I + 3]);         \
   }
+    if (wide) { PNMS_B1(2, 1024, 0) }
+    if (per <= 4) { PNMS_B1(4, kBinThreads, 4) }
+    PNMS_B1(8, kBinThreads, 8)
+#undef PNMS_B1
+  }
+  const size_t smem = b2_smem_bytes(npad);
+  static SmemCache c2[12];
+  if (impl == 2 && !wide && n_max <= 4 * kBinThreads) {  // experiment: two CTAs per SM, no spills
+    static SmemCache c3;
+    return launch_binned2_t<false, false, 4, kBinThreads, 2>(ba, batch, smem, st, c3);
+  }
+#define PNMS_B2(P, T, I)                                                                        \
+  switch (variant & 3) {                                                                        \
+    case 0: return launch_binned2_t<false, false, P, T>(ba, batch, smem, st, c2[I]);           \
+    case 1: return launch_binned2_t<true, false, P, T>(ba, batch, smem, st, c2[I + 1]);        \
+    case 2: return launch_binned2_t<false, true, P, T>(ba, batch, smem, st, c2[I + 2]);        \
+    default: return launch_binned2_t<true, true, P, T>(ba, batch, smem, st, c2[I + 3]);        \
+  }
+  if (wide) { PNMS_B2(2, 1024, 0) }
+  if (n_max <= 4 * kBinThreads) { PNMS_B2(4, kBinThreads, 4) }
+  PNMS_B2(4, 1024, 8)
+#undef PNMS_B2
 }
 
 template <bool B, bool C, int R>
@@ -625,12 +644,10 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
       // ---- exact spatial culling, one CTA per frame (pnms_binned.cuh)
       ba.pairs_tested = g_pairs_counter;
       ba.meta = nullptr;  // the frame-level sort rewrites FrameMeta of declined frames
-      const size_t smem = binned_smem_bytes(binned_npad(n_max));
       const int variant = (tie_break == PNMS_TIE_BY_INDEX ? 1 : 0) + (g_pairs_counter ? 2 : 0);
-      const int per = binned_per_thread(n_max, kBinThreads);
-      if (path == PNMS_PATH_BINNED_WIDE) e = launch_binned(variant, ba, batch, smem, st, true);
-      else if (per <= 4) e = launch_binned4(variant, ba, batch, smem, st);
-      else e = launch_binned(variant, ba, batch, smem, st, false);
+      // frames a CTA slot runs next: resident CTAs of the 512-thread kernel (3 per SM)
+      ba.prefetch_ahead = path == PNMS_PATH_BINNED_WIDE ? sm_count() : 3 * sm_count();
+      e = launch_binned(lc.binned_impl, variant, ba, batch, n_max, st, path == PNMS_PATH_BINNED_WIDE);
       if (e != cudaSuccess) return fail_cuda(e);
     } else if (path == PNMS_PATH_TILES) {
       // ---- large single frames: kTilesPerFrame independent tile CTAs per frame (pnms_binned_tiles.cuh)

@@ -34,6 +34,7 @@ class LaunchConfig:
     frames the culling kernel declined.
 
     path: "auto" | "small" | "binned" | "binned_wide" | "tiles" | "cluster" | "dense"
+    binned_impl: 0 the default binned kernel (pnms_binned2.cuh), 1 the first-generation one
     """
 
     path: str = "auto"
@@ -45,6 +46,7 @@ class LaunchConfig:
     small_col_tiles: int = 0
     host_chain: bool = False
     declined: torch.Tensor | None = None
+    binned_impl: int = 0
     path_taken: str | None = None
 
     def to_c(self) -> _lib.LaunchConfigC:
@@ -55,7 +57,8 @@ class LaunchConfig:
         return _lib.LaunchConfigC(_lib.PATHS[self.path], int(self.cluster_size), int(self.cell_q8),
                                   int(self.cell_sx), int(self.map_rows), int(self.map_chunk),
                                   int(self.small_col_tiles), int(bool(self.host_chain)),
-                                  self.declined.data_ptr() if self.declined is not None else None)
+                                  self.declined.data_ptr() if self.declined is not None else None,
+                                  int(self.binned_impl))
 
 
 _DEFAULT_LAUNCH: list[LaunchConfig | None] = [None]

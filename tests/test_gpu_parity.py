@@ -208,11 +208,13 @@ def _run_batch(x, y, z, s, counts, theta, tie, d_max=None, launch=None):
     return [ki[f, : kc[f]] for f in range(x.shape[0])]
 
 
-@pytest.mark.parametrize("host_chain", [False, True])
-def test_binned_mixed_batch_vs_oracle(host_chain):
+@pytest.mark.parametrize("host_chain,impl", [(False, 0), (True, 0), (False, 1), (True, 1)])
+def test_binned_mixed_batch_vs_oracle(host_chain, impl):
     """A batch where the binned kernel takes some frames and declines others (z > 126, a
-    zero side, a crowded cell, NaN scores, theta-independent ties) — all must be exact, with
-    the declined frames finished by the device-launched or the host-launched dense chain."""
+    zero side, NaN scores, theta-independent ties; crowded cells, which the first-generation
+    kernel (impl 1) declines; a tie group of 600 equal scores, which the default kernel declines)
+    — all must be exact, with the declined frames finished by the device-launched or the
+    host-launched dense chain."""
     from paper_2502_00535_b200 import _lib
 
     x, y, z, s = random_frames(12, 900, seed=123, frame_w=800, frame_h=600, z_range=(4, 60), duplicate_fraction=0.1)
@@ -225,15 +227,16 @@ def test_binned_mixed_batch_vs_oracle(host_chain):
     counts = np.full(12, 900, np.int32)
     counts[7] = 1
     counts[8] = 0
+    s[9, :600] = 0.7                     # 600 equal scores: one score bucket > 512 (impl 0 declines)
     counter = torch.zeros(1, dtype=torch.int64, device=DEV)
     declined = torch.zeros(1, dtype=torch.int32, device=DEV)
     _lib.load().pnms_debug_count_pairs(counter.data_ptr())
     try:
         for tie in ("paper_faithful", "by_index"):
             for theta in (0.3, 0.5, 1.0):
-                lc = LaunchConfig(path="binned", host_chain=host_chain, declined=declined)
+                lc = LaunchConfig(path="binned", host_chain=host_chain, declined=declined, binned_impl=impl)
                 got = _run_batch(x, y, z, s, counts, theta, tie, 950, launch=lc)
-                assert lc.path_taken == "binned" and int(declined.item()) >= 4
+                assert lc.path_taken == "binned" and int(declined.item()) == (3 if impl == 0 else 4)
                 for f in range(12):
                     want = c_oracle.run_frame(x[f], y[f], z[f], s[f], int(counts[f]), 950, theta, tie)
                     assert np.array_equal(got[f], want), (f, tie, theta)
@@ -705,7 +708,8 @@ def test_device_fallback_chain_direct_and_graph(chunks):
     F, n = 16, 600
     x, y, z, s = random_frames(F, n, seed=21, frame_w=640, frame_h=480, z_range=(4, 40))
     for f in (2, 7, 11):
-        x[f, :200] = 5; y[f, :200] = 5    # 200 boxes in one cell -> declined
+        x[f, :200] = 5; y[f, :200] = 5    # 200 boxes in one cell (declined by the first-generation kernel)
+        s[f, :550] = 0.25                 # a tie group of 550 scores -> declined
     z[9, 3] = 0                           # a zero side -> declined
 
     def expect(x, y, z, s):
@@ -743,11 +747,14 @@ def test_device_fallback_chain_direct_and_graph(chunks):
 
 
 @pytest.mark.parametrize("crowd", [100, 255, 256])
-@pytest.mark.parametrize("where", ["binned", "tiles", "cluster"])
+@pytest.mark.parametrize("where", ["binned", "binned_v1", "tiles", "cluster"])
 def test_crowded_cells_at_the_cell_limit(crowd, where):
-    """Cells of up to kBinCellMax = 255 boxes stay on the culling paths (skip distance and
-    in-cell ranks at their 8-bit field limits); 256 is declined to the dense pipeline — exact
-    either way, with equal scores inside the crowd."""
+    """Cells of up to kBinCellMax = 255 boxes stay on the tile / cluster / first-generation
+    binned paths (skip distance and in-cell ranks at their 8-bit field limits); 256 is declined
+    to the dense pipeline.  The default binned kernel has no cell limit (no in-cell order).
+    Exact either way, with equal scores inside the crowd."""
+    impl = 1 if where == "binned_v1" else 0
+    where = "binned" if where == "binned_v1" else where
     if where == "binned":
         B, n = 3, 1500
     else:
@@ -759,10 +766,12 @@ def test_crowded_cells_at_the_cell_limit(crowd, where):
     s[f, : crowd // 2] = 0.75                     # ties inside the crowd
     for tie in ("paper_faithful", "by_index"):
         declined = torch.zeros(1, dtype=torch.int32, device=DEV)
-        lc = LaunchConfig(path=where, declined=declined)
+        lc = LaunchConfig(path=where, declined=declined, binned_impl=impl)
         got = _run_batch(x, y, z, s, np.full(B, n, np.int32), 0.5, tie, n, launch=lc)
         assert lc.path_taken == where
-        if where == "binned" and crowd != 255:  # 255 + a random neighbour may tip the cell over
+        if where == "binned" and impl == 0:
+            assert int(declined.item()) == 0
+        elif where == "binned" and crowd != 255:  # 255 + a random neighbour may tip the cell over
             assert int(declined.item()) == (1 if crowd > 255 else 0)
         for g in range(B):
             want = c_oracle.run_frame(x[g], y[g], z[g], s[g], n, n, 0.5, tie)

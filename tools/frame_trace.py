@@ -2,7 +2,7 @@
 
 Prints, per phase, the median duration over frames, and each frame's start/end spread, for a
 batch of `frames x n` random_frame boxes (default: C4, 256 x 1024).
-usage: python tools/frame_trace.py [frames] [n]
+usage: python tools/frame_trace.py [frames] [n] [1|2 (binned kernel generation)]
 """
 import sys
 from pathlib import Path
@@ -18,14 +18,16 @@ from paper_2502_00535_b200.synth import random_frames  # noqa: E402
 F = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
 x, y, z, s = (torch.from_numpy(a).cuda() for a in random_frames(F, n, seed=4))
+from paper_2502_00535_b200.tensor_api import LaunchConfig  # noqa: E402
+lc = LaunchConfig(path="binned", binned_impl=0 if len(sys.argv) > 3 and sys.argv[3] == "2" else 1)
 for _ in range(3):
-    batched_nms_keep(x, y, z, s, None, 0.5)
+    batched_nms_keep(x, y, z, s, None, 0.5, launch=lc)
 buf = torch.zeros(F * 16, dtype=torch.int64, device="cuda")
 cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
 lib = _lib.load()
 lib.pnms_debug_trace(buf.data_ptr())
 lib.pnms_debug_count_pairs(cnt.data_ptr())  # the traced (diagnostic) kernel instantiation
-batched_nms_keep(x, y, z, s, None, 0.5)
+batched_nms_keep(x, y, z, s, None, 0.5, launch=lc)
 torch.cuda.synchronize()
 lib.pnms_debug_trace(None)
 lib.pnms_debug_count_pairs(None)
@@ -34,6 +36,9 @@ ok = (t > 0).all(axis=1)
 t = t[ok]
 t0 = t[:, 0].min()
 names = ["load+stats", "grid", "histogram", "scan", "scatter keys", "rank sort", "records", "row scan", "compaction"]
+if len(sys.argv) > 3 and sys.argv[3] == "2":  # pnms_binned2.cuh phases
+    names = ["load+stats+params", "histograms", "count scan", "bucket scatter", "rank+record+count", "row order",
+             "-", "row scan", "compaction"]
 print(f"{ok.sum()} of {F} frames traced (n = {n}); kernel span {(t[:, 9].max() - t0) / 1e3:.2f} us")
 print(f"frame start spread {(t[:, 0].max() - t0) / 1e3:.2f} us; median frame time {np.median(t[:, 9] - t[:, 0]) / 1e3:.2f} us")
 d = np.diff(t, axis=1)

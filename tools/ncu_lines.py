@@ -19,26 +19,26 @@ top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", str(ROOT / "paper_2502_00535_b200" / "libparnms_b200.so")], cwd=tmp,
                capture_output=True)
-# the library holds several device modules (whole-program unit, relocatable unit): find the one
-# with the kernel
+# the library holds several device modules (whole-program unit, relocatable unit) and several
+# instantiations per kernel: collect every matching function, then keep the one whose SASS
+# length equals the report's
+cands = []
 for cubin in sorted(glob.glob(tmp + "/*.cubin")):
     dis = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout.splitlines()
-    hits = [i for i, l in enumerate(dis) if l.startswith("//---") and fun in l]
-    if hits:
-        start = hits[0]
-        break
-else:
+    for start in [i for i, l in enumerate(dis) if l.startswith("//---") and fun in l]:
+        cur, seq = None, []
+        for l in dis[start + 1:]:
+            if l.startswith("//---"):
+                break
+            m = re.search(r'//## File "([^"]+)", line (\d+)', l)
+            if m:
+                cur = (m.group(1).split("/")[-1], int(m.group(2)))
+                continue
+            if re.match(r"\s+/\*[0-9a-f]{4,}\*/", l):
+                seq.append(cur)
+        cands.append(seq)
+if not cands:
     sys.exit(f"{fun} not found in the library's device modules")
-cur, seq = None, []
-for l in dis[start + 1:]:
-    if l.startswith("//---"):
-        break
-    m = re.search(r'//## File "([^"]+)", line (\d+)', l)
-    if m:
-        cur = (m.group(1).split("/")[-1], int(m.group(2)))
-        continue
-    if re.match(r"\s+/\*[0-9a-f]{4,}\*/", l):
-        seq.append(cur)
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(out.splitlines()))
@@ -46,8 +46,10 @@ hi = [i for i, r in enumerate(rows) if r and r[0] == "Address"][0]
 hdr = rows[hi]
 ix = {h: i for i, h in enumerate(hdr)}
 data = [r for r in rows[hi + 1:] if len(r) == len(hdr) and r[0] != "Address"]
-if len(data) != len(seq):
-    print(f"warning: {len(data)} SASS rows in report vs {len(seq)} in library (stale build?)")
+seq = next((c for c in cands if len(c) == len(data)), None)
+if seq is None:
+    seq = cands[0]
+    print(f"warning: no instantiation with {len(data)} SASS rows (stale build?)")
 agg, samp, thr = collections.Counter(), collections.Counter(), collections.Counter()
 for k, r in enumerate(data):
     loc = seq[k] if k < len(seq) else None
