@@ -201,8 +201,20 @@ def _survivors(d, keep: np.ndarray) -> tuple:
     package's own vectors build the Detection objects from whole columns."""
     if isinstance(d, DetectionVector):
         cols = (d.xs[keep].tolist(), d.ys[keep].tolist(), d.zs[keep].tolist(), d.ss[keep].tolist())
-        return tuple(map(Detection, *cols))
+        return tuple(map(_make_detection, *cols))
     return tuple(d.slot(int(i)) for i in keep)
+
+
+_new_object = object.__new__
+_set_x, _set_y, _set_z, _set_s = (Detection.__dict__[f].__set__ for f in ("x", "y", "z", "s"))
+
+
+def _make_detection(x, y, z, s) -> Detection:
+    """Detection(x, y, z, s) through its slot descriptors: the frozen dataclass's __init__
+    (four object.__setattr__ calls) is ~2x slower, which matters for ~10^4 survivors."""
+    o = _new_object(Detection)
+    _set_x(o, x); _set_y(o, y); _set_z(o, z); _set_s(o, s)  # noqa: E702
+    return o
 
 
 def run_nms(d: DetectionVector, cfg: NmsConfig) -> tuple[NmsResult, WorkCounters]:

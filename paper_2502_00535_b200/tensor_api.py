@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import contextlib
 import ctypes
+import functools
 from dataclasses import dataclass
 
 import torch
@@ -95,6 +96,8 @@ def _check_tie(tie_break: str) -> int:
 
 
 def _require_cuda(t: torch.Tensor, name: str, dtype: torch.dtype, ndim: int) -> None:
+    if type(t) is torch.Tensor and t.dtype is dtype and t.is_cuda and t.dim() == ndim and t.is_contiguous():
+        return  # the common case, checked with as few tensor attribute reads as possible
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor")
     if t.dtype != dtype:
@@ -115,13 +118,14 @@ def _check_planes(x, y, z, s, counts, keep_mask=None):
     """The planes of one batched call: int32 x, y, z and float64 s [B, n_max] on one CUDA
     device, counts int32 [B]; returns (B, n_max)."""
     _require_cuda(x, "x", torch.int32, 2)
-    B, n_max = x.shape
+    shape = x.shape
+    B, n_max = shape
     for t, nm in ((y, "y"), (z, "z")):
         _require_cuda(t, nm, torch.int32, 2)
-        if t.shape != x.shape:
+        if t.shape != shape:
             raise ValueError(f"{nm} shape {tuple(t.shape)} != x shape {tuple(x.shape)}")
     _require_cuda(s, "s", torch.float64, 2)
-    if s.shape != x.shape:
+    if s.shape != shape:
         raise ValueError(f"s shape {tuple(s.shape)} != x shape {tuple(x.shape)}")
     tensors = [y, z, s]
     if counts is not None:
@@ -157,6 +161,16 @@ class _WorkspaceCache:
 
 _WS = _WorkspaceCache()
 _VWS = _WorkspaceCache()
+_workspace_bytes = functools.lru_cache(maxsize=1024)(_lib.workspace_bytes)
+
+
+def _raw_stream(dev: torch.device) -> int:
+    """The current stream of `dev` as a cudaStream_t integer (one C call)."""
+    return torch._C._cuda_getCurrentRawStream(dev.index)
+
+
+def _same_device(dev: torch.device) -> bool:
+    return dev.index == torch.cuda.current_device()
 
 
 def _variant_ws(dev, stream: int, B: int, n_max: int):
@@ -208,20 +222,20 @@ def batched_nms_keep(x: torch.Tensor, y: torch.Tensor, z: torch.Tensor, s: torch
     _check_out(gate_pairs, "gate_pairs", torch.int64, (B,), dev)
     if launch is None:
         launch = _DEFAULT_LAUNCH[0]
-    with torch.cuda.device(dev):
-        stream = torch.cuda.current_stream(dev)
-        need = _lib.workspace_bytes(B, n_max)
+    need = _workspace_bytes(B, n_max)
+    # the library launches on the caller's current device: make it the planes' device
+    with contextlib.nullcontext() if _same_device(dev) else torch.cuda.device(dev):
+        stream = _raw_stream(dev)
         if workspace is None:
-            workspace = _WS.get(dev, stream.cuda_stream, need)
+            workspace = _WS.get(dev, stream, need)
         elif workspace.numel() < need:
             raise ValueError(f"workspace needs {need} bytes")
-        lib = _lib.load()
         p = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
         cfg = ctypes.byref(launch.to_c()) if launch is not None else None
         info = _lib.RunInfoC(0)
-        st = lib.pnms_run_ex(p(x), p(y), p(z), p(s), p(counts), B, n_max, int(d_max), theta, tie,
-                             p(keep_idx), p(keep_count), p(keep_mask), p(gate_pairs), p(workspace),
-                             workspace.numel(), stream.cuda_stream, cfg, ctypes.byref(info), None)
+        st = _lib.load().pnms_run_ex(p(x), p(y), p(z), p(s), p(counts), B, n_max, int(d_max), theta, tie,
+                                     p(keep_idx), p(keep_count), p(keep_mask), p(gate_pairs), workspace.data_ptr(),
+                                     workspace.numel(), stream, cfg, ctypes.byref(info), None)
         _lib.check(st, "pnms_run_ex")
     if launch is not None:
         launch.path_taken = _lib.PATH_NAMES.get(info.path, str(info.path))
@@ -350,13 +364,22 @@ def nms_keep(boxes: torch.Tensor, scores: torch.Tensor, theta: float = 0.5,
     n = boxes.shape[0]
     if n == 0:
         return torch.empty((0,), dtype=torch.int64, device=boxes.device)
-    b = boxes.to(torch.int32)
-    planes = b.t().contiguous()
-    sc = scores.to(torch.float64).reshape(1, n).contiguous()
-    idx, cnt = batched_nms_keep(planes[0:1], planes[1:2], planes[2:3], sc, None, theta, tie_break,
-                                d_max if d_max is not None else n)
+    b = boxes if boxes.dtype is torch.int32 else boxes.to(torch.int32)
+    planes = b.t().contiguous()  # [3, N]: the x, y, z planes of one frame
+    sc = scores if scores.dtype is torch.float64 and scores.is_contiguous() else scores.to(torch.float64).contiguous()
+    key = (planes.device.index, n)
+    bufs = _KEEP_BUFS.get(key)
+    if bufs is None:
+        bufs = (torch.empty((1, n), dtype=torch.int32, device=planes.device),
+                torch.empty((1,), dtype=torch.int32, device=planes.device))
+        _KEEP_BUFS[key] = bufs
+    idx, cnt = batched_nms_keep(planes[0:1], planes[1:2], planes[2:3], sc.reshape(1, n), None, theta, tie_break,
+                                d_max if d_max is not None else n, keep_idx=bufs[0], keep_count=bufs[1])
     k = int(cnt.item())
     return idx[0, :k].to(torch.int64)
+
+
+_KEEP_BUFS: dict = {}  # nms_keep's per-(device, n) device outputs (the result is a fresh copy)
 
 
 BOX32_MAX_XY = 4095
