@@ -102,6 +102,8 @@ int pnms_run_profiled(const int32_t* x, const int32_t* y, const int32_t* z, cons
  *   TILES        128 independent tile CTAs per frame (latency of large single frames)
  *   CLUSTER      one thread-block cluster per frame (frames of 4097..65536 slots, batches)
  *   DENSE        sorted N x N map (prep+sort -> map -> compact), any frame
+ *   COOP         one cooperative launch of up to 128 tile CTAs per frame sharing the frame's
+ *                statistics and binning through global memory (latency, <= 2 frames)
  * The culling paths decline frames outside their exactness preconditions (a zero side or
  * theta = 0, coordinates outside the 15-bit domain, a crowded cell); the device finishes those
  * frames on the dense pipeline. */
@@ -112,6 +114,7 @@ int pnms_run_profiled(const int32_t* x, const int32_t* y, const int32_t* z, cons
 #define PNMS_PATH_TILES 4
 #define PNMS_PATH_CLUSTER 5
 #define PNMS_PATH_DENSE 6
+#define PNMS_PATH_COOP 7
 
 /* Launch configuration (all fields 0 = the measured defaults).  Tests, tools and the
  * benchmark use it to pin a path or a decomposition; production callers pass NULL.

@@ -53,7 +53,7 @@ TIE_CODES = {"paper_faithful": 0, "by_index": 1}
 MAX_SLOTS = 65536
 
 # PNMS_PATH_* (include/parnms_b200.h)
-PATHS = {"auto": 0, "small": 1, "binned": 2, "binned_wide": 3, "tiles": 4, "cluster": 5, "dense": 6}
+PATHS = {"auto": 0, "small": 1, "binned": 2, "binned_wide": 3, "tiles": 4, "cluster": 5, "dense": 6, "coop": 7}
 PATH_NAMES = {v: k for k, v in PATHS.items()}
 
 

@@ -20,6 +20,7 @@
 #include "pnms_small.cuh"
 #include "pnms_binned.cuh"
 #include "pnms_binned2.cuh"
+#include "pnms_coop.cuh"
 #include "pnms_devchain.h"
 #include "pnms_fallback.cuh"
 #include "pnms_validate.cuh"
@@ -90,6 +91,7 @@ unsigned long long* g_trace = nullptr;          // diagnostics: phase timestamps
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Layout {
+  size_t coop;
   size_t rec, perm, lim, supp, meta, sk, idx, dense, list, tiles, total;
 };
 
@@ -111,6 +113,11 @@ Layout make_layout(int batch, int n_max) {
     L.idx = off; off = align_up(off + B * N * 4, 256);
   } else {
     L.sk = L.idx = L.tiles = 0;
+  }
+  // the cooperative latency path (batches of <= kCoopMaxFrames): tile lists
+  L.coop = 0;
+  if (batch <= kCoopMaxFrames) {
+    L.coop = off; off = align_up(off + B * kCoopMaxTiles * kCoopCap * sizeof(uint4), 256);
   }
   L.total = off;
   return L;
@@ -353,6 +360,24 @@ bool small_fits(int batch, int n_max) {
 
 bool cluster_fits(int n_max, int cs) { return cluster_slice(n_max, 16) > 0 && cluster_slice(n_max, cs) > 0; }
 
+// tile CTAs per frame of the cooperative path: ~128 boxes per tile, at most kCoopMaxTiles, and
+// every CTA of the call co-resident (0 when the call cannot be)
+int coop_tiles(int batch, int n_max) {
+  static std::atomic<int> per_sm[kMaxDevices];
+  const int dev = current_device();
+  int b = per_sm[dev].load();
+  if (b <= 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, pnms_coop<false>, kCoopThreads, 0) != cudaSuccess || b <= 0)
+      b = 1;
+    per_sm[dev].store(b);
+  }
+  int t = std::min(kCoopMaxTiles, std::max(16, n_max / 128));
+  const int resident = b * sm_count();
+  while (t > 1 && (long long)batch * t > resident) t /= 2;
+  // (each CTA stashes its slice of the frame in shared memory)
+  return (long long)batch * t <= resident && (n_max + t - 1) / t <= kCoopCap ? t : 0;
+}
+
 bool path_fits(int path, int batch, int n_max, int cs) {
   switch (path) {
     case PNMS_PATH_SMALL: return small_fits(batch, n_max);
@@ -361,6 +386,7 @@ bool path_fits(int path, int batch, int n_max, int cs) {
     case PNMS_PATH_TILES: return n_max <= PNMS_MAX_SLOTS;
     case PNMS_PATH_CLUSTER: return cluster_fits(n_max, cs);
     case PNMS_PATH_DENSE: return true;
+    case PNMS_PATH_COOP: return batch <= kCoopMaxFrames && n_max <= PNMS_MAX_SLOTS && coop_tiles(batch, n_max) > 0;
     default: return false;
   }
 }
@@ -372,6 +398,9 @@ int auto_path(int batch, int n_max, int cs) {
     // one wave of 1024-thread CTAs (two boxes per thread) when the batch fits the SMs
     return (n_max <= 2048 && batch <= sm_count()) ? PNMS_PATH_BINNED_WIDE : PNMS_PATH_BINNED;
   }
+  // single large frames: the cooperative path above 8192 slots (C3, 16384 boxes: 23.4 us
+  // against 30.5 on the tiles; they tie at 8192 — tools/single_frame_paths.py)
+  if (batch <= kCoopMaxFrames && n_max > 8192 && coop_tiles(batch, n_max) > 0) return PNMS_PATH_COOP;
   if (batch <= 2 || !cluster_fits(n_max, cs)) return PNMS_PATH_TILES;
   return PNMS_PATH_CLUSTER;
 }
@@ -673,6 +702,30 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
         return fail_cuda(e);
       if ((e = launch_maybe_pdl(true, pnms_mask_compact, dim3((unsigned)batch), dim3(512), 0, st, ta)) != cudaSuccess)
         return fail_cuda(e);
+    } else if (path == PNMS_PATH_COOP) {
+      // ---- large single frames: one cooperative launch of T tile CTAs per frame (pnms_coop.cuh)
+      ba.pairs_tested = nullptr;
+      ba.meta = reinterpret_cast<FrameMeta*>(ws + L.meta);  // the chunked sort accumulates into it
+      CoopArgs cargs;
+      cargs.b = ba;
+      cargs.b.trace = g_trace;
+      cargs.scr = reinterpret_cast<CoopFrame*>(ws + kTilesScratchOffset);
+      cargs.mask = reinterpret_cast<uint32_t*>(ws + kTilesScratchOffset + kCoopMaxFrames * sizeof(CoopFrame));
+      cargs.lists = reinterpret_cast<uint4*>(ws + L.coop);
+      cargs.tiles = coop_tiles(batch, n_max);
+      cargs.cap = kCoopCap;
+      cudaLaunchConfig_t clc = {};
+      clc.gridDim = dim3((unsigned)(batch * cargs.tiles));
+      clc.blockDim = dim3(kCoopThreads);
+      clc.dynamicSmemBytes = 0;
+      clc.stream = st;
+      cudaLaunchAttribute cattr[1];
+      cattr[0].id = cudaLaunchAttributeCooperative;
+      cattr[0].val.cooperative = 1;
+      clc.attrs = cattr;
+      clc.numAttrs = 1;
+      e = cudaLaunchKernelEx(&clc, tie_break == PNMS_TIE_BY_INDEX ? pnms_coop<true> : pnms_coop<false>, cargs);
+      if (e != cudaSuccess) return fail_cuda(e);
     } else {
       // ---- large frames in batches: one thread-block cluster per frame (pnms_binned_cluster.cuh)
       ba.pairs_tested = nullptr;

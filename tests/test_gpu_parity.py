@@ -18,7 +18,7 @@ from paper_2502_00535_b200.synth import random_frames  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 DEV = "cuda"
-PATHS = ["small", "binned", "binned_wide", "tiles", "cluster", "dense"]
+PATHS = ["small", "binned", "binned_wide", "tiles", "coop", "cluster", "dense"]
 
 
 @pytest.fixture(params=PATHS)
@@ -34,7 +34,8 @@ def path(request):
 def _path_fits(path, B, n):
     """Mirror of path_fits (pnms_capi.cu): whether a pinned path can take a B x n call."""
     return {"small": n <= 4096 and B <= 1024 and B * ((n + 31) // 32) <= 4096, "binned": n <= 4096,
-            "binned_wide": n <= 2048, "tiles": True, "cluster": n <= 16 * 4096, "dense": True}[path]
+            "binned_wide": n <= 2048, "tiles": True, "coop": B <= 2, "cluster": n <= 16 * 4096,
+            "dense": True}[path]
 
 
 def _vec(c):
@@ -145,7 +146,7 @@ def test_config_frames_match_reference(golden_configs, name, path):
     assert int(declined.item()) == 0
 
 
-@pytest.mark.parametrize("path_name", ["binned", "binned_wide", "tiles", "cluster", "small", "dense"])
+@pytest.mark.parametrize("path_name", ["binned", "binned_wide", "tiles", "coop", "cluster", "small", "dense"])
 def test_config_batches_match_reference(golden_configs, path_name):
     """The golden C4 and C5 frames as one batch each (the throughput launch shapes) through
     each path, path asserted, nothing declined."""
@@ -169,7 +170,7 @@ def test_config_batches_match_reference(golden_configs, path_name):
 
 def test_default_paths_of_the_configs(golden_configs):
     """Which path the library picks for each BASELINE config shape (the ones bench.py times)."""
-    want = {"C1": "small", "C2": "small", "C3": "tiles"}
+    want = {"C1": "small", "C2": "small", "C3": "coop"}
     for name, p in want.items():
         g = golden_configs[name]
         n = len(g["x"])
@@ -179,7 +180,7 @@ def test_default_paths_of_the_configs(golden_configs):
         assert lc.path_taken == p, name
         assert np.array_equal(ki[0, : int(kc.item())].cpu().numpy(), g["keep"])
     for (B, n), p in {(256, 1024): "binned", (100, 1024): "binned_wide", (400, 2048): "binned",
-                      (2, 4000): "tiles", (3, 9000): "cluster"}.items():
+                      (2, 4000): "tiles", (1, 8000): "tiles", (2, 9000): "coop", (3, 9000): "cluster"}.items():
         x, y, z, s = random_frames(B, n, seed=B, frame_w=3840, frame_h=2160)
         lc = LaunchConfig()
         ki, kc = batched_nms_keep(*(torch.from_numpy(a).to(DEV) for a in (x, y, z, s)), None, 0.5, launch=lc)
@@ -307,7 +308,7 @@ def test_declined_frame_list_grid_stride():
             assert np.array_equal(got[f], want[f]), (theta, f)
 
 
-LARGE_PATHS = {"tiles": ("tiles", 0), "cluster8": ("cluster", 8), "cluster16": ("cluster", 16)}
+LARGE_PATHS = {"tiles": ("tiles", 0), "cluster8": ("cluster", 8), "cluster16": ("cluster", 16), "coop": ("coop", 0)}
 
 
 def _large(large):
@@ -315,7 +316,7 @@ def _large(large):
     return LaunchConfig(path=p, cluster_size=cs)
 
 
-@pytest.mark.parametrize("large", list(LARGE_PATHS))
+@pytest.mark.parametrize("large", [k for k in LARGE_PATHS if k != "coop"])  # (coop: <= 2 frames per call)
 def test_cluster_path_large_frames(large):
     """Frames of 4097..20000 slots through the large-frame binned kernels (independent tile
     CTAs; one thread-block cluster per frame at both cluster sizes): ragged counts, exact ties,
@@ -338,7 +339,7 @@ def test_cluster_path_large_frames(large):
             assert np.array_equal(got[f], want), (cs, tie, f)
 
 
-@pytest.mark.parametrize("large", ["tiles", "cluster16"])
+@pytest.mark.parametrize("large", ["tiles", "coop", "cluster16"])
 def test_max_size_frame_cluster_path(large):
     """A 60000-slot frame (tile kernel; the cluster path's largest band layout, 16 CTAs x 3750
     slots) vs the C oracle, both tie policies."""
@@ -788,7 +789,7 @@ def test_one_workspace_across_paths_and_shapes():
     ws = torch.zeros(_lib.workspace_bytes(64, 9000), dtype=torch.uint8, device=DEV)
     rng = np.random.default_rng(5)
     cases = []
-    for (B, n, env) in ((3, 700, "small"), (20, 900, "binned"), (1, 3000, "tiles"), (2, 9000, "auto"),
+    for (B, n, env) in ((3, 700, "small"), (20, 900, "binned"), (1, 3000, "tiles"), (2, 9000, "auto"), (1, 5000, "coop"),
                         (3, 9000, "cluster"), (40, 1200, "binned"), (5, 800, "binned_wide"), (2, 500, "dense")):
         x, y, z, s = random_frames(B, n, seed=int(rng.integers(1 << 30)), frame_w=2000, frame_h=1500,
                                    z_range=(4, 70))
@@ -998,3 +999,62 @@ def test_variants_large_frames_vs_oracle(n):
             c = int(counts[f])
             want = c_oracle.soft_frame(x[f], y[f], z[f], s[f], c, mode, 0.3, 0.5)
             _soft_check(out[f, :c], want, mode, (n, f))
+
+
+@pytest.mark.parametrize("tie", ["paper_faithful", "by_index"])
+def test_coop_path_vs_oracle(golden_configs, tie):
+    """The cooperative latency path (pnms_coop.cuh): golden C1-C3 frames, random frames of
+    1000..65536 slots at several theta, pairs of ragged frames, NaN / negative scores with
+    padding, ties and crowds, and frames it declines (theta = 0, a zero side, a side > 126,
+    a tie group over kB2BucketMax) — every one equal to the oracle, path asserted."""
+    for nm in ("C1", "C2", "C3"):
+        g = golden_configs[nm]
+        n = len(g["x"])
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a).reshape(1, n)).to(DEV)  # noqa: E731
+        lc = LaunchConfig(path="coop")
+        ki, kc = batched_nms_keep(t(g["x"]), t(g["y"]), t(g["z"]), t(g["s"]), None, 0.5, tie, launch=lc)
+        assert lc.path_taken == "coop"
+        want = g["keep"] if tie == "paper_faithful" else c_oracle.run_frame(g["x"], g["y"], g["z"], g["s"], n, n, 0.5, tie)
+        assert np.array_equal(ki[0, : int(kc.item())].cpu().numpy(), want), nm
+    cases = [
+        (1000, [1000], 0.5, {}), (8192, [8192], 0.3, {}), (16384, [16384, 12000], 0.7, {}),
+        (65536, [65536], 0.5, {"frame_w": 8000, "frame_h": 8000}), (20000, [20000], 0.45, {"z_range": (1, 126)}),
+        (9000, [9000, 9000], 0.5, {"duplicate_fraction": 0.2}),
+    ]
+    for n, counts, theta, kw in cases:
+        B = len(counts)
+        gen = dict(frame_w=3840, frame_h=2160, z_range=(8, 64))
+        gen.update(kw)
+        x, y, z, s = random_frames(B, n, seed=n + B, **gen)
+        if n == 9000:
+            s[0, ::7] = np.nan
+            s[1, ::5] = -s[1, ::5]       # negative scores: suppressed by the padding slots below
+            x[1, :300] = 100; y[1, :300] = 120   # a crowd in one cell
+            s[1, 300:340] = 0.375        # ties
+        cnt = np.array(counts, np.int32)
+        lc = LaunchConfig(path="coop")
+        got = _run_batch(x, y, z, s, cnt, theta, tie, n + 7, launch=lc)
+        assert lc.path_taken == "coop"
+        for f in range(B):
+            want = c_oracle.run_frame(x[f], y[f], z[f], s[f], int(cnt[f]), n + 7, theta, tie)
+            assert np.array_equal(got[f], want), (n, f, theta, tie)
+    # declined frames: theta = 0, a zero side, a side over 126, 600 equal scores
+    x, y, z, s = random_frames(2, 6000, seed=9, frame_w=3840, frame_h=2160)
+    z[1, 17] = 0
+    for theta, mut in ((0.0, None), (0.5, "z0"), (0.5, "z200"), (0.5, "ties")):
+        xx, yy, zz, ss = x.copy(), y.copy(), z.copy(), s.copy()
+        if mut != "z0":
+            zz[1, 17] = 30
+        if mut == "z200":
+            zz[0, 3] = 200
+        if mut == "ties":
+            ss[0, :600] = 0.5
+        declined = torch.zeros(1, dtype=torch.int32, device=DEV)
+        lc = LaunchConfig(path="coop", declined=declined)
+        got = _run_batch(xx, yy, zz, ss, np.array([6000, 5000], np.int32), theta, tie, 6000, launch=lc)
+        assert lc.path_taken == "coop"
+        if mut != "ties":  # (equal scores spread over many tiles stay below the bucket limit)
+            assert int(declined.item()) >= 1, (theta, mut)
+        for f in range(2):
+            want = c_oracle.run_frame(xx[f], yy[f], zz[f], ss[f], [6000, 5000][f], 6000, theta, tie)
+            assert np.array_equal(got[f], want), (theta, mut, f)

@@ -40,7 +40,7 @@ for objs in (256, 1024):
     cases.append((f"clustered {4 * objs}", [torch.from_numpy(a.reshape(1, -1)).cuda() for a in (x, y, z, s)]))
 for name, args in cases:
     res = []
-    for path in ("auto", "small", "binned", "binned_wide", "tiles", "cluster", "dense"):
+    for path in ("auto", "small", "binned", "binned_wide", "tiles", "coop", "cluster", "dense"):
         t, taken = lat(args, LaunchConfig(path=path))
         if path == "auto" or taken == path:
             res.append(f"{path}{'=' + taken if path == 'auto' else ''} {t:6.2f}")
