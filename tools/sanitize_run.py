@@ -19,10 +19,13 @@ t = lambda arrs: [torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in arr
 small = t(random_frames(6, 700, seed=1, duplicate_fraction=0.1))
 big = t(random_frames(2, 9000, seed=2, frame_w=3840, frame_h=2160))
 gp = torch.empty(6, dtype=torch.int64, device=dev)
-for path in ("small", "binned", "binned_wide", "tiles", "cluster", "dense"):
+for path in ("small", "binned", "binned_wide", "tiles", "coop", "cluster", "dense"):
     for theta in (0.0, 0.5):  # theta 0: every frame declined by the culling kernels
-        batched_nms_keep(*small, None, theta, "by_index", gate_pairs=gp, launch=LaunchConfig(path=path))
-for path in ("tiles", "cluster"):
+        batched_nms_keep(*small[:1], None, theta, "by_index", gate_pairs=gp[:1], launch=LaunchConfig(path=path)) \
+            if path == "coop" else \
+            batched_nms_keep(*small, None, theta, "by_index", gate_pairs=gp, launch=LaunchConfig(path=path))
+batched_nms_keep(*small, None, 0.5, launch=LaunchConfig(path="binned", binned_impl=1))
+for path in ("tiles", "coop", "cluster"):
     batched_nms_keep(*big, None, 0.5, launch=LaunchConfig(path=path))
 validate_batch(*small)
 greedy_nms_keep(*small, None, 0.5)
