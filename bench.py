@@ -49,6 +49,7 @@ GEN = dict(frame_w=1920, frame_h=1080, z_range=(8, 64))
 WORKLOAD = (f"config 5: stream of {FRAMES} frames x {BOXES} boxes (random_frame distribution 1920x1080, "
             f"z 8..64), theta {THETA}, {TIE}, sharded contiguously over the GPUs")
 SEED = 20250200
+PROFILE_ROUND = "r02"  # profiles/<round>/: the committed ncu summaries the `traffic` fields cite
 DTYPE = "int32+f64"  # int32 geometry and products, float64 thresholds and score order (exact)
 
 
@@ -668,7 +669,7 @@ def main():
         peak_basis = f"{sms} SMs x 128 int lanes x {sm_mhz} MHz (median SM clock sampled during the timed region)"
 
         def prof(name):
-            f = ROOT / "profiles" / name
+            f = ROOT / "profiles" / PROFILE_ROUND / name
             return json.loads(f.read_text()).get("dram_bytes_per_launch") if f.exists() else None
 
         b_s = statistics.mean(binned_ms) / 1e3
@@ -723,17 +724,18 @@ def main():
             # the dominant kernel against the HBM roofline: algorithmic bytes per launch (SURVEY.md
             # §8d) = 20 B per slot read (x, y, z int32 + s float64) + 4 B per survivor index written
             "roofline": {"bound": "hbm", "achieved": hbm_bytes / b_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": hbm_bytes / b_s / 1e9 / hbm_peak, "traffic": prof("binned_kernel_ncu.json"),
-                         "kernel": "pnms_binned_frame", "bytes_per_launch": hbm_bytes,
+                         "frac": hbm_bytes / b_s / 1e9 / hbm_peak, "traffic": prof("binned2_kernel_ncu.json"),
+                         "kernel": "pnms_binned2_frame", "bytes_per_launch": hbm_bytes,
                          "peak_basis": ("of measured (MEASURED_PEAKS.json hbm_gbs)" if hbm_meas
                                         else "of fallback (B200_PROFILING.md)"),
-                         "note": "issue-bound (divergent per-row candidate loops), not bandwidth-bound: the input "
-                                 "is read once (traffic ~= algorithmic bytes)"},
+                         "note": "issue- and latency-bound (per-frame phases between CTA barriers, three frames "
+                                 "per SM), not bandwidth-bound: the input is read once (traffic ~= algorithmic "
+                                 "bytes)"},
             # the same kernel on the integer-op basis of SURVEY.md §8d (one unordered pair test = 8 int
             # ops, dense-equivalent count); the binned kernel culls pairs that cannot overlap, so this
             # fraction exceeds 1 — the executed-pair fraction is the one that measures its ALU use
             "roofline_alu": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
-                             "frac": achieved / peak, "kernel": "pnms_binned_frame", "ops_per_launch": ops,
+                             "frac": achieved / peak, "kernel": "pnms_binned2_frame", "ops_per_launch": ops,
                              "basis": "dense-equivalent ops (BASELINE.md §4)",
                              "executed_frac": pairs_executed * 8.0 / b_s / 1e12 / peak,
                              "pair_tests_executed_per_launch": pairs_executed,

@@ -131,6 +131,7 @@ typedef struct pnms_launch_config {
   int host_chain;      /* 1: the host launches the fallback chain for declined frames      */
   int32_t* declined;   /* device int32[1] or NULL: frames the culling kernel declined      */
   int binned_impl;     /* BINNED: 0 default (ranked, balanced rows), 1 first-generation     */
+  int coop_tiles;      /* COOP: tile CTAs per frame (0 = one per 128 slots, 16..512)       */
 } pnms_launch_config;
 
 /* Path report of one pnms_run_ex call (host memory). */

@@ -63,7 +63,7 @@ class LaunchConfigC(ctypes.Structure):
     _fields_ = [("path", ctypes.c_int), ("cluster_size", ctypes.c_int), ("cell_q8", ctypes.c_int),
                 ("cell_sx", ctypes.c_int), ("map_rows", ctypes.c_int), ("map_chunk", ctypes.c_int),
                 ("small_col_tiles", ctypes.c_int), ("host_chain", ctypes.c_int), ("declined", ctypes.c_void_p),
-                ("binned_impl", ctypes.c_int)]
+                ("binned_impl", ctypes.c_int), ("coop_tiles", ctypes.c_int)]
 
 
 class RunInfoC(ctypes.Structure):

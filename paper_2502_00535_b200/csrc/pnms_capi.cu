@@ -362,7 +362,7 @@ bool cluster_fits(int n_max, int cs) { return cluster_slice(n_max, 16) > 0 && cl
 
 // tile CTAs per frame of the cooperative path: ~128 boxes per tile, at most kCoopMaxTiles, and
 // every CTA of the call co-resident (0 when the call cannot be)
-int coop_tiles(int batch, int n_max) {
+int coop_tiles(int batch, int n_max, int want = 0) {
   static std::atomic<int> per_sm[kMaxDevices];
   const int dev = current_device();
   int b = per_sm[dev].load();
@@ -371,7 +371,7 @@ int coop_tiles(int batch, int n_max) {
       b = 1;
     per_sm[dev].store(b);
   }
-  int t = std::min(kCoopMaxTiles, std::max(16, n_max / 128));
+  int t = want > 0 ? std::min(want, kCoopMaxTiles) : std::min(kCoopMaxTiles, std::max(16, n_max / kCoopBoxesPerTile));
   const int resident = b * sm_count();
   while (t > 1 && (long long)batch * t > resident) t /= 2;
   // (each CTA stashes its slice of the frame in shared memory)
@@ -400,7 +400,7 @@ int auto_path(int batch, int n_max, int cs) {
   }
   // single large frames: the cooperative path above 8192 slots (C3, 16384 boxes: 23.4 us
   // against 30.5 on the tiles; they tie at 8192 — tools/single_frame_paths.py)
-  if (batch <= kCoopMaxFrames && n_max > 8192 && coop_tiles(batch, n_max) > 0) return PNMS_PATH_COOP;
+  if (batch <= kCoopMaxFrames && n_max > 4096 && coop_tiles(batch, n_max) > 0) return PNMS_PATH_COOP;
   if (batch <= 2 || !cluster_fits(n_max, cs)) return PNMS_PATH_TILES;
   return PNMS_PATH_CLUSTER;
 }
@@ -449,6 +449,9 @@ static_assert(kDeclCountOffset + 4 <= kSmallScratchBytes, "scratch");
 // the tile path's decline flags and survivor masks, re-zeroed by pnms_mask_compact
 constexpr size_t kTilesScratchOffset = 32 * 1024;
 static_assert(kDeclCountOffset + 4 <= kTilesScratchOffset, "scratch");
+// the cooperative path's frame scratch and survivor masks (frames of up to PNMS_MAX_SLOTS)
+static_assert(kTilesScratchOffset + kCoopMaxFrames * (sizeof(CoopFrame) + PNMS_MAX_SLOTS / 8) <= kSmallScratchBytes,
+              "scratch");
 
 template <int R>
 cudaError_t launch_map(const MapArgs& ma, long long grid, size_t smem, cudaStream_t st, bool list) {
@@ -712,7 +715,7 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
       cargs.scr = reinterpret_cast<CoopFrame*>(ws + kTilesScratchOffset);
       cargs.mask = reinterpret_cast<uint32_t*>(ws + kTilesScratchOffset + kCoopMaxFrames * sizeof(CoopFrame));
       cargs.lists = reinterpret_cast<uint4*>(ws + L.coop);
-      cargs.tiles = coop_tiles(batch, n_max);
+      cargs.tiles = coop_tiles(batch, n_max, lc.coop_tiles);
       cargs.cap = kCoopCap;
       cudaLaunchConfig_t clc = {};
       clc.gridDim = dim3((unsigned)(batch * cargs.tiles));

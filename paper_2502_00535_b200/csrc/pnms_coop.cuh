@@ -12,21 +12,20 @@
 //            and appends each box of its slice to the list of every tile whose region (tile
 //            plus halo) holds the box's cell: one 16 B entry {x|y<<16, z|dead<<7|slot<<16, key}
 //   barrier
-//   phase 2  CTA r owns tile r: its region's entries into shared memory, cells and exact
-//            region-local score ranks (value-linear buckets + in-bucket count, as
-//            pnms_binned2.cuh), 16 B records, and the rows of the tile's interior scanned
-//            against their windows (flattened runs, gate rank_j < rank_i); survivor bits into
-//            the frame's global mask
+//   phase 2  CTA r owns tile r: its region's entries into shared memory, a counting sort into
+//            the region's cells, 16 B records plus the 64-bit keys at the cell positions, and
+//            the rows of the tile's interior scanned against their windows with the
+//            reference's gate on the full keys (engine.py:233-235; the input slot breaks
+//            by_index ties); survivor bits into the frame's global mask
 //   barrier
 //   phase 3  CTA r compacts mask words [r*wpc, (r+1)*wpc) into ascending keep indices (its
 //            offset = popcount of the words before it); the last CTA to finish re-zeroes the
 //            frame's scratch for the next call
 //
 // Exactness is that of pnms_binned2.cuh: every column that can clear row i's bit lies in i's
-// window, the window of an interior row lies inside the tile's region, and region-local ranks
-// order every pair the scan compares exactly as the frame's keys do.  A frame is declined
-// (dense pipeline, through the device-side list) if it is not eligible, a tile list overflows
-// or a score bucket exceeds kB2BucketMax.
+// window, the window of an interior row lies inside the tile's region, and the gate compares
+// the frame's own 64-bit keys.  A frame is declined (dense pipeline, through the device-side
+// list) if it is not eligible or a tile region exceeds kCoopCap boxes.
 #pragma once
 #include "pnms_binned2.cuh"
 
@@ -35,15 +34,15 @@ namespace pnms {
 constexpr int kCoopThreads = 256;
 constexpr int kCoopCap = 1024;          // region entries a tile CTA holds
 constexpr int kCoopCells = 2048;        // region cells a tile CTA holds
-constexpr int kCoopBuckets = 2048;      // region score buckets
 constexpr int kCoopMaxFrames = 2;       // frames per call (latency path)
-constexpr int kCoopMaxTiles = 128;
+constexpr int kCoopMaxTiles = 512;
+constexpr int kCoopBoxesPerTile = 128;  // default tile count: one tile per this many slots
 
 // per-frame scratch in the caller's persistent zeroed workspace head; every field's identity
 // is 0 (minima are kept as maxima of complements), and the last CTA re-zeroes it all
 struct CoopFrame {
   uint32_t mode, nminz, maxz, nminx, nminy, maxx, maxy, n_act;  // ox(v) = v ^ 2^31: signed order
-  uint32_t maxL, nminW, nfmin, fmax;
+  uint32_t maxL, nminW, pad0, pad1;
   uint32_t barrier, done, overflow, big;
   uint32_t tile_cnt[kCoopMaxTiles];
 };
@@ -111,18 +110,14 @@ __global__ void __launch_bounds__(kCoopThreads) pnms_coop(CoopArgs ca) {
 
   __shared__ __align__(16) RecBin recS[kCoopCap];
   __shared__ __align__(16) uint4 ent[kCoopCap];          // region entries
-  __shared__ uint16_t idxS[kCoopCap];                     // cell order -> entry
-  __shared__ uint16_t idxB[kCoopCap];                     // bucket order -> entry
-  __shared__ __align__(16) uint16_t order[kCoopCap];
-  __shared__ __align__(16) uint16_t comb[kCoopCells + kCoopBuckets + 8];
+  __shared__ __align__(16) uint64_t keyR[kCoopCap];      // keys at the cell positions
+  __shared__ __align__(16) uint16_t comb[kCoopCells + 8];  // cell counts -> starts
   __shared__ uint32_t Tz[128];
   __shared__ uint32_t rowhist[kB2RowClasses];
   __shared__ uint32_t scan_tmp[64];
   __shared__ uint32_t red[16][NW];
-  uint64_t* keyB = reinterpret_cast<uint64_t*>(recS);     // bucket-order keys live in recS until the records
-  uint32_t* lcnt = reinterpret_cast<uint32_t*>(order);    // phase 1 (order is phase 2's): per-tile counts ...
+  uint32_t* lcnt = reinterpret_cast<uint32_t*>(keyR);     // phase 1 (keyR is phase 2's): per-tile counts ...
   uint32_t* gbase = lcnt + kCoopMaxTiles;                  // ... and reserved list offsets
-  static_assert(2 * kCoopMaxTiles * 4 <= kCoopCap * 2, "order aliases the phase-1 counters");
 
   if (threadIdx.x < 128) {
     const int zv = threadIdx.x;
@@ -160,8 +155,6 @@ __global__ void __launch_bounds__(kCoopThreads) pnms_coop(CoopArgs ca) {
         const uint32_t tw = Tz[zv & 127];
         v[8] = max(v[8], sgn_key(zv + 1 - (int)(tw >> 16)));
         v[9] = max(v[9], ~sgn_key((int)(tw >> 16)));
-        const float sf = __double2float_rn(sv);
-        if (!isinf(sf)) { const uint32_t fk = f32_key(sf); v[10] = max(v[10], ~fk); v[11] = max(v[11], fk); }
       } else {
         atomicOr(&mask[e >> 5], 1u << (e & 31));
       }
@@ -197,13 +190,6 @@ __global__ void __launch_bounds__(kCoopThreads) pnms_coop(CoopArgs ca) {
   const int L = n_act ? sgn_unkey(vf->maxL) : 0, R = n_act ? sgn_unkey(~vf->nminW) : 1;
   const int ox = sgn_unkey(~vf->nminx), oy = sgn_unkey(~vf->nminy);
   const int spanx = sgn_unkey(vf->maxx) - ox, spany = sgn_unkey(vf->maxy) - oy;
-  float smin = 0.0f, inv = 0.0f;
-  if (n_act && vf->nfmin != 0u) {
-    smin = f32_unkey(~vf->nfmin);
-    const float rng = __fsub_rn(f32_unkey(vf->fmax), smin);
-    if (rng > 0.0f) inv = __fdiv_rn((float)kCoopBuckets, rng);
-    if (isinf(inv)) inv = 0.0f;
-  }
   // cells as pnms_binned2.cuh: Sy = the power of two nearest L + 1, Sx = Sy / 4
   int Sy, Sx;
   {
@@ -293,79 +279,39 @@ __global__ void __launch_bounds__(kCoopThreads) pnms_coop(CoopArgs ca) {
     if (lcells + 1 > kCoopCells || m > kCoopCap) {
       if (threadIdx.x == 0) atomicOr(&cf->overflow, 2u);
     } else {
-      for (int w = threadIdx.x; w < (kCoopCells + kCoopBuckets + 8) / 8; w += kCoopThreads)
+      // the region's entries: cells by counting sort (no score order: the scan gates on the
+      // full 64-bit keys, with the input slot for by_index ties), 16 B records + keys at the
+      // cell positions, then every interior row against its window
+      for (int w = threadIdx.x; w < (kCoopCells + 8) / 8; w += kCoopThreads)
         reinterpret_cast<uint4*>(comb)[w] = make_uint4(0u, 0u, 0u, 0u);
       const uint4* lst = lists + (size_t)r * cap;
       for (int q = threadIdx.x; q < m; q += kCoopThreads) ent[q] = lst[q];
       __syncthreads();
       constexpr int PE = kCoopCap / kCoopThreads;
-      uint32_t cr[PE], br[PE];  // cell | rank-in-cell << 16, bucket | rank-in-bucket << 16
+      uint32_t cr[PE];  // local cell | rank in cell << 16
 #pragma unroll
       for (int k = 0; k < PE; ++k) {
         const int q = threadIdx.x + k * kCoopThreads;
-        cr[k] = br[k] = 0xFFFFFFFFu;
+        cr[k] = 0xFFFFFFFFu;
         if (q < m) {
           const uint4 en = ent[q];
           const int xv = (int)(en.x & 0xFFFFu), yv = (int)(en.x >> 16);
           const int lc = ((yv - py0) >> lsy) * LW + ((xv - px0) >> lsx);
           cr[k] = (uint32_t)lc | (atomic_inc_u16(comb, lc) << 16);
-          const float sf = __double2float_rn(key_to_double(((uint64_t)en.w << 32) | en.z));
-          const float t = __fmul_rn(__fsub_rn(sf, smin), inv);
-          const int bi = t >= (float)kCoopBuckets ? kCoopBuckets - 1 : (t > 0.0f ? (int)t : 0);
-          const int b = kCoopBuckets - 1 - bi;
-          br[k] = (uint32_t)b | (atomic_inc_u16(comb, lcells + b) << 16);
         }
       }
       __syncthreads();
-      // exclusive scan of [cells | buckets | 0]
-      uint32_t big = 0;
       {
-        const int len = lcells + kCoopBuckets + 1;
-        constexpr int PS = (kCoopCells + kCoopBuckets + 8 + kCoopThreads - 1) / kCoopThreads;
+        // exclusive scan of the cell counts (+ the sentinel m)
+        const int len = lcells + 1;
+        constexpr int PS = (kCoopCells + kCoopThreads - 1) / kCoopThreads;
         const int c0 = threadIdx.x * PS;
         uint32_t sum = 0;
-        for (int t = 0; t < PS; ++t) {
-          const int c = c0 + t;
-          if (c < len) { const uint32_t v = comb[c]; sum += v; if (c >= lcells) big = max(big, v); }
-        }
+        for (int t = 0; t < PS; ++t) if (c0 + t < len) sum += comb[c0 + t];
         uint32_t run = block_exclusive_scan(sum, scan_tmp, nullptr);
         for (int t = 0; t < PS; ++t) {
           const int c = c0 + t;
           if (c < len) { const uint32_t v = comb[c]; comb[c] = (uint16_t)run; run += v; }
-        }
-        big = __reduce_max_sync(0xFFFFFFFFu, big);
-        if (lane == 0 && big > (uint32_t)kB2BucketMax) atomicOr(&cf->overflow, 4u);
-      }
-      __syncthreads();
-      // keys into bucket order
-#pragma unroll
-      for (int k = 0; k < PE; ++k) {
-        const int q = threadIdx.x + k * kCoopThreads;
-        if (q < m) {
-          const int b = (int)(br[k] & 0xFFFFu);
-          const int pos = (int)comb[lcells + b] - m + (int)(br[k] >> 16);
-          keyB[pos] = ((uint64_t)ent[q].w << 32) | ent[q].z;
-          idxB[pos] = (uint16_t)q;
-        }
-      }
-      __syncthreads();
-      // ranks, then records at the cell positions (keyB lives in recS: ranks first)
-      uint32_t rk[PE];
-#pragma unroll
-      for (int k = 0; k < PE; ++k) {
-        const int q = threadIdx.x + k * kCoopThreads;
-        rk[k] = 0u;
-        if (q < m) {
-          const int b = (int)(br[k] & 0xFFFFu);
-          const int bs = (int)comb[lcells + b] - m, be = (int)comb[lcells + b + 1] - m;
-          const uint64_t key = ((uint64_t)ent[q].w << 32) | ent[q].z;
-          const int e = (int)(ent[q].y >> 16);
-          int rank = bs;
-          for (int j = bs; j < be; ++j) {
-            const uint64_t kj = keyB[j];
-            rank += kj < key || (BY_INDEX && kj == key && (int)(ent[idxB[j]].y >> 16) < e);
-          }
-          rk[k] = (uint32_t)rank;
         }
       }
       __syncthreads();
@@ -375,110 +321,56 @@ __global__ void __launch_bounds__(kCoopThreads) pnms_coop(CoopArgs ca) {
         if (q < m) {
           const uint4 en = ent[q];
           const int xv = (int)(en.x & 0xFFFFu), yv = (int)(en.x >> 16), zv = (int)(en.y & 0x7Fu);
-          const int lc = (int)(cr[k] & 0xFFFFu);
-          const int pos = (int)comb[lc] + (int)(cr[k] >> 16);
+          const int pos = (int)comb[cr[k] & 0xFFFFu] + (int)(cr[k] >> 16);
           const uint32_t Tv = Tz[zv] & 0xFFFFu;
           RecBin rb;
           rb.a = ((uint32_t)(xv + zv + 1) & 0xFFFFu) | ((uint32_t)(yv + zv + 1) << 16);
           rb.nb = ((uint32_t)(-xv) & 0xFFFFu) | ((uint32_t)(-yv) << 16);
           rb.w = -(int32_t)(Tv << 17) | (zv + 1);
-          rb.k = rk[k];
+          rb.k = en.y >> 16;  // input slot
           recS[pos] = rb;
-          idxS[pos] = (uint16_t)q;
+          keyR[pos] = ((uint64_t)en.w << 32) | en.z;
         }
       }
       __syncthreads();
-      // rows: the interior's live boxes, ordered by candidate count
       auto window = [&](int xv, int yv, int zv, int& wx0, int& wx1, int& wy0, int& wy1) {
         wx0 = max((xv - L - px0) >> lsx, 0);
         wx1 = min((xv + zv + 1 - R - px0) >> lsx, LW - 1);
         wy0 = max((yv - L - py0) >> lsy, 0);
         wy1 = min((yv + zv + 1 - R - py0) >> lsy, LH - 1);
       };
-      uint32_t rowinfo[PE];
+      const uint32_t rbase = static_cast<uint32_t>(__cvta_generic_to_shared(recS));
+      // rows: the interior's live boxes (dead = suppressed by the padding columns)
 #pragma unroll
       for (int k = 0; k < PE; ++k) {
         const int q = threadIdx.x + k * kCoopThreads;
-        rowinfo[k] = 0xFFFFFFFFu;
-        if (q < m && !(ent[q].y & 0x80u)) {
-          const uint4 en = ent[q];
-          const int xv = (int)(en.x & 0xFFFFu), yv = (int)(en.x >> 16), zv = (int)(en.y & 0x7Fu);
-          const int gcx = (xv - ox) >> shx, gcy = (yv - oy) >> shy;
-          if (gcx >= ix0 && gcx <= ix1 && gcy >= iy0 && gcy <= iy1) {
-            int wx0, wx1, wy0, wy1;
-            window(xv, yv, zv, wx0, wx1, wy0, wy1);
-            int nc = 0;
-            for (int yy = wy0; yy <= wy1; ++yy) nc += (int)comb[yy * LW + wx1 + 1] - (int)comb[yy * LW + wx0];
-            const int cls = min(nc, kB2RowClasses - 1);
-            const uint32_t slot = atomicAdd(&rowhist[cls], 1u);
-            const int pos = (int)comb[cr[k] & 0xFFFFu] + (int)(cr[k] >> 16);
-            rowinfo[k] = (uint32_t)pos | ((uint32_t)cls << 12) | (slot << 18);
-          }
-        }
-      }
-      __syncthreads();
-      uint32_t nrows;
-      {
-        const uint32_t h0 = rowhist[2 * lane], h1 = rowhist[2 * lane + 1];
-        uint32_t inc = h0 + h1;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
-          if (lane >= o) inc += t;
-        }
-        nrows = __shfl_sync(0xFFFFFFFFu, inc, 31);
-        const uint32_t ex0 = inc - h0 - h1;
-#pragma unroll
-        for (int k = 0; k < PE; ++k) {
-          const int cls = (int)((rowinfo[k] >> 12) & 63u);
-          const uint32_t st0 = __shfl_sync(0xFFFFFFFFu, ex0, cls >> 1);
-          const uint32_t h0c = __shfl_sync(0xFFFFFFFFu, h0, cls >> 1);
-          if (rowinfo[k] != 0xFFFFFFFFu)
-            order[st0 + ((cls & 1) ? h0c : 0u) + (rowinfo[k] >> 18)] = (uint16_t)(rowinfo[k] & 0xFFFu);
-        }
-      }
-      __syncthreads();
-      const uint32_t rbase = static_cast<uint32_t>(__cvta_generic_to_shared(recS));
-      for (int o = threadIdx.x; o < (int)nrows; o += kCoopThreads) {
-        const int p = order[o];
+        if (q >= m || (ent[q].y & 0x80u)) continue;
+        const uint4 en = ent[q];
+        const int xv = (int)(en.x & 0xFFFFu), yv = (int)(en.x >> 16), zv = (int)(en.y & 0x7Fu);
+        const int gcx = (xv - ox) >> shx, gcy = (yv - oy) >> shy;
+        if (gcx < ix0 || gcx > ix1 || gcy < iy0 || gcy > iy1) continue;
+        const int p = (int)comb[cr[k] & 0xFFFFu] + (int)(cr[k] >> 16);
         const uint4 ri = lds128(rbase + (uint32_t)p * 16u);
+        const uint64_t ki = keyR[p];
         const uint32_t zzi = __byte_perm(ri.z, 0u, 0x4040);
-        const int32_t ix = -(int32_t)(int16_t)(ri.y & 0xFFFFu), iy = -(int32_t)(int16_t)(ri.y >> 16);
-        const int32_t iz = (int32_t)(ri.z & 0xFFu) - 1;
         int wx0, wx1, wy0, wy1;
-        window(ix, iy, iz, wx0, wx1, wy0, wy1);
+        window(xv, yv, zv, wx0, wx1, wy0, wy1);
         bool hit = false;
-        for (int y0 = wy0; y0 <= wy1 && !hit; y0 += kB2RunGroup) {
-          int d[kB2RunGroup], c[kB2RunGroup + 1];
-          c[0] = 0;
-#pragma unroll
-          for (int s = 0; s < kB2RunGroup; ++s) {
-            const int yy = y0 + s;
-            int qb = 0, qe = 0;
-            if (yy <= wy1) { qb = comb[yy * LW + wx0]; qe = comb[yy * LW + wx1 + 1]; }
-            d[s] = qb - c[s];
-            c[s + 1] = c[s] + (qe - qb);
-          }
-          const int total = c[kB2RunGroup];
-          int k = 0;
-          bool more = total > 0;
-          while (more) {
-            int q = k + d[0];
-#pragma unroll
-            for (int s = 1; s < kB2RunGroup; ++s) q = k >= c[s] ? k + d[s] : q;
-            const uint4 g = lds128(rbase + (uint32_t)q * 16u);
+        for (int yy = wy0; yy <= wy1 && !hit; ++yy) {
+          int qq = comb[yy * LW + wx0];
+          const int qe = comb[yy * LW + wx1 + 1];
+          while (!hit && qq < qe) {
+            const uint4 g = lds128(rbase + (uint32_t)qq * 16u);
+            const uint64_t kj = keyR[qq];
             const uint32_t t1 = __viaddmin_s16x2(ri.x, g.y, zzi);
             const uint32_t t2 = __viaddmin_s16x2_relu(g.x, ri.y, t1);
             const uint32_t v = __vimin_s16x2_relu(t2, __byte_perm(g.z, 0u, 0x4040));
-            hit = g.w < ri.w && (int)(v * v) + (int)g.z >= 0;
-            ++k;
-            more = !hit && k < total;
+            const bool gate = kj < ki || (BY_INDEX && kj == ki && g.w < ri.w);
+            hit = gate && (int)(v * v) + (int)g.z >= 0;
+            ++qq;
           }
         }
-        if (!hit) {
-          const int e = (int)(ent[idxS[p]].y >> 16);
-          atomicOr(&mask[e >> 5], 1u << (e & 31));
-        }
+        if (!hit) atomicOr(&mask[ri.w >> 5], 1u << (ri.w & 31));
       }
     }
   }

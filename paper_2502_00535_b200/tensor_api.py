@@ -36,6 +36,7 @@ class LaunchConfig:
 
     path: "auto" | "small" | "binned" | "binned_wide" | "tiles" | "cluster" | "dense"
     binned_impl: 0 the default binned kernel (pnms_binned2.cuh), 1 the first-generation one
+    coop_tiles: tile CTAs per frame of the "coop" path (0: the library's choice)
     """
 
     path: str = "auto"
@@ -48,6 +49,7 @@ class LaunchConfig:
     host_chain: bool = False
     declined: torch.Tensor | None = None
     binned_impl: int = 0
+    coop_tiles: int = 0
     path_taken: str | None = None
 
     def to_c(self) -> _lib.LaunchConfigC:
@@ -59,7 +61,7 @@ class LaunchConfig:
                                   int(self.cell_sx), int(self.map_rows), int(self.map_chunk),
                                   int(self.small_col_tiles), int(bool(self.host_chain)),
                                   self.declined.data_ptr() if self.declined is not None else None,
-                                  int(self.binned_impl))
+                                  int(self.binned_impl), int(self.coop_tiles))
 
 
 _DEFAULT_LAUNCH: list[LaunchConfig | None] = [None]

@@ -21,8 +21,10 @@ big = t(random_frames(2, 9000, seed=2, frame_w=3840, frame_h=2160))
 gp = torch.empty(6, dtype=torch.int64, device=dev)
 for path in ("small", "binned", "binned_wide", "tiles", "coop", "cluster", "dense"):
     for theta in (0.0, 0.5):  # theta 0: every frame declined by the culling kernels
-        batched_nms_keep(*small[:1], None, theta, "by_index", gate_pairs=gp[:1], launch=LaunchConfig(path=path)) \
-            if path == "coop" else \
+        if path == "coop":  # (a latency path: at most two frames per call)
+            batched_nms_keep(*[a[:2] for a in small], None, theta, "by_index", gate_pairs=gp[:2],
+                             launch=LaunchConfig(path=path))
+        else:
             batched_nms_keep(*small, None, theta, "by_index", gate_pairs=gp, launch=LaunchConfig(path=path))
 batched_nms_keep(*small, None, 0.5, launch=LaunchConfig(path="binned", binned_impl=1))
 for path in ("tiles", "coop", "cluster"):
