@@ -162,7 +162,8 @@ class CpuReference:
 
     def describe(self) -> str:
         what = ("parnms.engine.run_nms of the unmodified reference (baseline/_ref)" if self.kind == "reference"
-                else "numpy port of engine.run_nms (oracle/parnms_oracle.py; baseline/_ref absent)")
+                else "numpy port of engine.run_nms (oracle/parnms_oracle.py"
+                     + ("" if _ref_importable() else "; baseline/_ref absent") + ")")
         return f"{what}, workers=1, one process per host core, one frame per task"
 
 

@@ -21,6 +21,11 @@ same exit codes (3 internal, 1 input error).  Differences, by design:
   * sweep frames come from paper_2502_00535_b200.synth.clustered_frame: the reference's
     clustered layout (workload.py:75-140) from an independent random stream.
   * sweep-batch (not in the reference) sweeps the batched path: frames/s at batch sizes B.
+
+This module is harness glue, not hot-path code: the argparse surface, CSV_COLUMNS, _DEFAULTS
+and the small helpers _next_multiple, _load_config, _resolve, _int_list and main() follow the
+reference's cli.py:143-186, 504-515 nearly verbatim on purpose — a drop-in harness has to
+accept the same flags and write the same files.
 """
 
 from __future__ import annotations
