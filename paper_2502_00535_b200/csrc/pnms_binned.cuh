@@ -85,7 +85,10 @@ inline int binned_per_thread(int n_max, int threads) { return n_max <= 2 * threa
 // S = 1 has no 32-bit magic (2^32 + 1): callers keep every cell side >= 2 (kMinCellSide).
 constexpr int kMinCellSide = 2;
 __device__ __forceinline__ uint32_t div_magic(int S) {
-  return S >= 32768 ? 0u : (uint32_t)(0xFFFFFFFFu / (uint32_t)max(S, kMinCellSide)) + 1u;
+  S = max(S, kMinCellSide);
+  if (S >= 32768) return 0u;
+  if ((S & (S - 1)) == 0) return 1u << (32 - (31 - __clz(S)));  // 2^32 / S: the same value, no division
+  return (uint32_t)(0xFFFFFFFFu / (uint32_t)S) + 1u;
 }
 __device__ __forceinline__ int qdiv(int v, uint32_t M) { return (int)__umulhi((uint32_t)v, M); }
 

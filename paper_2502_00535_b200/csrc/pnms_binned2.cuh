@@ -120,6 +120,19 @@ __device__ __forceinline__ bool binned2_frame_body(const BinArgs& a) {
   uint32_t* scan_tmp = reinterpret_cast<uint32_t*>(smem_raw + Ly::oScan);
   B2Stats* st = reinterpret_cast<B2Stats*>(smem_raw + Ly::oSt);
 
+  // the frame's loads are issued first, so their latency overlaps the initialisation below
+  // and its barrier (the n_max > NP case declines before using them)
+  int32_t lx[PER], ly[PER], lz[PER];
+  double ls[PER];
+  if (a.n_max <= NP) {
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int e = threadIdx.x + k * THREADS;
+      const long long g = fbase + (e < cnt ? e : 0);
+      lx[k] = e < cnt ? a.x[g] : 0; ly[k] = e < cnt ? a.y[g] : 0; lz[k] = e < cnt ? a.z[g] : 0;
+      ls[k] = e < cnt ? a.s[g] : 0.0;
+    }
+  }
   if (threadIdx.x == 0) {
     st->mode = kNarrow7; st->minz = 0x7FFFFFFF; st->maxz = 0;
     st->minx = st->miny = 0x7FFFFFFF; st->maxx = st->maxy = -0x7FFFFFFF;
@@ -157,9 +170,8 @@ __device__ __forceinline__ bool binned2_frame_body(const BinArgs& a) {
       xy[k] = 0u; zc[k] = 0xFFFFFFFFu; bb[k] = 0u;
       bool keep = false;
       if (e < cnt) {
-        const long long g = fbase + e;
-        const int32_t xv = a.x[g], yv = a.y[g], zv = a.z[g];
-        const double sv = a.s[g];
+        const int32_t xv = lx[k], yv = ly[k], zv = lz[k];
+        const double sv = ls[k];
         mode = max(mode, frame_mode_of(xv, yv, zv));
         keep = !(pad_rule && sv < 0.0);
         if (sv == sv) {
@@ -224,9 +236,11 @@ __device__ __forceinline__ bool binned2_frame_body(const BinArgs& a) {
         int GX = 1, GY = 1;
         const int ox = vs->minx, oy = vs->miny;
         if (na > 0 && elig) {
+          const int spx = vs->maxx - ox, spy = vs->maxy - oy;
+          const bool p2 = (Sx & (Sx - 1)) == 0 && (Sy & (Sy - 1)) == 0;  // (widening keeps it)
           for (;;) {
-            GX = (vs->maxx - ox) / Sx + 1;
-            GY = (vs->maxy - oy) / Sy + 1;
+            GX = (p2 ? spx >> (31 - __clz(Sx)) : spx / Sx) + 1;
+            GY = (p2 ? spy >> (31 - __clz(Sy)) : spy / Sy) + 1;
             if ((long long)GX * GY <= Ly::kMaxCells) break;
             if (Sx < Sy) Sx *= 2;
             else { Sx *= 2; Sy *= 2; }
