@@ -67,7 +67,7 @@ struct B2Layout {
   static constexpr size_t oScan = oHist + 4 * kB2RowClasses;
   static constexpr size_t oSt = oScan + 4 * 64;
   static constexpr size_t kBytes = oSt + sizeof(B2Stats);
-  static_assert(NP % 1024 == 0 && (NP & (NP - 1)) == 0, "NP: a power of two >= 1024");
+  static_assert(NP % 256 == 0, "NP: a multiple of 256");
   static_assert(oComb % 16 == 0 && oBits % 16 == 0 && oSt % 16 == 0, "alignment");
 };
 inline size_t b2_smem_bytes(int np) { return np <= 2048 ? B2Layout<2048>::kBytes : B2Layout<4096>::kBytes; }
@@ -473,13 +473,13 @@ __device__ __forceinline__ bool binned2_frame_body(const BinArgs& a) {
   // thread writes the ascending keep indices of its own slots (coalesced)
   uint32_t* wpre = rowhist;  // [NP/32] word offsets (rowhist + scan_tmp: 128 entries)
   if (warp == 0) {
-    constexpr int WPL = NP / 32 / 32;  // words per lane
+    constexpr int WPL = (NP / 32 + 31) / 32;  // words per lane
     const int W32 = a.W32;
     uint32_t c[WPL], sum = 0;
 #pragma unroll
     for (int t = 0; t < WPL; ++t) {
       const int w = lane * WPL + t;
-      const uint32_t bits = w < W32 ? kbits[w] : 0u;
+      const uint32_t bits = w < W32 && w < NP / 32 ? kbits[w] : 0u;
       if (a.keep_mask && w < W32) a.keep_mask[(long long)f * W32 + w] = bits;
       c[t] = __popc(bits);
       sum += c[t];
@@ -492,7 +492,10 @@ __device__ __forceinline__ bool binned2_frame_body(const BinArgs& a) {
     }
     uint32_t run = inc - sum;
 #pragma unroll
-    for (int t = 0; t < WPL; ++t) { wpre[lane * WPL + t] = run; run += c[t]; }
+    for (int t = 0; t < WPL; ++t) {
+      if (lane * WPL + t < NP / 32) wpre[lane * WPL + t] = run;
+      run += c[t];
+    }
     if (lane == 31) {
       if (a.keep_count) a.keep_count[f] = (int32_t)inc;
       a.fallback[f] = 0;

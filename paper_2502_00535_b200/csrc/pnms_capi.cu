@@ -306,10 +306,6 @@ cudaError_t launch_binned(int impl, int variant, const BinArgs& ba, int batch, i
   }
   const size_t smem = b2_smem_bytes(npad);
   static SmemCache c2[12];
-  if (impl == 2 && !wide && n_max <= 4 * kBinThreads) {  // experiment: two CTAs per SM, no spills
-    static SmemCache c3;
-    return launch_binned2_t<false, false, 4, kBinThreads, 2>(ba, batch, smem, st, c3);
-  }
 #define PNMS_B2(P, T, I)                                                                        \
   switch (variant & 3) {                                                                        \
     case 0: return launch_binned2_t<false, false, P, T>(ba, batch, smem, st, c2[I]);           \
