@@ -12,8 +12,9 @@
 // round decides at least the highest-ranked undecided box, so the loop ends after as many
 // rounds as the longest suppression chain (a handful on detector output).
 //
-// Candidates: greedy never covers on zero overlap, so spatial cells of side max_z + 1 (3x3
-// neighbourhood, see pnms_binned.cuh) are exact for every theta; frames with negative
+// Candidates: greedy never covers on zero overlap, so spatial cells are exact for every theta,
+// and a coverer's corner lies within the theta reach of pnms_binned2.cuh (L left / up,
+// z + 1 - R right / down, from w >= max(1, ceil(T_ref / (z_ref+1)))); frames with negative
 // coordinates or a crowded cell scan all slots instead.  One CTA per frame; covers() is
 // evaluated in exact 64-bit integer arithmetic against ceil(fl64(theta*a)).  The per-slot
 // state of frames up to kGreedyMaxSlots lives in shared memory; larger frames (up to
@@ -22,6 +23,7 @@
 #pragma once
 #include "pnms_common.cuh"
 #include "pnms_sort.cuh"
+#include "pnms_binned.cuh"  // qdiv / div_magic
 
 namespace pnms {
 
@@ -78,6 +80,11 @@ template <bool GLOBAL>
 __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_stat[8];   // 0 minx 1 miny 2 maxx 3 maxy 4 maxz 5 bin_ok 6 big 7 undecided
+  // the reach of a coverer (as pnms_binned2.cuh): ref i covers cand j only if w >= wmin_i =
+  // max(1, ceil(T_i / (z_i+1))) (h <= z_i + 1), so x_i lies in [x_j - L, x_j + z_j + 1 - R] with
+  // L = max_i (z_i + 1 - wmin_i), R = min_i wmin_i (same for y)
+  __shared__ long long s_L, s_R;
+  __shared__ int s_small;  // every cell coordinate below 2^16: one IMAD.HI per division
   __shared__ uint32_t scan_tmp[64];
   const int f = blockIdx.x;
   const long long fbase = (long long)f * a.n_max;
@@ -104,6 +111,7 @@ __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a
     s_stat[0] = s_stat[1] = 0x7FFFFFFF;
     s_stat[2] = s_stat[3] = -0x7FFFFFFF;
     s_stat[4] = 0; s_stat[5] = 1; s_stat[6] = 0; s_stat[7] = 0;
+    s_L = 0; s_R = 0x7FFFFFFFFFFFFFFFll; s_small = 0;
   }
   for (int w = threadIdx.x; w < npad / 32; w += kGreedyThreads) kbits[w] = 0u;
   __syncthreads();
@@ -114,7 +122,15 @@ __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a
     const double sv = a.s[g];
     sx[e] = xv; sy[e] = yv; sz[e] = zv;
     key[e] = sort_key(sv);
-    thr[e] = greedy_threshold(a.theta, zv);
+    const unsigned long long T = greedy_threshold(a.theta, zv);
+    thr[e] = T;
+    if (zv >= 0 && sv == sv) {
+      const unsigned long long zz = (unsigned long long)zv + 1ull;
+      const unsigned long long q = T / zz + (T % zz != 0ull);
+      const long long wmin = q < 1ull ? 1ll : (q > zz ? (long long)zz + 1 : (long long)q);  // > z+1: never covers
+      atomicMax(&s_L, (long long)zz - wmin);
+      atomicMin(&s_R, wmin);
+    }
     state[e] = (sv != sv) ? kKept : kUndecided;  // NaN: unordered, never covers (documented)
     dec[e] = kUndecided;
     if (xv < 0 || yv < 0 || zv < 0) atomicAnd(&s_stat[5], 0);
@@ -128,9 +144,10 @@ __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a
   // [x - max_z, x + z] x [y - max_z, y + z]); narrow cells tighten the x range of a scan,
   // tall ones keep the cell rows per scan few (as in pnms_binned.cuh)
   int Sx = 1, Sy = 1, GX = 1, GY = 1;
-  const int ox = s_stat[0], oy = s_stat[1], maxz = s_stat[4];
+  const int ox = s_stat[0], oy = s_stat[1];
+  const long long L = max(s_L, 0ll), R = min(s_R, 0x7FFFFFFFll);
   if (bin) {
-    Sy = s_stat[4] + 1;
+    Sy = (int)min(L + 1, (long long)s_stat[4] + 1);
     if (Sy <= 0) bin = false;  // z = INT_MAX
     Sx = max(Sy >> 2, 1);
   }
@@ -144,6 +161,8 @@ __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a
       else { Sx *= 2; Sy *= 2; }
     }
     const int cells = GX * GY;
+    if (threadIdx.x == 0)
+      s_small = s_stat[2] - ox + (long long)s_stat[4] + 1 < 32768 && s_stat[3] - oy + (long long)s_stat[4] + 1 < 32768;
     for (int c = threadIdx.x; c <= cells; c += kGreedyThreads) cstart[c] = 0u;
     __syncthreads();
     for (int e = threadIdx.x; e < cnt; e += kGreedyThreads) {
@@ -181,6 +200,8 @@ __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a
   }
   __syncthreads();
   // After the scatter, cstart[c] == end(c) == start(c+1); start(0) = 0.
+  const bool small = bin && s_small;
+  const uint32_t Mx = div_magic(Sx), My = div_magic(Sy);
   // ---- rounds over a compacted list of the undecided boxes; decisions go to dec[] and are
   // applied after a barrier (every box's slots are written only by its own thread)
   __shared__ int s_nund[2];
@@ -198,10 +219,19 @@ __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a
       bool kept_cov = false, undec_cov = false;
       if (bin) {
         // the cells the coverers' corners can lie in; one contiguous run per cell row
-        const int cx0 = (int)(max(0LL, (long long)jx - maxz - ox) / Sx);
-        const int cy0 = (int)(max(0LL, (long long)jy - maxz - oy) / Sy);
-        const int cx1 = (int)min((long long)GX - 1, ((long long)jx + jz - ox) / Sx);
-        const int cy1 = (int)min((long long)GY - 1, ((long long)jy + jz - oy) / Sy);
+        const long long lx = max(0LL, (long long)jx - L - ox), ly = max(0LL, (long long)jy - L - oy);
+        const long long hx = (long long)jx + jz + 1 - R - ox, hy = (long long)jy + jz + 1 - R - oy;
+        int cx0, cy0, cx1, cy1;
+        if (small) {  // (0 <= lx <= hx < 2^16 when hx >= 0)
+          cx0 = Sx == 1 ? (int)lx : qdiv((int)lx, Mx); cy0 = Sy == 1 ? (int)ly : qdiv((int)ly, My);
+          cx1 = Sx == 1 ? (int)hx : qdiv((int)max(hx, 0LL), Mx); cy1 = Sy == 1 ? (int)hy : qdiv((int)max(hy, 0LL), My);
+        } else {
+          cx0 = (int)(lx / Sx); cy0 = (int)(ly / Sy);
+          cx1 = (int)(max(hx, 0LL) / Sx); cy1 = (int)(max(hy, 0LL) / Sy);
+        }
+        cx1 = min(GX - 1, cx1);
+        // (hx or hy < 0: no ref reaches j — an empty range, so j is kept below)
+        cy1 = hx < 0 || hy < 0 ? cy0 - 1 : min(GY - 1, cy1);
         for (int yy = cy0; yy <= cy1 && !kept_cov; ++yy) {
           const int c0 = yy * GX + cx0, c1 = yy * GX + cx1;
           const int b = c0 == 0 ? 0 : (int)cstart[c0 - 1], en = (int)cstart[c1];

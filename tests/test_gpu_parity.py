@@ -1058,3 +1058,26 @@ def test_coop_path_vs_oracle(golden_configs, tie):
         for f in range(2):
             want = c_oracle.run_frame(xx[f], yy[f], zz[f], ss[f], [6000, 5000][f], 6000, theta, tie)
             assert np.array_equal(got[f], want), (theta, mut, f)
+
+
+@pytest.mark.parametrize("theta", [0.0, 1e-9, 0.37, 0.5, 0.99, 1.0])
+def test_greedy_reach_edge_cases_vs_oracle(theta):
+    """Greedy NMS with the theta reach (pnms_greedy.cuh): sides 1..4 (cells one pixel wide),
+    coordinates beyond 2^15 (the 64-bit window path), large sides in a small frame (crowds,
+    duplicates), exact score ties — vs the C oracle."""
+    from paper_2502_00535_b200 import greedy_nms_keep
+
+    frames = [random_frames(1, 900, seed=3, frame_w=200, frame_h=150, z_range=(1, 4)),
+              random_frames(1, 900, seed=4, frame_w=1920, frame_h=1080, z_range=(8, 120)),
+              random_frames(1, 900, seed=5, frame_w=300, frame_h=300, z_range=(20, 90), duplicate_fraction=0.2)]
+    x, y, z, s = (np.concatenate([f[i] for f in frames]) for i in range(4))
+    x[1] += 40000                              # beyond 2^15: 64-bit window arithmetic
+    s[2, ::9] = 0.625
+    s[0, ::4] = 0.25
+    counts = np.array([900, 900, 700], np.int32)
+    tt = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)  # noqa: E731
+    ki, kc = greedy_nms_keep(tt(x), tt(y), tt(z), tt(s), tt(counts), theta)
+    ki, kc = ki.cpu().numpy(), kc.cpu().numpy()
+    for f in range(3):
+        want = c_oracle.greedy_frame(x[f], y[f], z[f], s[f], int(counts[f]), theta)
+        assert np.array_equal(ki[f, : kc[f]], want), (f, theta)
