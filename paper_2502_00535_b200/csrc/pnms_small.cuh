@@ -50,7 +50,7 @@ struct SmallArgs {
 template <bool BY_INDEX, bool COUNT, int R>
 __global__ void __launch_bounds__(kSmallThreads) pnms_small_kernel(SmallArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ int s_mode;
+  __shared__ int s_wmode[kSmallThreads / 32];
   __shared__ unsigned int s_last;
   __shared__ unsigned long long s_gate;
   __shared__ uint32_t s_scan[kSmallThreads / 32 + 1];
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(kSmallThreads) pnms_small_kernel(SmallArgs a) 
   const int c1 = min(c0 + a.cols, cnt);
   const bool work = r0 < cnt && c0 < cnt;
 
-  if (threadIdx.x == 0) { s_mode = kNarrow7; s_gate = 0ull; }
+  if (threadIdx.x == 0) s_gate = 0ull;
   // one global load phase: this thread's rows and (first) column into registers
   int32_t rx[R], ry[R], rz[R];
   double rs[R];
@@ -80,26 +80,36 @@ __global__ void __launch_bounds__(kSmallThreads) pnms_small_kernel(SmallArgs a) 
         m = max(m, frame_mode_of(rx[r], ry[r], rz[r]));
       }
     }
-    for (int j = c0 + threadIdx.x; j < c1; j += kSmallThreads)
-      m = max(m, frame_mode_of(a.x[fbase + j], a.y[fbase + j], a.z[fbase + j]));
-    m = __reduce_max_sync(0xFFFFFFFFu, m);
   }
-  __syncthreads();
-  if (work && (threadIdx.x & 31) == 0 && m != kNarrow7) atomicMax(&s_mode, m);
-  __syncthreads();
-  // narrow16 tiles use the exact wide emulation (valid for every int32 input)
-  const int mode = s_mode == kNarrow7 ? kNarrow7 : kWide;
+  // the column tile in the same load phase: keys and narrow records straight into shared
+  // memory (one global round trip); a tile that turns out not narrow7 rebuilds wide records
   uint64_t* ckey = reinterpret_cast<uint64_t*>(smem_raw);                       // [cols]
   uint8_t* crec = reinterpret_cast<uint8_t*>(ckey + a.cols);                     // [cols] records
   if (work) {
     for (int j = c0 + threadIdx.x; j < c1; j += kSmallThreads) {
       const long long g = fbase + j;
+      const int32_t xv = a.x[g], yv = a.y[g], zv = a.z[g];
+      m = max(m, frame_mode_of(xv, yv, zv));
       ckey[j - c0] = sort_key(a.s[g]);
-      if (mode == kWide) reinterpret_cast<RecWide*>(crec)[j - c0] = make_rec_wide(a.x[g], a.y[g], a.z[g], a.theta);
-      else reinterpret_cast<RecNarrow*>(crec)[j - c0] = make_rec_narrow(a.x[g], a.y[g], a.z[g], a.theta, kNarrow7);
+      reinterpret_cast<RecNarrow*>(crec)[j - c0] = make_rec_narrow(xv, yv, zv, a.theta, kNarrow7);
     }
   }
+  // the tile's arithmetic mode: one slot per warp (no shared initialisation to race with)
+  m = __reduce_max_sync(0xFFFFFFFFu, m);
+  if ((threadIdx.x & 31) == 0) s_wmode[threadIdx.x >> 5] = m;
   __syncthreads();
+  int tile_mode = kNarrow7;
+#pragma unroll
+  for (int w = 0; w < kSmallThreads / 32; ++w) tile_mode = max(tile_mode, s_wmode[w]);
+  // narrow16 tiles use the exact wide emulation (valid for every int32 input)
+  const int mode = tile_mode == kNarrow7 ? kNarrow7 : kWide;
+  if (work && mode == kWide) {
+    for (int j = c0 + threadIdx.x; j < c1; j += kSmallThreads) {
+      const long long g = fbase + j;
+      reinterpret_cast<RecWide*>(crec)[j - c0] = make_rec_wide(a.x[g], a.y[g], a.z[g], a.theta);
+    }
+  }
+  if (mode == kWide) __syncthreads();
 
   bool sup[R];
 #pragma unroll
