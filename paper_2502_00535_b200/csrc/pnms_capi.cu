@@ -668,7 +668,41 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
   ba.cell_sx = lc.cell_sx;
   if (culling) {
     if ((e = mark(events, 0, st)) != cudaSuccess) return fail_cuda(e);
-    if (path == PNMS_PATH_BINNED || path == PNMS_PATH_BINNED_WIDE) {
+    if (path == PNMS_PATH_COOP) {
+      // ---- large single frames: one cooperative launch of T tile CTAs per frame (pnms_coop.cuh)
+      ba.pairs_tested = nullptr;
+      ba.meta = reinterpret_cast<FrameMeta*>(ws + L.meta);  // the chunked sort accumulates into it
+      CoopArgs cargs;
+      cargs.b = ba;
+      cargs.b.trace = g_trace;
+      cargs.scr = reinterpret_cast<CoopFrame*>(ws + kTilesScratchOffset);
+      cargs.mask = reinterpret_cast<uint32_t*>(ws + kTilesScratchOffset + kCoopMaxFrames * sizeof(CoopFrame));
+      cargs.lists = reinterpret_cast<uint4*>(ws + L.coop);
+      cargs.tiles = coop_tiles(batch, n_max, lc.coop_tiles);
+      cargs.cap = kCoopCap;
+      cudaLaunchConfig_t clc = {};
+      clc.gridDim = dim3((unsigned)(batch * cargs.tiles));
+      clc.blockDim = dim3(kCoopThreads);
+      clc.dynamicSmemBytes = 0;
+      clc.stream = st;
+      cudaLaunchAttribute cattr[1];
+      cattr[0].id = cudaLaunchAttributeCooperative;
+      cattr[0].val.cooperative = 1;
+      clc.attrs = cattr;
+      clc.numAttrs = 1;
+      e = cudaLaunchKernelEx(&clc, tie_break == PNMS_TIE_BY_INDEX ? pnms_coop<true> : pnms_coop<false>, cargs);
+      if (e == cudaErrorCooperativeLaunchTooLarge) {
+        // fewer SMs than the device reports (MPS / green contexts): the tile path instead
+        (void)cudaGetLastError();
+        path = PNMS_PATH_TILES;
+        if (info) info->path = path;
+      } else if (e != cudaSuccess) {
+        return fail_cuda(e);
+      }
+    }
+    if (path == PNMS_PATH_COOP) {
+      // launched above
+    } else if (path == PNMS_PATH_BINNED || path == PNMS_PATH_BINNED_WIDE) {
       // ---- exact spatial culling, one CTA per frame (pnms_binned.cuh)
       ba.pairs_tested = g_pairs_counter;
       ba.meta = nullptr;  // the frame-level sort rewrites FrameMeta of declined frames
@@ -701,30 +735,6 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
         return fail_cuda(e);
       if ((e = launch_maybe_pdl(true, pnms_mask_compact, dim3((unsigned)batch), dim3(512), 0, st, ta)) != cudaSuccess)
         return fail_cuda(e);
-    } else if (path == PNMS_PATH_COOP) {
-      // ---- large single frames: one cooperative launch of T tile CTAs per frame (pnms_coop.cuh)
-      ba.pairs_tested = nullptr;
-      ba.meta = reinterpret_cast<FrameMeta*>(ws + L.meta);  // the chunked sort accumulates into it
-      CoopArgs cargs;
-      cargs.b = ba;
-      cargs.b.trace = g_trace;
-      cargs.scr = reinterpret_cast<CoopFrame*>(ws + kTilesScratchOffset);
-      cargs.mask = reinterpret_cast<uint32_t*>(ws + kTilesScratchOffset + kCoopMaxFrames * sizeof(CoopFrame));
-      cargs.lists = reinterpret_cast<uint4*>(ws + L.coop);
-      cargs.tiles = coop_tiles(batch, n_max, lc.coop_tiles);
-      cargs.cap = kCoopCap;
-      cudaLaunchConfig_t clc = {};
-      clc.gridDim = dim3((unsigned)(batch * cargs.tiles));
-      clc.blockDim = dim3(kCoopThreads);
-      clc.dynamicSmemBytes = 0;
-      clc.stream = st;
-      cudaLaunchAttribute cattr[1];
-      cattr[0].id = cudaLaunchAttributeCooperative;
-      cattr[0].val.cooperative = 1;
-      clc.attrs = cattr;
-      clc.numAttrs = 1;
-      e = cudaLaunchKernelEx(&clc, tie_break == PNMS_TIE_BY_INDEX ? pnms_coop<true> : pnms_coop<false>, cargs);
-      if (e != cudaSuccess) return fail_cuda(e);
     } else {
       // ---- large frames in batches: one thread-block cluster per frame (pnms_binned_cluster.cuh)
       ba.pairs_tested = nullptr;
