@@ -70,7 +70,9 @@ struct B2Layout {
   static_assert(NP % 256 == 0, "NP: a multiple of 256");
   static_assert(oComb % 16 == 0 && oBits % 16 == 0 && oSt % 16 == 0, "alignment");
 };
-inline size_t b2_smem_bytes(int np) { return np <= 2048 ? B2Layout<2048>::kBytes : B2Layout<4096>::kBytes; }
+inline size_t b2_smem_bytes(int np) {
+  return np <= 1024 ? B2Layout<1024>::kBytes : (np <= 2048 ? B2Layout<2048>::kBytes : B2Layout<4096>::kBytes);
+}
 
 // 16-bit counter increment through the u32 word holding it; returns the old count (counts
 // stay below 2^16, so the low half never carries into the high half)

@@ -304,8 +304,8 @@ cudaError_t launch_binned(int impl, int variant, const BinArgs& ba, int batch, i
     PNMS_B1(8, kBinThreads, 8)
 #undef PNMS_B1
   }
-  const size_t smem = b2_smem_bytes(npad);
-  static SmemCache c2[12];
+  const size_t smem = b2_smem_bytes(wide ? 2048 : npad);
+  static SmemCache c2[16];
 #define PNMS_B2(P, T, I)                                                                        \
   switch (variant & 3) {                                                                        \
     case 0: return launch_binned2_t<false, false, P, T>(ba, batch, smem, st, c2[I]);           \
@@ -314,6 +314,7 @@ cudaError_t launch_binned(int impl, int variant, const BinArgs& ba, int batch, i
     default: return launch_binned2_t<true, true, P, T>(ba, batch, smem, st, c2[I + 3]);        \
   }
   if (wide) { PNMS_B2(2, 1024, 0) }
+  if (n_max <= 2 * kBinThreads) { PNMS_B2(2, kBinThreads, 12) }  // frames of <= 1024 slots: half the layout
   if (n_max <= 4 * kBinThreads) { PNMS_B2(4, kBinThreads, 4) }
   PNMS_B2(4, 1024, 8)
 #undef PNMS_B2
