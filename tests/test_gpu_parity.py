@@ -1081,3 +1081,37 @@ def test_greedy_reach_edge_cases_vs_oracle(theta):
     for f in range(3):
         want = c_oracle.greedy_frame(x[f], y[f], z[f], s[f], int(counts[f]), theta)
         assert np.array_equal(ki[f, : kc[f]], want), (f, theta)
+
+
+@pytest.mark.parametrize("path", ["binned", "coop"])
+def test_culling_paths_degenerate_frames(path):
+    """The default culling kernels on degenerate frames: every score NaN, one valid slot,
+    empty frames, sides at the narrow7 limit (126), theta = 1 (only contained boxes suppress:
+    the reach shrinks to nothing on the left), all boxes identical, and exact-boundary areas —
+    vs the C oracle, both tie policies."""
+    rng = np.random.default_rng(11)
+    n = 5000 if path == "coop" else 1500
+    cases = []
+    x, y, z, s = random_frames(1, n, seed=1, frame_w=3000, frame_h=2000, z_range=(100, 126))
+    cases.append(("sides 100..126", x, y, z, s, n, 0.5))
+    x, y, z, s = random_frames(1, n, seed=2, frame_w=800, frame_h=600, z_range=(4, 60))
+    cases.append(("theta 1", x, y, z, s, n, 1.0))
+    s2 = s.copy(); s2[:] = np.nan
+    cases.append(("all NaN", x, y, z, s2, n, 0.5))
+    cases.append(("one slot", x, y, z, s, 1, 0.5))
+    cases.append(("empty", x, y, z, s, 0, 0.5))
+    xi, yi, zi = (np.full((1, n), v, np.int32) for v in (40, 50, 30))
+    si = rng.uniform(0.1, 1.0, (1, n))
+    cases.append(("identical boxes", xi, yi, zi, si, n, 0.5))
+    # exact boundaries: w*h == ceil(theta*(z+1)^2) for pairs of a 10-pixel box grid
+    xb = (np.arange(n) % 97 * 9).astype(np.int32).reshape(1, n)
+    yb = (np.arange(n) // 97 * 9).astype(np.int32).reshape(1, n)
+    zb = np.full((1, n), 9, np.int32)
+    cases.append(("boundary grid", xb, yb, zb, rng.uniform(0.1, 1.0, (1, n)), n, 0.09))
+    for tie in ("paper_faithful", "by_index"):
+        for name, x, y, z, s, cnt, theta in cases:
+            lc = LaunchConfig(path=path)
+            got = _run_batch(x, y, z, s, np.array([cnt], np.int32), theta, tie, n, launch=lc)
+            assert lc.path_taken == path, name
+            want = c_oracle.run_frame(x[0], y[0], z[0], s[0], cnt, n, theta, tie)
+            assert np.array_equal(got[0], want), (name, tie)
