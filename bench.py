@@ -615,9 +615,17 @@ def main():
         return max_over_ranks(e0.elapsed_time(e1))
 
     copy_ms, h2d_gbs = link_bound([hx, hy, hz, hs])
+    # the kernels write the keep indices and counts straight into the pinned host buffers
+    # (zero-copy over PCIe: no device->host copy competes with the input copies)
+    eng.zero_copy = True
     e2e_ms = e2e_time(lambda: eng.run_host(hx, hy, hz, hs, hc, out_count=oc, out_idx=oi, graph=True))
     e2e_value = FRAMES * args.steps / (e2e_ms / 1e3)
-    e2e_ok = bool(torch.equal(oc.to(dev), eng.keep_count) and torch.equal(oi[:4], eng.keep_idx[:4].cpu()))
+    kc_dev = eng.keep_count.cpu()  # the device-resident run of the same frames
+    ki_dev = eng.keep_idx[:: max(1, F // 64)].cpu()
+    e2e_ok = bool(torch.equal(oc, kc_dev) and all(
+        torch.equal(oi[f * max(1, F // 64), : int(oc[f * max(1, F // 64)])], ki_dev[f, : int(oc[f * max(1, F // 64)])])
+        for f in range(ki_dev.shape[0])))
+    e2e_d2h = int(oc.sum().item()) * 4 + F * 4
 
     # the compact ingest format (pack_box32: x | y<<12 | z<<24, 12 B per box with the score) and
     # survivor masks out, with the host-side packing cost measured separately
@@ -683,7 +691,7 @@ def main():
         map_d = statistics.mean(p[1] for p in ph_d) / 1e3
         achieved_d = ops / map_d / 1e12
         h2d_bytes = int(F * BOXES * 20 + F * 4)
-        d2h_bytes = int(F * BOXES * 4 + F * 4)
+        d2h_bytes = e2e_d2h
         call_ms = max_total_ms / args.steps
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
@@ -703,10 +711,11 @@ def main():
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d_bytes,
                     "d2h_bytes_per_step": d2h_bytes, "matches_device_run": e2e_ok,
                     "input_format": "the C ABI's int32 x, y, z + float64 s planes (20 B per box), pinned host",
-                    "output": "int32 keep indices [F, 2048] + counts [F], pinned host",
-                    "api": "NmsEngine.run_host(out_idx=..., graph=True)",
-                    "pipeline": f"{e2e_chunks} chunks over 2 streams (H2D, NMS, D2H of keep indices + counts), "
-                                "replayed as one CUDA graph",
+                    "output": "int32 keep indices [F, 2048] (first count valid) + counts [F], pinned host, "
+                              "written by the kernels through the unified address space (zero-copy)",
+                    "api": "NmsEngine.run_host(out_idx=..., graph=True) with zero_copy",
+                    "pipeline": f"{e2e_chunks} chunks over 2 streams (H2D of the planes, NMS writing the "
+                                "results into host memory), replayed as one CUDA graph",
                     "h2d_link_gbs": h2d_gbs, "link_bound_frames_per_s": world * F / (copy_ms / 1e3),
                     "frac_of_link_bound": e2e_value / (world * F / (copy_ms / 1e3)),
                     "link_bound_basis": "the step's input planes copied host->device alone (no compute), best of 5"},

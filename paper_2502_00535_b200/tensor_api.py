@@ -431,6 +431,7 @@ class NmsEngine:
                    for _ in range(min(2, self.chunks))]
         self.ws_full = torch.zeros(_lib.workspace_bytes(self.batch, self.n_max), dtype=torch.uint8, device=dev)
         self.streams = [torch.cuda.Stream(device=dev) for _ in range(min(2, self.chunks))]
+        self.zero_copy = False  # run_host(out_idx=pinned): let the kernels write the host buffers directly
         self._dev_in = None
         self._graphs: dict = {}
 
@@ -457,7 +458,10 @@ class NmsEngine:
         int16 planes (pixel coordinates < 32768, 14 B per box; widened on the device by
         pnms_widen_i16).  graph=True replays the whole pipeline (copies, kernels, read-back) as
         one CUDA graph captured on the first call for this set of host buffers, which must then
-        stay allocated and be refilled in place between calls."""
+        stay allocated and be refilled in place between calls.  With `engine.zero_copy = True`
+        and pinned int32 out_idx / out_count (no out_mask), the kernels write the indices and
+        counts straight into the host buffers through the unified address space (only the
+        first out_count[f] entries of a row are written) instead of a device->host copy."""
         if out_count is None:
             raise ValueError("out_count is required")
         dx, dy, dz, _, _ = self._device_inputs()
@@ -521,6 +525,12 @@ class NmsEngine:
     def _pipeline(self, stage, hs, hcounts, out_mask, out_count, out_idx=None):
         dx, dy, dz, ds, dc = self._device_inputs()
         cur = torch.cuda.current_stream(self.device)
+        # zero-copy results: pinned host index / count buffers are written by the kernel itself
+        # through the unified address space (no device->host copy competes with the input copies)
+        direct = (self.zero_copy and out_idx is not None and out_mask is None and not out_idx.is_cuda
+                  and out_idx.is_pinned() and out_count.is_pinned()
+                  and out_idx.dtype == torch.int32 and out_idx.is_contiguous() and out_count.is_contiguous())
+        lib = _lib.load() if direct else None
         for k, (a, b) in enumerate(self.bounds):
             st = self.streams[k % len(self.streams)]
             st.wait_stream(cur)
@@ -528,6 +538,14 @@ class NmsEngine:
                 stage(a, b, st)
                 ds[a:b].copy_(hs[a:b], non_blocking=True)
                 dc[a:b].copy_(hcounts[a:b], non_blocking=True)
+                if direct:
+                    ws = self.ws[k % len(self.ws)]
+                    rc = lib.pnms_run_ex(dx[a:b].data_ptr(), dy[a:b].data_ptr(), dz[a:b].data_ptr(), ds[a:b].data_ptr(),
+                                         dc[a:b].data_ptr(), b - a, self.n_max, self.d_max, self.theta,
+                                         _TIE[self.tie_break], out_idx[a:b].data_ptr(), out_count[a:b].data_ptr(),
+                                         None, None, ws.data_ptr(), ws.numel(), st.cuda_stream, None, None, None)
+                    _lib.check(rc, "pnms_run_ex")
+                    continue
                 batched_nms_keep(dx[a:b], dy[a:b], dz[a:b], ds[a:b], dc[a:b], self.theta, self.tie_break,
                                  self.d_max, keep_idx=self.keep_idx[a:b] if out_idx is not None else None,
                                  keep_count=self.keep_count[a:b],

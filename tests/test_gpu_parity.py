@@ -666,17 +666,21 @@ def test_engine_run_host_int16_and_int32_agree():
         eng.run_host(hx, hy, hz, hs, hc, om, oc)
         torch.cuda.synchronize()
         assert torch.equal(om, ref_mask.cpu()) and torch.equal(oc, ref_cnt.cpu()), dt
-    # the reference layout end to end: int32 planes in, keep indices out, direct and replayed
+    # the reference layout end to end: int32 planes in, keep indices out, direct and replayed,
+    # copied back or written by the kernels themselves (zero-copy)
     hx, hy, hz = (torch.from_numpy(a).pin_memory() for a in (x, y, z))
     oi = torch.full((37, 500), -1, dtype=torch.int32).pin_memory()
-    for graph in (False, True, True):
-        oi.fill_(-1); oc.zero_()
-        eng.run_host(hx, hy, hz, hs, hc, out_count=oc, out_idx=oi, graph=graph)
-        torch.cuda.synchronize()
-        assert torch.equal(oc, ref_cnt.cpu())
-        for f in range(0, 37, 6):
-            want = c_oracle.run_frame(x[f], y[f], z[f], s[f], 500, 500, 0.5)
-            assert np.array_equal(oi[f, : int(oc[f])].numpy(), want), (graph, f)
+    for zero_copy in (False, True):
+        eng.zero_copy = zero_copy
+        for graph in (False, True, True):
+            oi.fill_(-1); oc.zero_()
+            eng.run_host(hx, hy, hz, hs, hc, out_count=oc, out_idx=oi, graph=graph)
+            torch.cuda.synchronize()
+            assert torch.equal(oc, ref_cnt.cpu())
+            for f in range(0, 37, 6):
+                want = c_oracle.run_frame(x[f], y[f], z[f], s[f], 500, 500, 0.5)
+                assert np.array_equal(oi[f, : int(oc[f])].numpy(), want), (zero_copy, graph, f)
+    eng.zero_copy = False
     # packed 32-bit boxes (x | y<<12 | z<<24), 12 B per box with the score
     from paper_2502_00535_b200 import pack_box32
 
