@@ -33,7 +33,7 @@ constexpr int kClCells = 2048;        // cells a CTA's band may hold
 constexpr int kClMaxSlice = 4096;     // input slots per CTA (register stash: 8 per thread)
 
 struct __align__(16) ClStats {
-  int mode, minz, maxz, minx, miny, maxx, maxy, big, n_act, over, pad_[6];
+  int mode, minz, maxz, minx, miny, maxx, maxy, big, n_act, over, maxL, minW, pad_[4];
   uint32_t total[16];                 // per-CTA survivor counts (compaction prefix)
 };
 
@@ -139,10 +139,17 @@ __global__ void __launch_bounds__(kClThreads, 1) pnms_binned_cluster(BinArgs a, 
   const int slice_words = slice / 32;
   unsigned long long* trace = a.trace;  // diagnostics: phase timestamps (pnms_debug_trace)
 
+  // T_z | wmin_z << 16 (pnms_binned2.cuh): the theta reach of a suppressing column
+  __shared__ uint32_t Tz[128];
+  if (threadIdx.x < 128) {
+    const int zv = threadIdx.x;
+    const uint32_t T = zv == 0 ? 0u : (uint32_t)ceil(ref_threshold(a.theta, zv));
+    Tz[zv] = T | (((T + zv) / (uint32_t)(zv + 1)) << 16);
+  }
   if (threadIdx.x == 0) {
     st->mode = kNarrow7; st->minz = 0x7FFFFFFF; st->maxz = 0;
     st->minx = st->miny = 0x7FFFFFFF; st->maxx = st->maxy = -0x7FFFFFFF;
-    st->big = 0; st->n_act = 0; st->over = 0;
+    st->big = 0; st->n_act = 0; st->over = 0; st->maxL = 0; st->minW = 0x7FFFFFFF;
   }
   for (int w = threadIdx.x; w < slice_words; w += kClThreads) kbits[w] = 0u;
   for (int c = threadIdx.x; c < kClCells + 4; c += kClThreads) cstart[c] = 0u;
@@ -151,7 +158,7 @@ __global__ void __launch_bounds__(kClThreads, 1) pnms_binned_cluster(BinArgs a, 
   // ---- pass 1: own input slice, once from HBM; statistics into CTA 0
   uint32_t xy[PER], zc[PER];
   {
-    int mode = kNarrow7, minz = 0x7FFFFFFF, maxz = 0, n_act = 0;
+    int mode = kNarrow7, minz = 0x7FFFFFFF, maxz = 0, n_act = 0, maxL = 0, minW = 0x7FFFFFFF;
     int minx = 0x7FFFFFFF, miny = 0x7FFFFFFF, maxx = -0x7FFFFFFF, maxy = -0x7FFFFFFF;
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
@@ -168,6 +175,8 @@ __global__ void __launch_bounds__(kClThreads, 1) pnms_binned_cluster(BinArgs a, 
           minz = min(minz, zv); maxz = max(maxz, zv);
           minx = min(minx, xv); maxx = max(maxx, xv);
           miny = min(miny, yv); maxy = max(maxy, yv);
+          const uint32_t tw = Tz[zv & 127];
+          maxL = max(maxL, zv + 1 - (int)(tw >> 16)); minW = min(minW, (int)(tw >> 16));
           xy[k] = ((uint32_t)xv & 0xFFFFu) | ((uint32_t)yv << 16);
           zc[k] = (uint32_t)zv & 0xFFu;
         } else {
@@ -181,7 +190,9 @@ __global__ void __launch_bounds__(kClThreads, 1) pnms_binned_cluster(BinArgs a, 
     n_act = __reduce_add_sync(0xFFFFFFFFu, n_act);
     minx = __reduce_min_sync(0xFFFFFFFFu, minx); maxx = __reduce_max_sync(0xFFFFFFFFu, maxx);
     miny = __reduce_min_sync(0xFFFFFFFFu, miny); maxy = __reduce_max_sync(0xFFFFFFFFu, maxy);
+    maxL = __reduce_max_sync(0xFFFFFFFFu, maxL); minW = __reduce_min_sync(0xFFFFFFFFu, minW);
     if ((threadIdx.x & 31) == 0) {
+      atomicMax(&st0->maxL, maxL); atomicMin(&st0->minW, minW);
       atomicMax(&st0->mode, mode); atomicMin(&st0->minz, minz); atomicMax(&st0->maxz, maxz);
       atomicAdd(&st0->n_act, n_act);
       atomicMin(&st0->minx, minx); atomicMax(&st0->maxx, maxx);
@@ -198,10 +209,12 @@ __global__ void __launch_bounds__(kClThreads, 1) pnms_binned_cluster(BinArgs a, 
     if (r == 0 && threadIdx.x == 0) binned_decline(a, f);
     return;
   }
-  // ---- cells Sy >= max side + 1 tall (a row reaches one cell row beyond its own band) and
-  // Sx = Sy / 4 wide (the x reach is range-based: narrow cells tighten it, pnms_binned.cuh),
-  // cell rows split into CS balanced bands
-  int Sy = max(g_maxz + 1, kMinCellSide), Sx = max(Sy >> 2, kMinCellSide), GX = 1, GY = 1;
+  // ---- the theta reach (pnms_binned2.cuh): a column that can suppress row i has its corner in
+  // [x_i - L, x_i + z_i + 1 - R] x [y_i - L, y_i + z_i + 1 - R].  Cells taller than either
+  // vertical reach (a row reaches one cell row beyond its own band) and Sy / 4 wide, cell rows
+  // split into CS balanced bands
+  const int g_L = n_act > 0 ? st0->maxL : 0, g_R = n_act > 0 ? st0->minW : 1;
+  int Sy = max(max(g_L, g_maxz + 1 - g_R) + 1, kMinCellSide), Sx = max(Sy >> 2, kMinCellSide), GX = 1, GY = 1;
   if (n_act > 0) {
     for (;;) {
       GX = (g_maxx - ox) / Sx + 1;
@@ -367,8 +380,8 @@ __global__ void __launch_bounds__(kClThreads, 1) pnms_binned_cluster(BinArgs a, 
     const RecBin ri = recS[p];
     const int32_t ix = -(int32_t)(int16_t)(ri.nb & 0xFFFFu), iy = -(int32_t)(int16_t)(ri.nb >> 16);
     const int32_t iz = (int32_t)(ri.w & 0xFF) - 1;
-    const int cx0 = qdiv(max(ix - g_maxz - ox, 0), Mx), cy0 = qdiv(max(iy - g_maxz - oy, 0), My);
-    const int cx1 = min(GX - 1, qdiv(ix + iz - ox, Mx)), cy1 = min(GY - 1, qdiv(iy + iz - oy, My));
+    const int cx0 = qdiv(max(ix - g_L - ox, 0), Mx), cy0 = qdiv(max(iy - g_L - oy, 0), My);
+    const int cx1 = min(GX - 1, qdiv(ix + iz + 1 - g_R - ox, Mx)), cy1 = min(GY - 1, qdiv(iy + iz + 1 - g_R - oy, My));
     bool sup;
     if (ext_ok) {
       sup = cluster_row_scan<BY_INDEX>(ri, p + own_off, cx0, cx1, cy0, cy1, [&](int yy) { return (yy - R0) * GX; },
