@@ -65,7 +65,7 @@ struct BinArgs {
 };
 
 struct __align__(16) BinStats {
-  int mode, minz, maxz, minx, miny, maxx, maxy, big, n_act, pad_;
+  int mode, minz, maxz, minx, miny, maxx, maxy, big, n_act, maxL, minW;  // (maxL/minW: tile kernel)
 };
 
 __host__ __device__ inline int binned_max_cells(int npad) {

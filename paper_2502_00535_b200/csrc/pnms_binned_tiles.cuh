@@ -66,8 +66,15 @@ __global__ void __launch_bounds__(kTileThreads, 1) pnms_binned_tiles(TileArgs ta
   if (threadIdx.x == 0) {
     st->mode = kNarrow7; st->minz = 0x7FFFFFFF; st->maxz = 0;
     st->minx = st->miny = 0x7FFFFFFF; st->maxx = st->maxy = -0x7FFFFFFF;
-    st->big = 0; st->n_act = 0;
+    st->big = 0; st->n_act = 0; st->maxL = 0; st->minW = 0x7FFFFFFF;
     s_n = 0; s_big = 0;
+  }
+  // T_z | wmin_z << 16 (pnms_binned2.cuh): the theta reach of a suppressing column
+  __shared__ uint32_t Tz[128];
+  if (threadIdx.x < 128) {
+    const int zv = threadIdx.x;
+    const uint32_t T = zv == 0 ? 0u : (uint32_t)ceil(ref_threshold(a.theta, zv));
+    Tz[zv] = T | (((T + zv) / (uint32_t)(zv + 1)) << 16);
   }
   for (int c = threadIdx.x; c < kTileCells + 4; c += kTileThreads) cstart[c] = 0u;
   __syncthreads();
@@ -75,7 +82,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) pnms_binned_tiles(TileArgs ta
   // frame is streamed from L2 by every CTA: 16 B vector loads, several in flight per thread.
   const bool vec = ((fbase & 3) == 0) && ((((uintptr_t)a.x) | ((uintptr_t)a.y) | ((uintptr_t)a.z) | ((uintptr_t)a.s)) & 15) == 0;
   {
-    int mode = kNarrow7, minz = 0x7FFFFFFF, maxz = 0, n_act = 0;
+    int mode = kNarrow7, minz = 0x7FFFFFFF, maxz = 0, n_act = 0, maxL = 0, minW = 0x7FFFFFFF;
     int minx = 0x7FFFFFFF, miny = 0x7FFFFFFF, maxx = -0x7FFFFFFF, maxy = -0x7FFFFFFF;
     auto visit = [&](int e, int32_t xv, int32_t yv, int32_t zv, double sv) {
       mode = max(mode, frame_mode_of(xv, yv, zv));
@@ -84,6 +91,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) pnms_binned_tiles(TileArgs ta
         minz = min(minz, zv); maxz = max(maxz, zv);
         minx = min(minx, xv); maxx = max(maxx, xv);
         miny = min(miny, yv); maxy = max(maxy, yv);
+        const uint32_t tw = Tz[zv & 127];
+        maxL = max(maxL, zv + 1 - (int)(tw >> 16)); minW = min(minW, (int)(tw >> 16));
       } else if (t == 0) {
         atomicOr(ta.mask + (long long)f * a.W32 + (e >> 5), 1u << (e & 31));  // NaN: survivor
       }
@@ -111,11 +120,13 @@ __global__ void __launch_bounds__(kTileThreads, 1) pnms_binned_tiles(TileArgs ta
     mode = __reduce_max_sync(0xFFFFFFFFu, mode);
     minz = __reduce_min_sync(0xFFFFFFFFu, minz);
     maxz = __reduce_max_sync(0xFFFFFFFFu, maxz);
+    maxL = __reduce_max_sync(0xFFFFFFFFu, maxL); minW = __reduce_min_sync(0xFFFFFFFFu, minW);
     n_act = __reduce_add_sync(0xFFFFFFFFu, n_act);
     minx = __reduce_min_sync(0xFFFFFFFFu, minx); maxx = __reduce_max_sync(0xFFFFFFFFu, maxx);
     miny = __reduce_min_sync(0xFFFFFFFFu, miny); maxy = __reduce_max_sync(0xFFFFFFFFu, maxy);
     if ((threadIdx.x & 31) == 0) {
       atomicMax(&st->mode, mode); atomicMin(&st->minz, minz); atomicMax(&st->maxz, maxz);
+      atomicMax(&st->maxL, maxL); atomicMin(&st->minW, minW);
       atomicAdd(&st->n_act, n_act);
       atomicMin(&st->minx, minx); atomicMax(&st->maxx, maxx);
       atomicMin(&st->miny, miny); atomicMax(&st->maxy, maxy);
@@ -132,10 +143,15 @@ __global__ void __launch_bounds__(kTileThreads, 1) pnms_binned_tiles(TileArgs ta
   if (n_act == 0) return;
   // ---- cells Sy = max_z + 1 tall and Sx = Sy / 4 wide (as pnms_binned.cuh: fewer runs per
   // row, tight x ranges) and a tile layout of at most kTilesPerFrame tiles, square in pixels
-  const int Sy = max(st->maxz + 1, kMinCellSide), Sx = max(Sy >> 2, kMinCellSide), ox = st->minx, oy = st->miny;
+  // the theta reach (pnms_binned2.cuh): a suppressing column's corner lies within
+  // [x - L, x + z + 1 - R] (same for y); cells taller than either vertical reach (a one-row halo)
+  const int g_L = st->maxL, g_R = st->minW;
+  const int Sy = max(max(g_L, st->maxz + 1 - g_R) + 1, kMinCellSide), Sx = max(Sy >> 2, kMinCellSide);
+  const int ox = st->minx, oy = st->miny;
   const uint32_t Mx = div_magic(Sx), My = div_magic(Sy);
   const int GX = (st->maxx - ox) / Sx + 1, GY = (st->maxy - oy) / Sy + 1;
-  const int hx = (st->maxz + Sx - 1) / Sx;  // halo columns: a row reaches max_z pixels either way
+  // halo columns: a row reaches L pixels left and z + 1 - R right
+  const int hxl = (g_L + Sx - 1) / Sx, hxr = (st->maxz + 1 - g_R + Sx - 1) / Sx;
   int TX = (int)sqrtf((float)kTilesPerFrame * (float)(GX * Sx) / (float)(GY * Sy) + 0.5f);
   TX = max(1, min(TX, min(GX, kTilesPerFrame)));
   int TY = max(1, min(GY, kTilesPerFrame / TX));
@@ -144,7 +160,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) pnms_binned_tiles(TileArgs ta
   TY = (GY + th - 1) / th;
   if (t >= TX * TY) return;
   const int tx = t % TX, ty = t / TX;
-  const int cx0 = max(tx * tw - hx, 0), cx1 = min((tx + 1) * tw - 1 + hx, GX - 1);  // region incl. halo
+  const int cx0 = max(tx * tw - hxl, 0), cx1 = min((tx + 1) * tw - 1 + hxr, GX - 1);  // region incl. halo
   const int cy0 = max(ty * th - 1, 0), cy1 = min((ty + 1) * th, GY - 1);
   const int ix0 = tx * tw, ix1 = min((tx + 1) * tw, GX) - 1;              // interior (own rows)
   const int iy0 = ty * th, iy1 = min((ty + 1) * th, GY) - 1;
@@ -258,7 +274,6 @@ __global__ void __launch_bounds__(kTileThreads, 1) pnms_binned_tiles(TileArgs ta
   __syncthreads();
   PNMS_TILE_TRACE(4);
   // ---- rows of the interior cells against their reachable cells (all inside the region)
-  const int maxz = st->maxz;
   const bool pad_rule = a.d_max > cnt;
   const int nl = (int)cstart[lcells];
   const uint32_t rbase = static_cast<uint32_t>(__cvta_generic_to_shared(recS));
@@ -270,8 +285,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) pnms_binned_tiles(TileArgs ta
     const uint32_t zzi = __byte_perm((uint32_t)ri.w, 0u, 0x4040);
     const int32_t ix = -(int32_t)(int16_t)(ri.nb & 0xFFFFu), iy = -(int32_t)(int16_t)(ri.nb >> 16);
     const int32_t iz = (int32_t)(ri.w & 0xFF) - 1;
-    const int rx0 = max(qdiv(max(ix - maxz - ox, 0), Mx), cx0), ry0 = max(qdiv(max(iy - maxz - oy, 0), My), cy0);
-    const int rx1 = min(cx1, qdiv(ix + iz - ox, Mx)), ry1 = min(cy1, qdiv(iy + iz - oy, My));
+    const int rx0 = max(qdiv(max(ix - g_L - ox, 0), Mx), cx0), ry0 = max(qdiv(max(iy - g_L - oy, 0), My), cy0);
+    const int rx1 = min(cx1, qdiv(ix + iz + 1 - g_R - ox, Mx)), ry1 = min(cy1, qdiv(iy + iz + 1 - g_R - oy, My));
     const uint32_t pb = rbase + (uint32_t)p * (uint32_t)sizeof(RecBin);
     bool sup = false;
     unsigned long long tested = 0;
