@@ -369,19 +369,10 @@ def nms_keep(boxes: torch.Tensor, scores: torch.Tensor, theta: float = 0.5,
     b = boxes if boxes.dtype is torch.int32 else boxes.to(torch.int32)
     planes = b.t().contiguous()  # [3, N]: the x, y, z planes of one frame
     sc = scores if scores.dtype is torch.float64 and scores.is_contiguous() else scores.to(torch.float64).contiguous()
-    key = (planes.device.index, _raw_stream(planes.device), n)  # per stream: calls on two streams never share
-    bufs = _KEEP_BUFS.get(key)
-    if bufs is None:
-        bufs = (torch.empty((1, n), dtype=torch.int32, device=planes.device),
-                torch.empty((1,), dtype=torch.int32, device=planes.device))
-        _KEEP_BUFS[key] = bufs
     idx, cnt = batched_nms_keep(planes[0:1], planes[1:2], planes[2:3], sc.reshape(1, n), None, theta, tie_break,
-                                d_max if d_max is not None else n, keep_idx=bufs[0], keep_count=bufs[1])
+                                d_max if d_max is not None else n)
     k = int(cnt.item())
     return idx[0, :k].to(torch.int64)
-
-
-_KEEP_BUFS: dict = {}  # nms_keep's per-(device, stream, n) device outputs (the result is a fresh copy)
 
 
 BOX32_MAX_XY = 4095
