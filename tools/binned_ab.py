@@ -25,6 +25,7 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 IMPLS = tuple(int(v) for v in sys.argv[2].split(",")) if len(sys.argv) > 2 else (0, 1)
 for name, B, n, theta, tie, impls in (("C5", 8192, 2048, 0.5, "paper_faithful", IMPLS),
                                       ("C4", 256, 1024, 0.5, "paper_faithful", IMPLS),
+                                      ("8192x1024", 8192, 1024, 0.5, "paper_faithful", IMPLS),
                                       ("C5-by_index-t0.3", 2048, 2048, 0.3, "by_index", IMPLS),
                                       ("C5-t0.7", 2048, 2048, 0.7, "paper_faithful", IMPLS)):
     planes = random_frames(B, n, seed=5, duplicate_fraction=0.05 if "by_index" in name else 0.0)
