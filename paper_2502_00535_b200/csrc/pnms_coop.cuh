@@ -378,45 +378,50 @@ __global__ void __launch_bounds__(kCoopThreads) pnms_coop(CoopArgs ca) {
   coop_barrier(&cf->barrier, 3u * T);
   PNMS_COOP_TRACE(6);
 
-  // ---- phase 3: compaction of this CTA's mask words (or the decline), then the cleanup
-  if (threadIdx.x == 0) hdr[12] = __ldcg(&cf->overflow);
-  __syncthreads();
-  const bool declined = !eligible || (n_act > 0 && hdr[12] != 0u);
-  if (declined) {
-    if (r == 0 && threadIdx.x == 0) binned_decline(a, f);
-  } else {
-    const int wpc = (a.W32 + T - 1) / T;
-    const int w0 = min(r * wpc, a.W32), w1 = min(w0 + wpc, a.W32);
-    uint32_t before = 0;
-    for (int w = threadIdx.x; w < w0; w += kCoopThreads) before += __popc(__ldcg(&mask[w]));
-    before = __reduce_add_sync(0xFFFFFFFFu, before);
-    if (lane == 0) scan_tmp[threadIdx.x >> 5] = before;
-    __syncthreads();
-    uint32_t off = 0;
-    for (int k = 0; k < NW; ++k) off += scan_tmp[k];
-    for (int base = w0 * 32; base < w1 * 32; base += kCoopThreads) {
-      // one slot per thread: 8 words per round, each word's offset from the words before it
-      const int sl = base + (int)threadIdx.x;
-      const int w = sl >> 5;
-      const uint32_t bits = w < w1 ? __ldcg(&mask[w]) : 0u;
-      const uint32_t pc = __popc(bits);
-      // exclusive prefix over the round's words (word index within the round = warp)
-      if (lane == 0) scan_tmp[16 + (threadIdx.x >> 5)] = pc;
-      __syncthreads();
-      uint32_t woff = off;
-      for (int k = 0; k < (int)(threadIdx.x >> 5); ++k) woff += scan_tmp[16 + k];
-      uint32_t round_total = 0;
-      for (int k = 0; k < NW; ++k) round_total += scan_tmp[16 + k];
-      if (w < w1 && ((bits >> lane) & 1u) && a.keep_idx) a.keep_idx[fbase + woff + __popc(bits & lanemask_lt())] = sl;
-      if (w < w1 && lane == 0 && a.keep_mask) a.keep_mask[(long long)f * a.W32 + w] = bits;
-      off += round_total;
-      __syncthreads();
+  // ---- phase 3: compaction of this CTA's mask words (or the decline), then the cleanup.  One
+  // L2 round trip: every thread loads its run of mask words (and thread 0 the overflow flag),
+  // one block scan of their popcounts gives every word's offset; the words of this CTA's chunk
+  // are published in shared memory and written out one slot per thread
+  {
+    constexpr int kMaxWpt = PNMS_MAX_SLOTS / 32 / kCoopThreads;
+    const int W32 = a.W32;
+    const int wpt = (W32 + kCoopThreads - 1) / kCoopThreads;
+    const int wb = (int)threadIdx.x * wpt;
+    uint32_t wv[kMaxWpt];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int i = 0; i < kMaxWpt; ++i) {
+      wv[i] = (i < wpt && wb + i < W32) ? __ldcg(&mask[wb + i]) : 0u;
+      sum += __popc(wv[i]);
     }
-    if (w1 == a.W32 && w0 < w1 && threadIdx.x == 0) {
-      if (a.keep_count) a.keep_count[f] = (int32_t)off;
+    if (threadIdx.x == 0) hdr[12] = __ldcg(&cf->overflow);
+    uint32_t total;
+    uint32_t off = block_exclusive_scan(sum, scan_tmp, &total);  // (its barriers publish hdr[12])
+    const bool declined = !eligible || (n_act > 0 && hdr[12] != 0u);
+    if (declined) {
+      if (r == 0 && threadIdx.x == 0) binned_decline(a, f);
+    } else {
+      __shared__ uint32_t s_cw[64], s_co[64];
+      const int wpc = (W32 + T - 1) / T;  // <= 32: T >= n / kCoopCap (coop_tiles)
+      const int w0 = min(r * wpc, W32), w1 = min(w0 + wpc, W32);
+#pragma unroll
+      for (int i = 0; i < kMaxWpt; ++i) {
+        const int w = wb + i;
+        if (i < wpt && w >= w0 && w < w1 && w - w0 < 64) { s_cw[w - w0] = wv[i]; s_co[w - w0] = off; }
+        off += __popc(wv[i]);
+      }
+      __syncthreads();
+      for (int sl = w0 * 32 + (int)threadIdx.x; sl < w1 * 32; sl += kCoopThreads) {
+        const int wi = (sl >> 5) - w0;
+        const uint32_t bits = s_cw[wi];
+        if (((bits >> lane) & 1u) && a.keep_idx) a.keep_idx[fbase + s_co[wi] + __popc(bits & lanemask_lt())] = sl;
+        if (lane == 0 && a.keep_mask) a.keep_mask[(long long)f * W32 + (sl >> 5)] = bits;
+      }
+      if (r == 0 && threadIdx.x == 0) {
+        if (a.keep_count) a.keep_count[f] = (int32_t)total;
+        a.fallback[f] = 0;
+      }
     }
-    if (a.W32 == 0 && r == 0 && threadIdx.x == 0 && a.keep_count) a.keep_count[f] = 0;
-    if (r == 0 && threadIdx.x == 0) a.fallback[f] = 0;
   }
   // the last CTA of the frame re-zeroes its scratch (every CTA has read the mask by now)
   __syncthreads();
