@@ -446,9 +446,10 @@ static_assert(kDeclCountOffset + 4 <= kSmallScratchBytes, "scratch");
 // the tile path's decline flags and survivor masks, re-zeroed by pnms_mask_compact
 constexpr size_t kTilesScratchOffset = 32 * 1024;
 static_assert(kDeclCountOffset + 4 <= kTilesScratchOffset, "scratch");
-// the cooperative path's frame scratch and survivor masks (frames of up to PNMS_MAX_SLOTS)
-static_assert(kTilesScratchOffset + kCoopMaxFrames * (sizeof(CoopFrame) + PNMS_MAX_SLOTS / 8) <= kSmallScratchBytes,
-              "scratch");
+// the cooperative path's frame scratch and its double-buffered survivor masks (frames of up to
+// PNMS_MAX_SLOTS): a region of its own, since a cooperative call leaves it non-zero
+constexpr size_t kCoopScratchOffset = 64 * 1024;
+static_assert(kCoopScratchOffset + kCoopScratchBytes <= kSmallScratchBytes, "scratch");
 
 template <int R>
 cudaError_t launch_map(const MapArgs& ma, long long grid, size_t smem, cudaStream_t st, bool list) {
@@ -611,7 +612,7 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
   // one-CTA dispatcher behind a declining kernel (pnms_fallback.cuh): snapshots the declined
   // count into `snap`, zeroes it and, when frames were declined, tail-launches the dense chain
   // over them; `*host_chain` is set when the host must launch the chain itself (profiled calls)
-  auto dispatch_fallback = [&](const int32_t* list, int* count, int* snap, bool* host_chain) -> cudaError_t {
+  auto make_plan = [&](const int32_t* list, const int* snap) {
     FallbackPlan plan{};
     chain_args(0, batch, ws + L.dense, list, snap, plan.pa, plan.ma, plan.ca);
     plan.chunked = n_max > kSortMax;
@@ -619,6 +620,10 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     plan.sort_smem = (int)(plan.chunked ? sort_smem_bytes(kSortMax) : sort_frame_smem_bytes(plan.pa.npad));
     plan.map_smem = (int)map_smem;
     plan.compact_smem = (int)compact_smem;
+    return plan;
+  };
+  auto dispatch_fallback = [&](const int32_t* list, int* count, int* snap, bool* host_chain) -> cudaError_t {
+    FallbackPlan plan = make_plan(list, snap);
 #ifdef PNMS_NO_DEVCHAIN  // diagnostic build without the relocatable unit (sanitizer tools)
     plan.enabled = 0;
 #else
@@ -676,11 +681,12 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
       CoopArgs cargs;
       cargs.b = ba;
       cargs.b.trace = g_trace;
-      cargs.scr = reinterpret_cast<CoopFrame*>(ws + kTilesScratchOffset);
-      cargs.mask = reinterpret_cast<uint32_t*>(ws + kTilesScratchOffset + kCoopMaxFrames * sizeof(CoopFrame));
+      cargs.scr = reinterpret_cast<CoopFrame*>(ws + kCoopScratchOffset);
+      cargs.mask = reinterpret_cast<uint32_t*>(ws + kCoopScratchOffset + kCoopMaxFrames * sizeof(CoopFrame));
       cargs.lists = reinterpret_cast<uint4*>(ws + L.coop);
       cargs.tiles = coop_tiles(batch, n_max, lc.coop_tiles);
       cargs.cap = kCoopCap;
+      cargs.count_fallback = lc.declined != nullptr;
       cudaLaunchConfig_t clc = {};
       clc.gridDim = dim3((unsigned)(batch * cargs.tiles));
       clc.blockDim = dim3(kCoopThreads);
@@ -722,7 +728,7 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
       // them) when they fit — the latency case, <= 2 frames — else zeroed per call
       const size_t fbytes = ((size_t)batch * 4 + 15) / 16 * 16;
       const size_t tbytes = fbytes + (size_t)batch * W32 * 4;
-      const bool in_scratch = kTilesScratchOffset + tbytes <= kSmallScratchBytes;
+      const bool in_scratch = kTilesScratchOffset + tbytes <= kCoopScratchOffset;
       uint8_t* tbase = in_scratch ? ws + kTilesScratchOffset : (L.tiles ? ws + L.tiles : ws + L.rec);
       ta.decline = reinterpret_cast<int*>(tbase);
       ta.mask = reinterpret_cast<uint32_t*>(tbase + fbytes);
@@ -748,6 +754,19 @@ int run_impl(const int32_t* x, const int32_t* y, const int32_t* z, const double*
     decl_list = ba.decl_list;
     int* snap = reinterpret_cast<int*>(ws + L.list);
     bool host_chain = false;
+    if (path == PNMS_PATH_COOP) {
+      // the cooperative kernel finishes the frames it declines itself (no fallback chain);
+      // the count of those frames, when the caller asks for it, through the snapshot kernel
+      if (lc.declined) {
+        int* snap = reinterpret_cast<int*>(ws + L.list);
+        if ((e = launch_maybe_pdl(true, pnms_count_snapshot, dim3(1), dim3(32), 0, st, ba.decl_count, snap, batch)) !=
+                cudaSuccess ||
+            (e = cudaMemcpyAsync(lc.declined, snap, sizeof(int32_t), cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+          return fail_cuda(e);
+      }
+      if ((e = mark(events, 3, st)) != cudaSuccess) return fail_cuda(e);
+      return finish();
+    }
     if ((e = dispatch_fallback(ba.decl_list, ba.decl_count, snap, &host_chain)) != cudaSuccess) return fail_cuda(e);
     if (!host_chain) {
       if ((e = mark(events, 3, st)) != cudaSuccess) return fail_cuda(e);

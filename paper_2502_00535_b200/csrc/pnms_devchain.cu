@@ -60,3 +60,4 @@ cudaError_t pnms_devchain_dispatch(const void* plan, int* decl_count, int* count
   return cudaLaunchKernelEx(&lc, pnms_dc::pnms_fallback_dispatch, *static_cast<const pnms_dc::FallbackPlan*>(plan),
                             decl_count, count_snap);
 }
+

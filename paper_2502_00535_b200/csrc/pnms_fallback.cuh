@@ -35,17 +35,8 @@ struct FallbackPlan {
 };
 
 #ifdef PNMS_DEVICE_CHAIN  // relocatable unit only (pnms_devchain.cu)
-// One CTA, launched programmatically right after the binned kernel: waits for it, snapshots
-// and zeroes the declined-frame count, and tail-launches the chain sized to it.  It must not
-// trigger its own dependents (griddepcontrol.launch_dependents in a grid that tail-launches
-// keeps the tail launch from ever starting — measured on B200).
-__global__ void __launch_bounds__(32) pnms_fallback_dispatch(FallbackPlan plan, int* decl_count, int* count_snap) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // the binned grid is complete and flushed
-  if (threadIdx.x != 0) return;
-  const int c = min(max(*decl_count, 0), plan.pa.batch);  // a workspace that was not zeroed
-  *decl_count = 0;                                          // cannot send the chain out of range
-  *count_snap = c;
-  if (c == 0 || !plan.enabled) return;
+// the chain over c declined frames (plan's list), as tail launches of the calling grid
+__device__ __forceinline__ void launch_fallback_chain(const FallbackPlan& plan, int c) {
   if (plan.chunked) {
     const long long chunks = (long long)c * plan.pa.nchunks;
     pnms_prep_sort_chunk<<<(int)min(chunks, 148LL * 2), kSortThreads, plan.sort_smem, cudaStreamTailLaunch>>>(plan.pa);
@@ -65,6 +56,20 @@ __global__ void __launch_bounds__(32) pnms_fallback_dispatch(FallbackPlan plan, 
   // a chain that could not be launched would leave the declined frames without output: fail
   // loudly (the stream reports the fault at the caller's next synchronisation)
   if (cudaGetLastError() != cudaSuccess) __trap();
+}
+
+// One CTA, launched programmatically right after the binned kernel: waits for it, snapshots
+// and zeroes the declined-frame count, and tail-launches the chain sized to it.  It must not
+// trigger its own dependents (griddepcontrol.launch_dependents in a grid that tail-launches
+// keeps the tail launch from ever starting — measured on B200).
+__global__ void __launch_bounds__(32) pnms_fallback_dispatch(FallbackPlan plan, int* decl_count, int* count_snap) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the binned grid is complete and flushed
+  if (threadIdx.x != 0) return;
+  const int c = min(max(*decl_count, 0), plan.pa.batch);  // a workspace that was not zeroed
+  *decl_count = 0;                                          // cannot send the chain out of range
+  *count_snap = c;
+  if (c == 0 || !plan.enabled) return;
+  launch_fallback_chain(plan, c);
 }
 #endif
 

@@ -28,7 +28,7 @@ constexpr int kSmallRowsMax = 4;       // rows per thread (1 for the tiniest cal
 // by every call): suppression words, per-frame tickets and gate accumulators.
 constexpr int kSmallMaxWords = 4096;
 constexpr int kSmallMaxFrames = 1024;
-constexpr size_t kSmallScratchBytes = 64 * 1024;  // small path words + binned/tiles counters and masks
+constexpr size_t kSmallScratchBytes = 128 * 1024;  // small path words + binned/tiles counters and masks
 static_assert(kSmallMaxWords * 4 + kSmallMaxFrames * 4 + kSmallMaxFrames * 8 <= kSmallScratchBytes, "scratch");
 
 struct SmallArgs {

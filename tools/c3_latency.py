@@ -17,7 +17,7 @@ for _ in range(5):
 torch.cuda.synchronize()
 assert np.array_equal(ki[0, : int(kc.item())].cpu().numpy(), g["C3_keep"])
 ts = []
-for _ in range(30):
+for _ in range(int(os.environ.get("ITERS", "200"))):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda._sleep(200_000)  # GPU busy while the host enqueues: the events see device time only
     e0.record()
@@ -25,4 +25,4 @@ for _ in range(30):
     e1.record()
     e1.synchronize()
     ts.append(e0.elapsed_time(e1) * 1e3)
-print(f"C3 device latency median {np.median(ts):.1f} us, min {np.min(ts):.1f} us")
+print(f"C3 device latency median {np.median(ts):.1f} us, min {np.min(ts):.1f} us, p10 {np.percentile(ts, 10):.1f}, p90 {np.percentile(ts, 90):.1f}")

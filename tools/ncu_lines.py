@@ -59,7 +59,10 @@ for k, r in enumerate(data):
 tot, ts = sum(agg.values()), sum(samp.values())
 print(f"warp instructions {tot}, avg active lanes {sum(thr.values()) / max(tot, 1):.1f}")
 src = {p.name: p.read_text().splitlines() for p in (ROOT / "paper_2502_00535_b200" / "csrc").glob("*.cuh")}
-for loc, n in agg.most_common(top):
+import os
+order = samp.most_common(top) if os.environ.get("BY_SAMPLES") else agg.most_common(top)
+for loc, _ in order:
+    n = agg[loc]
     line = src.get(loc[0], [""] * 99999)[loc[1] - 1].strip()[:78] if loc and loc[0] in src else ""
     print(f"{100 * n / tot:5.1f}% inst {100 * samp[loc] / max(ts, 1):5.1f}% samp lanes {thr[loc] / max(n, 1):4.1f} "
           f"{loc[0] if loc else '?'}:{loc[1] if loc else 0}  {line}")
