@@ -4,28 +4,32 @@
 // 128 CTAs twice).
 //
 //   phase 0  CTA r reads its slice of the frame once: statistics into the frame's global
-//            accumulators (shared-memory reduction, one atomic per field per CTA); NaN rows
-//            are survivors (their mask bits are set here)
+//            accumulators (shared-memory reduction, one atomic per field per CTA)
 //   barrier
 //   phase 1  every CTA derives the same parameters (eligibility, the theta reach L / R of
 //            pnms_binned2.cuh, cells, a tile layout of T tiles with halos covering the reach)
 //            and appends each box of its slice to the list of every tile whose region (tile
-//            plus halo) holds the box's cell: one 16 B entry {x|y<<16, z|dead<<7|slot<<16, key}
+//            plus halo) holds the box's cell: one 16 B entry {x|y<<16, z|dead<<7|slot<<16, key};
+//            NaN rows of the slice are survivors (their mask bits)
 //   barrier
-//   phase 2  CTA r owns tile r: its region's entries into shared memory, a counting sort into
-//            the region's cells, 16 B records plus the 64-bit keys at the cell positions, and
-//            the rows of the tile's interior scanned against their windows with the
-//            reference's gate on the full keys (engine.py:233-235; the input slot breaks
-//            by_index ties); survivor bits into the frame's global mask
+//   phase 2  CTA r owns tile r: its region's entries into shared memory (the first 256 loaded
+//            with the list's count), a counting sort into the region's cells, 16 B records
+//            plus the 64-bit keys at the cell positions, and the rows of the tile's interior
+//            scanned against their windows with the reference's gate on the full keys
+//            (engine.py:233-235; the input slot breaks by_index ties); survivor bits into the
+//            frame's global mask
 //   barrier
 //   phase 3  CTA r compacts mask words [r*wpc, (r+1)*wpc) into ascending keep indices (its
-//            offset = popcount of the words before it); the last CTA to finish re-zeroes the
-//            frame's scratch for the next call
+//            offset = popcount of the words before it), then clears the scratch the next call
+//            needs zero (stores only: no cleanup round trip, see CoopFrame)
 //
 // Exactness is that of pnms_binned2.cuh: every column that can clear row i's bit lies in i's
 // window, the window of an interior row lies inside the tile's region, and the gate compares
-// the frame's own 64-bit keys.  A frame is declined (dense pipeline, through the device-side
-// list) if it is not eligible or a tile region exceeds kCoopCap boxes.
+// the frame's own 64-bit keys.  A frame the culling cannot take (not narrow7, a T = 0 column,
+// a tile region over kCoopCap boxes or kCoopCells cells) is finished inside the kernel by an
+// exact O(n^2 / T)-per-CTA pass after barrier 3 (coop_exact_slice) and one more barrier — no
+// dispatcher or fallback chain runs behind the kernel, which is what a call of this path
+// costs on the device: the one launch.
 #pragma once
 #include "../../include/parnms_b200.h"
 #include "pnms_binned2.cuh"
@@ -37,19 +41,11 @@ constexpr int kCoopCap = 1024;          // region entries a tile CTA holds
 constexpr int kCoopCells = 2048;        // region cells a tile CTA holds
 constexpr int kCoopMaxFrames = 2;       // frames per call (latency path)
 constexpr int kCoopMaxTiles = 512;
-constexpr int kCoopBoxesPerTile = 128;
-#ifndef PNMS_COOP_UNROLL
-#define PNMS_COOP_UNROLL 2
-#endif
-#ifndef PNMS_COOP_GMIN
-#define PNMS_COOP_GMIN 1
-#endif
-constexpr int kCoopUnroll = PNMS_COOP_UNROLL;  // items per step of a row's walk
-constexpr int kCoopGMin = PNMS_COOP_GMIN;      // threads per row at least
-#ifndef PNMS_COOP_SPEC
-#define PNMS_COOP_SPEC 256
-#endif
-constexpr int kCoopSpecLoad = PNMS_COOP_SPEC;  // list entries loaded with the tile's count  // default tile count: one tile per this many slots
+constexpr int kCoopBoxesPerTile = 128;  // default tile count: one tile per this many slots
+// items per step of a row's walk (measured: 2 and 4 alike, 1 slower; more threads per row
+// slower — the per-row setup, not the candidate loop, sets the walk's time)
+constexpr int kCoopUnroll = 2;
+constexpr int kCoopSpecLoad = 256;  // list entries loaded with the tile's count
 
 constexpr int kCoopMaskWords = PNMS_MAX_SLOTS / 32;  // survivor words of one frame
 
@@ -64,7 +60,9 @@ struct CoopFrame {
   uint32_t mode, nminz, maxz, nminx, nminy, maxx, maxy, n_act;  // ox(v) = v ^ 2^31: signed order
   uint32_t maxL, nminW, pad0, pad1;
   unsigned long long bar;  // barrier arrivals, kCoopCallStride per call (coop_barrier)
+  unsigned long long bar4; // arrivals at the fourth barrier (declined frames only), T per such call
   uint32_t overflow[2];    // by call parity
+  uint32_t pad2[2];
   uint32_t tile_cnt[kCoopMaxTiles];
 };
 static_assert(sizeof(CoopFrame) % 16 == 0, "CoopFrame layout");
@@ -96,8 +94,9 @@ __device__ __forceinline__ void coop_barrier(unsigned long long* bar, unsigned l
                                              unsigned long long target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, add);
+    // release: the CTA's writes (ordered before thread 0 by the CTA barrier) become visible
+    // to every CTA that acquires the count
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" :: "l"(bar), "l"(add) : "memory");
     unsigned long long v;
     do {
       asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
@@ -121,7 +120,7 @@ __device__ __forceinline__ double key_to_double(uint64_t sk) {
 // bits of the slice are rewritten in `mask`.  Shared memory (the kernel's, free in phase 3):
 // sA 16 KB (column records, row keys), sB 16 KB (row geometry), sK 8 KB (column keys, row state).
 template <bool BY_INDEX>
-__device__ __noinline__ void coop_exact_slice(const BinArgs& a, int f, int s0, int s1, bool pad_rule, uint32_t* mask,
+__device__ __forceinline__ void coop_exact_slice(const BinArgs& a, int f, int s0, int s1, bool pad_rule, uint32_t* mask,
                                               uint32_t* sA, uint32_t* sB, uint64_t* sK) {
   static_assert(kCoopThreads * sizeof(RecWide) + kCoopCap * 8 <= kCoopCap * sizeof(RecBin), "sA");
   static_assert(kCoopThreads * 8 + kCoopCap * 4 <= kCoopCap * 8, "sK");
@@ -235,8 +234,9 @@ __global__ void __launch_bounds__(kCoopThreads) pnms_coop(CoopArgs ca) {
   if (threadIdx.x < kB2RowClasses) rowhist[threadIdx.x] = 0u;
   __syncthreads();
   // this call's barrier base and parity (coop_barrier), loaded under phase 0
-  __shared__ unsigned long long s_base;
-  const unsigned long long bar0 = threadIdx.x == 0 ? __ldcg(&cf->bar) : 0ull;
+  __shared__ unsigned long long s_base, s_base4;
+  ulonglong2 bar0 = make_ulonglong2(0ull, 0ull);
+  if (threadIdx.x == 0) bar0 = __ldcg(reinterpret_cast<const ulonglong2*>(&cf->bar));
 
   // ---- phase 0: this CTA's slice (kept in `ent` as list entries for phase 1; NaN rows get
   // z = 0x7F, never a valid narrow7 side); statistics; NaN rows are survivors
@@ -268,7 +268,10 @@ __global__ void __launch_bounds__(kCoopThreads) pnms_coop(CoopArgs ca) {
         v[9] = max(v[9], ~sgn_key((int)(tw >> 16)));
       }
     }
-    if (threadIdx.x == 0) s_base = bar0 & ~(kCoopCallStride - 1);
+    if (threadIdx.x == 0) {
+      s_base = bar0.x & ~(kCoopCallStride - 1);
+      s_base4 = bar0.y;  // exact: no CTA passes barrier 3 before this one reaches barrier 1
+    }
 #pragma unroll
     for (int i = 0; i < 12; ++i) {
       const uint32_t w = i == 7 ? __reduce_add_sync(0xFFFFFFFFu, v[i]) : __reduce_max_sync(0xFFFFFFFFu, v[i]);
@@ -500,7 +503,7 @@ __global__ void __launch_bounds__(kCoopThreads) pnms_coop(CoopArgs ca) {
       // (independent loads; an index past the run's end is clamped to its last record — an
       // extra test of a window record cannot change the row's outcome)
       const int nr = (int)rowhist[0];
-      const int G = nr <= kCoopThreads / 8 ? 8 : nr <= kCoopThreads / 4 ? 4 : nr <= kCoopThreads / 2 || kCoopGMin > 1 ? 2 : 1;
+            const int G = nr <= kCoopThreads / 8 ? 8 : nr <= kCoopThreads / 4 ? 4 : nr <= kCoopThreads / 2 ? 2 : 1;
       const int g = (int)threadIdx.x & (G - 1);
       const uint32_t rbase = static_cast<uint32_t>(__cvta_generic_to_shared(recS));
       for (int o = (int)threadIdx.x / G; o < nr; o += kCoopThreads / G) {
@@ -546,7 +549,7 @@ __global__ void __launch_bounds__(kCoopThreads) pnms_coop(CoopArgs ca) {
     }
   }
   PNMS_COOP_TRACE(5);
-  coop_barrier(&cf->bar, 1ull, bbase + 3ull * (unsigned long long)T);
+  coop_barrier(&cf->bar, r == 0 ? 1ull + kCoopCallStride - 3ull * (unsigned long long)T : 1ull, bbase + kCoopCallStride);
   PNMS_COOP_TRACE(6);
 
   // ---- phase 3: compaction of this CTA's mask words.  One L2 round trip: every thread loads
@@ -576,7 +579,7 @@ __global__ void __launch_bounds__(kCoopThreads) pnms_coop(CoopArgs ca) {
       coop_exact_slice<BY_INDEX>(a, f, s0, s1, pad_rule, mask, reinterpret_cast<uint32_t*>(recS),
                                  reinterpret_cast<uint32_t*>(ent), keyR);
       if (ca.count_fallback && r == 0 && threadIdx.x == 0) atomicAdd(a.decl_count, 1);
-      coop_barrier(&cf->bar, 1ull, bbase + 4ull * (unsigned long long)T);
+      coop_barrier(&cf->bar4, 1ull, s_base4 + (unsigned long long)T);
       sum = 0;
 #pragma unroll
       for (int i = 0; i < kMaxWpt; ++i) {
@@ -617,10 +620,6 @@ __global__ void __launch_bounds__(kCoopThreads) pnms_coop(CoopArgs ca) {
     for (int w = r * ch + (int)threadIdx.x; w < w1; w += kCoopThreads) omask[w] = 0u;
     if (r == 0 && threadIdx.x == 0) cf->overflow[par ^ 1] = 0u;
   }
-  // the call's remaining share of the counter (every CTA is past its last barrier's wait once
-  // CTA 0 is past it, and the next call reads the counter only after this grid)
-  if (r == 0 && threadIdx.x == 0)
-    atomicAdd(&cf->bar, kCoopCallStride - (declined ? 4ull : 3ull) * (unsigned long long)T);
   PNMS_COOP_TRACE(7);
 #undef PNMS_COOP_TRACE
 }
