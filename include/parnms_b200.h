@@ -55,7 +55,8 @@ typedef enum pnms_status {
  * Replaces the reference's per-call SuppressionMatrix.all_ones allocation
  * (engine.py:93-96, 187).  The workspace starts with a small persistent scratch region that
  * must be zero before the first call (allocate zeroed, or call pnms_workspace_init once);
- * every call leaves it zero again, so a workspace is reused across calls with no clearing. */
+ * every call leaves it valid for the next one, so a workspace is reused across calls with no
+ * clearing. */
 int pnms_workspace_bytes(int batch, int n_max, size_t* out_bytes);
 
 /* Zero the persistent scratch region of a workspace (stream-ordered). */
