@@ -819,6 +819,65 @@ def test_one_workspace_across_paths_and_shapes():
     assert int(ws[: 64 * 1024].count_nonzero().item()) == 0
 
 
+def test_coop_scratch_protocol_across_calls():
+    """The cooperative path keeps state in its workspace region between calls (a monotone
+    barrier counter per frame slot, survivor masks and overflow flags double-buffered by call
+    parity, a fourth-barrier counter for frames finished in-kernel): a long sequence on ONE
+    workspace — tile counts T from 16 to 512 (n from 3000 to 65536), one and two frames per
+    call, frames the culling cannot take (theta = 0, a side over 126, a crowd over a tile's
+    capacity) between culled ones, other paths interleaved on the same head, and a CUDA graph
+    replayed several times — every call against the oracle."""
+    from paper_2502_00535_b200 import _lib
+
+    ws = torch.zeros(_lib.workspace_bytes(2, 65536), dtype=torch.uint8, device=DEV)
+    tt = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)  # noqa: E731
+    rng = np.random.default_rng(17)
+    seq = [(1, 5000, 0.5, None), (2, 9000, 0.5, None), (1, 16384, 0.0, None), (1, 3000, 0.5, None),
+           (2, 6000, 0.5, "z200"), (1, 65536, 0.5, None), (1, 5000, 0.5, "crowd"), (2, 12000, 0.45, None),
+           (1, 700, 0.5, "small"), (1, 20000, 0.5, None), (2, 9000, 0.5, "binned"), (1, 16384, 0.5, None)]
+    for step, (B, n, theta, mut) in enumerate(seq):
+        fw = 8000 if n > 20000 else 3840
+        x, y, z, s = random_frames(B, n, seed=int(rng.integers(1 << 30)), frame_w=fw, frame_h=2160)
+        if mut == "z200":
+            z[B - 1, 11] = 200
+        if mut == "crowd":
+            x[0, :1500] = 77; y[0, :1500] = 88
+        path = "coop" if mut not in ("small", "binned") else mut
+        if path == "binned" and n > 2048:
+            path = "tiles"
+        counts = np.array([n - 13 * f for f in range(B)], np.int32)
+        for tie in ("paper_faithful", "by_index"):
+            lc = LaunchConfig(path=path)
+            ki, kc = batched_nms_keep(tt(x), tt(y), tt(z), tt(s), tt(counts), theta, tie, n, workspace=ws, launch=lc)
+            assert lc.path_taken == path, (step, lc.path_taken)
+            ki, kc = ki.cpu().numpy(), kc.cpu().numpy()
+            for f in range(B):
+                want = c_oracle.run_frame(x[f], y[f], z[f], s[f], int(counts[f]), n, theta, tie)
+                assert np.array_equal(ki[f, : kc[f]], want), (step, B, n, theta, mut, tie, f)
+    # a captured call replayed: each replay is a new call of the protocol
+    x, y, z, s = random_frames(1, 8000, seed=3, frame_w=3840, frame_h=2160)
+    want = c_oracle.run_frame(x[0], y[0], z[0], s[0], 8000, 8000, 0.5, "paper_faithful")
+    dx, dy, dz, ds = tt(x), tt(y), tt(z), tt(s)
+    ki = torch.empty((1, 8000), dtype=torch.int32, device=DEV)
+    kc = torch.empty((1,), dtype=torch.int32, device=DEV)
+    lc = LaunchConfig(path="coop")
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):
+        batched_nms_keep(dx, dy, dz, ds, None, 0.5, keep_idx=ki, keep_count=kc, workspace=ws, launch=lc)
+    torch.cuda.current_stream().wait_stream(st)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        batched_nms_keep(dx, dy, dz, ds, None, 0.5, keep_idx=ki, keep_count=kc, workspace=ws, launch=lc)
+    for rep in range(5):
+        ki.fill_(-1)
+        graph.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(ki[0, : int(kc.item())].cpu().numpy(), want), rep
+    # the head shared with the other paths is left zero
+    assert int(ws[: 64 * 1024].count_nonzero().item()) == 0
+
+
 def test_unpack_box32_extremes():
     """pnms_unpack_box32 round-trips the packable domain edges, ragged lengths included."""
     from paper_2502_00535_b200 import _lib, pack_box32

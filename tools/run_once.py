@@ -3,6 +3,7 @@ captures and launch lists).
 
     python tools/run_once.py {c1|c2|c3|c4|c5} [path] [binned_impl]
 """
+import os
 import sys
 from pathlib import Path
 
@@ -24,7 +25,7 @@ else:
     B, n = (256, 1024) if cfg == "c4" else (8192, 2048)
     arrs = random_frames(B, n, seed=5)
 x, y, z, s = (torch.from_numpy(a).cuda() for a in arrs)
-for _ in range(3):
+for _ in range(int(os.environ.get("ITERS", "3"))):
     lc = LaunchConfig(path=path, binned_impl=impl)
     batched_nms_keep(x, y, z, s, None, 0.5, launch=lc)
 torch.cuda.synchronize()
