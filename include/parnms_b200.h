@@ -222,6 +222,15 @@ int pnms_widen_i16(const int16_t* x16, const int16_t* y16, const int16_t* z16, i
  * planes pnms_run consumes.  n = number of slots. */
 int pnms_unpack_box32(const uint32_t* box, int32_t* x, int32_t* y, int32_t* z, long long n, void* stream);
 
+/* Compact ingest, host side: box[i] = x[i] | y[i] << 12 | z[i] << 24 for HOST int32 planes
+ * (the C ABI's own layout), on `threads` host threads (<= 0: every core), so a caller holding
+ * the reference's int32 columns (engine.py:191-193) ships 4 B of geometry per box instead of 12
+ * and the device unpacks them (pnms_unpack_box32).  *packable = 1 when every value is inside
+ * the packable domain (x, y in [0, 4095], z in [0, 255]), else 0 — then `box` is not valid and
+ * the caller sends the int32 planes.  No CUDA call; safe without a GPU. */
+int pnms_pack_box32_host(const int32_t* x, const int32_t* y, const int32_t* z, long long n, uint32_t* box,
+                         int threads, int* packable);
+
 /* Diagnostics: device counter (uint64) that the binned path atomically increments by the
  * number of pair tests it executes; NULL disables (default).  Process-wide, not reentrant. */
 int pnms_debug_count_pairs(uint64_t* device_counter);

@@ -31,6 +31,7 @@ EXPORTED_SYMBOLS = (
     "pnms_soft_rescore_ws",
     "pnms_widen_i16",
     "pnms_unpack_box32",
+    "pnms_pack_box32_host",
     "pnms_debug_count_pairs",
     "pnms_debug_exp",
     "pnms_debug_trace",
@@ -129,6 +130,8 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
     lib.pnms_widen_i16.restype = i32
     lib.pnms_unpack_box32.argtypes = [vp, vp, vp, vp, ctypes.c_longlong, vp]
     lib.pnms_unpack_box32.restype = i32
+    lib.pnms_pack_box32_host.argtypes = [vp, vp, vp, ctypes.c_longlong, vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+    lib.pnms_pack_box32_host.restype = i32
     lib.pnms_debug_trace.argtypes = [vp]
     lib.pnms_debug_trace.restype = i32
     lib.pnms_debug_exp.argtypes = [vp, vp, ctypes.c_longlong, vp]

@@ -21,7 +21,7 @@ NOCDP_PATH = PKG_DIR / "build_tmp" / "libparnms_b200_nocdp.so"  # diagnostics on
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC,-O2",
+    "-Xcompiler", "-fPIC,-O2,-fopenmp",
     "-Xptxas", "-O3",
     "-cudart", "static",
     "--expt-relaxed-constexpr",
@@ -65,9 +65,9 @@ def build(force: bool = False, verbose: bool = False, extra: list[str] | None = 
     ]
     links = [
         [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static", "-shared",
-         "-o", str(LIB_PATH) + ".tmp", str(tmp / "capi.o"), str(tmp / "devchain.o"), "-lcudadevrt"],
+         "-o", str(LIB_PATH) + ".tmp", str(tmp / "capi.o"), str(tmp / "devchain.o"), "-lcudadevrt", "-lgomp"],
         [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static", "-shared",
-         "-o", str(NOCDP_PATH), str(tmp / "capi_nocdp.o")],
+         "-o", str(NOCDP_PATH), str(tmp / "capi_nocdp.o"), "-lgomp"],
     ]
     if verbose:
         for cmd in compiles + links:

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstring>
 #include <utility>
+#include <omp.h>
 
 #include "../../include/parnms_b200.h"
 #include "pnms_common.cuh"
@@ -978,6 +979,21 @@ int pnms_unpack_box32(const uint32_t* box, int32_t* x, int32_t* y, int32_t* z, l
   pnms_unpack_box32_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(box, x, y, z, n);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? PNMS_OK : fail_cuda(e);
+}
+
+int pnms_pack_box32_host(const int32_t* x, const int32_t* y, const int32_t* z, long long n, uint32_t* box,
+                         int threads, int* packable) {
+  if (!packable || n < 0 || (n > 0 && (!x || !y || !z || !box))) return PNMS_EINVAL_ARG;
+  int bad = 0;
+  // one streaming pass over 16 B per box (12 read, 4 written): memory-bound, so every core
+#pragma omp parallel for schedule(static) reduction(| : bad) num_threads(threads > 0 ? threads : omp_get_num_procs())
+  for (long long i = 0; i < n; ++i) {
+    const uint32_t xv = (uint32_t)x[i], yv = (uint32_t)y[i], zv = (uint32_t)z[i];
+    bad |= (int)((xv > 4095u) | (yv > 4095u) | (zv > 255u));
+    box[i] = xv | (yv << 12) | (zv << 24);
+  }
+  *packable = bad ? 0 : 1;
+  return PNMS_OK;
 }
 
 int pnms_debug_exp(const double* x, double* y, long long n, void* stream) {

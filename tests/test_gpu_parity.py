@@ -680,6 +680,29 @@ def test_engine_run_host_int16_and_int32_agree():
             for f in range(0, 37, 6):
                 want = c_oracle.run_frame(x[f], y[f], z[f], s[f], 500, 500, 0.5)
                 assert np.array_equal(oi[f, : int(oc[f])].numpy(), want), (zero_copy, graph, f)
+    # the boxes packed on the host inside the call (every core), chunk by chunk; a chunk with
+    # a coordinate outside the packable domain travels as its int32 planes
+    for zero_copy in (False, True):
+        eng.zero_copy = zero_copy
+        for rep in range(2):
+            oi.fill_(-1); oc.zero_()
+            eng.run_host(hx, hy, hz, hs, hc, out_count=oc, out_idx=oi, host_pack=True)
+            torch.cuda.synchronize()
+            assert eng.last_packed_rows == 37 and torch.equal(oc, ref_cnt.cpu())
+            for f in range(0, 37, 6):
+                want = c_oracle.run_frame(x[f], y[f], z[f], s[f], 500, 500, 0.5)
+                assert np.array_equal(oi[f, : int(oc[f])].numpy(), want), (zero_copy, rep, f)
+    xw = x.copy(); xw[20, 3] = 5000  # frame 20's chunk is not packable
+    hxw = torch.from_numpy(xw).pin_memory()
+    oi.fill_(-1); oc.zero_()
+    eng.run_host(hxw, hy, hz, hs, hc, out_count=oc, out_idx=oi, host_pack=True)
+    torch.cuda.synchronize()
+    assert eng.last_packed_rows < 37
+    for f in range(37):
+        want = c_oracle.run_frame(xw[f], y[f], z[f], s[f], 500, 500, 0.5)
+        assert np.array_equal(oi[f, : int(oc[f])].numpy(), want), f
+    with pytest.raises(ValueError):
+        eng.run_host(hx, hy, hz, hs, hc, out_count=oc, out_idx=oi, host_pack=True, graph=True)
     eng.zero_copy = False
     # packed 32-bit boxes (x | y<<12 | z<<24), 12 B per box with the score
     from paper_2502_00535_b200 import pack_box32

@@ -139,3 +139,38 @@ def test_pack_box32_layout_and_domain():
     for bad in ((4096, 0, 0), (0, -1, 0), (0, 0, 256)):
         with pytest.raises(ValueError):
             pack_box32(*(np.array([v]) for v in bad))
+
+
+def test_pack_box32_host_matches_numpy_and_flags_the_domain():
+    """pnms_pack_box32_host (the C ABI's multi-threaded host packer, no GPU needed): the same
+    words as pack_box32 on the packable domain's edges and random planes, any thread count and
+    ragged lengths; packable = 0 for any value outside it."""
+    import ctypes
+
+    import numpy as np
+
+    from paper_2502_00535_b200 import _lib
+    from paper_2502_00535_b200.tensor_api import pack_box32
+
+    lib = _lib.load()
+    rng = np.random.default_rng(3)
+    ok = ctypes.c_int(-1)
+    for n in (0, 1, 31, 1000, 100003):
+        x = rng.integers(0, 4096, n).astype(np.int32)
+        y = rng.integers(0, 4096, n).astype(np.int32)
+        z = rng.integers(0, 256, n).astype(np.int32)
+        if n >= 3:
+            x[:3], y[:3], z[:3] = (0, 4095, 7), (0, 4095, 9), (0, 255, 1)
+        for threads in (0, 1, 3, 16):
+            out = np.full(n, -1, np.int32)
+            assert lib.pnms_pack_box32_host(x.ctypes.data, y.ctypes.data, z.ctypes.data, n, out.ctypes.data,
+                                            threads, ctypes.byref(ok)) == 0
+            assert ok.value == 1 and np.array_equal(out, pack_box32(x, y, z)), (n, threads)
+    x = np.zeros(64, np.int32); y = np.zeros(64, np.int32); z = np.ones(64, np.int32)
+    out = np.zeros(64, np.int32)
+    for arr, v in ((x, 4096), (y, -1), (z, 256), (x, -5), (z, -1)):
+        arr[37] = v
+        lib.pnms_pack_box32_host(x.ctypes.data, y.ctypes.data, z.ctypes.data, 64, out.ctypes.data, 4, ctypes.byref(ok))
+        assert ok.value == 0, v
+        arr[37] = 1 if arr is z else 0
+    assert lib.pnms_pack_box32_host(None, None, None, 5, None, 0, ctypes.byref(ok)) != 0
