@@ -618,6 +618,8 @@ def main():
     # the kernels write the keep indices and counts straight into the pinned host buffers
     # (zero-copy over PCIe: no device->host copy competes with the input copies)
     eng.zero_copy = True
+    # ranks on one host share its cores: each rank's host packer gets its share
+    eng.pack_threads = 0 if world == 1 else max(1, (os.cpu_count() or 1) // world)
     kc_dev = eng.keep_count.cpu()  # the device-resident run of the same frames
     ki_dev = eng.keep_idx[:: max(1, F // 64)].cpu()
 
@@ -731,6 +733,7 @@ def main():
                                     "(pnms_unpack_box32): 12 B per box on the wire; a chunk outside the "
                                     "packable domain travels as its int32 planes",
                     "packed_frames": packed_rows,
+                    "host_pack_threads": eng.pack_threads or (os.cpu_count() or 1),
                     "output": "int32 keep indices [F, 2048] (first count valid) + counts [F], pinned host, "
                               "written by the kernels through the unified address space (zero-copy)",
                     "api": "NmsEngine.run_host(out_idx=..., host_pack=True) with zero_copy",
