@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstring>
 #include <utility>
+#include <emmintrin.h>
 #include <omp.h>
 
 #include "../../include/parnms_b200.h"
@@ -985,9 +986,35 @@ int pnms_pack_box32_host(const int32_t* x, const int32_t* y, const int32_t* z, l
                          int threads, int* packable) {
   if (!packable || n < 0 || (n > 0 && (!x || !y || !z || !box))) return PNMS_EINVAL_ARG;
   int bad = 0;
-  // one streaming pass over 16 B per box (12 read, 4 written): memory-bound, so every core
-#pragma omp parallel for schedule(static) reduction(| : bad) num_threads(threads > 0 ? threads : omp_get_num_procs())
-  for (long long i = 0; i < n; ++i) {
+  // one streaming pass over 16 B per box (12 read, 4 written): memory-bound, so every core;
+  // four boxes per step with SSE2, the words written with non-temporal stores (no read for
+  // ownership of the output lines: the host memory bus is shared with the DMA reading them)
+  const long long head = std::min<long long>(n, (long long)((16 - (reinterpret_cast<uintptr_t>(box) & 15)) & 15) / 4);
+  const long long n4 = (n - head) / 4;
+  for (long long i = 0; i < head; ++i) {
+    const uint32_t xv = (uint32_t)x[i], yv = (uint32_t)y[i], zv = (uint32_t)z[i];
+    bad |= (int)((xv > 4095u) | (yv > 4095u) | (zv > 255u));
+    box[i] = xv | (yv << 12) | (zv << 24);
+  }
+#pragma omp parallel reduction(| : bad) num_threads(threads > 0 ? threads : omp_get_num_procs())
+  {
+#pragma omp for schedule(static) nowait
+  for (long long q = 0; q < n4; ++q) {
+    const long long i = head + 4 * q;
+    const __m128i xv = _mm_loadu_si128(reinterpret_cast<const __m128i*>(x + i));
+    const __m128i yv = _mm_loadu_si128(reinterpret_cast<const __m128i*>(y + i));
+    const __m128i zv = _mm_loadu_si128(reinterpret_cast<const __m128i*>(z + i));
+    // out of domain <=> any bit outside the field (as unsigned: negatives have the top bit)
+    const __m128i over = _mm_or_si128(_mm_or_si128(_mm_andnot_si128(_mm_set1_epi32(4095), xv),
+                                                   _mm_andnot_si128(_mm_set1_epi32(4095), yv)),
+                                      _mm_andnot_si128(_mm_set1_epi32(255), zv));
+    bad |= _mm_movemask_epi8(_mm_cmpeq_epi32(over, _mm_setzero_si128())) != 0xFFFF;
+    const __m128i w = _mm_or_si128(_mm_or_si128(xv, _mm_slli_epi32(yv, 12)), _mm_slli_epi32(zv, 24));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(box + i), w);
+  }
+  _mm_sfence();  // this thread's streaming stores are globally visible before the region ends
+  }
+  for (long long i = head + 4 * n4; i < n; ++i) {
     const uint32_t xv = (uint32_t)x[i], yv = (uint32_t)y[i], zv = (uint32_t)z[i];
     bad |= (int)((xv > 4095u) | (yv > 4095u) | (zv > 255u));
     box[i] = xv | (yv << 12) | (zv << 24);
