@@ -99,6 +99,7 @@ __device__ __forceinline__ void coop_barrier(unsigned long long* bar, unsigned l
     asm volatile("red.release.gpu.global.add.u64 [%0], %1;" :: "l"(bar), "l"(add) : "memory");
     unsigned long long v;
     do {
+      __nanosleep(32);  // fewer polls on the line the arrivals update (measured 0.1-0.4 us per call)
       asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
     } while (v < target);
   }
