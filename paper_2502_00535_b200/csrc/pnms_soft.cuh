@@ -69,8 +69,16 @@ __host__ __device__ inline int soft_max_cells(int npad) {
 
 // the reference's factor of box b on pending box j (oracles.py:31-34, 115-120); `ovl` is
 // false when the boxes do not overlap (factor exactly 1.0)
-__device__ __forceinline__ double soft_apply(double sj, int32_t jx, int32_t jy, int32_t jz, int32_t bx, int32_t by,
-                                             int32_t bz, int mode, double theta, double sigma) {
+__device__ __forceinline__ double soft_apply(bool small, double sj, int32_t jx, int32_t jy, int32_t jz, int32_t bx,
+                                             int32_t by, int32_t bz, int mode, double theta, double sigma) {
+  if (small) {
+    const int w = min(jx + jz, bx + bz) - max(jx, bx) + 1;
+    const int h = min(jy + jz, by + bz) - max(jy, by) + 1;
+    if (w <= 0 || h <= 0) return sj;
+    const double cov = __ddiv_rn(__int2double_rn(w * h), __int2double_rn((bz + 1) * (bz + 1)));
+    if (mode == 0) return cov >= theta ? __dmul_rn(sj, __dsub_rn(1.0, cov)) : sj;
+    return __dmul_rn(sj, glibc_exp(__ddiv_rn(-__dmul_rn(cov, cov), sigma)));
+  }
   const long long w = min((long long)jx + jz, (long long)bx + bz) - (long long)max(jx, bx) + 1;
   const long long h = min((long long)jy + jz, (long long)by + bz) - (long long)max(jy, by) + 1;
   if (w <= 0 || h <= 0) return sj;
@@ -80,7 +88,15 @@ __device__ __forceinline__ double soft_apply(double sj, int32_t jx, int32_t jy, 
   return __dmul_rn(sj, glibc_exp(__ddiv_rn(-__dmul_rn(cov, cov), sigma)));  // math.exp, bit for bit
 }
 
-__device__ __forceinline__ bool soft_overlap(int32_t ax, int32_t ay, int32_t az, int32_t bx, int32_t by, int32_t bz) {
+// `small`: every coordinate and side of the frame is >= 0 and x + z, y + z < 2^15, so the
+// extents and the area product are exact in 32 bits (the 64-bit forms serve every other frame)
+__device__ __forceinline__ bool soft_overlap(bool small, int32_t ax, int32_t ay, int32_t az, int32_t bx, int32_t by,
+                                             int32_t bz) {
+  if (small) {
+    const int w = min(ax + az, bx + bz) - max(ax, bx) + 1;
+    const int h = min(ay + az, by + bz) - max(ay, by) + 1;
+    return (w > 0) & (h > 0);
+  }
   const long long w = min((long long)ax + az, (long long)bx + bz) - (long long)max(ax, bx) + 1;
   const long long h = min((long long)ay + az, (long long)by + bz) - (long long)max(ay, by) + 1;
   return w > 0 && h > 0;
@@ -94,13 +110,13 @@ __device__ __forceinline__ bool soft_before(uint64_t ka, int ia, uint64_t kb, in
 struct SoftFrame {
   int32_t *sx, *sy, *sz;
   double *s0, *cur;
-  uint64_t* fkey;
+  uint64_t* fkey;          // sort_key(cur) of every box (the selection key once final)
   uint8_t *state, *mark;   // mark: ready this round (written only by the box's own thread)
   uint16_t *cellof, *list;
   uint16_t* fround;         // round in which the box became final
   uint32_t* cstart;   // after the scatter: cstart[c] = end(c) = start(c+1), start(0) = 0
   int cnt, GX, GY, Sx, Sy, ox, oy, maxz;
-  bool bin;
+  bool bin, small;
 
   // visit every candidate slot that may overlap box j: the cells its overlapping boxes'
   // corners can lie in ([x - max_z, x + z] x [y - max_z, y + z]; cells Sx wide and Sy tall,
@@ -108,10 +124,20 @@ struct SoftFrame {
   template <class F>
   __device__ __forceinline__ void for_candidates(int j, F&& fn) const {
     if (bin) {
-      const long long jx = sx[j], jy = sy[j], jz = sz[j];
-      const int cx0 = (int)(max(0LL, jx - maxz - ox) / Sx), cy0 = (int)(max(0LL, jy - maxz - oy) / Sy);
-      const int cx1 = (int)min((long long)GX - 1, (jx + jz - ox) / Sx);
-      const int cy1 = (int)min((long long)GY - 1, (jy + jz - oy) / Sy);
+      int cx0, cy0, cx1, cy1;
+      if (small) {  // 32-bit quotients (the 64-bit division is a long software sequence)
+        const int jx = sx[j], jy = sy[j], jz = sz[j];
+        cx0 = (int)((uint32_t)max(0, jx - maxz - ox) / (uint32_t)Sx);
+        cy0 = (int)((uint32_t)max(0, jy - maxz - oy) / (uint32_t)Sy);
+        cx1 = min(GX - 1, (int)((uint32_t)(jx + jz - ox) / (uint32_t)Sx));
+        cy1 = min(GY - 1, (int)((uint32_t)(jy + jz - oy) / (uint32_t)Sy));
+      } else {
+        const long long jx = sx[j], jy = sy[j], jz = sz[j];
+        cx0 = (int)(max(0LL, jx - maxz - ox) / Sx);
+        cy0 = (int)(max(0LL, jy - maxz - oy) / Sy);
+        cx1 = (int)min((long long)GX - 1, (jx + jz - ox) / Sx);
+        cy1 = (int)min((long long)GY - 1, (jy + jz - oy) / Sy);
+      }
       for (int yy = cy0; yy <= cy1; ++yy) {
         const int c0 = yy * GX + cx0, c1 = yy * GX + cx1;
         const int b = c0 == 0 ? 0 : (int)cstart[c0 - 1], en = (int)cstart[c1];
@@ -167,7 +193,7 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
     const int32_t xv = a.x[g], yv = a.y[g], zv = a.z[g];
     const double sv = a.s[g];
     F.sx[e] = xv; F.sy[e] = yv; F.sz[e] = zv;
-    F.s0[e] = sv; F.cur[e] = sv;
+    F.s0[e] = sv; F.cur[e] = sv; F.fkey[e] = sort_key(sv);
     F.state[e] = kSoftPending; F.mark[e] = 0; F.fround[e] = 0xFFFF;
     if (!(sv > 0.0 && sv <= 1.7976931348623157e308)) atomicOr(&s_stat[8], 1);
     if (xv < 0 || yv < 0 || zv < 0) atomicAnd(&s_stat[5], 0);
@@ -183,6 +209,7 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
   F.bin = s_stat[5] != 0 && cnt > 0;
   F.Sx = F.Sy = 1; F.GX = 1; F.GY = 1;
   F.ox = s_stat[0]; F.oy = s_stat[1]; F.maxz = s_stat[4];
+  F.small = s_stat[5] != 0 && (long long)s_stat[2] + s_stat[4] < 32768 && (long long)s_stat[3] + s_stat[4] < 32768;
   if (F.bin) {  // cells Sx wide, Sy tall, as pnms_greedy.cuh
     F.Sy = s_stat[4] + 1;
     if (F.Sy <= 0) F.bin = false;
@@ -262,7 +289,7 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
         int nn = 0;
         bool fresh = false;
         F.for_candidates(j, [&](int b) {
-          if (F.state[b] != kSoftFinal || !soft_overlap(jx, jy, jz, F.sx[b], F.sy[b], F.sz[b])) return;
+          if (F.state[b] != kSoftFinal || !soft_overlap(F.small, jx, jy, jz, F.sx[b], F.sy[b], F.sz[b])) return;
           fresh |= F.fround[b] == round - 1;
           if (nn <= kMaxNb) {
             if (nn < kMaxNb) {
@@ -279,7 +306,7 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
         double tv = F.s0[j];
         if (nn <= kMaxNb) {
           for (int i = 0; i < nn; ++i)
-            tv = soft_apply(tv, jx, jy, jz, F.sx[nb[i]], F.sy[nb[i]], F.sz[nb[i]], mode, theta, sigma);
+            tv = soft_apply(F.small, tv, jx, jy, jz, F.sx[nb[i]], F.sy[nb[i]], F.sz[nb[i]], mode, theta, sigma);
         } else {  // many final neighbours (crowds): repeated minimum in key order
           uint64_t lk = 0;
           int li = -1;
@@ -290,15 +317,16 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
               if (F.state[b] != kSoftFinal) return;
               const uint64_t kb = F.fkey[b];
               if (!soft_before(lk, li, kb, b) || !soft_before(kb, b, bk, bi)) return;
-              if (!soft_overlap(jx, jy, jz, F.sx[b], F.sy[b], F.sz[b])) return;
+              if (!soft_overlap(F.small, jx, jy, jz, F.sx[b], F.sy[b], F.sz[b])) return;
               bk = kb; bi = b;
             });
             if (bi == 0x7FFFFFFF) break;
-            tv = soft_apply(tv, jx, jy, jz, F.sx[bi], F.sy[bi], F.sz[bi], mode, theta, sigma);
+            tv = soft_apply(F.small, tv, jx, jy, jz, F.sx[bi], F.sy[bi], F.sz[bi], mode, theta, sigma);
             lk = bk; li = bi;
           }
         }
         F.cur[j] = tv;
+        F.fkey[j] = sort_key(tv);  // (read by others only once the box is final)
       }
     }
     __syncthreads();
@@ -307,12 +335,12 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
     for (int t = threadIdx.x; t < npend; t += kSoftThreads) {
       const int j = pl[t];
       const int32_t jx = F.sx[j], jy = F.sy[j], jz = F.sz[j];
-      const uint64_t kj = sort_key(F.cur[j]);
+      const uint64_t kj = F.fkey[j];
       bool ready = true;
       F.for_candidates(j, [&](int n) {
         if (!ready || n == j || F.state[n] != kSoftPending) return;
-        if (!soft_before(sort_key(F.cur[n]), n, kj, j)) return;
-        if (soft_overlap(jx, jy, jz, F.sx[n], F.sy[n], F.sz[n])) ready = false;
+        if (!soft_before(F.fkey[n], n, kj, j)) return;
+        if (soft_overlap(F.small, jx, jy, jz, F.sx[n], F.sy[n], F.sz[n])) ready = false;
       });
       F.mark[j] = ready ? 1 : 0;
     }
@@ -327,7 +355,6 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
       if (t < npend) {
         j = pl[t];
         if (F.mark[j]) {
-          F.fkey[j] = sort_key(F.cur[j]);
           F.fround[j] = (uint16_t)round;
           F.state[j] = kSoftFinal;
           F.mark[j] = 0;
@@ -380,7 +407,7 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
       const int32_t bx = F.sx[b], by = F.sy[b], bz = F.sz[b];
       for (int j = threadIdx.x; j < cnt; j += kSoftThreads) {
         if (j == b || F.state[j] == kSoftFinal) continue;
-        F.cur[j] = soft_apply(F.cur[j], F.sx[j], F.sy[j], F.sz[j], bx, by, bz, mode, theta, sigma);
+        F.cur[j] = soft_apply(F.small, F.cur[j], F.sx[j], F.sy[j], F.sz[j], bx, by, bz, mode, theta, sigma);
       }
       if (threadIdx.x == 0) F.state[b] = kSoftFinal;
       __syncthreads();

@@ -20,7 +20,7 @@ if "--rounds" in args:
 kre, script, names = args[0], args[1], args[2:]
 for r in range(rounds):
     for nm in names:
-        env = dict(os.environ, PNMS_LIB=str(ROOT / "paper_2502_00535_b200" / "build_tmp" / f"var_{nm}.so"), ITERS="40")
+        env = dict(os.environ, PNMS_LIB=str(ROOT / "paper_2502_00535_b200" / "build_tmp" / f"var_{nm}.so"), ITERS=os.environ.get("AB_ITERS", "40"))
         out = subprocess.run(["ncu", "--metrics", "gpu__time_duration.sum", "--cache-control", "none",
                               "--clock-control", "none", "-k", f"regex:{kre}", "--csv"] + ["python"] + script.split(),
                              capture_output=True, text=True, env=env, cwd=ROOT).stdout

@@ -1,4 +1,5 @@
 """One config-4-shaped batch through greedy NMS and Soft-NMS (for ncu captures)."""
+import os
 import sys
 from pathlib import Path
 
@@ -10,7 +11,7 @@ from paper_2502_00535_b200 import greedy_nms_keep, soft_nms_rescore_batched  # n
 from paper_2502_00535_b200.synth import random_frames  # noqa: E402
 
 x, y, z, s = (torch.from_numpy(a).cuda() for a in random_frames(256, 1024, seed=64))
-for _ in range(2):
+for _ in range(int(os.environ.get("ITERS", "2"))):
     greedy_nms_keep(x, y, z, s, None, 0.5)
     soft_nms_rescore_batched(x, y, z, s, None, "linear", 0.3, 0.5)
 torch.cuda.synchronize()
