@@ -68,6 +68,15 @@ __device__ __forceinline__ bool greedy_covers(int32_t cx, int32_t cy, int32_t cz
   return (unsigned long long)w * (unsigned long long)h >= T;
 }
 
+// the same in 32 bits, for frames whose x + z, y + z stay below 2^31 and whose sides are below
+// 2^16 - 1 (extents, product and T then all fit; every BASELINE frame)
+__device__ __forceinline__ bool greedy_covers32(int32_t cx, int32_t cy, int32_t cz, int32_t rx, int32_t ry, int32_t rz,
+                                                uint32_t T) {
+  const int w = min(cx + cz, rx + rz) - max(cx, rx) + 1;
+  const int h = min(cy + cz, ry + rz) - max(cy, ry) + 1;
+  return (w > 0) & (h > 0) && (uint32_t)w * (uint32_t)h >= T;
+}
+
 __device__ __forceinline__ unsigned long long greedy_threshold(double theta, int32_t z) {
   // Python: theta * ((z+1)*(z+1)) converts the exact integer area to float64, then multiplies
   const long long a = ((long long)z + 1) * ((long long)z + 1);
@@ -201,6 +210,10 @@ __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a
   __syncthreads();
   // After the scatter, cstart[c] == end(c) == start(c+1); start(0) = 0.
   const bool small = bin && s_small;
+  // 32-bit coverage tests (greedy_covers32): non-negative coordinates (bin), x + z and y + z
+  // below 2^31, sides below 2^16 - 1
+  const bool c32 = bin && (long long)s_stat[2] + s_stat[4] < 0x7FFFFFFFLL &&
+                   (long long)s_stat[3] + s_stat[4] < 0x7FFFFFFFLL && s_stat[4] < 65534;
   const uint32_t Mx = div_magic(Sx), My = div_magic(Sy);
   // ---- rounds over a compacted list of the undecided boxes; decisions go to dec[] and are
   // applied after a barrier (every box's slots are written only by its own thread)
@@ -241,7 +254,9 @@ __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a
             if (si == kRemoved) continue;
             const uint64_t ki = key[i];
             if (!(ki < kj || (ki == kj && i < j))) continue;
-            if (!greedy_covers(jx, jy, jz, sx[i], sy[i], sz[i], thr[i])) continue;
+            if (c32 ? !greedy_covers32(jx, jy, jz, sx[i], sy[i], sz[i], (uint32_t)thr[i])
+                    : !greedy_covers(jx, jy, jz, sx[i], sy[i], sz[i], thr[i]))
+              continue;
             if (si == kKept) { kept_cov = true; break; }
             undec_cov = true;
           }
