@@ -695,6 +695,21 @@ def main():
         peak = sms * 128 * sm_mhz * 1e6 / 1e12
         peak_basis = f"{sms} SMs x 128 int lanes x {sm_mhz} MHz (median SM clock sampled during the timed region)"
 
+        def prof_field(name, key):
+            f = ROOT / "profiles" / PROFILE_ROUND / name
+            return json.loads(f.read_text()).get(key) if f.exists() else None
+
+        def issue_roofline(inst, seconds, sms, mhz, frames):
+            if not inst:
+                return None
+            inst = inst * frames / 8192  # the capture is of the full 8192-frame workload
+            peak = sms * 4 * mhz * 1e6 / 1e9
+            achieved = inst / seconds / 1e9
+            return {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "G warp-inst/s",
+                    "frac": achieved / peak, "kernel": "pnms_binned2_frame", "warp_instructions_per_launch": inst,
+                    "basis": "warp instructions from profiles/%s/binned2_kernel_ncu.json (ncu, same workload) over "
+                             "the kernel time measured here; peak = SMs x 4 schedulers x SM clock" % PROFILE_ROUND}
+
         def prof(name):
             f = ROOT / "profiles" / PROFILE_ROUND / name
             return json.loads(f.read_text()).get("dram_bytes_per_launch") if f.exists() else None
@@ -793,6 +808,11 @@ def main():
                              "pair_tests_executed_per_launch": pairs_executed,
                              "pair_tests_dense_per_launch": int(BOXES * (BOXES - 1) // 2 * F),
                              "peak_basis": peak_basis},
+            # the kernel is issue-bound: its warp instructions (ncu, the same workload) over the
+            # measured kernel time, against the SMs' issue rate (4 schedulers x 1 warp
+            # instruction per clock each)
+            "roofline_issue": issue_roofline(prof_field("binned2_kernel_ncu.json", "inst_executed"), b_s, sms, sm_mhz,
+                                             F),
             "phase_ms": {"binned": statistics.mean(binned_ms), "dense_fallback": statistics.mean(fallback_ms),
                          "call": call_ms, "dispatcher_overhead": call_ms - statistics.mean(binned_ms),
                          "note": "binned = culling kernel + count snapshot (profiled steps); call = the default "
