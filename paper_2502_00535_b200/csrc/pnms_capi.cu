@@ -351,6 +351,7 @@ constexpr long long kSmallPairs = 24LL << 20;
 // calls of <= 2 frames above this many slots take the multi-CTA tile path (measured,
 // tools/single_frame_paths.py: a 4096-box random frame 22 us on tiles against 52 us on one CTA)
 constexpr int kTilesSmallSlots = 2048;
+constexpr long long kCoopPairs = 12LL << 20;
 
 bool small_fits(int batch, int n_max) {
   const int W32 = (n_max + 31) / 32;
@@ -391,15 +392,17 @@ bool path_fits(int path, int batch, int n_max, int cs) {
 }
 
 int auto_path(int batch, int n_max, int cs) {
+  // one or two frames above 12 Mi slot pairs: the cooperative path (measured,
+  // tools/single_frame_paths.py: 4096 clustered boxes 16.4 us against 18.4 on the small path,
+  // a tie at 3584 random boxes; two frames of 3000: 17.3 against 20.5; 2 x 4096: 16.4 against 26.6)
+  if (batch <= kCoopMaxFrames && (long long)batch * n_max * n_max > kCoopPairs && coop_tiles(batch, n_max) > 0)
+    return PNMS_PATH_COOP;
   if (small_fits(batch, n_max) && (long long)batch * n_max * n_max <= kSmallPairs) return PNMS_PATH_SMALL;
   if (n_max <= kBinMaxSlots) {
     if (batch <= 2 && n_max > kTilesSmallSlots) return PNMS_PATH_TILES;
     // one wave of 1024-thread CTAs (two boxes per thread) when the batch fits the SMs
     return (n_max <= 2048 && batch <= sm_count()) ? PNMS_PATH_BINNED_WIDE : PNMS_PATH_BINNED;
   }
-  // single large frames: the cooperative path above 8192 slots (C3, 16384 boxes: 23.4 us
-  // against 30.5 on the tiles; they tie at 8192 — tools/single_frame_paths.py)
-  if (batch <= kCoopMaxFrames && n_max > 4096 && coop_tiles(batch, n_max) > 0) return PNMS_PATH_COOP;
   if (batch <= 2 || !cluster_fits(n_max, cs)) return PNMS_PATH_TILES;
   return PNMS_PATH_CLUSTER;
 }

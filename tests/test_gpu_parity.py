@@ -170,7 +170,7 @@ def test_config_batches_match_reference(golden_configs, path_name):
 
 def test_default_paths_of_the_configs(golden_configs):
     """Which path the library picks for each BASELINE config shape (the ones bench.py times)."""
-    want = {"C1": "small", "C2": "small", "C3": "coop"}
+    want = {"C1": "small", "C2": "coop", "C3": "coop"}
     for name, p in want.items():
         g = golden_configs[name]
         n = len(g["x"])
@@ -180,7 +180,7 @@ def test_default_paths_of_the_configs(golden_configs):
         assert lc.path_taken == p, name
         assert np.array_equal(ki[0, : int(kc.item())].cpu().numpy(), g["keep"])
     for (B, n), p in {(256, 1024): "binned", (100, 1024): "binned_wide", (400, 2048): "binned",
-                      (2, 4000): "tiles", (1, 8000): "coop", (2, 9000): "coop", (3, 9000): "cluster"}.items():
+                      (2, 4000): "coop", (1, 3000): "small", (1, 8000): "coop", (2, 9000): "coop", (3, 9000): "cluster"}.items():
         x, y, z, s = random_frames(B, n, seed=B, frame_w=3840, frame_h=2160)
         lc = LaunchConfig()
         ki, kc = batched_nms_keep(*(torch.from_numpy(a).to(DEV) for a in (x, y, z, s)), None, 0.5, launch=lc)
