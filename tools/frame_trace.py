@@ -44,3 +44,10 @@ print(f"frame start spread {(t[:, 0].max() - t0) / 1e3:.2f} us; median frame tim
 d = np.diff(t, axis=1)
 for i, nm in enumerate(names):
     print(f"  {nm:14s} median {np.median(d[:, i]) / 1e3:7.3f} us   max {d[:, i].max() / 1e3:7.3f} us")
+if len(sys.argv) > 4:  # wave structure: frame start / end times and frame durations by start time
+    st, en = (t[:, 0] - t0) / 1e3, (t[:, 9] - t0) / 1e3
+    order = np.argsort(st)
+    for lo in range(0, len(order), max(1, len(order) // 12)):
+        sel = order[lo:lo + max(1, len(order) // 12)]
+        print(f"  frames {lo:5d}+: start {st[sel].min():7.2f}..{st[sel].max():7.2f} us, "
+              f"duration median {np.median(en[sel] - st[sel]):6.2f} us, end max {en[sel].max():7.2f} us")
