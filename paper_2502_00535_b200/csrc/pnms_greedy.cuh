@@ -175,7 +175,8 @@ __global__ void __launch_bounds__(kGreedyThreads) pnms_greedy_frame(GreedyArgs a
     for (int c = threadIdx.x; c <= cells; c += kGreedyThreads) cstart[c] = 0u;
     __syncthreads();
     for (int e = threadIdx.x; e < cnt; e += kGreedyThreads) {
-      const int c = (int)(((long long)sy[e] - oy) / Sy) * GX + (int)(((long long)sx[e] - ox) / Sx);
+      // (binned frames have non-negative coordinates: the offsets and quotients fit 32 bits)
+      const int c = (int)((uint32_t)(sy[e] - oy) / (uint32_t)Sy) * GX + (int)((uint32_t)(sx[e] - ox) / (uint32_t)Sx);
       cellof[e] = (uint16_t)c;
       atomicAdd(&cstart[c], 1u);
     }
