@@ -228,7 +228,9 @@ __global__ void __launch_bounds__(kSoftThreads) pnms_soft_frame(SoftArgs a) {
     for (int c = threadIdx.x; c <= cells; c += kSoftThreads) F.cstart[c] = 0u;
     __syncthreads();
     for (int e = threadIdx.x; e < cnt; e += kSoftThreads) {
-      const int c = (int)(((long long)F.sy[e] - F.oy) / F.Sy) * F.GX + (int)(((long long)F.sx[e] - F.ox) / F.Sx);
+      // (binned frames have non-negative coordinates: the offsets and quotients fit 32 bits)
+      const int c = (int)((uint32_t)(F.sy[e] - F.oy) / (uint32_t)F.Sy) * F.GX +
+                    (int)((uint32_t)(F.sx[e] - F.ox) / (uint32_t)F.Sx);
       F.cellof[e] = (uint16_t)c;
       atomicAdd(&F.cstart[c], 1u);
     }
