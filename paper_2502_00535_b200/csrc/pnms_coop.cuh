@@ -50,10 +50,10 @@ constexpr int kCoopSpecLoad = 256;  // list entries loaded with the tile's count
 constexpr int kCoopMaskWords = PNMS_MAX_SLOTS / 32;  // survivor words of one frame
 
 // per-frame scratch in the caller's persistent zeroed workspace head (zero before the first
-// call).  No call ends with a cleanup round trip: the barrier counter is monotone (a call's
-// parity is bit 0 of its index, coop_barrier); the statistics are
-// re-zeroed by CTA 0 once every CTA has read them (after barrier 2), a tile's list count by its
-// own CTA once read, and the survivor mask and overflow flag are double-buffered by call parity
+// call).  No call ends with a cleanup round trip: the barrier counters are monotone (a call's
+// parity is bit 0 of its index, coop_barrier); the statistics (read by every CTA in phase 1) and
+// each tile's list count (read by its own CTA in phase 2) are re-zeroed with plain stores at the
+// end of the call, and the survivor mask and overflow flag are double-buffered by call parity
 // (a call zeroes the other parity's, which the previous call used).  Every statistics field's
 // identity is 0 (minima are kept as maxima of complements).
 struct CoopFrame {
@@ -71,8 +71,8 @@ constexpr size_t kCoopScratchBytes = (size_t)kCoopMaxFrames * (sizeof(CoopFrame)
 
 struct CoopArgs {
   BinArgs b;
-  CoopFrame* scr;      // [kCoopMaxFrames] frame scratch (zero at entry, zero at exit)
-  uint32_t* mask;      // [kCoopMaxFrames][W32 rounded to 4] survivor bits (zero at entry and exit)
+  CoopFrame* scr;      // [kCoopMaxFrames] frame scratch (CoopFrame: valid between calls)
+  uint32_t* mask;      // [kCoopMaxFrames][2][kCoopMaskWords] survivor bits by call parity
   uint4* lists;        // [batch][T][cap] tile entries
   int tiles;           // T: CTAs per frame
   int cap;             // entries per tile list
